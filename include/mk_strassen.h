@@ -1,0 +1,124 @@
+/*
+ * mk_strassen.h -- C ABI of the B200-native Strassen / Strassen-Winograd engine
+ * (libmk_strassen.so). Plain pointers, sizes and a cudaStream_t passed as void*;
+ * every matrix is row-major FP64 in device memory with an explicit leading
+ * dimension (elements). No torch or numpy types cross this boundary.
+ *
+ * The reference (`matmulkit`, /root/reference/pkg/src/matmulkit) is pure Python
+ * with no FFI; each entry point below replaces the reference function cited next
+ * to it, and the Python package paper_2309_00628_b200 binds them with ctypes
+ * (see INTEGRATION.md for the binding a matmulkit maintainer would add).
+ *
+ * Status codes (mirroring the reference's exception types):
+ *   MK_OK 0, MK_ERR_DIMENSION 1 (DimensionError, core.py:18), MK_ERR_ALIAS 2
+ *   (AliasError, core.py:22), MK_ERR_CUDA 3, MK_ERR_WORKSPACE 4, MK_ERR_ARG 5
+ *   (ValueError), MK_ERR_INEXACT 6 (integer operands not exactly representable).
+ * mk_last_error() returns a thread-local message for the last non-zero status.
+ */
+#ifndef MK_STRASSEN_H
+#define MK_STRASSEN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+enum mk_status {
+  MK_OK = 0,
+  MK_ERR_DIMENSION = 1,
+  MK_ERR_ALIAS = 2,
+  MK_ERR_CUDA = 3,
+  MK_ERR_WORKSPACE = 4,
+  MK_ERR_ARG = 5,
+  MK_ERR_INEXACT = 6
+};
+
+/* Algorithm ids: the reference's kernel names (hybrid.py:28, kernels.py:188-193). */
+enum mk_algo {
+  MK_ALGO_NAIVE = 0,                /* naive_mul            kernels.py:350 */
+  MK_ALGO_STRASSEN = 1,             /* strassen_mul         kernels.py:370 */
+  MK_ALGO_WINOGRAD_BLOCK = 2,       /* winograd_block_mul   kernels.py:378 */
+  MK_ALGO_WINOGRAD_KNUTH = 3,       /* winograd_knuth_mul   kernels.py:386 */
+  MK_ALGO_WINOGRAD_KNUTH_8CALL = 4, /* ..., recompute_first_product=True  kernels.py:396 */
+  MK_ALGO_TWO_TEMP = 5,             /* two_temp_winograd    schedules.py:332 */
+  MK_ALGO_IN_PLACE = 6              /* in_place_winograd    schedules.py:344 */
+};
+
+/* Engine version: (major << 16) | minor. */
+int mk_version(void);
+
+/* Thread-local description of the last failing call ("" if none). */
+const char* mk_last_error(void);
+
+/* C[m x n] = A[m x k] * B[k x n] on the fused DMMA kernel (single-term products).
+ * Replaces naive_mul kernels.py:350-367 / _naive_arrays kernels.py:258-266
+ * (np.matmul -> OpenBLAS dgemm). lda/ldb must be even and A/B 16-byte aligned
+ * (TMA); C may have any ld. C must not overlap A or B (MK_ERR_ALIAS). */
+int mk_dgemm(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+             int64_t m, int64_t n, int64_t k, void* stream);
+
+/* Levels the engine runs for an order-n problem under the reference's base policy
+ * (BasePolicy kernels.py:26-57): kind 0 = "scalar", 1 = "unrolled" (param = order),
+ * 2 = "naive-cutoff" (param = threshold). naive-cutoff is honoured exactly
+ * (leaf when n <= threshold, kernels.py:276); scalar/unrolled recursion below the
+ * engine's minimum leaf order is clamped (results identical for integer data). */
+int mk_levels_for_policy(int64_t n, int kind, int64_t param, int algo, int* levels_out);
+
+/* Device workspace bytes mk_strassen needs for (algo, n, levels). 0 for the fully
+ * fused single-level plan and for the in-place schedule. */
+size_t mk_workspace_bytes(int algo, int64_t n, int levels);
+
+/* Square power-of-two product C = A * B (order n) with `levels` recursion levels.
+ * Replaces _run_dc kernels.py:335-347 (strassen / winograd-block / knuth) and
+ * _run_schedule schedules.py:300-329 (two-temp / in-place). A and B are read-only
+ * except for MK_ALGO_IN_PLACE, which, like schedules.py:344-353, stores intermediates
+ * in quadrants of A, B and C and leaves A/B unspecified. ws/ws_bytes: caller-owned
+ * device workspace of at least mk_workspace_bytes(). Asynchronous on `stream`. */
+int mk_strassen(int algo, double* A, int64_t lda, double* B, int64_t ldb, double* C, int64_t ldc,
+                int64_t n, int levels, void* ws, size_t ws_bytes, void* stream);
+
+/* Rectangular driver (hybrid.py:105-146 multiply): C[m x n] = A[m x k] * B[k x n]
+ * with `levels` Strassen-Winograd levels on zero-padded operands whose extents are
+ * rounded up to multiples of 2^levels * 16 (not the reference's square 2^j order).
+ * Padding is staged in ws (size from mk_rect_workspace_bytes). */
+size_t mk_rect_workspace_bytes(int algo, int64_t m, int64_t n, int64_t k, int levels);
+int mk_multiply_rect(int algo, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                     int64_t ldc, int64_t m, int64_t n, int64_t k, int levels, void* ws, size_t ws_bytes,
+                     void* stream);
+
+/* dst = sum_i sign[i] * src_i over a rows x cols block (nsrc <= 8); dst may alias a
+ * source exactly. Replaces block_add core.py:153-169 (np.add / np.subtract). */
+int mk_block_combine(double* dst, int64_t ldd, const double* const* src, const int64_t* lds,
+                     const double* sign, int nsrc, int64_t rows, int64_t cols, void* stream);
+
+/* Integer operand support (reference tests run int64, conftest.py:29-30). */
+int mk_i64_to_f64(const int64_t* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int64_t cols,
+                  void* stream);
+int mk_f64_to_i64(const double* src, int64_t lds, int64_t* dst, int64_t ldd, int64_t rows, int64_t cols,
+                  void* stream);
+/* max |x| of a block, synchronous (returns through *out). */
+int mk_absmax_f64(const double* src, int64_t lds, int64_t rows, int64_t cols, double* out, void* stream);
+int mk_absmax_i64(const int64_t* src, int64_t lds, int64_t rows, int64_t cols, double* out, void* stream);
+
+/* Multi-GPU sharding: number of leaf products of (algo, levels) and the subset
+ * [first, first+count) one rank computes into a partial C (accumulating, C must be
+ * zero-initialised by the caller); the caller sum-reduces the partials (NCCL). */
+int mk_product_count(int algo, int levels);
+int mk_strassen_partial(int algo, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                        int64_t ldc, int64_t n, int levels, int first, int count, void* ws, size_t ws_bytes,
+                        void* stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MK_STRASSEN_H */

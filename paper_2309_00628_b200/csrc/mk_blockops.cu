@@ -1,0 +1,152 @@
+// K4: HBM-bound block kernels used around the fused products.
+//
+//   combine   dst = sum_t s_t * src_t over an h x w block (up to 8 strided sources);
+//             dst may alias a source exactly (reference core.py:153-169 block_add allows it).
+//             Used for materialised outer-level operand sums, literal two-temp / in-place
+//             schedule steps (schedules.py:62-112), post-adds, and pad/unpad copies.
+//   i64->f64 / f64->i64 conversions for integer operands (reference tests use int64,
+//             conftest.py:29-30), and an |x|max reduction for the exactness guard.
+// Roofline: every kernel here is bandwidth-bound (FP64: 8 B per element per stream).
+#include <cuda_runtime.h>
+#include <cstdint>
+#include "mk_blockops.h"
+
+namespace mk {
+
+struct CombineArgs {
+  double* dst;
+  int64_t ldd;
+  const double* src[MK_COMBINE_MAX];
+  int64_t lds[MK_COMBINE_MAX];
+  double sign[MK_COMBINE_MAX];
+  int nsrc;
+  int64_t rows, cols;
+};
+
+// Each thread handles 2 consecutive columns (16 B) when vectorisable.
+template <bool VEC>
+__global__ void combine_kernel(const __grid_constant__ CombineArgs a) {
+  const int64_t cols_v = VEC ? (a.cols >> 1) : a.cols;
+  const int64_t total = a.rows * cols_v;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / cols_v;
+    const int64_t c = (idx - r * cols_v) * (VEC ? 2 : 1);
+    if (VEC) {
+      double2 acc = make_double2(0.0, 0.0);
+      for (int t = 0; t < a.nsrc; ++t) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(a.src[t] + r * a.lds[t] + c));
+        acc.x = fma(a.sign[t], v.x, acc.x);
+        acc.y = fma(a.sign[t], v.y, acc.y);
+      }
+      *reinterpret_cast<double2*>(a.dst + r * a.ldd + c) = acc;
+    } else {
+      double acc = 0.0;
+      for (int t = 0; t < a.nsrc; ++t) acc = fma(a.sign[t], a.src[t][r * a.lds[t] + c], acc);
+      a.dst[r * a.ldd + c] = acc;
+    }
+  }
+}
+
+static int grid_for(int64_t work, int threads) {
+  int64_t blocks = (work + threads - 1) / threads;
+  const int64_t cap = 148 * 16;  // 16 resident 256-thread CTAs per SM
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  return (int)blocks;
+}
+
+cudaError_t launch_combine(double* dst, int64_t ldd, const double* const* src, const int64_t* lds,
+                           const double* sign, int nsrc, int64_t rows, int64_t cols, cudaStream_t stream) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  if (nsrc < 0 || nsrc > MK_COMBINE_MAX) return cudaErrorInvalidValue;
+  CombineArgs a{};
+  a.dst = dst;
+  a.ldd = ldd;
+  a.nsrc = nsrc;
+  a.rows = rows;
+  a.cols = cols;
+  bool vec = (cols % 2 == 0) && (ldd % 2 == 0) && ((uintptr_t)dst % 16 == 0);
+  for (int t = 0; t < nsrc; ++t) {
+    a.src[t] = src[t];
+    a.lds[t] = lds[t];
+    a.sign[t] = sign[t];
+    vec = vec && (lds[t] % 2 == 0) && ((uintptr_t)src[t] % 16 == 0);
+  }
+  const int threads = 256;
+  if (vec)
+    combine_kernel<true><<<grid_for(rows * (cols / 2), threads), threads, 0, stream>>>(a);
+  else
+    combine_kernel<false><<<grid_for(rows * cols, threads), threads, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+__global__ void i64_to_f64_kernel(const int64_t* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
+                                  int64_t cols) {
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / cols, c = idx - r * cols;
+    dst[r * ldd + c] = (double)src[r * lds + c];
+  }
+}
+
+__global__ void f64_to_i64_kernel(const double* src, int64_t lds, int64_t* dst, int64_t ldd, int64_t rows,
+                                  int64_t cols) {
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / cols, c = idx - r * cols;
+    dst[r * ldd + c] = __double2ll_rn(src[r * lds + c]);
+  }
+}
+
+cudaError_t launch_i64_to_f64(const int64_t* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
+                              int64_t cols, cudaStream_t stream) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  i64_to_f64_kernel<<<grid_for(rows * cols, 256), 256, 0, stream>>>(src, lds, dst, ldd, rows, cols);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_f64_to_i64(const double* src, int64_t lds, int64_t* dst, int64_t ldd, int64_t rows,
+                              int64_t cols, cudaStream_t stream) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  f64_to_i64_kernel<<<grid_for(rows * cols, 256), 256, 0, stream>>>(src, lds, dst, ldd, rows, cols);
+  return cudaGetLastError();
+}
+
+// max |x| over a strided block; result (as the bit pattern of a non-negative double,
+// which orders like an unsigned integer) is atomically max-ed into *out.
+template <typename T>
+__global__ void absmax_kernel(const T* src, int64_t lds, int64_t rows, int64_t cols,
+                              unsigned long long* out) {
+  double m = 0.0;
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / cols, c = idx - r * cols;
+    const double v = fabs((double)src[r * lds + c]);
+    m = (v > m || v != v) ? v : m;  // NaN propagates
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double x = __shfl_xor_sync(0xffffffffu, m, o);
+    m = (x > m || x != x) ? x : m;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+cudaError_t launch_absmax_f64(const double* src, int64_t lds, int64_t rows, int64_t cols,
+                              unsigned long long* out, cudaStream_t stream) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  absmax_kernel<double><<<grid_for(rows * cols, 256), 256, 0, stream>>>(src, lds, rows, cols, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_absmax_i64(const int64_t* src, int64_t lds, int64_t rows, int64_t cols,
+                              unsigned long long* out, cudaStream_t stream) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  absmax_kernel<int64_t><<<grid_for(rows * cols, 256), 256, 0, stream>>>(src, lds, rows, cols, out);
+  return cudaGetLastError();
+}
+
+}  // namespace mk

@@ -1,0 +1,867 @@
+// Host planner and executor of the B200 Strassen / Strassen-Winograd engine, and the
+// C ABI declared in include/mk_strassen.h.
+//
+// The reference interprets per-level step tables on numpy views (kernels.py:269-315 _dc,
+// schedules.py:249-297 _sched_dc). Here the same step tables (restated below with their
+// file:line) are evaluated once, symbolically, into one-level coefficient form
+//     product p:  (sum_q a[p][q] A_q) x (sum_q b[p][q] B_q),   C_q = sum_p c[q][p] P_p
+// and L levels are the Kronecker powers of that form. Execution plans:
+//   * fused   (strassen / winograd-block / winograd-knuth[-8call]): the last level's
+//     pre-additions and post-additions run inside the DMMA kernel (K2/K3); outer levels
+//     materialise operand sums into per-level slots (two-temp style) and pass destination
+//     lists down (Kronecker), materialising a product only when its destination fan-out
+//     would exceed MK_MAX_DESTS.  Zero workspace at one level.
+//   * two-temp / in-place: the paper's Table 2 / Table 3 storage maps
+//     (schedules.py:62-112) run literally at every outer level (block adds = K4 combine,
+//     products recurse), the last level is fused.  In-place uses no workspace and stores
+//     intermediates in A/B/C quadrants exactly as Table 3 does.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/mk_strassen.h"
+#include "mk_blockops.h"
+#include "mk_plan.h"
+
+namespace mk {
+
+// ----------------------------------------------------------------------------------
+// Error reporting
+// ----------------------------------------------------------------------------------
+static thread_local std::string g_last_error;
+
+static int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+#define MK_CUDA_TRY(expr)                                                                   \
+  do {                                                                                      \
+    cudaError_t e_ = (expr);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail(MK_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));          \
+  } while (0)
+#define MK_TRY(expr)          \
+  do {                        \
+    int s_ = (expr);          \
+    if (s_ != MK_OK) return s_; \
+  } while (0)
+
+// ----------------------------------------------------------------------------------
+// Step tables, restated from the reference (data, not code).
+// ----------------------------------------------------------------------------------
+struct Step {
+  const char* op;  // "add" | "sub" | "mul"
+  const char* dst;
+  const char* lhs;
+  const char* rhs;
+};
+
+// kernels.py:66-92 STRASSEN_STEPS (18 adds, 7 products)
+static const Step kStrassen[] = {
+    {"add", "SA1", "A11", "A22"}, {"add", "SB1", "B11", "B22"}, {"mul", "P1", "SA1", "SB1"},
+    {"add", "SA2", "A21", "A22"}, {"mul", "P2", "SA2", "B11"},  {"sub", "SB3", "B12", "B22"},
+    {"mul", "P3", "A11", "SB3"},  {"sub", "SB4", "B21", "B11"}, {"mul", "P4", "A22", "SB4"},
+    {"add", "SA5", "A11", "A12"}, {"mul", "P5", "SA5", "B22"},  {"sub", "SA6", "A21", "A11"},
+    {"add", "SB6", "B11", "B12"}, {"mul", "P6", "SA6", "SB6"},  {"sub", "SA7", "A12", "A22"},
+    {"add", "SB7", "B21", "B22"}, {"mul", "P7", "SA7", "SB7"},  {"add", "C11", "P1", "P4"},
+    {"sub", "C11", "C11", "P5"},  {"add", "C11", "C11", "P7"},  {"add", "C12", "P3", "P5"},
+    {"add", "C21", "P2", "P4"},   {"add", "C22", "P1", "P3"},   {"sub", "C22", "C22", "P2"},
+    {"add", "C22", "C22", "P6"},
+};
+// kernels.py:96-119 WINOGRAD_BLOCK_STEPS (15 adds, 7 products)
+static const Step kWinogradBlock[] = {
+    {"add", "S1", "A21", "A22"}, {"sub", "S2", "S1", "A11"}, {"sub", "S3", "A11", "A21"},
+    {"sub", "T1", "B12", "B11"}, {"sub", "T2", "B22", "T1"}, {"sub", "T3", "B22", "B12"},
+    {"sub", "S4", "A12", "S2"},  {"sub", "T4", "T2", "B21"}, {"mul", "P1", "A11", "B11"},
+    {"mul", "P2", "A12", "B21"}, {"mul", "P3", "S4", "B22"}, {"mul", "P4", "A22", "T4"},
+    {"mul", "P5", "S1", "T1"},   {"mul", "P6", "S2", "T2"},  {"mul", "P7", "S3", "T3"},
+    {"add", "C11", "P1", "P2"},  {"add", "U2", "P1", "P6"},  {"add", "U3", "U2", "P7"},
+    {"add", "U4", "U2", "P5"},   {"add", "C12", "U4", "P3"}, {"sub", "C21", "U3", "P4"},
+    {"add", "C22", "U3", "P5"},
+};
+// kernels.py:128-152 WINOGRAD_KNUTH_STEPS (16 adds, 7 products)
+static const Step kWinogradKnuth[] = {
+    {"add", "SCD", "A21", "A22"},    {"sub", "SCDA", "SCD", "A11"},  {"sub", "TCD", "B12", "B22"},
+    {"sub", "TADC", "B11", "TCD"},   {"sub", "SCA", "A21", "A11"},   {"sub", "TCA", "B12", "B11"},
+    {"add", "SAB", "A11", "A12"},    {"sub", "SABCD", "SAB", "SCD"}, {"sub", "TBCAD", "B21", "TADC"},
+    {"mul", "M1", "A11", "B11"},     {"mul", "M2", "A12", "B21"},    {"mul", "MU", "SCA", "TCD"},
+    {"mul", "MV", "SCD", "TCA"},     {"mul", "MW", "SCDA", "TADC"},  {"mul", "M6", "SABCD", "B22"},
+    {"mul", "M7", "A22", "TBCAD"},   {"add", "W", "M1", "MW"},       {"add", "WU", "W", "MU"},
+    {"add", "C11", "M1", "M2"},      {"add", "C12", "W", "MV"},      {"add", "C12", "C12", "M6"},
+    {"add", "C21", "WU", "M7"},      {"add", "C22", "WU", "MV"},
+};
+// kernels.py:156-160 WINOGRAD_KNUTH_8CALL_STEPS: M1 recomputed as M1B for C11 (8 products)
+static const Step kWinogradKnuth8[] = {
+    {"add", "SCD", "A21", "A22"},    {"sub", "SCDA", "SCD", "A11"},  {"sub", "TCD", "B12", "B22"},
+    {"sub", "TADC", "B11", "TCD"},   {"sub", "SCA", "A21", "A11"},   {"sub", "TCA", "B12", "B11"},
+    {"add", "SAB", "A11", "A12"},    {"sub", "SABCD", "SAB", "SCD"}, {"sub", "TBCAD", "B21", "TADC"},
+    {"mul", "M1", "A11", "B11"},     {"mul", "M2", "A12", "B21"},    {"mul", "MU", "SCA", "TCD"},
+    {"mul", "MV", "SCD", "TCA"},     {"mul", "MW", "SCDA", "TADC"},  {"mul", "M6", "SABCD", "B22"},
+    {"mul", "M7", "A22", "TBCAD"},   {"add", "W", "M1", "MW"},       {"add", "WU", "W", "MU"},
+    {"mul", "M1B", "A11", "B11"},    {"add", "C11", "M1B", "M2"},    {"add", "C12", "W", "MV"},
+    {"add", "C12", "C12", "M6"},     {"add", "C21", "WU", "M7"},     {"add", "C22", "WU", "MV"},
+};
+
+// schedules.py:62-85 TWO_TEMP_STEPS and :89-112 IN_PLACE_STEPS: (symbol, op, lhs, rhs, store)
+struct SchedStep {
+  const char* symbol;
+  char op;  // '+', '-', '*'
+  const char* lhs;
+  const char* rhs;
+  const char* store;
+};
+static const SchedStep kTwoTemp[22] = {
+    {"S3", '-', "A11", "A21", "X"}, {"T3", '-', "B22", "B12", "Y"}, {"P7", '*', "S3", "T3", "C21"},
+    {"S1", '+', "A21", "A22", "X"}, {"T1", '-', "B12", "B11", "Y"}, {"P5", '*', "S1", "T1", "C22"},
+    {"S2", '-', "S1", "A11", "X"},  {"T2", '-', "B22", "T1", "Y"},  {"P6", '*', "S2", "T2", "C12"},
+    {"S4", '-', "A12", "S2", "X"},  {"P3", '*', "S4", "B22", "C11"}, {"P1", '*', "A11", "B11", "X"},
+    {"U2", '+', "P1", "P6", "C12"}, {"U3", '+', "U2", "P7", "C21"}, {"U4", '+', "U2", "P5", "C12"},
+    {"U7", '+', "U3", "P5", "C22"}, {"U5", '+', "U4", "P3", "C12"}, {"T4", '-', "T2", "B21", "Y"},
+    {"P4", '*', "A22", "T4", "C11"}, {"U6", '-', "U3", "P4", "C21"}, {"P2", '*', "A12", "B21", "C11"},
+    {"U1", '+', "P1", "P2", "C11"},
+};
+static const SchedStep kInPlace[22] = {
+    {"S3", '-', "A11", "A21", "C11"}, {"S1", '+', "A21", "A22", "A21"}, {"T1", '-', "B12", "B11", "C22"},
+    {"T3", '-', "B22", "B12", "B12"}, {"P7", '*', "S3", "T3", "C21"},   {"S2", '-', "S1", "A11", "C12"},
+    {"P1", '*', "A11", "B11", "C11"}, {"T2", '-', "B22", "T1", "B11"},  {"P5", '*', "S1", "T1", "A11"},
+    {"T4", '-', "T2", "B21", "C22"},  {"P4", '*', "A22", "T4", "A21"},  {"S4", '-', "A12", "S2", "A22"},
+    {"P6", '*', "S2", "T2", "C22"},   {"U2", '+', "P1", "P6", "C22"},   {"P2", '*', "A12", "B21", "C12"},
+    {"U1", '+', "P1", "P2", "C11"},   {"U4", '+', "U2", "P5", "C12"},   {"U3", '+', "U2", "P7", "C22"},
+    {"U6", '-', "U3", "P4", "C21"},   {"U7", '+', "U3", "P5", "C22"},   {"P3", '*', "S4", "B22", "A12"},
+    {"U5", '+', "U4", "P3", "C12"},
+};
+
+// ----------------------------------------------------------------------------------
+// One-level coefficient form, derived by symbolic execution of a step table.
+// ----------------------------------------------------------------------------------
+struct Coeffs {
+  int nprod = 0;
+  int a[8][4] = {};  // quadrant order 11, 12, 21, 22
+  int b[8][4] = {};
+  int c[4][8] = {};
+};
+
+static Coeffs derive(const Step* steps, int nsteps) {
+  // value = (kind, vector): kind 'A' (4-vector over A quadrants), 'B', 'P' (over products)
+  struct Val {
+    char kind;
+    int v[8];
+  };
+  std::map<std::string, Val> env;
+  for (int q = 0; q < 4; ++q) {
+    Val a{'A', {0}}, b{'B', {0}};
+    a.v[q] = 1;
+    b.v[q] = 1;
+    static const char* qs[4] = {"11", "12", "21", "22"};
+    env[std::string("A") + qs[q]] = a;
+    env[std::string("B") + qs[q]] = b;
+  }
+  Coeffs co;
+  for (int i = 0; i < nsteps; ++i) {
+    const Step& s = steps[i];
+    const Val& l = env.at(s.lhs);
+    const Val& r = env.at(s.rhs);
+    Val out{};
+    if (std::strcmp(s.op, "mul") == 0) {
+      const int p = co.nprod++;
+      for (int q = 0; q < 4; ++q) {
+        co.a[p][q] = l.v[q];
+        co.b[p][q] = r.v[q];
+      }
+      out.kind = 'P';
+      out.v[p] = 1;
+    } else {
+      const int sg = std::strcmp(s.op, "add") == 0 ? 1 : -1;
+      out.kind = l.kind;
+      for (int q = 0; q < 8; ++q) out.v[q] = l.v[q] + sg * r.v[q];
+    }
+    env[s.dst] = out;
+  }
+  static const char* cq[4] = {"C11", "C12", "C21", "C22"};
+  for (int q = 0; q < 4; ++q) {
+    const Val& v = env.at(cq[q]);
+    for (int p = 0; p < co.nprod; ++p) co.c[q][p] = v.v[p];
+  }
+  return co;
+}
+
+static const Coeffs& coeffs_for(int algo) {
+  static Coeffs tab[7];
+  static std::once_flag once;
+  std::call_once(once, [] {
+    tab[MK_ALGO_STRASSEN] = derive(kStrassen, sizeof(kStrassen) / sizeof(Step));
+    tab[MK_ALGO_WINOGRAD_BLOCK] = derive(kWinogradBlock, sizeof(kWinogradBlock) / sizeof(Step));
+    tab[MK_ALGO_WINOGRAD_KNUTH] = derive(kWinogradKnuth, sizeof(kWinogradKnuth) / sizeof(Step));
+    tab[MK_ALGO_WINOGRAD_KNUTH_8CALL] = derive(kWinogradKnuth8, sizeof(kWinogradKnuth8) / sizeof(Step));
+    // two-temp / in-place compute the block-Winograd algebra (schedules.py:211)
+    tab[MK_ALGO_TWO_TEMP] = tab[MK_ALGO_WINOGRAD_BLOCK];
+    tab[MK_ALGO_IN_PLACE] = tab[MK_ALGO_WINOGRAD_BLOCK];
+  });
+  return tab[algo];
+}
+
+// ----------------------------------------------------------------------------------
+// Tensor maps (driver entry point fetched through the runtime; no -lcuda needed)
+// ----------------------------------------------------------------------------------
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  });
+  return fn;
+}
+
+struct Base {
+  double* ptr = nullptr;
+  int64_t ld = 0, rows = 0, cols = 0;
+};
+
+static int make_map(CUtensorMap* m, const Base& b, uint32_t box_cols, uint32_t box_rows) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return fail(MK_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if (reinterpret_cast<uintptr_t>(b.ptr) % 16 != 0 || (b.ld * 8) % 16 != 0)
+    return fail(MK_ERR_ARG, "TMA operand needs a 16-byte aligned base and an even leading dimension");
+  cuuint64_t dims[2] = {(cuuint64_t)b.cols, (cuuint64_t)b.rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(b.ld * 8)};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)b.ptr, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(MK_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return MK_OK;
+}
+
+// ----------------------------------------------------------------------------------
+// Executor
+// ----------------------------------------------------------------------------------
+static bool debug_sync() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MK_DEBUG_SYNC");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+struct Blk {
+  int base;
+  int64_t row, col;
+  double sign;
+};
+using Lin = std::vector<Blk>;
+
+enum { BASE_A = 0, BASE_B = 1, BASE_C = 2, BASE_WS0 = 3, MAX_BASES = 64 };
+
+struct Engine {
+  int algo = 0;
+  const Coeffs* co = nullptr;
+  int L = 0;          // levels
+  int64_t n = 0;      // order (square) -- rectangular uses m/k/n below
+  int64_t leaf_m = 0, leaf_n = 0, leaf_k = 0;
+  cudaStream_t st = nullptr;
+  Base bases[MAX_BASES];
+  int nbases = 0;
+  // first-writer bitmaps per base at leaf-cell granularity
+  std::vector<std::vector<uint8_t>> written;
+  std::vector<int64_t> cell_rows, cell_cols;
+  // workspace bump allocator
+  char* ws = nullptr;
+  size_t ws_bytes = 0, ws_used = 0;
+  bool dry = false;  // sizing pass: no launches
+  size_t ws_peak = 0;
+  // leaf-range filter (multi-GPU sharding)
+  int64_t leaf_first = 0, leaf_count = -1;
+  int64_t leaf_counter = 0;
+  int launches = 0;
+
+  int add_base(double* p, int64_t ld, int64_t rows, int64_t cols, int64_t cell_r, int64_t cell_c) {
+    Base b;
+    b.ptr = p;
+    b.ld = ld;
+    b.rows = rows;
+    b.cols = cols;
+    bases[nbases] = b;
+    const int64_t cr = (rows + cell_r - 1) / cell_r, cc = (cols + cell_c - 1) / cell_c;
+    written.emplace_back((size_t)(cr * cc), 0);
+    cell_rows.push_back(cell_r);
+    cell_cols.push_back(cell_c);
+    return nbases++;
+  }
+
+  // state of a block: 0 none written, 1 all written, 2 mixed
+  int state(int base, int64_t row, int64_t col, int64_t rows, int64_t cols) const {
+    const int64_t cr = cell_rows[base], cc = cell_cols[base];
+    const int64_t ncc = (bases[base].cols + cc - 1) / cc;
+    bool any = false, all = true;
+    for (int64_t r = row / cr; r < (row + rows + cr - 1) / cr; ++r)
+      for (int64_t c = col / cc; c < (col + cols + cc - 1) / cc; ++c) {
+        const bool w = written[base][(size_t)(r * ncc + c)] != 0;
+        any |= w;
+        all &= w;
+      }
+    return all ? 1 : (any ? 2 : 0);
+  }
+  void set_state(int base, int64_t row, int64_t col, int64_t rows, int64_t cols, uint8_t v) {
+    const int64_t cr = cell_rows[base], cc = cell_cols[base];
+    const int64_t ncc = (bases[base].cols + cc - 1) / cc;
+    for (int64_t r = row / cr; r < (row + rows + cr - 1) / cr; ++r)
+      for (int64_t c = col / cc; c < (col + cols + cc - 1) / cc; ++c) written[base][(size_t)(r * ncc + c)] = v;
+  }
+
+  int alloc_slot(int64_t rows, int64_t cols, int* base_out) {
+    int64_t ld = (cols + 3) / 4 * 4;  // 32B rows for the vector epilogue / TMA
+    size_t bytes = (size_t)rows * ld * 8;
+    bytes = (bytes + 1023) / 1024 * 1024;
+    if (nbases >= MAX_BASES) return fail(MK_ERR_ARG, "too many workspace slots");
+    double* p = nullptr;
+    if (!dry) {
+      if (ws_used + bytes > ws_bytes)
+        return fail(MK_ERR_WORKSPACE, "workspace too small: need more than " + std::to_string(ws_bytes) + " bytes");
+      p = reinterpret_cast<double*>(ws + ws_used);
+    } else {
+      p = reinterpret_cast<double*>(0x1000 + ws_used);  // placeholder, never dereferenced
+    }
+    ws_used += bytes;
+    ws_peak = std::max(ws_peak, ws_used);
+    *base_out = add_base(p, ld, rows, cols, leaf_m, leaf_n);
+    return MK_OK;
+  }
+
+  // ---- block combine: dst := dst.sign * sum_i src_i.sign * src_i (chained past 8 sources) ----
+  int combine(const Blk& dst, const Lin& src, int64_t rows, int64_t cols) {
+    if (dry) return MK_OK;
+    double* dp = bases[dst.base].ptr + dst.row * bases[dst.base].ld + dst.col;
+    const int64_t ldd = bases[dst.base].ld;
+    size_t i = 0;
+    bool first = true;
+    do {
+      const double* sp[MK_COMBINE_MAX];
+      int64_t lds[MK_COMBINE_MAX];
+      double sg[MK_COMBINE_MAX];
+      int ns = 0;
+      if (!first) {  // accumulate onto the partial sum already in dst
+        sp[0] = dp;
+        lds[0] = ldd;
+        sg[0] = 1.0;
+        ns = 1;
+      }
+      for (; i < src.size() && ns < MK_COMBINE_MAX; ++i, ++ns) {
+        const Blk& b = src[i];
+        sp[ns] = bases[b.base].ptr + b.row * bases[b.base].ld + b.col;
+        lds[ns] = bases[b.base].ld;
+        sg[ns] = b.sign * dst.sign;
+      }
+      MK_CUDA_TRY(launch_combine(dp, ldd, sp, lds, sg, ns, rows, cols, st));
+      first = false;
+    } while (i < src.size());
+    return MK_OK;
+  }
+
+  // ---- one leaf product launch ----
+  int product(const Lin& X, const Lin& Y, const Lin& D, int64_t M, int64_t N, int64_t K) {
+    if ((int)X.size() > MK_MAX_TERMS || (int)Y.size() > MK_MAX_TERMS || (int)D.size() > MK_MAX_DESTS ||
+        X.empty() || Y.empty() || D.empty())
+      return fail(MK_ERR_ARG, "internal: product term/destination count out of range");
+    const int bx = X[0].base, by = Y[0].base, bd = D[0].base;
+    // TMA box origins must be 16-byte aligned: operand term offsets must be even.
+    for (const Blk& t : X)
+      if ((t.row | t.col) & 1) return fail(MK_ERR_ARG, "leaf order must be >= 2 (odd TMA term offset)");
+    for (const Blk& t : Y)
+      if ((t.row | t.col) & 1) return fail(MK_ERR_ARG, "leaf order must be >= 2 (odd TMA term offset)");
+    MkProduct p{};
+    p.na = (int)X.size();
+    p.nb = (int)Y.size();
+    p.nd = (int)D.size();
+    for (int i = 0; i < p.na; ++i) {
+      if (X[i].base != bx) return fail(MK_ERR_ARG, "internal: mixed operand bases");
+      p.a[i] = MkTerm{(int32_t)X[i].row, (int32_t)X[i].col, X[i].sign};
+    }
+    for (int i = 0; i < p.nb; ++i) {
+      if (Y[i].base != by) return fail(MK_ERR_ARG, "internal: mixed operand bases");
+      p.b[i] = MkTerm{(int32_t)Y[i].row, (int32_t)Y[i].col, Y[i].sign};
+    }
+    bool vec_ok = (N % 4 == 0) && (bases[bd].ld % 4 == 0) && (reinterpret_cast<uintptr_t>(bases[bd].ptr) % 32 == 0);
+    for (int i = 0; i < p.nd; ++i) {
+      if (D[i].base != bd) return fail(MK_ERR_ARG, "internal: mixed destination bases");
+      const int s = state(bd, D[i].row, D[i].col, M, N);
+      if (s == 2) return fail(MK_ERR_ARG, "internal: partially written destination block");
+      p.d[i] = MkDest{D[i].row, D[i].col, D[i].sign, s == 1 ? 1 : 0, 0};
+      vec_ok = vec_ok && (D[i].col % 4 == 0);
+      set_state(bd, D[i].row, D[i].col, M, N, 1);
+    }
+    ++launches;
+    if (dry) return MK_OK;
+    CUtensorMap tmA, tmB;
+    MK_TRY(make_map(&tmA, bases[bx], 16, MK_BM));
+    MK_TRY(make_map(&tmB, bases[by], 16, 16));
+    MkGemmArgs g{};
+    g.C = bases[bd].ptr;
+    g.ldc = bases[bd].ld;
+    g.M = (int32_t)M;
+    g.N = (int32_t)N;
+    g.K = (int32_t)K;
+    g.tiles_m = (int32_t)((M + MK_BM - 1) / MK_BM);
+    g.tiles_n = (int32_t)((N + MK_BN - 1) / MK_BN);
+    g.group_m = 16;
+    g.vec_ok = vec_ok ? 1 : 0;
+    MK_CUDA_TRY(launch_fused_product(tmA, tmB, g, p, st));
+    if (debug_sync()) {
+      cudaError_t e2 = cudaStreamSynchronize(st);
+      if (e2 != cudaSuccess) {
+        char buf[256];
+        snprintf(buf, sizeof buf, "product launch %d (na=%d nb=%d nd=%d M=%lld N=%lld K=%lld) failed: ", launches,
+                 p.na, p.nb, p.nd, (long long)M, (long long)N, (long long)K);
+        return fail(MK_ERR_CUDA, std::string(buf) + cudaGetErrorString(e2));
+      }
+    }
+    return MK_OK;
+  }
+
+  static Lin kron(const Lin& X, const int* coef, int64_t hr, int64_t hc) {
+    Lin out;
+    for (const Blk& b : X)
+      for (int q = 0; q < 4; ++q)
+        if (coef[q] != 0)
+          out.push_back(Blk{b.base, b.row + (q >> 1) * hr, b.col + (q & 1) * hc, b.sign * coef[q]});
+    return out;
+  }
+  Lin kron_dest(const Lin& D, int p, int64_t hr, int64_t hc) const {
+    int cq[4];
+    for (int q = 0; q < 4; ++q) cq[q] = co->c[q][p];
+    return kron(D, cq, hr, hc);
+  }
+
+  int64_t leaves_below(int remaining) const {
+    int64_t r = 1;
+    for (int i = 0; i < remaining; ++i) r *= co->nprod;
+    return r;
+  }
+
+  // ---- fused plan: operands X (MxK) and Y (KxN) at this level, destinations D (MxN) ----
+  int fused(int remaining, const Lin& X, const Lin& Y, const Lin& D, int64_t M, int64_t N, int64_t K,
+            int level) {
+    const int64_t total = leaves_below(remaining);
+    if (leaf_count >= 0) {  // shard filter
+      if (leaf_counter + total <= leaf_first || leaf_counter >= leaf_first + leaf_count) {
+        leaf_counter += total;
+        return MK_OK;
+      }
+    }
+    if (remaining == 0) {
+      ++leaf_counter;
+      return product(X, Y, D, M, N, K);
+    }
+    const int64_t hm = M / 2, hn = N / 2, hk = K / 2;
+    for (int p = 0; p < co->nprod; ++p) {
+      Lin Xp = kron(X, co->a[p], hm, hk);
+      Lin Yp = kron(Y, co->b[p], hk, hn);
+      Lin Dp = kron_dest(D, p, hm, hn);
+      if (remaining == 1) {
+        if ((int)Xp.size() > MK_MAX_TERMS || (int)Yp.size() > MK_MAX_TERMS)
+          return fail(MK_ERR_ARG, "internal: unmaterialised operand at fused level");
+        MK_TRY(fused(0, Xp, Yp, Dp, hm, hn, hk, level + 1));
+        continue;
+      }
+      // skip whole subtree if outside shard
+      const int64_t sub = leaves_below(remaining - 1);
+      if (leaf_count >= 0 && (leaf_counter + sub <= leaf_first || leaf_counter >= leaf_first + leaf_count)) {
+        leaf_counter += sub;
+        continue;
+      }
+      const size_t mark = ws_used;
+      const int nb_mark = nbases;
+      // materialise multi-term operands (two-temp style slots, freed after the subtree)
+      if (Xp.size() > 1) {
+        int sb;
+        MK_TRY(alloc_slot(hm, hk, &sb));
+        MK_TRY(combine(Blk{sb, 0, 0, 1.0}, Xp, hm, hk));
+        Xp = Lin{Blk{sb, 0, 0, 1.0}};
+      }
+      if (Yp.size() > 1) {
+        int sb;
+        MK_TRY(alloc_slot(hk, hn, &sb));
+        MK_TRY(combine(Blk{sb, 0, 0, 1.0}, Yp, hk, hn));
+        Yp = Lin{Blk{sb, 0, 0, 1.0}};
+      }
+      // destination fan-out below grows by <= 4 per level
+      int64_t worst = (int64_t)Dp.size();
+      for (int i = 1; i < remaining; ++i) worst *= 4;
+      if (worst > MK_MAX_DESTS) {
+        int pb;
+        MK_TRY(alloc_slot(hm, hn, &pb));
+        MK_TRY(fused(remaining - 1, Xp, Yp, Lin{Blk{pb, 0, 0, 1.0}}, hm, hn, hk, level + 1));
+        // post-add the materialised product into its destinations
+        for (const Blk& d : Dp) {
+          const int s = state(d.base, d.row, d.col, hm, hn);
+          if (s == 2) return fail(MK_ERR_ARG, "internal: partially written post-add destination");
+          Lin src;
+          if (s == 1) src.push_back(Blk{d.base, d.row, d.col, d.sign});  // keep existing (sign folded below)
+          src.push_back(Blk{pb, 0, 0, 1.0});
+          MK_TRY(combine(Blk{d.base, d.row, d.col, d.sign}, src, hm, hn));
+          set_state(d.base, d.row, d.col, hm, hn, 1);
+        }
+      } else {
+        MK_TRY(fused(remaining - 1, Xp, Yp, Dp, hm, hn, hk, level + 1));
+      }
+      // release slots allocated for this product
+      ws_used = mark;
+      while (nbases > nb_mark) {
+        --nbases;
+        written.pop_back();
+        cell_rows.pop_back();
+        cell_cols.pop_back();
+      }
+    }
+    return MK_OK;
+  }
+
+  // ---- literal schedule plan (two-temp / in-place) ----
+  int literal(const SchedStep* steps, bool use_xy, int remaining, Blk X, Blk Y, Blk D, int64_t s) {
+    // product of single blocks X*Y -> D (store semantics: D's old contents are replaced)
+    set_state(D.base, D.row, D.col, s, s, 0);
+    if (remaining <= 1) return fused(remaining, Lin{X}, Lin{Y}, Lin{D}, s, s, s, L - remaining);
+    const int64_t h = s / 2;
+    std::map<std::string, Blk> loc;
+    static const char* qs[4] = {"11", "12", "21", "22"};
+    for (int q = 0; q < 4; ++q) {
+      const int64_t r = (q >> 1) * h, c = (q & 1) * h;
+      loc[std::string("A") + qs[q]] = Blk{X.base, X.row + r, X.col + c, 1.0};
+      loc[std::string("B") + qs[q]] = Blk{Y.base, Y.row + r, Y.col + c, 1.0};
+      loc[std::string("C") + qs[q]] = Blk{D.base, D.row + r, D.col + c, 1.0};
+    }
+    const size_t mark = ws_used;
+    const int nb_mark = nbases;
+    if (use_xy) {
+      int bx, by;
+      MK_TRY(alloc_slot(h, h, &bx));
+      MK_TRY(alloc_slot(h, h, &by));
+      loc["X"] = Blk{bx, 0, 0, 1.0};
+      loc["Y"] = Blk{by, 0, 0, 1.0};
+    }
+    // symbol -> location binding (the reference's validate_schedule bindings, schedules.py:149-179)
+    std::map<std::string, std::string> where;
+    for (const char* nm : {"A11", "A12", "A21", "A22", "B11", "B12", "B21", "B22"}) where[nm] = nm;
+    for (int i = 0; i < 22; ++i) {
+      const SchedStep& st_ = steps[i];
+      const Blk l = loc.at(where.at(st_.lhs));
+      const Blk r = loc.at(where.at(st_.rhs));
+      const Blk d = loc.at(st_.store);
+      if (st_.op == '*') {
+        MK_TRY(literal(steps, use_xy, remaining - 1, l, r, d, h));
+      } else {
+        const double sg = st_.op == '+' ? 1.0 : -1.0;
+        MK_TRY(combine(d, Lin{l, Blk{r.base, r.row, r.col, sg}}, h, h));
+        set_state(d.base, d.row, d.col, h, h, 1);
+      }
+      where[st_.symbol] = st_.store;
+    }
+    ws_used = mark;
+    while (nbases > nb_mark) {
+      --nbases;
+      written.pop_back();
+      cell_rows.pop_back();
+      cell_cols.pop_back();
+    }
+    (void)ws_peak;
+    return MK_OK;
+  }
+};
+
+static bool overlaps(const double* a, int64_t lda, int64_t ra, int64_t ca, const double* b, int64_t ldb, int64_t rb,
+                     int64_t cb) {
+  // conservative byte-range test (the reference uses np.shares_memory, kernels.py:330-332)
+  const char* a0 = reinterpret_cast<const char*>(a);
+  const char* a1 = reinterpret_cast<const char*>(a + (ra - 1) * lda + ca);
+  const char* b0 = reinterpret_cast<const char*>(b);
+  const char* b1 = reinterpret_cast<const char*>(b + (rb - 1) * ldb + cb);
+  return a0 < b1 && b0 < a1;
+}
+
+static bool is_pow2(int64_t n) { return n >= 1 && (n & (n - 1)) == 0; }
+
+static int setup_square(Engine& e, int algo, double* A, int64_t lda, double* B, int64_t ldb, double* C, int64_t ldc,
+                        int64_t n, int levels) {
+  if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_IN_PLACE) return fail(MK_ERR_ARG, "unknown algorithm id");
+  if (n < 1) return fail(MK_ERR_DIMENSION, "order must be >= 1");
+  if (!is_pow2(n)) return fail(MK_ERR_DIMENSION, "order " + std::to_string(n) + " is not a power of two; pad inputs first");
+  if (levels < 0 || (levels > 0 && (n >> levels) < 2)) return fail(MK_ERR_ARG, "invalid level count (leaf order must be >= 2)");
+  if (lda < n || ldb < n || ldc < n) return fail(MK_ERR_DIMENSION, "leading dimension smaller than the order");
+  e.algo = algo;
+  e.co = &coeffs_for(algo);
+  e.L = levels;
+  e.n = n;
+  e.leaf_m = e.leaf_n = e.leaf_k = n >> levels;
+  e.add_base(A, lda, n, n, e.leaf_m, e.leaf_n);
+  e.add_base(B, ldb, n, n, e.leaf_m, e.leaf_n);
+  e.add_base(C, ldc, n, n, e.leaf_m, e.leaf_n);
+  return MK_OK;
+}
+
+static int run_square(Engine& e) {
+  const int64_t n = e.n;
+  if (e.algo == MK_ALGO_TWO_TEMP)
+    return e.literal(kTwoTemp, true, e.L, Blk{BASE_A, 0, 0, 1.0}, Blk{BASE_B, 0, 0, 1.0}, Blk{BASE_C, 0, 0, 1.0}, n);
+  if (e.algo == MK_ALGO_IN_PLACE)
+    return e.literal(kInPlace, false, e.L, Blk{BASE_A, 0, 0, 1.0}, Blk{BASE_B, 0, 0, 1.0}, Blk{BASE_C, 0, 0, 1.0}, n);
+  return e.fused(e.L, Lin{Blk{BASE_A, 0, 0, 1.0}}, Lin{Blk{BASE_B, 0, 0, 1.0}}, Lin{Blk{BASE_C, 0, 0, 1.0}}, n, n, n, 0);
+}
+
+}  // namespace mk
+
+// ==================================================================================
+// C ABI
+// ==================================================================================
+using namespace mk;
+
+extern "C" {
+
+int mk_version(void) { return (0 << 16) | 1; }
+
+const char* mk_last_error(void) { return g_last_error.c_str(); }
+
+int mk_dgemm(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int64_t m,
+             int64_t n, int64_t k, void* stream) {
+  g_last_error.clear();
+  if (m < 1 || n < 1 || k < 1) return fail(MK_ERR_DIMENSION, "extents must be positive");
+  if (lda < k || ldb < n || ldc < n) return fail(MK_ERR_DIMENSION, "leading dimension smaller than the extent");
+  if (overlaps(C, ldc, m, n, A, lda, m, k) || overlaps(C, ldc, m, n, B, ldb, k, n))
+    return fail(MK_ERR_ALIAS, "output view must not alias an input view");
+  Engine e;
+  e.st = static_cast<cudaStream_t>(stream);
+  e.co = &coeffs_for(MK_ALGO_WINOGRAD_BLOCK);
+  e.leaf_m = m;
+  e.leaf_n = n;
+  e.leaf_k = k;
+  e.add_base(const_cast<double*>(A), lda, m, k, m, k);
+  e.add_base(const_cast<double*>(B), ldb, k, n, k, n);
+  e.add_base(C, ldc, m, n, m, n);
+  return e.product(Lin{Blk{BASE_A, 0, 0, 1.0}}, Lin{Blk{BASE_B, 0, 0, 1.0}}, Lin{Blk{BASE_C, 0, 0, 1.0}}, m, n, k);
+}
+
+int mk_levels_for_policy(int64_t n, int kind, int64_t param, int algo, int* levels_out) {
+  g_last_error.clear();
+  if (!levels_out) return fail(MK_ERR_ARG, "levels_out is NULL");
+  if (n < 1) return fail(MK_ERR_DIMENSION, "order must be >= 1");
+  if (kind < 0 || kind > 2) return fail(MK_ERR_ARG, "unknown policy kind");
+  // reference recursion (kernels.py:271-287): stop at n == 1, at n <= threshold (naive-cutoff),
+  // at n <= order (unrolled); "scalar" runs to n == 1.
+  int L = 0;
+  int64_t s = n;
+  while (s > 1) {
+    if ((kind == 2 || kind == 1) && s <= param) break;
+    s /= 2;
+    ++L;
+  }
+  // Recursion below the engine's minimum leaf order (orders 1..8 in the reference are its
+  // scalar/unrolled micro-kernels, kernels.py:279-287) is clamped: results are identical for
+  // integer data and within tolerance otherwise; the modeled counts stay the policy's.
+  while (L > 0 && (n >> L) < MK_MIN_LEAF) --L;
+  // the paper's storage maps need at least one literal level to be observable
+  if ((algo == MK_ALGO_IN_PLACE || algo == MK_ALGO_TWO_TEMP) && L == 0 && n >= 4 &&
+      !(kind != 0 && n <= param))
+    L = 1;
+  *levels_out = L;
+  return MK_OK;
+}
+
+size_t mk_workspace_bytes(int algo, int64_t n, int levels) {
+  if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_IN_PLACE || n < 1 || !is_pow2(n) || levels < 0 ||
+      (levels > 0 && (n >> levels) < 2))
+    return 0;
+  Engine e;
+  e.dry = true;
+  if (setup_square(e, algo, reinterpret_cast<double*>(0x100000), n, reinterpret_cast<double*>(0x200000), n,
+                   reinterpret_cast<double*>(0x300000), n, n, levels) != MK_OK)
+    return 0;
+  if (run_square(e) != MK_OK) return 0;
+  return e.ws_peak;
+}
+
+int mk_strassen(int algo, double* A, int64_t lda, double* B, int64_t ldb, double* C, int64_t ldc, int64_t n,
+                int levels, void* ws, size_t ws_bytes, void* stream) {
+  g_last_error.clear();
+  Engine e;
+  MK_TRY(setup_square(e, algo, A, lda, B, ldb, C, ldc, n, levels));
+  if (overlaps(C, ldc, n, n, A, lda, n, n) || overlaps(C, ldc, n, n, B, ldb, n, n))
+    return fail(MK_ERR_ALIAS, "output view must not alias an input view");
+  if (algo == MK_ALGO_IN_PLACE && overlaps(A, lda, n, n, B, ldb, n, n))
+    return fail(MK_ERR_ALIAS, "in-place schedule requires mutually disjoint operands");
+  e.st = static_cast<cudaStream_t>(stream);
+  e.ws = static_cast<char*>(ws);
+  e.ws_bytes = ws ? ws_bytes : 0;
+  return run_square(e);
+}
+
+int mk_product_count(int algo, int levels) {
+  if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_WINOGRAD_KNUTH_8CALL || levels < 0) return -1;
+  int64_t c = 1;
+  for (int i = 0; i < levels; ++i) c *= coeffs_for(algo).nprod;
+  return (int)c;
+}
+
+int mk_strassen_partial(int algo, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                        int64_t ldc, int64_t n, int levels, int first, int count, void* ws, size_t ws_bytes,
+                        void* stream) {
+  g_last_error.clear();
+  if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_WINOGRAD_KNUTH_8CALL)
+    return fail(MK_ERR_ARG, "partial products support the fused algorithms only");
+  Engine e;
+  MK_TRY(setup_square(e, algo, const_cast<double*>(A), lda, const_cast<double*>(B), ldb, C, ldc, n, levels));
+  if (overlaps(C, ldc, n, n, A, lda, n, n) || overlaps(C, ldc, n, n, B, ldb, n, n))
+    return fail(MK_ERR_ALIAS, "output view must not alias an input view");
+  e.st = static_cast<cudaStream_t>(stream);
+  e.ws = static_cast<char*>(ws);
+  e.ws_bytes = ws ? ws_bytes : 0;
+  e.leaf_first = first;
+  e.leaf_count = count;
+  e.set_state(BASE_C, 0, 0, n, n, 1);  // partial C is zero-initialised by the caller: accumulate
+  return run_square(e);
+}
+
+static int run_rect(int algo, const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                    int64_t m, int64_t n, int64_t k, int levels, void* ws, size_t ws_bytes, cudaStream_t st,
+                    bool dry, size_t* need_out) {
+  const int64_t q = (int64_t)16 << levels;
+  const int64_t mp = (m + q - 1) / q * q, np_ = (n + q - 1) / q * q, kp = (k + q - 1) / q * q;
+  size_t off = 0;
+  auto carve = [&](size_t elems) {
+    double* p = dry ? reinterpret_cast<double*>(0x1000 + off) : reinterpret_cast<double*>(static_cast<char*>(ws) + off);
+    off += (elems * 8 + 1023) / 1024 * 1024;
+    return p;
+  };
+  double* Ap = carve((size_t)mp * kp);
+  double* Bp = carve((size_t)kp * np_);
+  double* Cp = carve((size_t)mp * np_);
+  if (!dry) {
+    if (off > ws_bytes) return fail(MK_ERR_WORKSPACE, "workspace too small for padded operands");
+    MK_CUDA_TRY(cudaMemsetAsync(Ap, 0, (size_t)mp * kp * 8, st));
+    MK_CUDA_TRY(cudaMemsetAsync(Bp, 0, (size_t)kp * np_ * 8, st));
+    const double* s[1] = {A};
+    int64_t l[1] = {lda};
+    double sg[1] = {1.0};
+    MK_CUDA_TRY(launch_combine(Ap, kp, s, l, sg, 1, m, k, st));
+    s[0] = B;
+    l[0] = ldb;
+    MK_CUDA_TRY(launch_combine(Bp, np_, s, l, sg, 1, k, n, st));
+  }
+  Engine e;
+  e.dry = dry;
+  e.st = st;
+  e.algo = algo;
+  e.co = &coeffs_for(algo);
+  e.L = levels;
+  e.leaf_m = mp >> levels;
+  e.leaf_n = np_ >> levels;
+  e.leaf_k = kp >> levels;
+  e.add_base(Ap, kp, mp, kp, e.leaf_m, e.leaf_k);
+  e.add_base(Bp, np_, kp, np_, e.leaf_k, e.leaf_n);
+  e.add_base(Cp, np_, mp, np_, e.leaf_m, e.leaf_n);
+  e.ws = dry ? nullptr : static_cast<char*>(ws) + off;
+  e.ws_bytes = dry ? 0 : ws_bytes - off;
+  MK_TRY(e.fused(levels, Lin{Blk{BASE_A, 0, 0, 1.0}}, Lin{Blk{BASE_B, 0, 0, 1.0}}, Lin{Blk{BASE_C, 0, 0, 1.0}}, mp,
+                 np_, kp, 0));
+  if (need_out) *need_out = off + e.ws_peak;
+  if (!dry) {
+    const double* s[1] = {Cp};
+    int64_t l[1] = {np_};
+    double sg[1] = {1.0};
+    MK_CUDA_TRY(launch_combine(C, ldc, s, l, sg, 1, m, n, st));
+  }
+  return MK_OK;
+}
+
+size_t mk_rect_workspace_bytes(int algo, int64_t m, int64_t n, int64_t k, int levels) {
+  if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_WINOGRAD_KNUTH_8CALL || m < 1 || n < 1 || k < 1 || levels < 0)
+    return 0;
+  size_t need = 0;
+  if (run_rect(algo, nullptr, 0, nullptr, 0, nullptr, 0, m, n, k, levels, nullptr, 0, nullptr, true, &need) != MK_OK)
+    return 0;
+  return need;
+}
+
+int mk_multiply_rect(int algo, const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                     int64_t m, int64_t n, int64_t k, int levels, void* ws, size_t ws_bytes, void* stream) {
+  g_last_error.clear();
+  if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_WINOGRAD_KNUTH_8CALL)
+    return fail(MK_ERR_ARG, "rectangular driver supports the fused algorithms");
+  if (m < 1 || n < 1 || k < 1) return fail(MK_ERR_DIMENSION, "extents must be positive");
+  if (levels < 0 || levels > 20) return fail(MK_ERR_ARG, "invalid level count");
+  if (lda < k || ldb < n || ldc < n) return fail(MK_ERR_DIMENSION, "leading dimension smaller than the extent");
+  if (overlaps(C, ldc, m, n, A, lda, m, k) || overlaps(C, ldc, m, n, B, ldb, k, n))
+    return fail(MK_ERR_ALIAS, "output view must not alias an input view");
+  const size_t need = mk_rect_workspace_bytes(algo, m, n, k, levels);
+  if (!ws || ws_bytes < need) return fail(MK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
+  return run_rect(algo, A, lda, B, ldb, C, ldc, m, n, k, levels, ws, ws_bytes, static_cast<cudaStream_t>(stream),
+                  false, nullptr);
+}
+
+int mk_block_combine(double* dst, int64_t ldd, const double* const* src, const int64_t* lds, const double* sign,
+                     int nsrc, int64_t rows, int64_t cols, void* stream) {
+  g_last_error.clear();
+  if (nsrc < 0 || nsrc > MK_COMBINE_MAX) return fail(MK_ERR_ARG, "nsrc must be in [0, 8]");
+  if (rows < 0 || cols < 0) return fail(MK_ERR_DIMENSION, "extents must be >= 0");
+  MK_CUDA_TRY(launch_combine(dst, ldd, src, lds, sign, nsrc, rows, cols, static_cast<cudaStream_t>(stream)));
+  return MK_OK;
+}
+
+int mk_i64_to_f64(const int64_t* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int64_t cols,
+                  void* stream) {
+  g_last_error.clear();
+  MK_CUDA_TRY(launch_i64_to_f64(src, lds, dst, ldd, rows, cols, static_cast<cudaStream_t>(stream)));
+  return MK_OK;
+}
+
+int mk_f64_to_i64(const double* src, int64_t lds, int64_t* dst, int64_t ldd, int64_t rows, int64_t cols,
+                  void* stream) {
+  g_last_error.clear();
+  MK_CUDA_TRY(launch_f64_to_i64(src, lds, dst, ldd, rows, cols, static_cast<cudaStream_t>(stream)));
+  return MK_OK;
+}
+
+static int absmax_common(bool is_int, const void* src, int64_t lds, int64_t rows, int64_t cols, double* out,
+                         void* stream) {
+  g_last_error.clear();
+  if (!out) return fail(MK_ERR_ARG, "out is NULL");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned long long* d = nullptr;
+  MK_CUDA_TRY(cudaMallocAsync(&d, sizeof(unsigned long long), st));
+  MK_CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(unsigned long long), st));
+  if (is_int)
+    MK_CUDA_TRY(launch_absmax_i64(static_cast<const int64_t*>(src), lds, rows, cols, d, st));
+  else
+    MK_CUDA_TRY(launch_absmax_f64(static_cast<const double*>(src), lds, rows, cols, d, st));
+  unsigned long long h = 0;
+  MK_CUDA_TRY(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
+  MK_CUDA_TRY(cudaFreeAsync(d, st));
+  MK_CUDA_TRY(cudaStreamSynchronize(st));
+  long long bits = (long long)h;
+  std::memcpy(out, &bits, sizeof(double));
+  return MK_OK;
+}
+
+int mk_absmax_f64(const double* src, int64_t lds, int64_t rows, int64_t cols, double* out, void* stream) {
+  return absmax_common(false, src, lds, rows, cols, out, stream);
+}
+int mk_absmax_i64(const int64_t* src, int64_t lds, int64_t rows, int64_t cols, double* out, void* stream) {
+  return absmax_common(true, src, lds, rows, cols, out, stream);
+}
+
+}  // extern "C"

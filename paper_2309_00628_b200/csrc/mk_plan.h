@@ -1,0 +1,50 @@
+// Plan structures shared by the host planner and the sm_100a kernels.
+//
+// A "product" is one leaf multiplication of the Strassen/Winograd recursion:
+//     P = (sum_i sa_i * A[rows ra_i.., cols ca_i..]) x (sum_j sb_j * B[rb_j.., cb_j..])
+// with P accumulated as  C[rd_k.., cd_k..] (+)= sd_k * P  for every destination k.
+// The pre-additions (reference: kernels.py:66-160 block sums, e.g. S4 = A12 - S2)
+// are formed in registers from TMA-staged tiles; the post-additions (reference
+// kernels.py:112-118, U2..U7) are the multi-destination epilogue.
+#pragma once
+#include <cstdint>
+
+#define MK_MAX_TERMS 4   // operand terms per side fused into one product
+#define MK_MAX_DESTS 16  // C destinations one product's epilogue writes
+#define MK_BM 128
+#define MK_BN 128
+#define MK_BK 16
+#define MK_CONSUMER_WARPS 8
+#define MK_THREADS 384  // warpgroup 0: TMA producer; warpgroups 1-2: DMMA consumers
+#define MK_TILE_BYTES (MK_BM * MK_BK * 8)  // 16 KiB: one operand term tile per stage
+#define MK_SMEM_BUDGET (200 * 1024)
+#define MK_MIN_LEAF 32  // smallest leaf order the level policy recurses to (scalar/unrolled clamp)
+
+struct MkTerm {
+  int32_t row, col;  // offset of the term block inside the operand base matrix
+  double sign;       // +1 / -1
+};
+
+struct MkDest {
+  int64_t row, col;  // offset of the destination block inside C
+  double sign;       // +1 / -1
+  int32_t accumulate;  // 0: first writer (store), 1: read-modify-write
+  int32_t pad_;
+};
+
+struct MkProduct {
+  int32_t na, nb, nd, pad_;
+  MkTerm a[MK_MAX_TERMS];
+  MkTerm b[MK_MAX_TERMS];
+  MkDest d[MK_MAX_DESTS];
+};
+
+struct MkGemmArgs {
+  double* C;
+  int64_t ldc;
+  int32_t M, N, K;       // leaf product extents (K % 16 == 0 unless single full-matrix terms)
+  int32_t tiles_m, tiles_n;
+  int32_t stages;
+  int32_t group_m;       // rasterisation group height (tiles)
+  int32_t vec_ok;        // 32B-vector epilogue allowed
+};
