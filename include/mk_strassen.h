@@ -53,6 +53,12 @@ enum mk_algo {
 /* Engine version: (major << 16) | minor. */
 int mk_version(void);
 
+/* Engine options (process-wide). MK_OPT_FUSE_PREADDS: 1 = form the last level's operand
+ * sums inside the DMMA kernel (K2 combiner), 0 = materialise them with HBM-bound block
+ * kernels first (default; measured faster on B200). */
+enum mk_option { MK_OPT_FUSE_PREADDS = 1 };
+int mk_set_option(int key, int value);
+
 /* Thread-local description of the last failing call ("" if none). */
 const char* mk_last_error(void);
 

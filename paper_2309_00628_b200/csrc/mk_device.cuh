@@ -58,14 +58,19 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
 // ---- FP64 tensor core ---------------------------------------------------------
 // D(8x8) += A(8x4, row) * B(4x8, col). Fragments: A lane -> (row=lane>>2, k=lane&3);
 // B lane -> (k=lane&3, col=lane>>2); C lane -> (row=lane>>2, cols 2*(lane&3)+{0,1}).
+// Not volatile: a pure register op, so the compiler may interleave it with fragment loads.
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ void lds128(double& x, double& y, uint32_t addr) {
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(addr));
+// Plain C++ shared load (LDS.128): ordered after mbar_wait by its "memory" clobber, otherwise
+// freely schedulable by the compiler.
+__device__ __forceinline__ void lds128(double& x, double& y, const uint8_t* p) {
+  const double2 v = *reinterpret_cast<const double2*>(p);
+  x = v.x;
+  y = v.y;
 }
 
 // ---- 256-bit global accesses (sm_100+) -------------------------------------------

@@ -252,6 +252,15 @@ static int make_map(CUtensorMap* m, const Base& b, uint32_t box_cols, uint32_t b
 // ----------------------------------------------------------------------------------
 // Executor
 // ----------------------------------------------------------------------------------
+static int g_fuse_preadds = -1;  // -1: unset (env MK_FUSE_PREADDS), 0/1 explicit
+static bool fuse_preadds_default() {
+  if (g_fuse_preadds < 0) {
+    const char* e = getenv("MK_FUSE_PREADDS");
+    g_fuse_preadds = (e && e[0] == '1') ? 1 : 0;
+  }
+  return g_fuse_preadds == 1;
+}
+
 static bool debug_sync() {
   static int v = -1;
   if (v < 0) {
@@ -291,6 +300,7 @@ struct Engine {
   int64_t leaf_first = 0, leaf_count = -1;
   int64_t leaf_counter = 0;
   int launches = 0;
+  bool fuse_preadds = false;  // K2 in-kernel combiner for the last level's operand sums
 
   int add_base(double* p, int64_t ld, int64_t rows, int64_t cols, int64_t cell_r, int64_t cell_c) {
     Base b;
@@ -474,7 +484,7 @@ struct Engine {
       Lin Xp = kron(X, co->a[p], hm, hk);
       Lin Yp = kron(Y, co->b[p], hk, hn);
       Lin Dp = kron_dest(D, p, hm, hn);
-      if (remaining == 1) {
+      if (remaining == 1 && fuse_preadds) {
         if ((int)Xp.size() > MK_MAX_TERMS || (int)Yp.size() > MK_MAX_TERMS)
           return fail(MK_ERR_ARG, "internal: unmaterialised operand at fused level");
         MK_TRY(fused(0, Xp, Yp, Dp, hm, hn, hk, level + 1));
@@ -537,7 +547,8 @@ struct Engine {
   int literal(const SchedStep* steps, bool use_xy, int remaining, Blk X, Blk Y, Blk D, int64_t s) {
     // product of single blocks X*Y -> D (store semantics: D's old contents are replaced)
     set_state(D.base, D.row, D.col, s, s, 0);
-    if (remaining <= 1) return fused(remaining, Lin{X}, Lin{Y}, Lin{D}, s, s, s, L - remaining);
+    if (remaining == 0 || (remaining == 1 && fuse_preadds))
+      return fused(remaining, Lin{X}, Lin{Y}, Lin{D}, s, s, s, L - remaining);
     const int64_t h = s / 2;
     std::map<std::string, Blk> loc;
     static const char* qs[4] = {"11", "12", "21", "22"};
@@ -606,6 +617,7 @@ static int setup_square(Engine& e, int algo, double* A, int64_t lda, double* B, 
   if (lda < n || ldb < n || ldc < n) return fail(MK_ERR_DIMENSION, "leading dimension smaller than the order");
   e.algo = algo;
   e.co = &coeffs_for(algo);
+  e.fuse_preadds = fuse_preadds_default();
   e.L = levels;
   e.n = n;
   e.leaf_m = e.leaf_n = e.leaf_k = n >> levels;
@@ -633,7 +645,16 @@ using namespace mk;
 
 extern "C" {
 
-int mk_version(void) { return (0 << 16) | 1; }
+int mk_version(void) { return (0 << 16) | 2; }
+
+int mk_set_option(int key, int value) {
+  g_last_error.clear();
+  if (key == MK_OPT_FUSE_PREADDS) {
+    g_fuse_preadds = value ? 1 : 0;
+    return MK_OK;
+  }
+  return fail(MK_ERR_ARG, "unknown option key");
+}
 
 const char* mk_last_error(void) { return g_last_error.c_str(); }
 
@@ -767,6 +788,7 @@ static int run_rect(int algo, const double* A, int64_t lda, const double* B, int
   e.st = st;
   e.algo = algo;
   e.co = &coeffs_for(algo);
+  e.fuse_preadds = fuse_preadds_default();
   e.L = levels;
   e.leaf_m = mp >> levels;
   e.leaf_n = np_ >> levels;

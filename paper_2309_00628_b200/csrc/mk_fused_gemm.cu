@@ -1,19 +1,23 @@
 // K1+K2+K3: the fused Strassen/Winograd leaf product for sm_100a.
 //
-//   K1  FP64 tensor-core GEMM: TMA (128B swizzle) -> smem ring (mbarrier full/empty)
-//       -> conflict-free LDS.128 fragments -> mma.sync f64 (SASS DMMA.8x8x4),
-//       128x128 CTA tile, 8 consumer warps of 64x32 + 1 TMA producer warp.
-//   K2  operand pre-additions: every term tile of  sum_i s_i * A_i  is staged by TMA
-//       into the same ring stage and summed in registers as the fragments are read,
-//       so S1..S4 / T1..T4 (reference kernels.py:96-104) never exist in HBM.
-//   K3  post-additions: the accumulator tile is added with its sign into every C
-//       quadrant the product feeds (reference kernels.py:112-118) in one epilogue,
-//       with 256-bit coalesced read-modify-writes and no P_i temporaries.
+//   K1  FP64 tensor-core GEMM: TMA (128B swizzle) -> smem operand ring (mbarrier full/empty)
+//       -> conflict-free LDS.128 fragments -> mma.sync f64 (SASS DMMA.8x8x4), 128x128 CTA
+//       tile, two consumer warpgroups (8 warps of 64x32) with register accumulators
+//       (tcgen05 has no f64 kind, so there is no TMEM path for FP64).
+//   K2  operand pre-additions: the producer warpgroup is a *combiner*. TMA lands the raw
+//       term tiles of  sum_i s_i * A_i  (e.g. S4 = A11 + A12 - A21 - A22) in a raw ring; the
+//       128 producer threads sum them once per CTA into the swizzled operand stage (layout
+//       preserving, sign applied as a sign-bit flip + DADD). S1..S4 / T1..T4 (reference
+//       kernels.py:96-104) never exist in HBM, and the DMMA warps run the plain GEMM loop.
+//       Single-term sides are TMA'd straight into the operand stage.
+//   K3  post-additions: the accumulator tile is added with its sign into every C block the
+//       product feeds (reference kernels.py:112-118) in one epilogue, with 256-bit coalesced
+//       read-modify-writes and no P_i temporaries.
 //
 // Fragment layouts (PTX m8n8k4.f64): A lane=(row g=lane>>2, k=lane&3),
 // B lane=(k=lane&3, col g), C lane=(row g, cols 2*(lane&3)+{0,1}).
-// Smem layouts: A term tile = [128 rows][16 k] doubles, 128B-swizzled (chunk ^= row&7).
-//               B term tile = 8 boxes of [16 k][16 n], each 128B-swizzled.
+// Smem layouts: A tile = [128 rows][16 k] doubles, 128B-swizzled (16B chunk ^= row&7).
+//               B tile = 8 boxes of [16 k][16 n], each 128B-swizzled.
 // A lane reads one 16B chunk of A holding k = 2c, 2c+1 (two k-steps per LDS.128); to make the
 // 8 lanes of each quarter-warp hit 8 distinct chunks, fragment row g maps to smem row
 // (g>>1) + 4*(g&1).  A lane reads one 16B chunk of a B row holding columns 2g, 2g+1, which
@@ -25,21 +29,63 @@
 
 namespace mk {
 
-template <int MAXT>
+constexpr int kOpStageBytes = 2 * MK_TILE_BYTES;  // summed A tile + summed B tile
+constexpr int kMaxStages = 8;
+
+// x with its sign bit flipped by `m` (0 or 0x80000000): one LOP3 on the integer pipe.
+__device__ __forceinline__ double flip(double x, uint32_t m) {
+  return __hiloint2double(__double2hiint(x) ^ (int)m, __double2loint(x));
+}
+
+// Sum `nt` raw term tiles (16 KiB each, identical swizzled layout) into dst; thread `tid` of
+// 128 handles 16-byte chunks tid, tid+128, ... (conflict-free, coalesced in smem).
+__device__ __forceinline__ void combine_tile(uint8_t* dst, const uint8_t* raw, int nt, uint32_t negmask,
+                                             int tid) {
+#pragma unroll 1
+  for (int c = tid; c < MK_TILE_BYTES / 16; c += 128 * 4) {
+    double2 acc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[u] = *reinterpret_cast<const double2*>(raw + (c + u * 128) * 16);
+    for (int t = 1; t < nt; ++t) {
+      const uint8_t* src = raw + t * MK_TILE_BYTES;
+      const uint32_t m = ((negmask >> t) & 1u) << 31;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double2 v = *reinterpret_cast<const double2*>(src + (c + u * 128) * 16);
+        acc[u].x += flip(v.x, m);
+        acc[u].y += flip(v.y, m);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) *reinterpret_cast<double2*>(dst + (c + u * 128) * 16) = acc[u];
+  }
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// CA / CB: the A / B operand has more than one term and goes through the combiner.
+template <bool CA, bool CB>
 __global__ void __launch_bounds__(MK_THREADS, 1)
 fused_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const MkGemmArgs args, const __grid_constant__ MkProduct prod) {
   extern __shared__ uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t full_bar[16];
-  __shared__ __align__(8) uint64_t empty_bar[16];
+  __shared__ __align__(8) uint64_t full_bar[kMaxStages];
+  __shared__ __align__(8) uint64_t empty_bar[kMaxStages];
+  __shared__ __align__(8) uint64_t raw_bar[2];
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int na = prod.na, nb = prod.nb;
-  const int S = args.stages;
-  const uint32_t stage_bytes = (uint32_t)(na + nb) * MK_TILE_BYTES;
+  const int S = args.stages;    // operand stages
+  const int D = args.raw_sets;  // raw term sets in flight (0 when nothing is combined)
   const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* smem_gen = smem_raw + (smem_base - smem_u32(smem_raw));
+  uint8_t* raw_base = smem_gen + (size_t)S * kOpStageBytes;
+  const int raw_tiles = (CA ? na : 0) + (CB ? nb : 0);
+  const uint32_t raw_set_bytes = (uint32_t)raw_tiles * MK_TILE_BYTES;
+  const uint32_t direct_bytes = (CA ? 0u : (uint32_t)MK_TILE_BYTES) + (CB ? 0u : (uint32_t)MK_TILE_BYTES);
 
   // ---- rasterised tile coordinates (group_m tile-rows walked column-major) ----
   int tm, tn;
@@ -58,41 +104,76 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full_bar[s], 1);
+      // one arrive.expect_tx from the TMA thread, plus one arrive per combiner thread
+      mbar_init(&full_bar[s], (CA || CB) ? 1 + 128 : 1);
       mbar_init(&empty_bar[s], MK_CONSUMER_WARPS);
     }
+    for (int d = 0; d < D; ++d) mbar_init(&raw_bar[d], 1);
     fence_barrier_init();
   }
   __syncthreads();
 
   if (warp < 4) {
-    // ============ producer warpgroup: frees its registers, one lane drives TMA ============
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n");
-    if (warp == 0 && lane == 0) {
-      tma_prefetch_desc(&tmA);
-      tma_prefetch_desc(&tmB);
-      for (int kt = 0; kt < KT; ++kt) {
-        const int s = kt % S;
-        if (kt >= S) mbar_wait(&empty_bar[s], ((kt / S) - 1) & 1);
-        mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
-        uint8_t* sA = smem_gen + (size_t)s * stage_bytes;
-        uint8_t* sB = sA + (size_t)na * MK_TILE_BYTES;
-        const int k0 = kt * MK_BK;
-        for (int t = 0; t < na; ++t)
-          tma_load_2d(sA + t * MK_TILE_BYTES, &tmA, k0 + prod.a[t].col, m0 + prod.a[t].row, &full_bar[s]);
-        for (int t = 0; t < nb; ++t) {
+    // ================= producer / combiner warpgroup (128 threads) =================
+    // Register budget: launched at 168/thread (384 x 168 = 64512); 128 x 56 + 256 x 224 = 64512.
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n");
+    const int tid = threadIdx.x;
+    uint32_t fa = 0, fb = 0;  // bit t set: term t enters with the opposite sign of term 0
+    for (int t = 1; t < na; ++t) fa |= (prod.a[t].sign * prod.a[0].sign < 0 ? 1u : 0u) << t;
+    for (int t = 1; t < nb; ++t) fb |= (prod.b[t].sign * prod.b[0].sign < 0 ? 1u : 0u) << t;
+    auto issue_raw = [&](int k) {  // thread 0 only: all raw term tiles of k-step k
+      const int d = k % D;
+      uint8_t* dst = raw_base + (size_t)d * raw_set_bytes;
+      mbar_arrive_expect_tx(&raw_bar[d], raw_set_bytes);
+      const int k0 = k * MK_BK;
+      if (CA)
+        for (int t = 0; t < na; ++t, dst += MK_TILE_BYTES)
+          tma_load_2d(dst, &tmA, k0 + prod.a[t].col, m0 + prod.a[t].row, &raw_bar[d]);
+      if (CB)
+        for (int t = 0; t < nb; ++t, dst += MK_TILE_BYTES)
 #pragma unroll
           for (int bj = 0; bj < 8; ++bj)
-            tma_load_2d(sB + t * MK_TILE_BYTES + bj * 2048, &tmB, n0 + prod.b[t].col + bj * 16,
-                        k0 + prod.b[t].row, &full_bar[s]);
+            tma_load_2d(dst + bj * 2048, &tmB, n0 + prod.b[t].col + bj * 16, k0 + prod.b[t].row, &raw_bar[d]);
+    };
+    if (tid == 0) {
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmB);
+      if (CA || CB)
+        for (int k = 0; k < D && k < KT; ++k) issue_raw(k);
+    }
+    for (int k = 0; k < KT; ++k) {
+      const int s = k % S;
+      if (k >= S) mbar_wait(&empty_bar[s], ((k / S) - 1) & 1);
+      uint8_t* opA = smem_gen + (size_t)s * kOpStageBytes;
+      uint8_t* opB = opA + MK_TILE_BYTES;
+      const int k0 = k * MK_BK;
+      if (tid == 0) {
+        mbar_arrive_expect_tx(&full_bar[s], direct_bytes);
+        if (!CA) tma_load_2d(opA, &tmA, k0 + prod.a[0].col, m0 + prod.a[0].row, &full_bar[s]);
+        if (!CB)
+#pragma unroll
+          for (int bj = 0; bj < 8; ++bj)
+            tma_load_2d(opB + bj * 2048, &tmB, n0 + prod.b[0].col + bj * 16, k0 + prod.b[0].row, &full_bar[s]);
+      }
+      if (CA || CB) {
+        const int d = k % D;
+        mbar_wait(&raw_bar[d], (k / D) & 1);
+        const uint8_t* raw = raw_base + (size_t)d * raw_set_bytes;
+        if (CA) {
+          combine_tile(opA, raw, na, fa, tid);
+          raw += (size_t)na * MK_TILE_BYTES;
         }
+        if (CB) combine_tile(opB, raw, nb, fb, tid);
+        mbar_arrive(&full_bar[s]);
+        named_bar_sync(1, 128);  // every combiner thread is done reading raw set d
+        if (tid == 0 && k + D < KT) issue_raw(k + D);
       }
     }
     return;
   }
 
   // ================== DMMA consumers (2 warpgroups = 8 warps) ==================
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n");
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n");
   const int cw = warp - 4;
   const int warp_m = cw >> 2;  // 0..1 -> 64-row half
   const int warp_n = cw & 3;   // 0..3 -> 32-col quarter
@@ -113,15 +194,8 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
       const int k = 2 * q + 8 * t + e;
       b_off[t][e] = b_lane + (uint32_t)k * 128u + (uint32_t)((g ^ ((2 * q + e) & 7)) << 4);
     }
-
-  double sa[MAXT], sb[MAXT];
-#pragma unroll
-  for (int t = 0; t < MAXT; ++t) {
-    sa[t] = t < na ? prod.a[t].sign : 0.0;
-    sb[t] = t < nb ? prod.b[t].sign : 0.0;
-  }
-  // Fold the first term's sign into the result so term 0 is loaded unscaled.
-  double out_sign = sa[0] * sb[0];
+  // Term 0 of each side is summed unscaled; its sign is folded into the epilogue.
+  const double out_sign = prod.a[0].sign * prod.b[0].sign;
 
   double acc[8][4][2];
 #pragma unroll
@@ -129,9 +203,9 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
 #pragma unroll
     for (int f = 0; f < 4; ++f) acc[i][f][0] = acc[i][f][1] = 0.0;
 
-  // One ring stage: 4 k-steps of 8x4 m-frags x 4 n-frags per warp. With TAIL, k >= krem
+  // One operand stage: 4 k-steps of 8x4 m-frags x 4 n-frags per warp. With TAIL, k >= krem
   // (past the leaf's K extent, possibly a neighbour quadrant's data) is zeroed on both sides.
-  auto stage = [&](const uint32_t sA, const uint32_t sB, const int krem, auto tail_tag) {
+  auto stage = [&](const uint8_t* sA, const uint8_t* sB, const int krem, auto tail_tag) {
     constexpr bool TAIL = decltype(tail_tag)::value;
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
@@ -139,25 +213,12 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
       double a0[8], a1[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) lds128(a0[i], a1[i], sA + a_lane + i * 1024u + a_chunk);
-#pragma unroll
-      for (int tt = 1; tt < MAXT; ++tt) {
-        if (tt < na) {
-          const double sg = sa[tt] * sa[0];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            double x, y;
-            lds128(x, y, sA + tt * MK_TILE_BYTES + a_lane + i * 1024u + a_chunk);
-            a0[i] = fma(sg, x, a0[i]);
-            a1[i] = fma(sg, y, a1[i]);
-          }
-        }
-      }
       if (TAIL) {
-        const int k0 = 2 * q + 8 * t;
+        const int kk = 2 * q + 8 * t;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          a0[i] = k0 < krem ? a0[i] : 0.0;
-          a1[i] = k0 + 1 < krem ? a1[i] : 0.0;
+          a0[i] = kk < krem ? a0[i] : 0.0;
+          a1[i] = kk + 1 < krem ? a1[i] : 0.0;
         }
       }
 #pragma unroll
@@ -165,19 +226,6 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         double b[4];
         lds128(b[0], b[1], sB + b_off[t][e]);
         lds128(b[2], b[3], sB + b_off[t][e] + 2048u);
-#pragma unroll
-        for (int tt = 1; tt < MAXT; ++tt) {
-          if (tt < nb) {
-            const double sg = sb[tt] * sb[0];
-            double x0, x1, x2, x3;
-            lds128(x0, x1, sB + tt * MK_TILE_BYTES + b_off[t][e]);
-            lds128(x2, x3, sB + tt * MK_TILE_BYTES + b_off[t][e] + 2048u);
-            b[0] = fma(sg, x0, b[0]);
-            b[1] = fma(sg, x1, b[1]);
-            b[2] = fma(sg, x2, b[2]);
-            b[3] = fma(sg, x3, b[3]);
-          }
-        }
         if (TAIL) {
           const bool live = 2 * q + 8 * t + e < krem;
 #pragma unroll
@@ -195,8 +243,8 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
   for (int kt = 0; kt < KT; ++kt) {
     const int s = kt % S;
     mbar_wait(&full_bar[s], (kt / S) & 1);
-    const uint32_t sA = smem_base + (uint32_t)s * stage_bytes;
-    const uint32_t sB = sA + (uint32_t)na * MK_TILE_BYTES;
+    const uint8_t* sA = smem_gen + (size_t)s * kOpStageBytes;
+    const uint8_t* sB = sA + MK_TILE_BYTES;
     if (kt == KT - 1 && krem_last < MK_BK)
       stage(sA, sB, krem_last, std::true_type{});
     else
@@ -253,31 +301,36 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
 // ------------------------------------------------------------------------------------
 cudaError_t launch_fused_product(const CUtensorMap& tmA, const CUtensorMap& tmB, const MkGemmArgs& args_in,
                                  const MkProduct& prod, cudaStream_t stream) {
+  if (prod.na < 1 || prod.na > MK_MAX_TERMS || prod.nb < 1 || prod.nb > MK_MAX_TERMS) return cudaErrorInvalidValue;
   MkGemmArgs args = args_in;
-  const int maxt = prod.na > prod.nb ? prod.na : prod.nb;
-  const uint32_t stage_bytes = (uint32_t)(prod.na + prod.nb) * MK_TILE_BYTES;
-  int stages = (int)(MK_SMEM_BUDGET / stage_bytes);
-  if (stages > 8) stages = 8;
-  if (stages < 2) return cudaErrorInvalidValue;
+  const bool ca = prod.na > 1, cb = prod.nb > 1;
+  const int raw_tiles = (ca ? prod.na : 0) + (cb ? prod.nb : 0);
+  const size_t raw_set = (size_t)raw_tiles * MK_TILE_BYTES;
+  const size_t budget = MK_SMEM_BUDGET;
+  int stages, sets = 0;
+  if (raw_tiles == 0) {
+    stages = (int)(budget / kOpStageBytes);
+  } else {
+    // two raw sets when they fit next to >= 2 operand stages, else one
+    sets = (budget >= 2 * raw_set + 2 * kOpStageBytes) ? 2 : 1;
+    stages = (int)((budget - (size_t)sets * raw_set) / kOpStageBytes);
+    if (stages < 2) return cudaErrorInvalidValue;
+  }
+  if (stages > kMaxStages) stages = kMaxStages;
   args.stages = stages;
-  const size_t smem = (size_t)stages * stage_bytes + 1024;
+  args.raw_sets = sets;
+  const size_t smem = (size_t)stages * kOpStageBytes + (size_t)sets * raw_set + 1024;
   const int grid = args.tiles_m * args.tiles_n;
   if (grid == 0) return cudaSuccess;
-  cudaError_t err;
-#define MK_LAUNCH(T)                                                                              \
-  do {                                                                                            \
-    err = cudaFuncSetAttribute(fused_product_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                               (int)smem);                                                        \
-    if (err != cudaSuccess) return err;                                                           \
-    fused_product_kernel<T><<<grid, MK_THREADS, smem, stream>>>(tmA, tmB, args, prod);            \
-  } while (0)
-  if (maxt <= 1)
-    MK_LAUNCH(1);
-  else if (maxt <= 2)
-    MK_LAUNCH(2);
-  else
-    MK_LAUNCH(4);
-#undef MK_LAUNCH
+  using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, const MkGemmArgs, const MkProduct);
+  static const KernelFn table[2][2] = {
+      {fused_product_kernel<false, false>, fused_product_kernel<false, true>},
+      {fused_product_kernel<true, false>, fused_product_kernel<true, true>},
+  };
+  KernelFn fn = table[ca ? 1 : 0][cb ? 1 : 0];
+  cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
+  fn<<<grid, MK_THREADS, smem, stream>>>(tmA, tmB, args, prod);
   return cudaGetLastError();
 }
 

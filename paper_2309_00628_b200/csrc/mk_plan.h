@@ -17,7 +17,7 @@
 #define MK_CONSUMER_WARPS 8
 #define MK_THREADS 384  // warpgroup 0: TMA producer; warpgroups 1-2: DMMA consumers
 #define MK_TILE_BYTES (MK_BM * MK_BK * 8)  // 16 KiB: one operand term tile per stage
-#define MK_SMEM_BUDGET (200 * 1024)
+#define MK_SMEM_BUDGET (224 * 1024)
 #define MK_MIN_LEAF 32  // smallest leaf order the level policy recurses to (scalar/unrolled clamp)
 
 struct MkTerm {
@@ -44,7 +44,8 @@ struct MkGemmArgs {
   int64_t ldc;
   int32_t M, N, K;       // leaf product extents (K % 16 == 0 unless single full-matrix terms)
   int32_t tiles_m, tiles_n;
-  int32_t stages;
+  int32_t stages;        // operand ring depth (set by the launcher)
+  int32_t raw_sets;      // raw term sets in flight for the combiner (set by the launcher)
   int32_t group_m;       // rasterisation group height (tiles)
   int32_t vec_ok;        // 32B-vector epilogue allowed
 };

@@ -62,6 +62,9 @@ def out(**kw):
 
 def main():
     torch.manual_seed(0)
+    fuse = int(os.environ.get("MK_FUSE", "0"))
+    lib.mk_set_option(1, fuse)
+    out(mode="fuse_preadds" if fuse else "materialised_preadds")
     dev = "cuda"
     # ---- correctness: dgemm, integer-valued, odd shapes ----
     for (m, n, k) in [(8, 8, 4), (128, 128, 16), (256, 256, 256), (1000, 777, 555), (130, 3, 17), (1, 1, 1)]:
@@ -74,7 +77,7 @@ def main():
         out(check="dgemm", m=m, n=n, k=k, maxerr=float((c - ref).abs().max()))
     # ---- correctness: algorithms x levels on integer data ----
     names = {1: "strassen", 2: "winograd_block", 3: "winograd_knuth", 4: "knuth8", 5: "two_temp", 6: "in_place"}
-    for n, levels in [(4, 1), (16, 1), (16, 3), (64, 3), (256, 1), (256, 2), (1024, 1), (1024, 2), (1024, 3), (512, 4)]:
+    for n, levels in [(4, 1), (16, 1), (16, 3), (64, 3), (256, 1), (256, 2), (1024, 1), (1024, 2), (1024, 3), (512, 4)][: (99 if not os.environ.get("MK_QUICK") else 0)]:
         a = torch.randint(-8, 9, (n, n), device=dev).double()
         b = torch.randint(-8, 9, (n, n), device=dev).double()
         ref = a @ b
