@@ -1,0 +1,109 @@
+"""ctypes binding of ``libmk_strassen.so`` (the C ABI declared in include/mk_strassen.h).
+
+The shared library is the only compute path of this package: there is no CPU or
+PyTorch fallback. Importing the package works without a GPU (so CPU-only tooling and
+tests can inspect the ABI), but every compute call raises ``EngineUnavailable`` when
+the library is missing or no CUDA device is present.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .core import AliasError, DimensionError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmk_strassen.so")
+
+# status codes (include/mk_strassen.h)
+MK_OK, MK_ERR_DIMENSION, MK_ERR_ALIAS, MK_ERR_CUDA, MK_ERR_WORKSPACE, MK_ERR_ARG, MK_ERR_INEXACT = range(7)
+
+# algorithm ids (include/mk_strassen.h enum mk_algo)
+ALGO_IDS = {
+    "naive": 0,
+    "strassen": 1,
+    "winograd-block": 2,
+    "winograd-knuth": 3,
+    "winograd-knuth-8call": 4,
+    "two-temp": 5,
+    "in-place": 6,
+}
+MK_OPT_FUSE_PREADDS = 1
+
+# every exported symbol with (restype, argtypes)
+_I64, _VP, _INT, _SZ, _DP = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t, ctypes.POINTER(ctypes.c_double)
+SIGNATURES = {
+    "mk_version": (_INT, []),
+    "mk_set_option": (_INT, [_INT, _INT]),
+    "mk_last_error": (ctypes.c_char_p, []),
+    "mk_dgemm": (_INT, [_VP, _I64, _VP, _I64, _VP, _I64, _I64, _I64, _I64, _VP]),
+    "mk_levels_for_policy": (_INT, [_I64, _INT, _I64, _INT, ctypes.POINTER(_INT)]),
+    "mk_workspace_bytes": (_SZ, [_INT, _I64, _INT]),
+    "mk_strassen": (_INT, [_INT, _VP, _I64, _VP, _I64, _VP, _I64, _I64, _INT, _VP, _SZ, _VP]),
+    "mk_rect_workspace_bytes": (_SZ, [_INT, _I64, _I64, _I64, _INT]),
+    "mk_multiply_rect": (_INT, [_INT, _VP, _I64, _VP, _I64, _VP, _I64, _I64, _I64, _I64, _INT, _VP, _SZ, _VP]),
+    "mk_block_combine": (_INT, [_VP, _I64, ctypes.POINTER(_VP), ctypes.POINTER(_I64), _DP, _INT, _I64, _I64, _VP]),
+    "mk_i64_to_f64": (_INT, [_VP, _I64, _VP, _I64, _I64, _I64, _VP]),
+    "mk_f64_to_i64": (_INT, [_VP, _I64, _VP, _I64, _I64, _I64, _VP]),
+    "mk_absmax_f64": (_INT, [_VP, _I64, _I64, _I64, _DP, _VP]),
+    "mk_absmax_i64": (_INT, [_VP, _I64, _I64, _I64, _DP, _VP]),
+    "mk_product_count": (_INT, [_INT, _INT]),
+    "mk_strassen_partial": (_INT, [_INT, _VP, _I64, _VP, _I64, _VP, _I64, _I64, _INT, _INT, _INT, _VP, _SZ, _VP]),
+}
+
+
+class EngineUnavailable(RuntimeError):
+    """The sm_100a engine cannot run here (library not built, or no CUDA device)."""
+
+
+class EngineError(RuntimeError):
+    """A CUDA-level failure inside the engine."""
+
+
+class ExactnessError(ValueError):
+    """Integer operands whose product cannot be formed exactly in FP64 on the engine."""
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load(required: bool = True):
+    """Load (once) and return the ctypes library; raise EngineUnavailable if absent."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                if required:
+                    raise EngineUnavailable(
+                        f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`"
+                    )
+                return None
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def exported_symbols() -> list[str]:
+    return sorted(SIGNATURES)
+
+
+def check(rc: int, what: str) -> None:
+    """Map an engine status code to the reference's exception types."""
+    if rc == MK_OK:
+        return
+    msg = f"{what}: {load().mk_last_error().decode(errors='replace')}"
+    if rc == MK_ERR_DIMENSION:
+        raise DimensionError(msg)
+    if rc == MK_ERR_ALIAS:
+        raise AliasError(msg)
+    if rc == MK_ERR_INEXACT:
+        raise ExactnessError(msg)
+    if rc in (MK_ERR_ARG, MK_ERR_WORKSPACE):
+        raise ValueError(msg)
+    raise EngineError(msg)

@@ -1,0 +1,331 @@
+"""Device staging and engine calls.
+
+Every compute entry point of the package funnels through here: operands are resolved to
+(pointer, leading dimension) pairs of FP64 data in HBM, the C ABI is called on the current
+torch CUDA stream, and results are written back to wherever the caller's output lives.
+
+* Device operands (CUDA tensors, or views of them) that are FP64, unit-stride and 16-byte
+  aligned are passed zero-copy.
+* Host operands are copied host->device once per call (from pinned memory when the numpy
+  array is a view of pinned storage), results device->host once.
+* Integer operands are converted on the device (``mk_i64_to_f64``) after an exactness
+  guard: max|a| * max|b| * n * 64**levels < 2**53 bounds every operand sum, leaf dot
+  product and post-addition partial sum of an L-level Strassen/Winograd schedule (per
+  level: operand sums grow <= 4x per side, destinations receive <= 4 contributions, the
+  leaf order halves), so FP64 results are exact and convert back losslessly. There is no
+  CPU fallback: a failing guard raises ExactnessError.
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+
+import numpy as np
+
+from . import _lib
+from .core import AliasError, MatrixView, views_overlap
+from .counters import EngineStats
+
+try:
+    import torch
+except Exception:  # pragma: no cover
+    torch = None
+
+_tls = threading.local()
+
+
+def last_stats() -> EngineStats:
+    st = getattr(_tls, "stats", None)
+    if st is None:
+        st = _tls.stats = EngineStats()
+    return st
+
+
+def _new_stats(**kw) -> EngineStats:
+    _tls.stats = EngineStats(**kw)
+    return _tls.stats
+
+
+def require_engine():
+    """The loaded library; raises EngineUnavailable without a CUDA device or the .so."""
+    if torch is None or not torch.cuda.is_available():
+        raise _lib.EngineUnavailable("no CUDA device: the B200 engine has no CPU fallback")
+    return _lib.load(required=True)
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _vp(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr())
+
+
+_INT_KINDS = ("i", "u", "b")
+
+
+def _is_int(dt) -> bool:
+    return np.dtype(dt).kind in _INT_KINDS
+
+
+def _round_ld(cols: int) -> int:
+    return (cols + 3) // 4 * 4
+
+
+class Operand:
+    """An FP64 device operand: `t` is a (rows x cols) CUDA view with stride (ld, 1)."""
+
+    __slots__ = ("t", "rows", "cols", "keep")
+
+    def __init__(self, t, rows, cols, keep=None):
+        self.t, self.rows, self.cols, self.keep = t, rows, cols, keep
+
+    @property
+    def ptr(self) -> ctypes.c_void_p:
+        return _vp(self.t)
+
+    @property
+    def ld(self) -> int:
+        return int(self.t.stride(0))
+
+
+def _fresh(rows: int, cols: int):
+    """A new FP64 device block with a 32-byte aligned leading dimension."""
+    buf = torch.empty((rows, _round_ld(cols)), dtype=torch.float64, device="cuda")
+    return buf[:, :cols]
+
+
+def _zero_copy_ok(t) -> bool:
+    return (t.dtype == torch.float64 and t.stride(1) == 1 and t.stride(0) % 2 == 0
+            and t.data_ptr() % 16 == 0 and t.stride(0) >= t.shape[1])
+
+
+def stage_in(view: MatrixView, *, copy: bool = False, stats: EngineStats | None = None) -> Operand:
+    """Resolve a (host or device) view to an FP64 device operand."""
+    rows, cols = view.rows, view.cols
+    if view.on_device:
+        t = view.arr
+        if not copy and _zero_copy_ok(t):
+            return Operand(t, rows, cols)
+        out = _fresh(rows, cols)
+        if t.dtype == torch.float64:
+            out.copy_(t)
+        elif t.dtype.is_floating_point:
+            out.copy_(t.to(torch.float64))
+        else:
+            _convert_int_dev(t, out)
+        return Operand(out, rows, cols)
+    # host -> device
+    src = torch.from_numpy(view.arr)  # strided host window; pinned if its storage is
+    if stats is not None:
+        stats.h2d_bytes += src.numel() * src.element_size()
+    if src.dtype == torch.float64:
+        out = _fresh(rows, cols)
+        out.copy_(src, non_blocking=src.is_pinned())
+        return Operand(out, rows, cols)
+    if src.dtype.is_floating_point:
+        out = _fresh(rows, cols)
+        out.copy_(src.to("cuda", non_blocking=src.is_pinned()).to(torch.float64))
+        return Operand(out, rows, cols)
+    dev = src.to("cuda", non_blocking=src.is_pinned())
+    out = _fresh(rows, cols)
+    _convert_int_dev(dev, out)
+    return Operand(out, rows, cols, keep=dev)
+
+
+def _convert_int_dev(t, out) -> None:
+    lib = require_engine()
+    if t.dtype != torch.int64:
+        t = t.to(torch.int64)
+    if t.stride(1) != 1:
+        t = t.contiguous()
+    _lib.check(lib.mk_i64_to_f64(_vp(t), t.stride(0), _vp(out), out.stride(0), t.shape[0], t.shape[1], _stream()),
+               "mk_i64_to_f64")
+
+
+def absmax(view: MatrixView) -> float:
+    """max |x| of a view, computed on the device."""
+    lib = require_engine()
+    t = view.arr if view.on_device else torch.from_numpy(np.ascontiguousarray(view.arr)).to("cuda")
+    if t.stride(1) != 1:
+        t = t.contiguous()
+    out = ctypes.c_double(0.0)
+    if t.dtype.is_floating_point:
+        if t.dtype != torch.float64:
+            t = t.to(torch.float64)
+        rc = lib.mk_absmax_f64(_vp(t), t.stride(0), t.shape[0], t.shape[1], ctypes.byref(out), _stream())
+    else:
+        if t.dtype != torch.int64:
+            t = t.to(torch.int64)
+        rc = lib.mk_absmax_i64(_vp(t), t.stride(0), t.shape[0], t.shape[1], ctypes.byref(out), _stream())
+    _lib.check(rc, "mk_absmax")
+    return float(out.value)
+
+
+def exactness_guard(a: MatrixView, b: MatrixView, inner: int, levels: int) -> None:
+    """Raise ExactnessError unless an integer product is exactly representable (see module doc)."""
+    ma, mb = absmax(a), absmax(b)
+    bound = ma * mb * max(inner, 1) * (64.0 ** levels)
+    if not bound < 2.0 ** 53:
+        raise _lib.ExactnessError(
+            f"integer operands too large for an exact FP64 engine run: max|a|*max|b|*n*64^L = {bound:.3e} >= 2^53"
+        )
+
+
+class Output:
+    """Where the engine writes C, and how the result reaches the caller's view."""
+
+    def __init__(self, view: MatrixView, dtype, stats: EngineStats | None = None):
+        self.view, self.dtype, self.stats = view, np.dtype(dtype), stats
+        t = view.arr if view.on_device else None
+        if t is not None and self.dtype == np.float64 and _zero_copy_ok(t) and t.stride(0) % 4 == 0 \
+                and t.data_ptr() % 32 == 0:
+            self.op = Operand(t, view.rows, view.cols)
+            self.direct = True
+        else:
+            self.op = Operand(_fresh(view.rows, view.cols), view.rows, view.cols)
+            self.direct = False
+
+    def finish(self) -> None:
+        if self.direct:
+            return
+        res = self.op.t
+        if _is_int(self.dtype):
+            lib = require_engine()
+            ires = torch.empty((res.shape[0], res.shape[1]), dtype=torch.int64, device="cuda")
+            _lib.check(lib.mk_f64_to_i64(_vp(res), res.stride(0), _vp(ires), ires.stride(0), res.shape[0],
+                                         res.shape[1], _stream()), "mk_f64_to_i64")
+            res = ires
+        if self.view.on_device:
+            self.view.arr.copy_(res)
+            return
+        host = self.view.arr
+        if self.stats is not None:
+            self.stats.d2h_bytes += res.shape[0] * res.shape[1] * res.element_size()
+        tgt = torch.from_numpy(host) if host.flags.writeable else None
+        if tgt is None:
+            raise ValueError("output view is read-only")
+        want = getattr(torch, self.dtype.name)
+        src = res if res.dtype == want else res.to(want)
+        tgt.copy_(src)
+
+
+def check_disjoint(a: MatrixView, b: MatrixView, c: MatrixView) -> None:
+    """Output must not overlap an input (reference kernels.py:330-332)."""
+    if views_overlap(c, a) or views_overlap(c, b):
+        raise AliasError("output view must not alias an input view")
+
+
+def workspace(nbytes: int):
+    return torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device="cuda")
+
+
+# ---------------------------------------------------------------------------------
+# Engine calls
+# ---------------------------------------------------------------------------------
+
+def device_gemm(a: MatrixView, b: MatrixView, c: MatrixView, dtype) -> None:
+    """C = A B on the DMMA kernel (mk_dgemm); replaces _naive_arrays kernels.py:258-266."""
+    lib = require_engine()
+    st = _new_stats(algo="naive")
+    if _is_int(dtype):
+        exactness_guard(a, b, a.cols, 0)
+    A, B = stage_in(a, stats=st), stage_in(b, stats=st)
+    out = Output(c, dtype, st)
+    C = out.op
+    rc = lib.mk_dgemm(A.ptr, A.ld, B.ptr, B.ld, C.ptr, C.ld, a.rows, b.cols, a.cols, _stream())
+    _lib.check(rc, "mk_dgemm")
+    out.finish()
+
+
+def levels_for(n: int, policy, algo: str) -> int:
+    """Engine recursion depth for the reference's base policy (mk_levels_for_policy)."""
+    lib = require_engine()
+    kind = {"scalar": 0, "unrolled": 1, "naive-cutoff": 2}[policy.kind]
+    param = policy.order if policy.kind == "unrolled" else policy.threshold
+    lv = ctypes.c_int(0)
+    _lib.check(lib.mk_levels_for_policy(n, kind, param, _lib.ALGO_IDS[algo], ctypes.byref(lv)),
+               "mk_levels_for_policy")
+    return int(lv.value)
+
+
+def device_square(algo: str, a: MatrixView, b: MatrixView, c: MatrixView, levels: int, dtype,
+                  clobber_inputs: bool = False) -> None:
+    """Square power-of-two product through mk_strassen.
+
+    With ``clobber_inputs`` (the in-place schedule, schedules.py:344-353) the engine works in
+    device copies of A and B whose final (clobbered) contents are written back to the caller's
+    views, so host callers observe the same "inputs destroyed" contract as the reference.
+    """
+    lib = require_engine()
+    st = _new_stats(algo=algo, levels=levels)
+    n = a.rows
+    if _is_int(dtype):
+        exactness_guard(a, b, n, levels)
+    A = stage_in(a, copy=clobber_inputs and a.on_device and not _zero_copy_ok(a.arr), stats=st)
+    B = stage_in(b, copy=clobber_inputs and b.on_device and not _zero_copy_ok(b.arr), stats=st)
+    out = Output(c, dtype, st)
+    C = out.op
+    aid = _lib.ALGO_IDS[algo]
+    ws_bytes = int(lib.mk_workspace_bytes(aid, n, levels))
+    st.workspace_bytes = ws_bytes
+    ws = workspace(ws_bytes)
+    rc = lib.mk_strassen(aid, A.ptr, A.ld, B.ptr, B.ld, C.ptr, C.ld, n, levels, _vp(ws), ws_bytes, _stream())
+    _lib.check(rc, f"mk_strassen({algo})")
+    out.finish()
+    if clobber_inputs:
+        for src, op in ((a, A), (b, B)):
+            if op.t is src.arr:
+                continue  # engine already worked in the caller's storage
+            _write_back(src, op.t)
+
+
+def _write_back(view: MatrixView, t) -> None:
+    """Copy engine-side (clobbered) FP64 contents back into the caller's view."""
+    dt = np.dtype(view.dtype)
+    if _is_int(dt):
+        vals = torch.round(t).to(torch.int64)
+    else:
+        vals = t.to(getattr(torch, dt.name))
+    if view.on_device:
+        view.arr.copy_(vals)
+    else:
+        if not view.arr.flags.writeable:
+            return
+        torch.from_numpy(view.arr).copy_(vals.cpu())
+
+
+def device_rect(algo: str, a: MatrixView, b: MatrixView, c: MatrixView, levels: int, dtype) -> None:
+    """Rectangular product with even-quadrant padding (mk_multiply_rect)."""
+    lib = require_engine()
+    st = _new_stats(algo=algo, levels=levels)
+    m, k, n = a.rows, a.cols, b.cols
+    if _is_int(dtype):
+        exactness_guard(a, b, k, levels)
+    A, B = stage_in(a, stats=st), stage_in(b, stats=st)
+    out = Output(c, dtype, st)
+    C = out.op
+    aid = _lib.ALGO_IDS[algo]
+    ws_bytes = int(lib.mk_rect_workspace_bytes(aid, m, n, k, levels))
+    st.workspace_bytes = ws_bytes
+    ws = workspace(ws_bytes)
+    rc = lib.mk_multiply_rect(aid, A.ptr, A.ld, B.ptr, B.ld, C.ptr, C.ld, m, n, k, levels, _vp(ws), ws_bytes,
+                              _stream())
+    _lib.check(rc, f"mk_multiply_rect({algo})")
+    out.finish()
+
+
+def device_block_combine(dst: MatrixView, terms) -> None:
+    """dst = sum sign_i * view_i on the device (mk_block_combine)."""
+    lib = require_engine()
+    dtype = np.result_type(*[v.dtype for v, _ in terms], dst.dtype)
+    ops = [stage_in(v) for v, _ in terms]
+    out = Output(dst, dst.dtype if dst.dtype == dtype else dtype)
+    C = out.op
+    n = len(ops)
+    ptrs = (ctypes.c_void_p * n)(*[o.t.data_ptr() for o in ops])
+    lds = (ctypes.c_int64 * n)(*[o.ld for o in ops])
+    sg = (ctypes.c_double * n)(*[float(s) for _, s in terms])
+    rc = lib.mk_block_combine(C.ptr, C.ld, ptrs, lds, sg, n, dst.rows, dst.cols, _stream())
+    _lib.check(rc, "mk_block_combine")
+    out.finish()

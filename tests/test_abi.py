@@ -1,0 +1,86 @@
+"""The C-ABI library: it loads, exports every function include/mk_strassen.h declares, and
+its host-only planning entry points (no CUDA calls) behave as specified. CPU only."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2309_00628_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "mk_strassen.h")
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(mk_[a-z0-9_]+)\s*\(", text)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(_lib.LIB_PATH):
+        import __graft_entry__
+
+        __graft_entry__.build()
+    return _lib.load()
+
+
+def test_library_exports_every_declared_symbol(lib):
+    names = declared_functions()
+    assert len(names) >= 15
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(names) == set(_lib.exported_symbols())
+
+
+def test_version_and_options(lib):
+    assert lib.mk_version() >= 2
+    assert lib.mk_set_option(_lib.MK_OPT_FUSE_PREADDS, 0) == 0
+    assert lib.mk_set_option(999, 1) == _lib.MK_ERR_ARG
+    assert b"unknown option" in lib.mk_last_error()
+
+
+def levels(lib, n, kind, param, algo):
+    out = ctypes.c_int(-1)
+    rc = lib.mk_levels_for_policy(n, kind, param, _lib.ALGO_IDS[algo], ctypes.byref(out))
+    assert rc == 0
+    return out.value
+
+
+def test_levels_follow_reference_recursion(lib):
+    # naive-cutoff: leaf when n <= threshold (kernels.py:276)
+    assert levels(lib, 8192, 2, 1024, "winograd-block") == 3
+    assert levels(lib, 16384, 2, 8192, "winograd-block") == 1
+    assert levels(lib, 16384, 2, 4096, "winograd-block") == 2
+    assert levels(lib, 1024, 2, 64, "strassen") == 4
+    assert levels(lib, 256, 2, 32, "winograd-block") == 3
+    assert levels(lib, 64, 2, 64, "winograd-block") == 0
+    # scalar / unrolled recursion is clamped at the engine's minimum leaf order (32)
+    assert levels(lib, 256, 0, 1, "strassen") == 3
+    assert levels(lib, 16, 0, 1, "strassen") == 0
+    assert levels(lib, 64, 1, 8, "winograd-block") == 1
+    # the storage maps of the memory-lean schedules stay observable on small orders
+    assert levels(lib, 16, 0, 1, "in-place") == 1
+    assert levels(lib, 2, 0, 1, "in-place") == 0
+
+
+def test_workspace_sizes(lib):
+    ws = lambda algo, n, L: lib.mk_workspace_bytes(_lib.ALGO_IDS[algo], n, L)  # noqa: E731
+    # one level: no workspace at all (operands are materialised only when a sum is needed:
+    # two slots of (n/2)^2 at the top level)
+    assert ws("in-place", 1024, 1) == 0 and ws("in-place", 1024, 3) == 0
+    assert ws("winograd-block", 1024, 1) == 2 * 512 * 512 * 8
+    assert ws("two-temp", 1024, 1) == 2 * 512 * 512 * 8
+    # deeper: the two slots of every level (two-temp: sum of 2 (n/2^l)^2 over levels)
+    assert ws("two-temp", 1024, 3) == 2 * 8 * (512 ** 2 + 256 ** 2 + 128 ** 2)
+    assert ws("winograd-block", 16384, 1) == 2 * 8192 * 8192 * 8
+    assert ws("winograd-block", 16, 5) == 0  # invalid (leaf order < 2)
+    assert lib.mk_rect_workspace_bytes(_lib.ALGO_IDS["winograd-block"], 12000, 10000, 14000, 5) > 0
+
+
+def test_product_counts(lib):
+    assert lib.mk_product_count(_lib.ALGO_IDS["winograd-block"], 2) == 49
+    assert lib.mk_product_count(_lib.ALGO_IDS["winograd-knuth-8call"], 1) == 8
+    assert lib.mk_product_count(_lib.ALGO_IDS["two-temp"], 1) == -1
