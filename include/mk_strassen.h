@@ -59,6 +59,16 @@ int mk_version(void);
 enum mk_option { MK_OPT_FUSE_PREADDS = 1 };
 int mk_set_option(int key, int value);
 
+/* Instrumentation (bench.py). mk_launch_count: kernels this thread has launched so far.
+ * mk_timing_begin / mk_timing_end: bracket engine calls; every leaf-product (DMMA) launch in
+ * between is timed with CUDA events on its own stream; _end synchronises and returns the
+ * summed kernel time, the number of product launches and their algorithmic flops (2mnk).
+ * mk_fp64_peak: DMMA-only microbenchmark on all SMs (the FP64 tensor roofline), TFLOP/s. */
+long long mk_launch_count(void);
+int mk_timing_begin(void);
+int mk_timing_end(double* kernel_ms, int* launches, double* flops);
+int mk_fp64_peak(double* tflops, void* stream);
+
 /* Thread-local description of the last failing call ("" if none). */
 const char* mk_last_error(void);
 

@@ -317,3 +317,56 @@ def tolerance(n: int, amax: float, bmax: float, c: float = 1.0) -> float:
     contract and holds with a wide margin in practice.)
     """
     return c * float(n) ** np.log2(12.0) * 2.0 ** -53 * amax * bmax
+
+
+# ---- leaf-product decomposition (for the multi-GPU sharding checks) --------------------
+def one_level_coefficients(kernel: str):
+    """(a, b, c) one-level coefficient form of a step table, by symbolic execution."""
+    steps = TABLES[kernel]
+    env = {}
+    for i, q in enumerate(("11", "12", "21", "22")):
+        env["A" + q] = [int(j == i) for j in range(4)]
+        env["B" + q] = [int(j == i) for j in range(4)]
+    a, b = [], []
+    nprod = sum(op == "mul" for op, *_ in steps)
+    for op, dst, x, y in steps:
+        if op == "mul":
+            a.append(env[x])
+            b.append(env[y])
+            env[dst] = [int(j == len(a) - 1) for j in range(nprod)]
+        else:
+            s = 1 if op == "add" else -1
+            env[dst] = [u + s * v for u, v in zip(env[x], env[y])]
+    c = [env["C" + q] for q in ("11", "12", "21", "22")]
+    return a, b, c
+
+
+def leaf_partial(kernel: str, a: np.ndarray, b: np.ndarray, levels: int, first: int, count: int) -> np.ndarray:
+    """Sum of the contributions of leaves [first, first+count) (level-major order) to C."""
+    ca, cb, cc = one_level_coefficients(kernel)
+    nprod = len(ca)
+    n = a.shape[0]
+    out = np.zeros((n, n), dtype=np.result_type(a, b))
+
+    def rec(level, xs, ys, ds, size, index):
+        # xs / ys / ds: lists of (row, col, sign) blocks of A / B / C at this size
+        sub = nprod ** (levels - level)
+        if index + sub <= first or index >= first + count:
+            return
+        if level == levels:
+            x = sum(s * a[r:r + size, c:c + size] for r, c, s in xs)
+            y = sum(s * b[r:r + size, c:c + size] for r, c, s in ys)
+            p = x @ y
+            for r, c, s in ds:
+                out[r:r + size, c:c + size] += s * p
+            return
+        h = size // 2
+        off = [(0, 0), (0, h), (h, 0), (h, h)]
+        for p in range(nprod):
+            nx = [(r + off[q][0], c + off[q][1], s * ca[p][q]) for r, c, s in xs for q in range(4) if ca[p][q]]
+            ny = [(r + off[q][0], c + off[q][1], s * cb[p][q]) for r, c, s in ys for q in range(4) if cb[p][q]]
+            nd = [(r + off[q][0], c + off[q][1], s * cc[q][p]) for r, c, s in ds for q in range(4) if cc[q][p]]
+            rec(level + 1, nx, ny, nd, h, index + p * nprod ** (levels - level - 1))
+
+    rec(0, [(0, 0, 1)], [(0, 0, 1)], [(0, 0, 1)], n, 0)
+    return out

@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmk_strassen.so")
-SOURCES = ["mk_fused_gemm.cu", "mk_blockops.cu", "mk_engine.cu"]
+SOURCES = ["mk_fused_gemm.cu", "mk_blockops.cu", "mk_peak.cu", "mk_engine.cu"]
 HEADERS = ["mk_device.cuh", "mk_plan.h", "mk_blockops.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

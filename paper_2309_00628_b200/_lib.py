@@ -35,6 +35,10 @@ MK_OPT_FUSE_PREADDS = 1
 _I64, _VP, _INT, _SZ, _DP = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t, ctypes.POINTER(ctypes.c_double)
 SIGNATURES = {
     "mk_version": (_INT, []),
+    "mk_launch_count": (ctypes.c_longlong, []),
+    "mk_timing_begin": (_INT, []),
+    "mk_timing_end": (_INT, [_DP, ctypes.POINTER(_INT), _DP]),
+    "mk_fp64_peak": (_INT, [_DP, _VP]),
     "mk_set_option": (_INT, [_INT, _INT]),
     "mk_last_error": (ctypes.c_char_p, []),
     "mk_dgemm": (_INT, [_VP, _I64, _VP, _I64, _VP, _I64, _I64, _I64, _I64, _VP]),

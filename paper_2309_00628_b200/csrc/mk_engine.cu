@@ -252,6 +252,15 @@ static int make_map(CUtensorMap* m, const Base& b, uint32_t box_cols, uint32_t b
 // ----------------------------------------------------------------------------------
 // Executor
 // ----------------------------------------------------------------------------------
+// ---- instrumentation (bench.py): launch counter and per-product CUDA-event timing ----
+static thread_local long long g_launch_count = 0;
+struct ProductTiming {
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  std::vector<double> flops;
+};
+static thread_local ProductTiming g_timing;
+
 static int g_fuse_preadds = -1;  // -1: unset (env MK_FUSE_PREADDS), 0/1 explicit
 static bool fuse_preadds_default() {
   if (g_fuse_preadds < 0) {
@@ -380,6 +389,7 @@ struct Engine {
         sg[ns] = b.sign * dst.sign;
       }
       MK_CUDA_TRY(launch_combine(dp, ldd, sp, lds, sg, ns, rows, cols, st));
+      ++g_launch_count;
       first = false;
     } while (i < src.size());
     return MK_OK;
@@ -432,7 +442,19 @@ struct Engine {
     g.tiles_n = (int32_t)((N + MK_BN - 1) / MK_BN);
     g.group_m = 16;
     g.vec_ok = vec_ok ? 1 : 0;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    if (g_timing.on) {
+      MK_CUDA_TRY(cudaEventCreate(&t0));
+      MK_CUDA_TRY(cudaEventCreate(&t1));
+      MK_CUDA_TRY(cudaEventRecord(t0, st));
+    }
     MK_CUDA_TRY(launch_fused_product(tmA, tmB, g, p, st));
+    ++g_launch_count;
+    if (g_timing.on) {
+      MK_CUDA_TRY(cudaEventRecord(t1, st));
+      g_timing.ev.emplace_back(t0, t1);
+      g_timing.flops.push_back(2.0 * (double)M * (double)N * (double)K);
+    }
     if (debug_sync()) {
       cudaError_t e2 = cudaStreamSynchronize(st);
       if (e2 != cudaSuccess) {
@@ -647,6 +669,50 @@ extern "C" {
 
 int mk_version(void) { return (0 << 16) | 2; }
 
+long long mk_launch_count(void) { return g_launch_count; }
+
+int mk_timing_begin(void) {
+  g_last_error.clear();
+  for (auto& pr : g_timing.ev) {
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
+  g_timing.ev.clear();
+  g_timing.flops.clear();
+  g_timing.on = true;
+  return MK_OK;
+}
+
+int mk_timing_end(double* kernel_ms, int* launches, double* flops) {
+  g_last_error.clear();
+  g_timing.on = false;
+  double ms_total = 0.0, fl = 0.0;
+  int err = MK_OK;
+  for (size_t i = 0; i < g_timing.ev.size(); ++i) {
+    float ms = 0.f;
+    cudaError_t e = cudaEventSynchronize(g_timing.ev[i].second);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, g_timing.ev[i].first, g_timing.ev[i].second);
+    if (e != cudaSuccess && err == MK_OK) err = fail(MK_ERR_CUDA, std::string("timing: ") + cudaGetErrorString(e));
+    ms_total += ms;
+    fl += g_timing.flops[i];
+    cudaEventDestroy(g_timing.ev[i].first);
+    cudaEventDestroy(g_timing.ev[i].second);
+  }
+  if (kernel_ms) *kernel_ms = ms_total;
+  if (launches) *launches = (int)g_timing.ev.size();
+  if (flops) *flops = fl;
+  g_timing.ev.clear();
+  g_timing.flops.clear();
+  return err;
+}
+
+int mk_fp64_peak(double* tflops, void* stream) {
+  g_last_error.clear();
+  if (!tflops) return fail(MK_ERR_ARG, "tflops is NULL");
+  MK_CUDA_TRY(measure_dmma_peak(tflops, static_cast<cudaStream_t>(stream)));
+  return MK_OK;
+}
+
 int mk_set_option(int key, int value) {
   g_last_error.clear();
   if (key == MK_OPT_FUSE_PREADDS) {
@@ -848,6 +914,7 @@ int mk_i64_to_f64(const int64_t* src, int64_t lds, double* dst, int64_t ldd, int
                   void* stream) {
   g_last_error.clear();
   MK_CUDA_TRY(launch_i64_to_f64(src, lds, dst, ldd, rows, cols, static_cast<cudaStream_t>(stream)));
+  ++g_launch_count;
   return MK_OK;
 }
 
@@ -855,6 +922,7 @@ int mk_f64_to_i64(const double* src, int64_t lds, int64_t* dst, int64_t ldd, int
                   void* stream) {
   g_last_error.clear();
   MK_CUDA_TRY(launch_f64_to_i64(src, lds, dst, ldd, rows, cols, static_cast<cudaStream_t>(stream)));
+  ++g_launch_count;
   return MK_OK;
 }
 

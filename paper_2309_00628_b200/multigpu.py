@@ -1,0 +1,90 @@
+"""Multi-GPU Strassen-Winograd: the 7^L leaf products of one multiplication spread over the
+GPUs of one node, partial C blocks sum-reduced over NVLink.
+
+Decomposition. An L-level product is a sum of 7^L leaf contributions (Kronecker powers of
+the one-level coefficients). Rank r of W computes a contiguous range of leaf indices in
+level-major order (``shard_range``), so leaves sharing an outer-level operand sum land on
+the same rank and that sum is materialised once there. Each rank accumulates its leaves
+into a zero-initialised partial C with the fused multi-destination epilogue
+(``mk_strassen_partial``); the partials are then summed with one collective
+(``torch.distributed.reduce``, NCCL on GPUs, gloo in the CPU tests). That reduce is the
+path's only exchange step: operands are replicated (inputs resident on every GPU, as
+BASELINE.json's multi-GPU config states) and nothing else crosses GPUs.
+
+Load balance: 7 leaves over 8 GPUs cap efficiency at 7/8; 49 over 8 at 49/56; 49 over 4
+at 49/52 -- bench.py uses two levels for N > 1.
+"""
+from __future__ import annotations
+
+import ctypes
+
+from . import _lib
+
+
+def shard_range(total: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous, balanced [first, first+count) of ``total`` leaf products for ``rank``."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    base, extra = divmod(total, world)
+    first = rank * base + min(rank, extra)
+    return first, base + (1 if rank < extra else 0)
+
+
+def leaf_count(algo: str, levels: int) -> int:
+    lib = _lib.load()
+    n = lib.mk_product_count(_lib.ALGO_IDS[algo], levels)
+    if n < 0:
+        raise ValueError(f"{algo} has no leaf-product form")
+    return n
+
+
+def partial_product(algo: str, a, b, c_partial, levels: int, first: int, count: int, stream=None, ws=None) -> int:
+    """c_partial += sum of leaves [first, first+count) of A B (all CUDA FP64, square order n).
+
+    ``c_partial`` must be zero-initialised (or hold earlier partial sums). Returns the
+    workspace bytes used.
+    """
+    import torch
+
+    lib = _lib.load()
+    n = a.shape[0]
+    aid = _lib.ALGO_IDS[algo]
+    need = int(lib.mk_workspace_bytes(aid, n, levels))
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(max(need, 16), dtype=torch.uint8, device=a.device)
+    st = ctypes.c_void_p((stream or torch.cuda.current_stream()).cuda_stream)
+    rc = lib.mk_strassen_partial(aid, ctypes.c_void_p(a.data_ptr()), a.stride(0), ctypes.c_void_p(b.data_ptr()),
+                                 b.stride(0), ctypes.c_void_p(c_partial.data_ptr()), c_partial.stride(0), n, levels,
+                                 first, count, ctypes.c_void_p(ws.data_ptr()), need, st)
+    _lib.check(rc, "mk_strassen_partial")
+    return need
+
+
+def assemble(partial, dst_rank: int = 0, group=None):
+    """Sum the ranks' partial C blocks onto ``dst_rank`` (the path's single exchange step)."""
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.reduce(partial, dst=dst_rank, op=dist.ReduceOp.SUM, group=group)
+    return partial
+
+
+def sharded_multiply(algo: str, a, b, levels: int, group=None, out=None, ws=None):
+    """C = A B with this rank's share of the leaves plus the reduce; C is valid on rank 0.
+
+    a, b: replicated CUDA FP64 operands (square, power-of-two order). Returns ``out``.
+    """
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    total = leaf_count(algo, levels)
+    first, count = shard_range(total, world, rank)
+    if out is None:
+        out = torch.zeros_like(a)
+    else:
+        out.zero_()
+    if count:
+        partial_product(algo, a, b, out, levels, first, count, ws=ws)
+    return assemble(out, 0, group)
