@@ -18,6 +18,7 @@ cudaError_t launch_absmax_f64(const double* src, int64_t lds, int64_t rows, int6
 cudaError_t launch_absmax_i64(const int64_t* src, int64_t lds, int64_t rows, int64_t cols,
                               unsigned long long* out, cudaStream_t stream);
 cudaError_t measure_dmma_peak(double* tflops_out, cudaStream_t st);
-cudaError_t launch_fused_product(const CUtensorMap& tmA, const CUtensorMap& tmB, const MkGemmArgs& args,
-                                 const MkProduct& prod, cudaStream_t stream);
+cudaError_t launch_fused_product(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
+                                 const MkGemmArgs& args, const MkProduct& prod, cudaStream_t stream);
+int consumer_layout();
 }  // namespace mk

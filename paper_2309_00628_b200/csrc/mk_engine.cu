@@ -270,6 +270,15 @@ static bool fuse_preadds_default() {
   return g_fuse_preadds == 1;
 }
 
+static bool async_epilogue_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MK_ASYNC_EPI");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static bool debug_sync() {
   static int v = -1;
   if (v < 0) {
@@ -429,9 +438,15 @@ struct Engine {
     }
     ++launches;
     if (dry) return MK_OK;
-    CUtensorMap tmA, tmB;
+    CUtensorMap tmA, tmB, tmC;
     MK_TRY(make_map(&tmA, bases[bx], 16, MK_BM));
     MK_TRY(make_map(&tmB, bases[by], 16, 16));
+    const int slab = consumer_layout() == 16 ? 32 : 64;  // rows per consumer warp
+    bool async_ok = async_epilogue_enabled() && (M % slab == 0) && (N % 16 == 0) &&
+                    (reinterpret_cast<uintptr_t>(bases[bd].ptr) % 16 == 0) && (bases[bd].ld % 2 == 0);
+    for (int i = 0; i < p.nd; ++i) async_ok = async_ok && ((D[i].row | D[i].col) % 2 == 0);
+    if (async_ok) MK_TRY(make_map(&tmC, bases[bd], 16, (uint32_t)slab));
+    else std::memset(&tmC, 0, sizeof tmC);
     MkGemmArgs g{};
     g.C = bases[bd].ptr;
     g.ldc = bases[bd].ld;
@@ -442,13 +457,14 @@ struct Engine {
     g.tiles_n = (int32_t)((N + MK_BN - 1) / MK_BN);
     g.group_m = 16;
     g.vec_ok = vec_ok ? 1 : 0;
+    g.async_epi = async_ok ? 1 : 0;
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     if (g_timing.on) {
       MK_CUDA_TRY(cudaEventCreate(&t0));
       MK_CUDA_TRY(cudaEventCreate(&t1));
       MK_CUDA_TRY(cudaEventRecord(t0, st));
     }
-    MK_CUDA_TRY(launch_fused_product(tmA, tmB, g, p, st));
+    MK_CUDA_TRY(launch_fused_product(tmA, tmB, tmC, g, p, st));
     ++g_launch_count;
     if (g_timing.on) {
       MK_CUDA_TRY(cudaEventRecord(t1, st));

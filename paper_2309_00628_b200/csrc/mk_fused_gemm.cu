@@ -23,6 +23,7 @@
 // (g>>1) + 4*(g&1).  A lane reads one 16B chunk of a B row holding columns 2g, 2g+1, which
 // feeds two n-fragments per LDS.128; the k order (2q+8t+e) matches A's.
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <type_traits>
 #include "mk_device.cuh"
 #include "mk_plan.h"
@@ -65,11 +66,39 @@ __device__ __forceinline__ void named_bar_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
+// Consumer layouts: MT = m-fragments (8 rows each) per warp.
+//   MT = 8: 8 consumer warps of 64x32 (2 per SMSP), 384 threads, 224 registers per consumer.
+//   MT = 4: 16 consumer warps of 32x32 (4 per SMSP), 640 threads, 104-112 registers per
+//           consumer: twice the warps to hide LDS / dependency latency behind DMMA.
+template <int MT>
+struct Layout {
+  static constexpr int kConsumerWarps = 4 * (16 / MT);
+  static constexpr int kThreads = 128 + 32 * kConsumerWarps;
+};
+
+// Register budgets (setmaxnreg immediates). The CTA is launched with floor(65536/threads)
+// rounded down to 8 registers per thread; producer decrease + consumer increase must fit it.
+template <int MT, bool COMBINE>
+struct Regs;
+template <bool C>
+struct Regs<8, C> {  // 384 x 168 = 64512 = 128 x 56 + 256 x 224
+  static constexpr int kProducer = 56, kConsumer = 224;
+};
+template <>
+struct Regs<4, false> {  // 640 x 96 = 61440 = 128 x 32 + 512 x 112
+  static constexpr int kProducer = 32, kConsumer = 112;
+};
+template <>
+struct Regs<4, true> {  // 61440 >= 128 x 40 + 512 x 104
+  static constexpr int kProducer = 40, kConsumer = 104;
+};
+
 // CA / CB: the A / B operand has more than one term and goes through the combiner.
-template <bool CA, bool CB>
-__global__ void __launch_bounds__(MK_THREADS, 1)
+template <bool CA, bool CB, int MT>
+__global__ void __launch_bounds__(Layout<MT>::kThreads, 1)
 fused_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const MkGemmArgs args, const __grid_constant__ MkProduct prod) {
+                     const __grid_constant__ CUtensorMap tmC, const MkGemmArgs args,
+                     const __grid_constant__ MkProduct prod) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kMaxStages];
   __shared__ __align__(8) uint64_t empty_bar[kMaxStages];
@@ -106,7 +135,7 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     for (int s = 0; s < S; ++s) {
       // one arrive.expect_tx from the TMA thread, plus one arrive per combiner thread
       mbar_init(&full_bar[s], (CA || CB) ? 1 + 128 : 1);
-      mbar_init(&empty_bar[s], MK_CONSUMER_WARPS);
+      mbar_init(&empty_bar[s], Layout<MT>::kConsumerWarps);
     }
     for (int d = 0; d < D; ++d) mbar_init(&raw_bar[d], 1);
     fence_barrier_init();
@@ -115,9 +144,9 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
 
   if (warp < 4) {
     // ================= producer / combiner warpgroup (128 threads) =================
-    // Register budget: launched at 168/thread (384 x 168 = 64512); 128 x 56 + 256 x 224 = 64512.
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(Regs<MT, CA || CB>::kProducer));
     const int tid = threadIdx.x;
+    if (!(CA || CB) && tid != 0) return;  // plain GEMM: one thread drives TMA, the rest idle
     uint32_t fa = 0, fb = 0;  // bit t set: term t enters with the opposite sign of term 0
     for (int t = 1; t < na; ++t) fa |= (prod.a[t].sign * prod.a[0].sign < 0 ? 1u : 0u) << t;
     for (int t = 1; t < nb; ++t) fb |= (prod.b[t].sign * prod.b[0].sign < 0 ? 1u : 0u) << t;
@@ -173,15 +202,15 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
   }
 
   // ================== DMMA consumers (2 warpgroups = 8 warps) ==================
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n");
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(Regs<MT, CA || CB>::kConsumer));
   const int cw = warp - 4;
-  const int warp_m = cw >> 2;  // 0..1 -> 64-row half
-  const int warp_n = cw & 3;   // 0..3 -> 32-col quarter
+  const int warp_m = cw >> 2;  // 64-row (MT=8) or 32-row (MT=4) slab
+  const int warp_n = cw & 3;   // 32-col quarter
   const int q = lane & 3, g = lane >> 2;
   const int prow = (g >> 1) + 4 * (g & 1);
 
   // A: row (warp_m*64 + 8i + prow), chunk (q + 4t) ^ prow
-  const uint32_t a_lane = (uint32_t)(warp_m * 64 + prow) * 128u;
+  const uint32_t a_lane = (uint32_t)(warp_m * (8 * MT) + prow) * 128u;
   const uint32_t a_chunk0 = (uint32_t)(((q + 0) ^ prow) << 4);
   const uint32_t a_chunk1 = (uint32_t)(((q + 4) ^ prow) << 4);
   // B: box (warp_n*2 + j), row k = 2q + 8t + e, chunk g ^ ((2q + e) & 7)
@@ -197,9 +226,9 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
   // Term 0 of each side is summed unscaled; its sign is folded into the epilogue.
   const double out_sign = prod.a[0].sign * prod.b[0].sign;
 
-  double acc[8][4][2];
+  double acc[MT][4][2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < MT; ++i)
 #pragma unroll
     for (int f = 0; f < 4; ++f) acc[i][f][0] = acc[i][f][1] = 0.0;
 
@@ -210,13 +239,13 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
       const uint32_t a_chunk = t ? a_chunk1 : a_chunk0;
-      double a0[8], a1[8];
+      double a0[MT], a1[MT];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) lds128(a0[i], a1[i], sA + a_lane + i * 1024u + a_chunk);
+      for (int i = 0; i < MT; ++i) lds128(a0[i], a1[i], sA + a_lane + i * 1024u + a_chunk);
       if (TAIL) {
         const int kk = 2 * q + 8 * t;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < MT; ++i) {
           a0[i] = kk < krem ? a0[i] : 0.0;
           a1[i] = kk + 1 < krem ? a1[i] : 0.0;
         }
@@ -232,7 +261,7 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
           for (int f = 0; f < 4; ++f) b[f] = live ? b[f] : 0.0;
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < MT; ++i)
 #pragma unroll
           for (int f = 0; f < 4; ++f) dmma(acc[i][f][0], acc[i][f][1], e ? a1[i] : a0[i], b[f]);
       }
@@ -254,16 +283,81 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
   }
 
   // ============================ multi-destination epilogue ============================
-  // Lane owns, per (i, j): row m0 + warp_m*64 + 8i + prow, cols n0 + warp_n*32 + 16j + 4q .. +3
+  // Lane owns, per (i, j): row m0 + warp_m*8*MT + 8i + prow, cols n0 + warp_n*32 + 16j + 4q .. +3
   // holding {acc[i][2j][0], acc[i][2j+1][0], acc[i][2j][1], acc[i][2j+1][1]}.
   const int nd = prod.nd;
+  if (args.async_epi) {
+    // Asynchronous epilogue: the warp stages its (8*MT) x 32 fragment as two TMA boxes of
+    // [8*MT rows][16 cols] (128B swizzle) in the now idle operand ring, then one lane issues,
+    // per destination, a TMA store (first writer) or a TMA reduce-add (accumulate); the adds
+    // run at L2. Positive-signed destinations go first; the tile is negated in place for the rest.
+    named_bar_sync(2, 32 * Layout<MT>::kConsumerWarps);  // every consumer is done with the ring
+    constexpr int kBoxRows = 8 * MT;
+    uint8_t* stg = smem_gen + (size_t)cw * (2 * kBoxRows * 128);
+    const int c_first = (g & 1) ? 1 : 0;  // store order making each quarter-warp conflict-free
+    auto stage_out = [&](double sgn) {
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const int r = 8 * i + prow;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          uint8_t* rowp = stg + j * (kBoxRows * 128) + r * 128;
+          const double v0 = sgn * acc[i][2 * j][0], v1 = sgn * acc[i][2 * j + 1][0];
+          const double v2 = sgn * acc[i][2 * j][1], v3 = sgn * acc[i][2 * j + 1][1];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = 2 * q + (h ^ c_first);  // logical 16B chunk: cols 2c, 2c+1 of the box
+            double2 v = (c & 1) ? make_double2(v2, v3) : make_double2(v0, v1);
+            *reinterpret_cast<double2*>(rowp + ((c ^ prow) << 4)) = v;
+          }
+        }
+      }
+      fence_proxy_async();
+      __syncwarp();
+    };
+    const int row0 = m0 + warp_m * kBoxRows;
+    const int col0 = n0 + warp_n * 32;
+    const bool slab_live = row0 < args.M && col0 < args.N;
+    int issued = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+      const double want = pass == 0 ? 1.0 : -1.0;
+      bool any = false;
+      for (int d = 0; d < nd; ++d) any |= (prod.d[d].sign * out_sign) == want;
+      if (!any) continue;
+      if (issued) {  // the previous pass's TMA reads of the staging must be done
+        if (lane == 0) bulk_wait_read_all();
+        __syncwarp();
+      }
+      stage_out(want);
+      if (lane == 0 && slab_live) {
+        for (int d = 0; d < nd; ++d) {
+          const MkDest dst = prod.d[d];
+          if ((dst.sign * out_sign) != want) continue;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int cc = (int)dst.col + col0 + 16 * j, rr = (int)dst.row + row0;
+            if (col0 + 16 * j >= args.N) continue;
+            if (dst.accumulate)
+              tma_reduce_add_2d(&tmC, cc, rr, stg + j * (kBoxRows * 128));
+            else
+              tma_store_2d(&tmC, cc, rr, stg + j * (kBoxRows * 128));
+          }
+        }
+        bulk_commit();
+      }
+      issued = 1;
+    }
+    if (lane == 0) bulk_wait_read_all();  // smem must stay valid until the TMA unit has read it
+    __syncwarp();
+    return;
+  }
   for (int d = 0; d < nd; ++d) {
     const MkDest dst = prod.d[d];
     const double sg = dst.sign * out_sign;
     double* Cd = args.C + dst.row * args.ldc + dst.col;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int row = m0 + warp_m * 64 + 8 * i + prow;
+    for (int i = 0; i < MT; ++i) {
+      const int row = m0 + warp_m * (8 * MT) + 8 * i + prow;
       if (row >= args.M) continue;
       double* crow = Cd + (int64_t)row * args.ldc;
 #pragma unroll
@@ -299,8 +393,19 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
 // ------------------------------------------------------------------------------------
 // Host-side launcher (called by the planner).
 // ------------------------------------------------------------------------------------
-cudaError_t launch_fused_product(const CUtensorMap& tmA, const CUtensorMap& tmB, const MkGemmArgs& args_in,
-                                 const MkProduct& prod, cudaStream_t stream) {
+// Consumer warps per CTA: 8 (MT=8, default) or 16 (MT=4); env MK_CONSUMER_WARPS overrides.
+static int g_consumer_layout = 0;
+int consumer_layout() {
+  if (g_consumer_layout == 0) {
+    const char* e = getenv("MK_CONSUMER_WARPS");
+    g_consumer_layout = (e && atoi(e) == 16) ? 16 : 8;
+  }
+  return g_consumer_layout;
+}
+void set_consumer_layout(int warps) { g_consumer_layout = (warps == 8) ? 8 : 16; }
+
+cudaError_t launch_fused_product(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
+                                 const MkGemmArgs& args_in, const MkProduct& prod, cudaStream_t stream) {
   if (prod.na < 1 || prod.na > MK_MAX_TERMS || prod.nb < 1 || prod.nb > MK_MAX_TERMS) return cudaErrorInvalidValue;
   MkGemmArgs args = args_in;
   const bool ca = prod.na > 1, cb = prod.nb > 1;
@@ -322,15 +427,20 @@ cudaError_t launch_fused_product(const CUtensorMap& tmA, const CUtensorMap& tmB,
   const size_t smem = (size_t)stages * kOpStageBytes + (size_t)sets * raw_set + 1024;
   const int grid = args.tiles_m * args.tiles_n;
   if (grid == 0) return cudaSuccess;
-  using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, const MkGemmArgs, const MkProduct);
-  static const KernelFn table[2][2] = {
-      {fused_product_kernel<false, false>, fused_product_kernel<false, true>},
-      {fused_product_kernel<true, false>, fused_product_kernel<true, true>},
+  using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const MkGemmArgs,
+                            const MkProduct);
+  static const KernelFn table[2][2][2] = {
+      {{fused_product_kernel<false, false, 8>, fused_product_kernel<false, true, 8>},
+       {fused_product_kernel<true, false, 8>, fused_product_kernel<true, true, 8>}},
+      {{fused_product_kernel<false, false, 4>, fused_product_kernel<false, true, 4>},
+       {fused_product_kernel<true, false, 4>, fused_product_kernel<true, true, 4>}},
   };
-  KernelFn fn = table[ca ? 1 : 0][cb ? 1 : 0];
+  const int wide = consumer_layout() == 16 ? 1 : 0;
+  KernelFn fn = table[wide][ca ? 1 : 0][cb ? 1 : 0];
+  const int threads = wide ? Layout<4>::kThreads : Layout<8>::kThreads;
   cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
-  fn<<<grid, MK_THREADS, smem, stream>>>(tmA, tmB, args, prod);
+  fn<<<grid, threads, smem, stream>>>(tmA, tmB, tmC, args, prod);
   return cudaGetLastError();
 }
 

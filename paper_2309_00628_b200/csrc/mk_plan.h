@@ -14,8 +14,7 @@
 #define MK_BM 128
 #define MK_BN 128
 #define MK_BK 16
-#define MK_CONSUMER_WARPS 8
-#define MK_THREADS 384  // warpgroup 0: TMA producer; warpgroups 1-2: DMMA consumers
+// CTA = warpgroup 0 (TMA producer / pre-add combiner) + 2 or 4 DMMA consumer warpgroups
 #define MK_TILE_BYTES (MK_BM * MK_BK * 8)  // 16 KiB: one operand term tile per stage
 #define MK_SMEM_BUDGET (224 * 1024)
 #define MK_MIN_LEAF 32  // smallest leaf order the level policy recurses to (scalar/unrolled clamp)
@@ -48,4 +47,5 @@ struct MkGemmArgs {
   int32_t raw_sets;      // raw term sets in flight for the combiner (set by the launcher)
   int32_t group_m;       // rasterisation group height (tiles)
   int32_t vec_ok;        // 32B-vector epilogue allowed
+  int32_t async_epi;     // TMA store / reduce-add epilogue (tile-aligned leaf, tmC valid)
 };
