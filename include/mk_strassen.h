@@ -101,7 +101,8 @@ int mk_strassen(int algo, double* A, int64_t lda, double* B, int64_t ldb, double
 
 /* Rectangular driver (hybrid.py:105-146 multiply): C[m x n] = A[m x k] * B[k x n]
  * with `levels` Strassen-Winograd levels on zero-padded operands whose extents are
- * rounded up to multiples of 2^levels * 16 (not the reference's square 2^j order).
+ * rounded up to multiples of 2^(levels+1) (m, k) and 2^(levels+2) (n) -- not the
+ * reference's square 2^j order.
  * Padding is staged in ws (size from mk_rect_workspace_bytes). */
 size_t mk_rect_workspace_bytes(int algo, int64_t m, int64_t n, int64_t k, int levels);
 int mk_multiply_rect(int algo, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,

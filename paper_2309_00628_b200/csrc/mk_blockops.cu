@@ -81,6 +81,71 @@ cudaError_t launch_combine(double* dst, int64_t ldd, const double* const* src, c
   return cudaGetLastError();
 }
 
+// Batched quadrant transform: blockIdx.y = job, grid-stride over the job's elements. Each
+// thread reads every source once (16-byte vectors when VEC) and writes every destination.
+template <bool VEC>
+__global__ void __launch_bounds__(256) xform_kernel(const MkXformJob* __restrict__ jobs, int64_t rows, int64_t cols) {
+  const MkXformJob& jb = jobs[blockIdx.y];
+  const int ns = jb.nsrc, nd = jb.ndst;
+  const int64_t cv = VEC ? (cols >> 1) : cols;
+  // rows x cv < 2^32 for every block the planner forms (checked by the launcher)
+  const uint32_t total = (uint32_t)(rows * cv), ucv = (uint32_t)cv;
+  for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    const uint32_t r = idx / ucv;
+    const int64_t c = (int64_t)(idx - r * ucv) * (VEC ? 2 : 1);
+    double2 v[MK_XFORM_MAX];
+#pragma unroll
+    for (int i = 0; i < MK_XFORM_MAX; ++i) {
+      if (i < ns) {
+        const double* p = jb.src[i] + r * jb.lds[i] + c;
+        v[i] = VEC ? __ldg(reinterpret_cast<const double2*>(p)) : make_double2(__ldg(p), 0.0);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < MK_XFORM_MAX; ++j) {
+      if (j < nd) {
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int i = 0; i < MK_XFORM_MAX; ++i) {
+          const int cf = i < ns ? jb.coef[j][i] : 0;  // job-uniform: zero terms are skipped,
+          if (cf > 0) {                               // so an inf elsewhere cannot become NaN
+            acc.x += v[i].x;
+            acc.y += v[i].y;
+          } else if (cf < 0) {
+            acc.x -= v[i].x;
+            acc.y -= v[i].y;
+          }
+        }
+        double* q = jb.dst[j] + r * jb.ldd[j] + c;
+        if (VEC)
+          *reinterpret_cast<double2*>(q) = acc;
+        else
+          *q = acc.x;
+      }
+    }
+  }
+}
+
+cudaError_t launch_xform_batch(const MkXformJob* jobs_dev, int njobs, int64_t rows, int64_t cols, bool vec,
+                               cudaStream_t stream) {
+  if (njobs <= 0 || rows <= 0 || cols <= 0) return cudaSuccess;
+  const int64_t work = rows * (vec ? cols / 2 : cols);
+  if (work >= (int64_t)1 << 32) return cudaErrorInvalidValue;
+  int64_t bx = (work + 255) / 256;
+  const int64_t cap = (148 * 8 + njobs - 1) / njobs;  // ~8 resident CTAs per SM across all jobs
+  if (bx > cap) bx = cap;
+  if (bx < 1) bx = 1;
+  for (int j0 = 0; j0 < njobs; j0 += 65535) {
+    const int nj = njobs - j0 < 65535 ? njobs - j0 : 65535;
+    dim3 grid((unsigned)bx, (unsigned)nj);
+    if (vec)
+      xform_kernel<true><<<grid, 256, 0, stream>>>(jobs_dev + j0, rows, cols);
+    else
+      xform_kernel<false><<<grid, 256, 0, stream>>>(jobs_dev + j0, rows, cols);
+  }
+  return cudaGetLastError();
+}
+
 __global__ void i64_to_f64_kernel(const int64_t* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
                                   int64_t cols) {
   const int64_t total = rows * cols;

@@ -5,6 +5,27 @@
 #include "mk_plan.h"
 
 #define MK_COMBINE_MAX 8
+#define MK_XFORM_MAX 8
+
+// One job of a batched "quadrant transform": dst_j = sum_i coef[j][i] * src_i (all blocks
+// rows x cols). Used for a node's operand sums (4 quadrant sources -> up to 8 children, one
+// pass) and for hierarchical post-additions (7-8 child products -> 4 parent quadrants).
+struct MkXformJob {
+  const double* src[MK_XFORM_MAX];
+  double* dst[MK_XFORM_MAX];
+  int64_t lds[MK_XFORM_MAX];
+  int64_t ldd[MK_XFORM_MAX];
+  int32_t nsrc, ndst;
+  int8_t coef[MK_XFORM_MAX][MK_XFORM_MAX];  // [dst][src] in {-1, 0, 1}
+};
+
+// One product of a batched leaf launch (device table, 64-byte aligned entries).
+struct alignas(64) MkBatchEntry {
+  CUtensorMap tmA, tmB, tmC;
+  MkProduct prod;
+  double* C;
+  int64_t ldc;
+};
 
 namespace mk {
 cudaError_t launch_combine(double* dst, int64_t ldd, const double* const* src, const int64_t* lds,
@@ -17,8 +38,15 @@ cudaError_t launch_absmax_f64(const double* src, int64_t lds, int64_t rows, int6
                               unsigned long long* out, cudaStream_t stream);
 cudaError_t launch_absmax_i64(const int64_t* src, int64_t lds, int64_t rows, int64_t cols,
                               unsigned long long* out, cudaStream_t stream);
+// jobs_dev: device array of njobs jobs (identical rows x cols).
+cudaError_t launch_xform_batch(const MkXformJob* jobs_dev, int njobs, int64_t rows, int64_t cols, bool vec,
+                               cudaStream_t stream);
 cudaError_t measure_dmma_peak(double* tflops_out, cudaStream_t st);
 cudaError_t launch_fused_product(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
                                  const MkGemmArgs& args, const MkProduct& prod, cudaStream_t stream);
 int consumer_layout();
+
+// Launch `nprod` single-term products of identical M x N x K (entries already in device memory).
+cudaError_t launch_product_batch(const MkBatchEntry* entries_dev, int nprod, const MkGemmArgs& args,
+                                 cudaStream_t stream);
 }  // namespace mk

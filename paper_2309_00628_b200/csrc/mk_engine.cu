@@ -295,7 +295,7 @@ struct Blk {
 };
 using Lin = std::vector<Blk>;
 
-enum { BASE_A = 0, BASE_B = 1, BASE_C = 2, BASE_WS0 = 3, MAX_BASES = 64 };
+enum { BASE_A = 0, BASE_B = 1, BASE_C = 2, BASE_WS0 = 3 };
 
 struct Engine {
   int algo = 0;
@@ -304,8 +304,9 @@ struct Engine {
   int64_t n = 0;      // order (square) -- rectangular uses m/k/n below
   int64_t leaf_m = 0, leaf_n = 0, leaf_k = 0;
   cudaStream_t st = nullptr;
-  Base bases[MAX_BASES];
+  std::vector<Base> bases;
   int nbases = 0;
+  std::map<std::pair<int, int>, CUtensorMap> tmap_cache;  // (base, box kind) -> encoded map
   // first-writer bitmaps per base at leaf-cell granularity
   std::vector<std::vector<uint8_t>> written;
   std::vector<int64_t> cell_rows, cell_cols;
@@ -326,7 +327,9 @@ struct Engine {
     b.ld = ld;
     b.rows = rows;
     b.cols = cols;
+    if ((int)bases.size() <= nbases) bases.resize(nbases + 1);
     bases[nbases] = b;
+    for (int kind = 0; kind < 4; ++kind) tmap_cache.erase({nbases, kind});
     const int64_t cr = (rows + cell_r - 1) / cell_r, cc = (cols + cell_c - 1) / cell_c;
     written.emplace_back((size_t)(cr * cc), 0);
     cell_rows.push_back(cell_r);
@@ -358,7 +361,6 @@ struct Engine {
     int64_t ld = (cols + 3) / 4 * 4;  // 32B rows for the vector epilogue / TMA
     size_t bytes = (size_t)rows * ld * 8;
     bytes = (bytes + 1023) / 1024 * 1024;
-    if (nbases >= MAX_BASES) return fail(MK_ERR_ARG, "too many workspace slots");
     double* p = nullptr;
     if (!dry) {
       if (ws_used + bytes > ws_bytes)
@@ -370,6 +372,20 @@ struct Engine {
     ws_used += bytes;
     ws_peak = std::max(ws_peak, ws_used);
     *base_out = add_base(p, ld, rows, cols, leaf_m, leaf_n);
+    return MK_OK;
+  }
+
+  // Tensor map of a base for one of the kernel's box shapes (cached: many leaves share a base).
+  // kind 0: A box {16, 128}; 1: B box {16, 16}; 2: C box {16, 64}; 3: C box {16, 32}
+  int cached_map(int base, int kind, CUtensorMap* out) {
+    auto it = tmap_cache.find({base, kind});
+    if (it != tmap_cache.end()) {
+      *out = it->second;
+      return MK_OK;
+    }
+    static const uint32_t rows[4] = {MK_BM, 16, 64, 32};
+    MK_TRY(make_map(out, bases[base], 16, rows[kind]));
+    tmap_cache[{base, kind}] = *out;
     return MK_OK;
   }
 
@@ -439,13 +455,13 @@ struct Engine {
     ++launches;
     if (dry) return MK_OK;
     CUtensorMap tmA, tmB, tmC;
-    MK_TRY(make_map(&tmA, bases[bx], 16, MK_BM));
-    MK_TRY(make_map(&tmB, bases[by], 16, 16));
+    MK_TRY(cached_map(bx, 0, &tmA));
+    MK_TRY(cached_map(by, 1, &tmB));
     const int slab = consumer_layout() == 16 ? 32 : 64;  // rows per consumer warp
     bool async_ok = async_epilogue_enabled() && (M % slab == 0) && (N % 16 == 0) &&
                     (reinterpret_cast<uintptr_t>(bases[bd].ptr) % 16 == 0) && (bases[bd].ld % 2 == 0);
     for (int i = 0; i < p.nd; ++i) async_ok = async_ok && ((D[i].row | D[i].col) % 2 == 0);
-    if (async_ok) MK_TRY(make_map(&tmC, bases[bd], 16, (uint32_t)slab));
+    if (async_ok) MK_TRY(cached_map(bd, slab == 64 ? 2 : 3, &tmC));
     else std::memset(&tmC, 0, sizeof tmC);
     MkGemmArgs g{};
     g.C = bases[bd].ptr;
@@ -632,6 +648,209 @@ struct Engine {
     (void)ws_peak;
     return MK_OK;
   }
+
+  // =====================================================================================
+  // Breadth-first plan (small leaves). All operand sums of a depth are formed by one batched
+  // quadrant-transform launch per side (each node's quadrants read once, all its multi-term
+  // children written); leaves run as batched launches of one product per parent (siblings are
+  // ordered, different parents write different output blocks, so a launch has no write races);
+  // post-additions are batched transforms from child outputs into parent quadrants, depth by
+  // depth, ending in C. Workspace: every depth's operand sums and every inner node's output.
+  // =====================================================================================
+  int upload(const void* host, size_t bytes, void** dev_out) {
+    const size_t al = (bytes + 1023) / 1024 * 1024;
+    *dev_out = nullptr;
+    if (!dry) {
+      if (ws_used + al > ws_bytes)
+        return fail(MK_ERR_WORKSPACE, "workspace too small for device plan tables");
+      *dev_out = ws + ws_used;
+      MK_CUDA_TRY(cudaMemcpyAsync(*dev_out, host, bytes, cudaMemcpyHostToDevice, st));
+    }
+    ws_used += al;
+    ws_peak = std::max(ws_peak, ws_used);
+    return MK_OK;
+  }
+
+  double* ptr_of(const Blk& b) const { return bases[b.base].ptr + b.row * bases[b.base].ld + b.col; }
+
+  int xform_batch(std::vector<MkXformJob>& jobs, int64_t rows, int64_t cols) {
+    if (jobs.empty()) return MK_OK;
+    bool vec = cols % 2 == 0;
+    for (const MkXformJob& j : jobs) {
+      for (int i = 0; i < j.nsrc; ++i)
+        vec = vec && j.lds[i] % 2 == 0 && reinterpret_cast<uintptr_t>(j.src[i]) % 16 == 0;
+      for (int i = 0; i < j.ndst; ++i)
+        vec = vec && j.ldd[i] % 2 == 0 && reinterpret_cast<uintptr_t>(j.dst[i]) % 16 == 0;
+    }
+    void* dev = nullptr;
+    MK_TRY(upload(jobs.data(), jobs.size() * sizeof(MkXformJob), &dev));
+    if (dry) return MK_OK;
+    MK_CUDA_TRY(launch_xform_batch(static_cast<const MkXformJob*>(dev), (int)jobs.size(), rows, cols, vec, st));
+    ++g_launch_count;
+    return MK_OK;
+  }
+
+  struct BNode {
+    Blk x, y;          // operands: single signed blocks (views or materialised sums)
+    int out = -1;      // output block base (inner nodes)
+  };
+
+  int bfs(int64_t M, int64_t N, int64_t K) {
+    const int np = co->nprod;
+    std::vector<std::vector<BNode>> lv(1);
+    lv[0].push_back(BNode{Blk{BASE_A, 0, 0, 1.0}, Blk{BASE_B, 0, 0, 1.0}, -1});
+    // ---- operand sums, depth by depth ----
+    for (int d = 0; d < L; ++d) {
+      const int64_t hm = (M >> d) / 2, hn = (N >> d) / 2, hk = (K >> d) / 2;
+      const std::vector<BNode>& cur = lv[d];
+      std::vector<BNode> next(cur.size() * np);
+      std::vector<MkXformJob> ja, jb;
+      for (size_t i = 0; i < cur.size(); ++i) {
+        for (int side = 0; side < 2; ++side) {
+          const Blk& src = side == 0 ? cur[i].x : cur[i].y;
+          const int64_t hr = side == 0 ? hm : hk, hc = side == 0 ? hk : hn;
+          MkXformJob job{};
+          job.nsrc = 4;
+          for (int q = 0; q < 4; ++q) {
+            job.src[q] = ptr_of(Blk{src.base, src.row + (q >> 1) * hr, src.col + (q & 1) * hc, 1.0});
+            job.lds[q] = bases[src.base].ld;
+          }
+          for (int p = 0; p < np; ++p) {
+            const int* cf = side == 0 ? co->a[p] : co->b[p];
+            int terms = 0, q1 = -1;
+            for (int q = 0; q < 4; ++q)
+              if (cf[q]) {
+                ++terms;
+                q1 = q;
+              }
+            Blk& tgt = side == 0 ? next[i * np + p].x : next[i * np + p].y;
+            if (terms == 1) {  // a view: no data movement
+              tgt = Blk{src.base, src.row + (q1 >> 1) * hr, src.col + (q1 & 1) * hc, src.sign * cf[q1]};
+              continue;
+            }
+            int sb;
+            MK_TRY(alloc_slot(hr, hc, &sb));
+            tgt = Blk{sb, 0, 0, 1.0};
+            const int j = job.ndst++;
+            job.dst[j] = bases[sb].ptr;
+            job.ldd[j] = bases[sb].ld;
+            for (int q = 0; q < 4; ++q) job.coef[j][q] = (int8_t)(cf[q] * (src.sign < 0 ? -1 : 1));
+          }
+          if (job.ndst) (side == 0 ? ja : jb).push_back(job);
+        }
+      }
+      MK_TRY(xform_batch(ja, hm, hk));
+      MK_TRY(xform_batch(jb, hk, hn));
+      lv.push_back(std::move(next));
+    }
+    // ---- leaves: one batched launch per sibling index ----
+    std::vector<BNode>& par = lv[L - 1];
+    const int64_t lm = M >> L, ln = N >> L, lk = K >> L;
+    if (L == 1) {
+      par[0].out = BASE_C;
+    } else {
+      for (BNode& pn : par) MK_TRY(alloc_slot(2 * lm, 2 * ln, &pn.out));
+    }
+    const int slab = consumer_layout() == 16 ? 32 : 64;
+    bool touched[4] = {false, false, false, false};
+    std::vector<MkBatchEntry> ents(par.size());
+    for (int p = 0; p < np; ++p) {
+      MkDest dt[4];
+      int nd = 0;
+      for (int q = 0; q < 4; ++q)
+        if (co->c[q][p]) {
+          dt[nd++] = MkDest{(q >> 1) * lm, (q & 1) * ln, (double)co->c[q][p], touched[q] ? 1 : 0, 0};
+          touched[q] = true;
+        }
+      if (L == 1) {
+        const BNode& lf = lv[1][p];
+        Lin D;
+        for (int i = 0; i < nd; ++i) D.push_back(Blk{BASE_C, dt[i].row, dt[i].col, dt[i].sign});
+        MK_TRY(product(Lin{lf.x}, Lin{lf.y}, D, lm, ln, lk));
+        continue;
+      }
+      bool async_ok = async_epilogue_enabled() && lm % slab == 0 && ln % 16 == 0;
+      bool vec_ok = ln % 4 == 0;
+      for (size_t i = 0; i < par.size(); ++i) {
+        const BNode& lf = lv[L][i * np + p];
+        if (((lf.x.row | lf.x.col | lf.y.row | lf.y.col) & 1) != 0)
+          return fail(MK_ERR_ARG, "leaf order must be >= 2 (odd TMA term offset)");
+        MkBatchEntry& e = ents[i];
+        std::memset(&e, 0, sizeof e);
+        e.prod.na = e.prod.nb = 1;
+        e.prod.nd = nd;
+        e.prod.a[0] = MkTerm{(int32_t)lf.x.row, (int32_t)lf.x.col, lf.x.sign};
+        e.prod.b[0] = MkTerm{(int32_t)lf.y.row, (int32_t)lf.y.col, lf.y.sign};
+        for (int k = 0; k < nd; ++k) e.prod.d[k] = dt[k];
+        e.C = bases[par[i].out].ptr;
+        e.ldc = bases[par[i].out].ld;
+        vec_ok = vec_ok && e.ldc % 4 == 0 && reinterpret_cast<uintptr_t>(e.C) % 32 == 0;
+        if (!dry) {
+          MK_TRY(cached_map(lf.x.base, 0, &e.tmA));
+          MK_TRY(cached_map(lf.y.base, 1, &e.tmB));
+          if (async_ok) MK_TRY(cached_map(par[i].out, slab == 64 ? 2 : 3, &e.tmC));
+        }
+      }
+      void* dev = nullptr;
+      MK_TRY(upload(ents.data(), ents.size() * sizeof(MkBatchEntry), &dev));
+      launches += (int)par.size();
+      if (dry) continue;
+      MkGemmArgs g{};
+      g.M = (int32_t)lm;
+      g.N = (int32_t)ln;
+      g.K = (int32_t)lk;
+      g.tiles_m = (int32_t)((lm + MK_BM - 1) / MK_BM);
+      g.tiles_n = (int32_t)((ln + MK_BN - 1) / MK_BN);
+      g.group_m = 16;
+      g.vec_ok = vec_ok ? 1 : 0;
+      g.async_epi = async_ok ? 1 : 0;
+      cudaEvent_t t0 = nullptr, t1 = nullptr;
+      if (g_timing.on) {
+        MK_CUDA_TRY(cudaEventCreate(&t0));
+        MK_CUDA_TRY(cudaEventCreate(&t1));
+        MK_CUDA_TRY(cudaEventRecord(t0, st));
+      }
+      MK_CUDA_TRY(launch_product_batch(static_cast<const MkBatchEntry*>(dev), (int)par.size(), g, st));
+      ++g_launch_count;
+      if (g_timing.on) {
+        MK_CUDA_TRY(cudaEventRecord(t1, st));
+        g_timing.ev.emplace_back(t0, t1);
+        g_timing.flops.push_back(2.0 * (double)lm * (double)ln * (double)lk * (double)par.size());
+      }
+      if (debug_sync()) {
+        cudaError_t e2 = cudaStreamSynchronize(st);
+        if (e2 != cudaSuccess) return fail(MK_ERR_CUDA, std::string("batched leaf launch: ") + cudaGetErrorString(e2));
+      }
+    }
+    // ---- post-additions: child outputs -> parent quadrants, deepest first ----
+    for (int d = L - 1; d >= 1; --d) {
+      std::vector<BNode>& ch = lv[d];
+      std::vector<BNode>& pa = lv[d - 1];
+      const int64_t cm = M >> d, cn = N >> d;
+      std::vector<MkXformJob> jobs;
+      for (size_t j = 0; j < pa.size(); ++j) {
+        if (d - 1 == 0)
+          pa[j].out = BASE_C;
+        else
+          MK_TRY(alloc_slot(2 * cm, 2 * cn, &pa[j].out));
+        MkXformJob job{};
+        job.nsrc = np;
+        for (int p = 0; p < np; ++p) {
+          job.src[p] = bases[ch[j * np + p].out].ptr;
+          job.lds[p] = bases[ch[j * np + p].out].ld;
+        }
+        job.ndst = 4;
+        for (int q = 0; q < 4; ++q) {
+          job.dst[q] = ptr_of(Blk{pa[j].out, (q >> 1) * cm, (q & 1) * cn, 1.0});
+          job.ldd[q] = bases[pa[j].out].ld;
+          for (int p = 0; p < np; ++p) job.coef[q][p] = (int8_t)co->c[q][p];
+        }
+        jobs.push_back(job);
+      }
+      MK_TRY(xform_batch(jobs, cm, cn));
+    }
+    return MK_OK;
+  }
 };
 
 static bool overlaps(const double* a, int64_t lda, int64_t ra, int64_t ca, const double* b, int64_t ldb, int64_t rb,
@@ -665,8 +884,21 @@ static int setup_square(Engine& e, int algo, double* A, int64_t lda, double* B, 
   return MK_OK;
 }
 
+// Plan choice for the fused algorithms at L >= 2: breadth-first (batched leaves, hierarchical
+// post-adds) by default -- measured faster at every size tried (n = 8192 L=3: 58.7 -> 26.0 ms;
+// n = 16384 L=2: 202.8 -> 197.6 ms); MK_PLAN=dfs selects the depth-first Kronecker plan.
+static bool use_bfs(const Engine& e, int64_t lm, int64_t ln) {
+  (void)lm;
+  (void)ln;
+  if (e.fuse_preadds || e.leaf_count >= 0 || e.L < 2) return false;
+  if (e.algo < MK_ALGO_STRASSEN || e.algo > MK_ALGO_WINOGRAD_KNUTH_8CALL) return false;
+  const char* env = getenv("MK_PLAN");
+  return !(env && std::string(env) == "dfs");
+}
+
 static int run_square(Engine& e) {
   const int64_t n = e.n;
+  if (use_bfs(e, e.leaf_m, e.leaf_n)) return e.bfs(n, n, n);
   if (e.algo == MK_ALGO_TWO_TEMP)
     return e.literal(kTwoTemp, true, e.L, Blk{BASE_A, 0, 0, 1.0}, Blk{BASE_B, 0, 0, 1.0}, Blk{BASE_C, 0, 0, 1.0}, n);
   if (e.algo == MK_ALGO_IN_PLACE)
@@ -842,8 +1074,10 @@ int mk_strassen_partial(int algo, const double* A, int64_t lda, const double* B,
 static int run_rect(int algo, const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                     int64_t m, int64_t n, int64_t k, int levels, void* ws, size_t ws_bytes, cudaStream_t st,
                     bool dry, size_t* need_out) {
-  const int64_t q = (int64_t)16 << levels;
-  const int64_t mp = (m + q - 1) / q * q, np_ = (n + q - 1) / q * q, kp = (k + q - 1) / q * q;
+  // every level halves each extent and the leaves need even extents (16-byte TMA origins) and
+  // a leaf N divisible by 4 (32-byte epilogue rows): pad m, k to 2^(L+1) and n to 2^(L+2)
+  const int64_t qm = (int64_t)2 << levels, qn = (int64_t)4 << levels;
+  const int64_t mp = (m + qm - 1) / qm * qm, np_ = (n + qn - 1) / qn * qn, kp = (k + qm - 1) / qm * qm;
   size_t off = 0;
   auto carve = [&](size_t elems) {
     double* p = dry ? reinterpret_cast<double*>(0x1000 + off) : reinterpret_cast<double*>(static_cast<char*>(ws) + off);
@@ -880,8 +1114,11 @@ static int run_rect(int algo, const double* A, int64_t lda, const double* B, int
   e.add_base(Cp, np_, mp, np_, e.leaf_m, e.leaf_n);
   e.ws = dry ? nullptr : static_cast<char*>(ws) + off;
   e.ws_bytes = dry ? 0 : ws_bytes - off;
-  MK_TRY(e.fused(levels, Lin{Blk{BASE_A, 0, 0, 1.0}}, Lin{Blk{BASE_B, 0, 0, 1.0}}, Lin{Blk{BASE_C, 0, 0, 1.0}}, mp,
-                 np_, kp, 0));
+  if (use_bfs(e, e.leaf_m, e.leaf_n))
+    MK_TRY(e.bfs(mp, np_, kp));
+  else
+    MK_TRY(e.fused(levels, Lin{Blk{BASE_A, 0, 0, 1.0}}, Lin{Blk{BASE_B, 0, 0, 1.0}}, Lin{Blk{BASE_C, 0, 0, 1.0}},
+                   mp, np_, kp, 0));
   if (need_out) *need_out = off + e.ws_peak;
   if (!dry) {
     const double* s[1] = {Cp};

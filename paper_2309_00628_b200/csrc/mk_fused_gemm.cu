@@ -27,6 +27,7 @@
 #include <type_traits>
 #include "mk_device.cuh"
 #include "mk_plan.h"
+#include "mk_blockops.h"
 
 namespace mk {
 
@@ -96,13 +97,24 @@ struct Regs<4, true> {  // 61440 >= 128 x 40 + 512 x 104
 // CA / CB: the A / B operand has more than one term and goes through the combiner.
 template <bool CA, bool CB, int MT>
 __global__ void __launch_bounds__(Layout<MT>::kThreads, 1)
-fused_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmC, const MkGemmArgs args,
-                     const __grid_constant__ MkProduct prod) {
+fused_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const __grid_constant__ CUtensorMap tmB_param,
+                     const __grid_constant__ CUtensorMap tmC_param, const MkGemmArgs args,
+                     const __grid_constant__ MkProduct prod_param) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kMaxStages];
   __shared__ __align__(8) uint64_t empty_bar[kMaxStages];
   __shared__ __align__(8) uint64_t raw_bar[2];
+
+  // Single product: maps and descriptor are kernel parameters. Batched launch: CTA blockIdx.x
+  // works on tile (blockIdx.x % tiles_per_prod) of product (blockIdx.x / tiles_per_prod), whose
+  // tensor maps (64-byte aligned, written before launch) and descriptor live in global memory.
+  const MkBatchEntry* ent = args.batch ? args.batch + blockIdx.x / args.tiles_per_prod : nullptr;
+  const MkProduct& prod = ent ? ent->prod : prod_param;
+  const CUtensorMap* tmA = ent ? &ent->tmA : &tmA_param;
+  const CUtensorMap* tmB = ent ? &ent->tmB : &tmB_param;
+  const CUtensorMap* tmC = ent ? &ent->tmC : &tmC_param;
+  double* const Cbase = ent ? ent->C : args.C;
+  const int64_t ldc = ent ? ent->ldc : args.ldc;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -119,7 +131,7 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
   // ---- rasterised tile coordinates (group_m tile-rows walked column-major) ----
   int tm, tn;
   {
-    const int bid = blockIdx.x;
+    const int bid = ent ? (int)(blockIdx.x % args.tiles_per_prod) : (int)blockIdx.x;
     const int per_group = args.group_m * args.tiles_n;
     const int g = bid / per_group;
     const int first_m = g * args.group_m;
@@ -157,16 +169,16 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
       const int k0 = k * MK_BK;
       if (CA)
         for (int t = 0; t < na; ++t, dst += MK_TILE_BYTES)
-          tma_load_2d(dst, &tmA, k0 + prod.a[t].col, m0 + prod.a[t].row, &raw_bar[d]);
+          tma_load_2d(dst, tmA, k0 + prod.a[t].col, m0 + prod.a[t].row, &raw_bar[d]);
       if (CB)
         for (int t = 0; t < nb; ++t, dst += MK_TILE_BYTES)
 #pragma unroll
           for (int bj = 0; bj < 8; ++bj)
-            tma_load_2d(dst + bj * 2048, &tmB, n0 + prod.b[t].col + bj * 16, k0 + prod.b[t].row, &raw_bar[d]);
+            tma_load_2d(dst + bj * 2048, tmB, n0 + prod.b[t].col + bj * 16, k0 + prod.b[t].row, &raw_bar[d]);
     };
     if (tid == 0) {
-      tma_prefetch_desc(&tmA);
-      tma_prefetch_desc(&tmB);
+      tma_prefetch_desc(tmA);
+      tma_prefetch_desc(tmB);
       if (CA || CB)
         for (int k = 0; k < D && k < KT; ++k) issue_raw(k);
     }
@@ -178,11 +190,11 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
       const int k0 = k * MK_BK;
       if (tid == 0) {
         mbar_arrive_expect_tx(&full_bar[s], direct_bytes);
-        if (!CA) tma_load_2d(opA, &tmA, k0 + prod.a[0].col, m0 + prod.a[0].row, &full_bar[s]);
+        if (!CA) tma_load_2d(opA, tmA, k0 + prod.a[0].col, m0 + prod.a[0].row, &full_bar[s]);
         if (!CB)
 #pragma unroll
           for (int bj = 0; bj < 8; ++bj)
-            tma_load_2d(opB + bj * 2048, &tmB, n0 + prod.b[0].col + bj * 16, k0 + prod.b[0].row, &full_bar[s]);
+            tma_load_2d(opB + bj * 2048, tmB, n0 + prod.b[0].col + bj * 16, k0 + prod.b[0].row, &full_bar[s]);
       }
       if (CA || CB) {
         const int d = k % D;
@@ -338,9 +350,9 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
             const int cc = (int)dst.col + col0 + 16 * j, rr = (int)dst.row + row0;
             if (col0 + 16 * j >= args.N) continue;
             if (dst.accumulate)
-              tma_reduce_add_2d(&tmC, cc, rr, stg + j * (kBoxRows * 128));
+              tma_reduce_add_2d(tmC, cc, rr, stg + j * (kBoxRows * 128));
             else
-              tma_store_2d(&tmC, cc, rr, stg + j * (kBoxRows * 128));
+              tma_store_2d(tmC, cc, rr, stg + j * (kBoxRows * 128));
           }
         }
         bulk_commit();
@@ -354,12 +366,12 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
   for (int d = 0; d < nd; ++d) {
     const MkDest dst = prod.d[d];
     const double sg = dst.sign * out_sign;
-    double* Cd = args.C + dst.row * args.ldc + dst.col;
+    double* Cd = Cbase + dst.row * ldc + dst.col;
 #pragma unroll
     for (int i = 0; i < MT; ++i) {
       const int row = m0 + warp_m * (8 * MT) + 8 * i + prow;
       if (row >= args.M) continue;
-      double* crow = Cd + (int64_t)row * args.ldc;
+      double* crow = Cd + (int64_t)row * ldc;
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int col = n0 + warp_n * 32 + 16 * j + 4 * q;
@@ -441,6 +453,33 @@ cudaError_t launch_fused_product(const CUtensorMap& tmA, const CUtensorMap& tmB,
   cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   fn<<<grid, threads, smem, stream>>>(tmA, tmB, tmC, args, prod);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_product_batch(const MkBatchEntry* entries_dev, int nprod, const MkGemmArgs& args_in,
+                                 cudaStream_t stream) {
+  if (nprod <= 0) return cudaSuccess;
+  MkGemmArgs args = args_in;
+  const int tiles = args.tiles_m * args.tiles_n;
+  if (tiles == 0) return cudaSuccess;
+  if ((int64_t)tiles * nprod > 0x7fffffff) return cudaErrorInvalidValue;
+  args.stages = (int)(MK_SMEM_BUDGET / kOpStageBytes);
+  if (args.stages > kMaxStages) args.stages = kMaxStages;
+  args.raw_sets = 0;
+  args.tiles_per_prod = tiles;
+  args.batch = entries_dev;
+  const size_t smem = (size_t)args.stages * kOpStageBytes + 1024;
+  const bool wide = consumer_layout() == 16;
+  auto fn = wide ? fused_product_kernel<false, false, 4> : fused_product_kernel<false, false, 8>;
+  const int threads = wide ? Layout<4>::kThreads : Layout<8>::kThreads;
+  cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
+  // parameter copies are unused in batched mode; pass the first entry's maps by value is not
+  // possible from the host (device memory), so hand over zeroed placeholders
+  CUtensorMap z{};
+  MkProduct zp{};
+  zp.na = zp.nb = 1;
+  fn<<<(unsigned)(tiles * nprod), threads, smem, stream>>>(z, z, z, args, zp);
   return cudaGetLastError();
 }
 

@@ -38,6 +38,9 @@ struct MkProduct {
   MkDest d[MK_MAX_DESTS];
 };
 
+
+struct MkBatchEntry;
+
 struct MkGemmArgs {
   double* C;
   int64_t ldc;
@@ -48,4 +51,6 @@ struct MkGemmArgs {
   int32_t group_m;       // rasterisation group height (tiles)
   int32_t vec_ok;        // 32B-vector epilogue allowed
   int32_t async_epi;     // TMA store / reduce-add epilogue (tile-aligned leaf, tmC valid)
+  int32_t tiles_per_prod;             // batched launch: CTAs per product
+  const MkBatchEntry* batch;          // batched launch: per-product maps/descriptors (nullptr: single)
 };

@@ -15,6 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 lib = ctypes.CDLL(os.path.join(HERE, "..", "paper_2309_00628_b200", "libmk_strassen.so"))
 lib.mk_last_error.restype = ctypes.c_char_p
 lib.mk_workspace_bytes.restype = ctypes.c_size_t
+lib.mk_rect_workspace_bytes.restype = ctypes.c_size_t
 I64, VP = ctypes.c_int64, ctypes.c_void_p
 
 
@@ -106,6 +107,25 @@ def main():
         torch.cuda.synchronize()
         out(check="float", algo=algo, n=n, maxerr=float((c - ref).abs().max()))
     # ---- timing ----
+    # rectangular cfg5 and small-leaf plans
+    m_, k_, n_ = 12000, 14000, 10000
+    a = torch.rand(m_, k_, device=dev, dtype=torch.float64) * 2 - 1
+    b = torch.rand(k_, n_, device=dev, dtype=torch.float64) * 2 - 1
+    c = torch.empty(m_, n_, device=dev, dtype=torch.float64)
+    ref = a @ b
+    for L in (1, 2, 3, 5):
+        ws_b = lib.mk_rect_workspace_bytes(2, I64(m_), I64(n_), I64(k_), L)
+        ws = torch.empty(max(ws_b, 8), dtype=torch.uint8, device=dev)
+        def run():
+            rc = lib.mk_multiply_rect(2, VP(a.data_ptr()), I64(k_), VP(b.data_ptr()), I64(n_), VP(c.data_ptr()),
+                                      I64(n_), I64(m_), I64(n_), I64(k_), L, VP(ws.data_ptr()), ctypes.c_size_t(ws_b),
+                                      stream())
+            if rc:
+                raise RuntimeError(lib.mk_last_error().decode())
+        ms = timeit(run, reps=2)
+        out(time="rect_cfg5", levels=L, ms=round(ms, 3), eff_tflops=round(2 * m_ * n_ * k_ / ms / 1e9, 3),
+            maxerr=float((c - ref).abs().max()), ws_gib=round(ws_b / 2**30, 2))
+    del a, b, c, ref
     for n in (8192, 16384):
         a = torch.randn(n, n, device=dev, dtype=torch.float64)
         b = torch.randn(n, n, device=dev, dtype=torch.float64)
