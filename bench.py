@@ -45,11 +45,13 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--n", type=int, default=16384)
+    p.add_argument("--order", dest="n", type=int, default=16384)
     p.add_argument("--cutoff", type=int, default=4096)
     p.add_argument("--algo", default="winograd-block")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only for 1-GPU plumbing checks")
+    p.add_argument("--alt", default="8192,2048", help="extra cutoffs to report (comma list, '' for none)")
     return p.parse_args()
 
 
@@ -216,10 +218,13 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.dist_backend)
     lib = require_engine()
     n = args.n
     levels = levels_for(n, args.cutoff)
@@ -359,6 +364,26 @@ def main():
         "peak_mem_delta_bytes": int(peak_mem),
         "roofline": roofline, "clocks": clocks, "gpu_launches": int(launches), "e2e": e2e,
     }
+    if world == 1 and args.alt:
+        alts = []
+        for cut in [int(x) for x in args.alt.split(",") if x]:
+            pol = pk.BasePolicy.naive_cutoff(cut)
+            lv = levels_for(n, cut)
+            for _ in range(2):
+                pk.winograd_block_mul(A, B, C, pol)
+            torch.cuda.synchronize()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            for _ in range(3):
+                pk.winograd_block_mul(A, B, C, pol)
+            g1.record(stream)
+            torch.cuda.synchronize()
+            ams = g0.elapsed_time(g1) / 3
+            alts.append({"cutoff": cut, "levels": lv, "ms_per_step": round(ams, 3),
+                         "value": round(2.0 * n ** 3 / (ams * 1e-3) / 1e12, 4),
+                         "actual_tflops": round(actual_flops(n, lv, args.algo) / (ams * 1e-3) / 1e12, 4),
+                         "workspace_bytes": int(lib.mk_workspace_bytes(_lib.ALGO_IDS[args.algo], n, lv))})
+        line["alt_cutoffs"] = alts
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, levels)
     print(json.dumps(line), flush=True)

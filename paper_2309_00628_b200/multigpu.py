@@ -65,7 +65,12 @@ def assemble(partial, dst_rank: int = 0, group=None):
     import torch.distributed as dist
 
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.reduce(partial, dst=dst_rank, op=dist.ReduceOp.SUM, group=group)
+        if partial.is_cuda and dist.get_backend(group) == "gloo":  # plumbing checks on one GPU
+            host = partial.cpu()
+            dist.reduce(host, dst=dst_rank, op=dist.ReduceOp.SUM, group=group)
+            partial.copy_(host)
+        else:
+            dist.reduce(partial, dst=dst_rank, op=dist.ReduceOp.SUM, group=group)
     return partial
 
 

@@ -333,3 +333,27 @@ def test_fused_preadd_kernel_variant_matches(rng):
                 assert np.array_equal(c.arr, want), (name, cut)
     finally:
         lib.mk_set_option(_lib.MK_OPT_FUSE_PREADDS, 0)
+
+
+@pytest.mark.parametrize("levels", [1, 2])
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_sharded_partials_sum_to_product(levels, world):
+    """Each rank's share of the leaves (mk_strassen_partial), emulated one after another on this
+    GPU, sums to the exact product -- the data path of multigpu.sharded_multiply minus NCCL."""
+    import torch
+
+    from paper_2309_00628_b200 import multigpu
+
+    r = np.random.default_rng(21)
+    n = 1024
+    a = torch.from_numpy(r.integers(-8, 9, (n, n)).astype(np.float64)).cuda()
+    b = torch.from_numpy(r.integers(-8, 9, (n, n)).astype(np.float64)).cuda()
+    total = multigpu.leaf_count("winograd-block", levels)
+    acc = torch.zeros_like(a)
+    for rank in range(world):
+        first, count = multigpu.shard_range(total, world, rank)
+        part = torch.zeros_like(a)
+        if count:
+            multigpu.partial_product("winograd-block", a, b, part, levels, first, count)
+        acc += part
+    assert torch.equal(acc, a @ b)
