@@ -104,6 +104,7 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const __grid
   __shared__ __align__(8) uint64_t full_bar[kMaxStages];
   __shared__ __align__(8) uint64_t empty_bar[kMaxStages];
   __shared__ __align__(8) uint64_t raw_bar[2];
+  __shared__ uint32_t tmem_base_sh;
 
   // Single product: maps and descriptor are kernel parameters. Batched launch: CTA blockIdx.x
   // works on tile (blockIdx.x % tiles_per_prod) of product (blockIdx.x / tiles_per_prod), whose
@@ -280,6 +281,53 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const __grid
     }
   };
 
+  // Two-level accumulation: every `chunk` stages the register partial sums are added into a
+  // master copy kept in tensor memory (this warp's 32 TMEM lanes x 16*MT columns) and reset,
+  // so each output is a short register sum of <= 16*chunk products plus a sum of K/(16*chunk)
+  // chunk totals -- the error growth of OpenBLAS-style K blocking, with the DMMA pipe idle for
+  // only ~0.2% of the time. Disabled (chunk = 0) when K fits in one chunk.
+  const int chunk = (args.chunk_stages > 0 && KT > args.chunk_stages) ? args.chunk_stages : 0;
+  constexpr int kWords = 16 * MT;  // 32-bit words of accumulator per thread
+  uint32_t taddr = 0;
+  if (chunk) {
+    if (cw == 0) tmem_alloc(&tmem_base_sh, 256);
+    tmem_fence_before();
+    named_bar_sync(3, 32 * Layout<MT>::kConsumerWarps);
+    tmem_fence_after();
+    taddr = tmem_base_sh + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((cw >> 2) * kWords);
+  }
+  // Fold: master (+)= registers, registers = 0, two 8-double pieces (2 x 16 TMEM columns) per
+  // tcgen05.ld round trip. All warps fold at the same k-step (measured cheaper than staggering or
+  // rotating single pieces: every tcgen05.wait is costly).
+  constexpr int kPieces = kWords / 16;
+  bool master_live = false;
+  auto fold_to_tmem = [&]() {
+#pragma unroll
+    for (int pc = 0; pc < kPieces; pc += 2) {
+      uint32_t w[2][16];
+      if (master_live) {
+        tmem_ld16(taddr + pc * 16, w[0]);
+        tmem_ld16(taddr + pc * 16 + 16, w[1]);
+        tmem_wait_ld();
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = (pc + h) * 8 + u;  // flat index into acc[MT][4][2]
+          double& a = acc[e >> 3][(e >> 1) & 3][e & 1];
+          const double m = master_live ? __hiloint2double((int)w[h][2 * u + 1], (int)w[h][2 * u]) + a : a;
+          w[h][2 * u] = (uint32_t)__double2loint(m);
+          w[h][2 * u + 1] = (uint32_t)__double2hiint(m);
+          a = 0.0;
+        }
+      tmem_st16(taddr + pc * 16, w[0]);
+      tmem_st16(taddr + pc * 16 + 16, w[1]);
+    }
+    tmem_wait_st();
+    master_live = true;
+  };
+
   const int krem_last = args.K - (KT - 1) * MK_BK;  // 1..16
   for (int kt = 0; kt < KT; ++kt) {
     const int s = kt % S;
@@ -292,6 +340,27 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const __grid
       stage(sA, sB, MK_BK, std::false_type{});
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[s]);
+    if (chunk && (kt + 1) % chunk == 0 && kt + 1 < KT) fold_to_tmem();
+  }
+  if (chunk) {
+    if (master_live) {  // acc += master
+#pragma unroll
+      for (int pc = 0; pc < kPieces; ++pc) {
+        uint32_t w[16];
+        tmem_ld16(taddr + pc * 16, w);
+        tmem_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = pc * 8 + u;
+          double& a = acc[e >> 3][(e >> 1) & 3][e & 1];
+          a = __hiloint2double((int)w[2 * u + 1], (int)w[2 * u]) + a;
+        }
+      }
+    }
+    tmem_fence_before();
+    named_bar_sync(3, 32 * Layout<MT>::kConsumerWarps);
+    tmem_fence_after();
+    if (cw == 0) tmem_dealloc(tmem_base_sh, 256);
   }
 
   // ============================ multi-destination epilogue ============================
@@ -416,6 +485,18 @@ int consumer_layout() {
 }
 void set_consumer_layout(int warps) { g_consumer_layout = (warps == 8) ? 8 : 16; }
 
+// Stages per register chunk of the two-level (register + TMEM) accumulation; 0 disables it.
+// Default 32 stages = 512 k. Env MK_ACC_CHUNK overrides (0 = single-level accumulation).
+static int g_chunk = -1;
+int accumulate_chunk_stages() {
+  if (g_chunk < 0) {
+    const char* e = getenv("MK_ACC_CHUNK");
+    g_chunk = e ? atoi(e) : 32;
+    if (g_chunk < 0) g_chunk = 0;
+  }
+  return g_chunk;
+}
+
 cudaError_t launch_fused_product(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
                                  const MkGemmArgs& args_in, const MkProduct& prod, cudaStream_t stream) {
   if (prod.na < 1 || prod.na > MK_MAX_TERMS || prod.nb < 1 || prod.nb > MK_MAX_TERMS) return cudaErrorInvalidValue;
@@ -436,6 +517,7 @@ cudaError_t launch_fused_product(const CUtensorMap& tmA, const CUtensorMap& tmB,
   if (stages > kMaxStages) stages = kMaxStages;
   args.stages = stages;
   args.raw_sets = sets;
+  args.chunk_stages = accumulate_chunk_stages();
   const size_t smem = (size_t)stages * kOpStageBytes + (size_t)sets * raw_set + 1024;
   const int grid = args.tiles_m * args.tiles_n;
   if (grid == 0) return cudaSuccess;
@@ -466,6 +548,7 @@ cudaError_t launch_product_batch(const MkBatchEntry* entries_dev, int nprod, con
   args.stages = (int)(MK_SMEM_BUDGET / kOpStageBytes);
   if (args.stages > kMaxStages) args.stages = kMaxStages;
   args.raw_sets = 0;
+  args.chunk_stages = accumulate_chunk_stages();
   args.tiles_per_prod = tiles;
   args.batch = entries_dev;
   const size_t smem = (size_t)args.stages * kOpStageBytes + 1024;

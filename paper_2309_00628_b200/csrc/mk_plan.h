@@ -51,6 +51,7 @@ struct MkGemmArgs {
   int32_t group_m;       // rasterisation group height (tiles)
   int32_t vec_ok;        // 32B-vector epilogue allowed
   int32_t async_epi;     // TMA store / reduce-add epilogue (tile-aligned leaf, tmC valid)
+  int32_t chunk_stages;               // >0: two-level accumulation, flush registers to TMEM every N stages
   int32_t tiles_per_prod;             // batched launch: CTAs per product
   const MkBatchEntry* batch;          // batched launch: per-product maps/descriptors (nullptr: single)
 };
