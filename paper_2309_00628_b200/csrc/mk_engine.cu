@@ -1084,10 +1084,18 @@ static int run_rect(int algo, const double* A, int64_t lda, const double* B, int
     off += (elems * 8 + 1023) / 1024 * 1024;
     return p;
   };
-  double* Ap = carve((size_t)mp * kp);
-  double* Bp = carve((size_t)kp * np_);
-  double* Cp = carve((size_t)mp * np_);
-  if (!dry) {
+  // Extents that already satisfy the recursion are used in place (no staging copies); this
+  // needs TMA-compatible operands (16-byte aligned, even leading dimensions). Sizing assumes
+  // the in-place case whenever the extents conform.
+  auto tma_ok = [](const void* p, int64_t ld) { return reinterpret_cast<uintptr_t>(p) % 16 == 0 && ld % 2 == 0; };
+  const bool conform = mp == m && np_ == n && kp == k;
+  const bool direct = conform && (dry || (tma_ok(A, lda) && tma_ok(B, ldb) && tma_ok(C, ldc)));
+  if (conform && !direct) return fail(MK_ERR_ARG, "operands need 16-byte alignment and even leading dimensions");
+  double* Ap = direct ? const_cast<double*>(A) : carve((size_t)mp * kp);
+  double* Bp = direct ? const_cast<double*>(B) : carve((size_t)kp * np_);
+  double* Cp = direct ? C : carve((size_t)mp * np_);
+  const int64_t ldap = direct ? lda : kp, ldbp = direct ? ldb : np_, ldcp = direct ? ldc : np_;
+  if (!dry && !direct) {
     if (off > ws_bytes) return fail(MK_ERR_WORKSPACE, "workspace too small for padded operands");
     MK_CUDA_TRY(cudaMemsetAsync(Ap, 0, (size_t)mp * kp * 8, st));
     MK_CUDA_TRY(cudaMemsetAsync(Bp, 0, (size_t)kp * np_ * 8, st));
@@ -1109,9 +1117,9 @@ static int run_rect(int algo, const double* A, int64_t lda, const double* B, int
   e.leaf_m = mp >> levels;
   e.leaf_n = np_ >> levels;
   e.leaf_k = kp >> levels;
-  e.add_base(Ap, kp, mp, kp, e.leaf_m, e.leaf_k);
-  e.add_base(Bp, np_, kp, np_, e.leaf_k, e.leaf_n);
-  e.add_base(Cp, np_, mp, np_, e.leaf_m, e.leaf_n);
+  e.add_base(Ap, ldap, mp, kp, e.leaf_m, e.leaf_k);
+  e.add_base(Bp, ldbp, kp, np_, e.leaf_k, e.leaf_n);
+  e.add_base(Cp, ldcp, mp, np_, e.leaf_m, e.leaf_n);
   e.ws = dry ? nullptr : static_cast<char*>(ws) + off;
   e.ws_bytes = dry ? 0 : ws_bytes - off;
   if (use_bfs(e, e.leaf_m, e.leaf_n))
@@ -1120,7 +1128,7 @@ static int run_rect(int algo, const double* A, int64_t lda, const double* B, int
     MK_TRY(e.fused(levels, Lin{Blk{BASE_A, 0, 0, 1.0}}, Lin{Blk{BASE_B, 0, 0, 1.0}}, Lin{Blk{BASE_C, 0, 0, 1.0}},
                    mp, np_, kp, 0));
   if (need_out) *need_out = off + e.ws_peak;
-  if (!dry) {
+  if (!dry && !direct) {
     const double* s[1] = {Cp};
     int64_t l[1] = {np_};
     double sg[1] = {1.0};
