@@ -357,3 +357,60 @@ def test_sharded_partials_sum_to_product(levels, world):
             multigpu.partial_product("winograd-block", a, b, part, levels, first, count)
         acc += part
     assert torch.equal(acc, a @ b)
+
+
+def test_device_resident_multiply_rect_and_presets(rng):
+    import torch
+
+    for (m, k, n) in ((300, 517, 129), (64, 64, 64), (1000, 1000, 1000)):
+        a = rng.integers(-8, 9, (m, k)).astype(np.float64)
+        b = rng.integers(-8, 9, (k, n)).astype(np.float64)
+        A, B = pk.Matrix(torch.from_numpy(a).cuda()), pk.Matrix(torch.from_numpy(b).cuda())
+        for preset in ("winograd-mod2", "strassen-mod2", "two-temp-mod", "in-place-mod", "naive"):
+            ctr = pk.OpCounter()
+            c = pk.multiply(A, B, pk.get_variant(preset, cutoff=64), ctr)
+            assert c.on_device and c.arr.shape == (m, n)
+            assert np.array_equal(c.numpy(), a @ b), (preset, m, k, n)
+        # caller operands untouched (in-place runs on staged copies)
+        assert np.array_equal(A.numpy(), a) and np.array_equal(B.numpy(), b)
+
+
+def test_in_place_on_device_storage_clobbers_and_int64_device(rng):
+    import torch
+
+    n = 256
+    a = rng.integers(-8, 9, (n, n))
+    b = rng.integers(-8, 9, (n, n))
+    want = a @ b
+    A = pk.Matrix(torch.from_numpy(a.astype(np.float64)).cuda())
+    B = pk.Matrix(torch.from_numpy(b.astype(np.float64)).cuda())
+    C = pk.Matrix.zeros(n, n, device="cuda")
+    ctr = pk.in_place_winograd(A, B, C, pk.BasePolicy.naive_cutoff(32))
+    assert np.array_equal(C.numpy(), want.astype(np.float64))
+    assert not np.array_equal(A.numpy(), a)  # the schedule stored intermediates in A
+    assert ctr.temp_buffers == 0 and pk.last_stats().workspace_bytes == 0
+    # int64 device tensors: converted on the device, exactness-guarded, result int64
+    Ai = pk.Matrix(torch.from_numpy(a).cuda())
+    Bi = pk.Matrix(torch.from_numpy(b).cuda())
+    Ci = pk.Matrix(torch.zeros((n, n), dtype=torch.int64, device="cuda"))
+    pk.strassen_mul(Ai, Bi, Ci, pk.BasePolicy.naive_cutoff(64))
+    assert Ci.arr.dtype == torch.int64 and np.array_equal(Ci.numpy(), want)
+
+
+def test_pipelined_host_path_matches_device_path():
+    """Pinned host operands take the overlapped row-panel path; same result within tolerance."""
+    import torch
+
+    n = 4096
+    r = np.random.default_rng(5)
+    ha = torch.from_numpy(r.uniform(-1, 1, (n, n))).pin_memory()
+    hb = torch.from_numpy(r.uniform(-1, 1, (n, n))).pin_memory()
+    hc = torch.zeros((n, n), dtype=torch.float64).pin_memory()
+    pol = pk.BasePolicy.naive_cutoff(1024)
+    pk.winograd_block_mul(pk.Matrix(ha.numpy()), pk.Matrix(hb.numpy()), pk.Matrix(hc.numpy()), pol)
+    st = pk.last_stats()
+    assert st.h2d_bytes == 2 * n * n * 8 and st.d2h_bytes == n * n * 8
+    dc = pk.Matrix.zeros(n, n, device="cuda")
+    pk.winograd_block_mul(pk.Matrix(ha.cuda()), pk.Matrix(hb.cuda()), dc, pol)
+    err = float((hc - dc.arr.cpu()).abs().max())
+    assert err <= tol(n, ha.numpy(), hb.numpy()) and err < 1e-11, err

@@ -134,8 +134,14 @@ def main():
         out(time="mk_dgemm", n=n, ms=round(ms, 3), tflops=round(2 * n**3 / ms / 1e9, 3))
         ms = timeit(lambda: torch.matmul(a, b, out=c), reps=2 if n == 16384 else 3)
         out(time="cublas", n=n, ms=round(ms, 3), tflops=round(2 * n**3 / ms / 1e9, 3))
-        for algo in (2, 1):
+        for algo in (2, 1, 5, 6):
             for levels in ((1, 2, 3) if n == 8192 else (1, 2)):
+                if algo == 6:  # in-place clobbers: give it copies
+                    a2, b2 = a.clone(), b.clone()
+                    ms = timeit(lambda: strassen(algo, a2, b2, c, levels), reps=2)
+                    L = levels
+                    out(time=names[algo], n=n, levels=L, ms=round(ms, 3), eff_tflops=round(2 * n**3 / ms / 1e9, 3))
+                    continue
                 ms = timeit(lambda: strassen(algo, a, b, c, levels), reps=2)
                 L = levels
                 n0 = n >> L
