@@ -753,47 +753,81 @@ struct Engine {
     }
     const int slab = consumer_layout() == 16 ? 32 : 64;
     bool touched[4] = {false, false, false, false};
-    std::vector<MkBatchEntry> ents(par.size());
+    // Siblings conflict only through a shared output quadrant: colour them greedily (in table
+    // order) so that each launch holds products with disjoint quadrants -- e.g. Winograd
+    // {P1} {P2,P6} {P3,P7} {P4,P5}: 4 launches instead of 7, still race-free and deterministic
+    // (per quadrant, contributions land in launch order; the first one stores).
+    std::vector<std::vector<int>> groups;
     for (int p = 0; p < np; ++p) {
-      MkDest dt[4];
-      int nd = 0;
-      for (int q = 0; q < 4; ++q)
-        if (co->c[q][p]) {
-          dt[nd++] = MkDest{(q >> 1) * lm, (q & 1) * ln, (double)co->c[q][p], touched[q] ? 1 : 0, 0};
-          touched[q] = true;
+      bool placed = false;
+      for (auto& gr : groups) {
+        bool clash = false;
+        for (int o : gr)
+          for (int q = 0; q < 4; ++q) clash |= co->c[q][p] != 0 && co->c[q][o] != 0;
+        if (!clash) {
+          gr.push_back(p);
+          placed = true;
+          break;
         }
+      }
+      if (!placed) groups.push_back({p});
+    }
+    if (L == 1) {  // one parent (the root): plain sequential launches
+      groups.clear();
+      for (int p = 0; p < np; ++p) groups.push_back({p});
+    }
+    std::vector<MkBatchEntry> ents;
+    for (const auto& gr : groups) {
+      struct Dests {
+        MkDest dt[4];
+        int nd = 0;
+      };
+      std::vector<Dests> dd(gr.size());
+      for (size_t gi = 0; gi < gr.size(); ++gi)
+        for (int q = 0; q < 4; ++q)
+          if (co->c[q][gr[gi]])
+            dd[gi].dt[dd[gi].nd++] = MkDest{(q >> 1) * lm, (q & 1) * ln, (double)co->c[q][gr[gi]], touched[q] ? 1 : 0, 0};
+      for (size_t gi = 0; gi < gr.size(); ++gi)
+        for (int q = 0; q < 4; ++q)
+          if (co->c[q][gr[gi]]) touched[q] = true;
       if (L == 1) {
+        const int p = gr[0];
         const BNode& lf = lv[1][p];
         Lin D;
-        for (int i = 0; i < nd; ++i) D.push_back(Blk{BASE_C, dt[i].row, dt[i].col, dt[i].sign});
+        for (int i = 0; i < dd[0].nd; ++i) D.push_back(Blk{BASE_C, dd[0].dt[i].row, dd[0].dt[i].col, dd[0].dt[i].sign});
         MK_TRY(product(Lin{lf.x}, Lin{lf.y}, D, lm, ln, lk));
         continue;
       }
       bool async_ok = async_epilogue_enabled() && lm % slab == 0 && ln % 16 == 0;
       bool vec_ok = ln % 4 == 0;
-      for (size_t i = 0; i < par.size(); ++i) {
-        const BNode& lf = lv[L][i * np + p];
-        if (((lf.x.row | lf.x.col | lf.y.row | lf.y.col) & 1) != 0)
-          return fail(MK_ERR_ARG, "leaf order must be >= 2 (odd TMA term offset)");
-        MkBatchEntry& e = ents[i];
-        std::memset(&e, 0, sizeof e);
-        e.prod.na = e.prod.nb = 1;
-        e.prod.nd = nd;
-        e.prod.a[0] = MkTerm{(int32_t)lf.x.row, (int32_t)lf.x.col, lf.x.sign};
-        e.prod.b[0] = MkTerm{(int32_t)lf.y.row, (int32_t)lf.y.col, lf.y.sign};
-        for (int k = 0; k < nd; ++k) e.prod.d[k] = dt[k];
-        e.C = bases[par[i].out].ptr;
-        e.ldc = bases[par[i].out].ld;
-        vec_ok = vec_ok && e.ldc % 4 == 0 && reinterpret_cast<uintptr_t>(e.C) % 32 == 0;
-        if (!dry) {
-          MK_TRY(cached_map(lf.x.base, 0, &e.tmA));
-          MK_TRY(cached_map(lf.y.base, 1, &e.tmB));
-          if (async_ok) MK_TRY(cached_map(par[i].out, slab == 64 ? 2 : 3, &e.tmC));
+      ents.assign(par.size() * gr.size(), MkBatchEntry{});
+      for (size_t gi = 0; gi < gr.size(); ++gi) {
+        const int p = gr[gi];
+        for (size_t i = 0; i < par.size(); ++i) {
+          const BNode& lf = lv[L][i * np + p];
+          if (((lf.x.row | lf.x.col | lf.y.row | lf.y.col) & 1) != 0)
+            return fail(MK_ERR_ARG, "leaf order must be >= 2 (odd TMA term offset)");
+          MkBatchEntry& e = ents[gi * par.size() + i];
+          std::memset(&e, 0, sizeof e);
+          e.prod.na = e.prod.nb = 1;
+          e.prod.nd = dd[gi].nd;
+          e.prod.a[0] = MkTerm{(int32_t)lf.x.row, (int32_t)lf.x.col, lf.x.sign};
+          e.prod.b[0] = MkTerm{(int32_t)lf.y.row, (int32_t)lf.y.col, lf.y.sign};
+          for (int k = 0; k < dd[gi].nd; ++k) e.prod.d[k] = dd[gi].dt[k];
+          e.C = bases[par[i].out].ptr;
+          e.ldc = bases[par[i].out].ld;
+          vec_ok = vec_ok && e.ldc % 4 == 0 && reinterpret_cast<uintptr_t>(e.C) % 32 == 0;
+          if (!dry) {
+            MK_TRY(cached_map(lf.x.base, 0, &e.tmA));
+            MK_TRY(cached_map(lf.y.base, 1, &e.tmB));
+            if (async_ok) MK_TRY(cached_map(par[i].out, slab == 64 ? 2 : 3, &e.tmC));
+          }
         }
       }
+      const int nprod_launch = (int)ents.size();
       void* dev = nullptr;
       MK_TRY(upload(ents.data(), ents.size() * sizeof(MkBatchEntry), &dev));
-      launches += (int)par.size();
+      launches += nprod_launch;
       if (dry) continue;
       MkGemmArgs g{};
       g.M = (int32_t)lm;
@@ -810,12 +844,12 @@ struct Engine {
         MK_CUDA_TRY(cudaEventCreate(&t1));
         MK_CUDA_TRY(cudaEventRecord(t0, st));
       }
-      MK_CUDA_TRY(launch_product_batch(static_cast<const MkBatchEntry*>(dev), (int)par.size(), g, st));
+      MK_CUDA_TRY(launch_product_batch(static_cast<const MkBatchEntry*>(dev), nprod_launch, g, st));
       ++g_launch_count;
       if (g_timing.on) {
         MK_CUDA_TRY(cudaEventRecord(t1, st));
         g_timing.ev.emplace_back(t0, t1);
-        g_timing.flops.push_back(2.0 * (double)lm * (double)ln * (double)lk * (double)par.size());
+        g_timing.flops.push_back(2.0 * (double)lm * (double)ln * (double)lk * (double)nprod_launch);
       }
       if (debug_sync()) {
         cudaError_t e2 = cudaStreamSynchronize(st);
