@@ -414,3 +414,34 @@ def test_pipelined_host_path_matches_device_path():
     pk.winograd_block_mul(pk.Matrix(ha.cuda()), pk.Matrix(hb.cuda()), dc, pol)
     err = float((hc - dc.arr.cpu()).abs().max())
     assert err <= tol(n, ha.numpy(), hb.numpy()) and err < 1e-11, err
+
+
+@pytest.mark.parametrize("algo", ["strassen", "winograd-block", "winograd-knuth", "winograd-knuth-8call",
+                                  "two-temp", "in-place"])
+def test_guard_bands_no_out_of_bounds_writes(algo):
+    """Operands and result are interior views of NaN-sentinel buffers (odd offsets, wide leading
+    dimensions): results exact, sentinels intact, inputs intact (except in-place's own views)."""
+    import torch
+
+    r = np.random.default_rng(33)
+    n, pad = 256, 40
+    def guarded(vals):
+        big = torch.full((n + 2 * pad, n + 3 * pad), float("nan"), dtype=torch.float64, device="cuda")
+        big[pad:pad + n, 2 * pad:2 * pad + n] = torch.from_numpy(vals).cuda()
+        return big
+    a = r.integers(-8, 9, (n, n)).astype(np.float64)
+    b = r.integers(-8, 9, (n, n)).astype(np.float64)
+    want = a @ b
+    for cut in (128, 64, 32):
+        GA, GB = guarded(a), guarded(b)
+        GC = torch.full_like(GA, float("nan"))
+        view = lambda G: pk.MatrixView(pk.Matrix(G), pad, 2 * pad, n, n)  # noqa: E731
+        CALL[algo](view(GA), view(GB), view(GC), pk.BasePolicy.naive_cutoff(cut))
+        inner = (slice(pad, pad + n), slice(2 * pad, 2 * pad + n))
+        assert np.array_equal(GC[inner].cpu().numpy(), want), (algo, cut)
+        for G in (GA, GB, GC):
+            mask = torch.ones_like(G, dtype=torch.bool)
+            mask[inner] = False
+            assert bool(torch.isnan(G[mask]).all()), (algo, cut, "write outside the view")
+        if algo != "in-place":
+            assert np.array_equal(GA[inner].cpu().numpy(), a) and np.array_equal(GB[inner].cpu().numpy(), b)
