@@ -17,8 +17,8 @@ roofline  = the dominant kernel (fused DMMA leaf product): algorithmic flops per
             measured in the same run by a DMMA-only microbenchmark (mk_fp64_peak).
 cpu_baseline = the oracle (numpy restatement of the reference, bit-identical to it) on the
             host cores, bounded sample: n = 8192 with the same 2-level recursion.
-N > 1     = strong scaling of one product: the 49 leaves sharded over ranks, partial C
-            sum-reduced to rank 0 over NVLink (NCCL).
+N > 1     = strong scaling of one product: the 49 leaves, split into 8 row panels each, sharded
+            evenly over ranks; partial C sum-reduced to rank 0 over NVLink (NCCL).
 """
 from __future__ import annotations
 
@@ -35,7 +35,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "effective FP64 TFLOP/s (2n^3/t) of Strassen-Winograd, n=16384"
+METRIC = "effective FP64 TFLOP/s (2n^3/t) of Strassen-Winograd, n={n}"
 UNIT = "TFLOP/s"
 
 
@@ -190,7 +190,7 @@ def run_reference(args):
     ms = 1e3 * sum(ts) / len(ts)
     value = 2.0 * n_s ** 3 / (ms * 1e-3) / 1e12
     line = {
-        "metric": METRIC, "value": round(value, 4), "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+        "metric": METRIC.format(n=args.n), "value": round(value, 4), "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 2), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded standard normal)",
         "config": config(args, levels),
@@ -246,7 +246,7 @@ def main():
     A, B, C = pk.Matrix(da), pk.Matrix(db), pk.Matrix(dc)
     ws = None
     if world > 1:
-        need = int(lib.mk_workspace_bytes(_lib.ALGO_IDS[args.algo], n, levels))
+        need = int(lib.mk_partial_workspace_bytes(_lib.ALGO_IDS[args.algo], n, levels))
         ws = torch.empty(max(need, 16), dtype=torch.uint8, device=dev)
 
     def step():
@@ -354,7 +354,7 @@ def main():
     }
     f_act = actual_flops(n, levels, args.algo)
     line = {
-        "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": METRIC.format(n=n), "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded standard normal)",
         "config": config(args, levels),

@@ -123,13 +123,16 @@ int mk_f64_to_i64(const double* src, int64_t lds, int64_t* dst, int64_t ldd, int
 int mk_absmax_f64(const double* src, int64_t lds, int64_t rows, int64_t cols, double* out, void* stream);
 int mk_absmax_i64(const int64_t* src, int64_t lds, int64_t rows, int64_t cols, double* out, void* stream);
 
-/* Multi-GPU sharding: number of leaf products of (algo, levels) and the subset
- * [first, first+count) one rank computes into a partial C (accumulating, C must be
- * zero-initialised by the caller); the caller sum-reduces the partials (NCCL). */
+/* Multi-GPU sharding. mk_product_count: leaf products of (algo, levels). A partial product
+ * computes shard units [first, first+count), where unit u is row panel (u mod panels) of leaf
+ * (u div panels) -- leaves split into `panels` equal row panels so ranks get equal work -- and
+ * accumulates them into C (zero-initialised by the caller); the caller sum-reduces the partials
+ * (NCCL). Workspace from mk_partial_workspace_bytes. */
 int mk_product_count(int algo, int levels);
+size_t mk_partial_workspace_bytes(int algo, int64_t n, int levels);
 int mk_strassen_partial(int algo, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
-                        int64_t ldc, int64_t n, int levels, int first, int count, void* ws, size_t ws_bytes,
-                        void* stream);
+                        int64_t ldc, int64_t n, int levels, int first, int count, int panels, void* ws,
+                        size_t ws_bytes, void* stream);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -341,8 +341,10 @@ def one_level_coefficients(kernel: str):
     return a, b, c
 
 
-def leaf_partial(kernel: str, a: np.ndarray, b: np.ndarray, levels: int, first: int, count: int) -> np.ndarray:
-    """Sum of the contributions of leaves [first, first+count) (level-major order) to C."""
+def leaf_partial(kernel: str, a: np.ndarray, b: np.ndarray, levels: int, first: int, count: int,
+                 panels: int = 1) -> np.ndarray:
+    """Sum of the contributions of shard units [first, first+count) to C; unit u is row panel
+    (u mod panels) of leaf (u div panels), leaves in level-major order."""
     ca, cb, cc = one_level_coefficients(kernel)
     nprod = len(ca)
     n = a.shape[0]
@@ -350,15 +352,19 @@ def leaf_partial(kernel: str, a: np.ndarray, b: np.ndarray, levels: int, first: 
 
     def rec(level, xs, ys, ds, size, index):
         # xs / ys / ds: lists of (row, col, sign) blocks of A / B / C at this size
-        sub = nprod ** (levels - level)
-        if index + sub <= first or index >= first + count:
+        sub = nprod ** (levels - level) * panels
+        if index * panels + sub <= first or index * panels >= first + count:
             return
         if level == levels:
-            x = sum(s * a[r:r + size, c:c + size] for r, c, s in xs)
+            u0 = index * panels
+            lo, hi = max(u0, first) - u0, min(u0 + panels, first + count) - u0
+            pr = size // panels
+            r0, r1 = lo * pr, hi * pr
+            x = sum(s * a[r + r0:r + r1, c:c + size] for r, c, s in xs)
             y = sum(s * b[r:r + size, c:c + size] for r, c, s in ys)
             p = x @ y
             for r, c, s in ds:
-                out[r:r + size, c:c + size] += s * p
+                out[r + r0:r + r1, c:c + size] += s * p
             return
         h = size // 2
         off = [(0, 0), (0, h), (h, 0), (h, h)]

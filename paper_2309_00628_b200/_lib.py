@@ -53,7 +53,9 @@ SIGNATURES = {
     "mk_absmax_f64": (_INT, [_VP, _I64, _I64, _I64, _DP, _VP]),
     "mk_absmax_i64": (_INT, [_VP, _I64, _I64, _I64, _DP, _VP]),
     "mk_product_count": (_INT, [_INT, _INT]),
-    "mk_strassen_partial": (_INT, [_INT, _VP, _I64, _VP, _I64, _VP, _I64, _I64, _INT, _INT, _INT, _VP, _SZ, _VP]),
+    "mk_partial_workspace_bytes": (_SZ, [_INT, _I64, _INT]),
+    "mk_strassen_partial": (_INT, [_INT, _VP, _I64, _VP, _I64, _VP, _I64, _I64, _INT, _INT, _INT, _INT, _VP, _SZ,
+                                   _VP]),
 }
 
 

@@ -22,6 +22,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <string>
@@ -316,8 +317,11 @@ struct Engine {
   bool dry = false;  // sizing pass: no launches
   size_t ws_peak = 0;
   // leaf-range filter (multi-GPU sharding)
+  // Shard filter in units of leaf row panels: leaf i covers units [i*panels, (i+1)*panels);
+  // a partial product computes only units [leaf_first, leaf_first + leaf_count).
   int64_t leaf_first = 0, leaf_count = -1;
   int64_t leaf_counter = 0;
+  int64_t panels = 1;
   int launches = 0;
   bool fuse_preadds = false;  // K2 in-kernel combiner for the last level's operand sums
 
@@ -513,8 +517,8 @@ struct Engine {
     return kron(D, cq, hr, hc);
   }
 
-  int64_t leaves_below(int remaining) const {
-    int64_t r = 1;
+  int64_t leaves_below(int remaining) const {  // in shard units (leaves x row panels)
+    int64_t r = panels;
     for (int i = 0; i < remaining; ++i) r *= co->nprod;
     return r;
   }
@@ -530,8 +534,16 @@ struct Engine {
       }
     }
     if (remaining == 0) {
-      ++leaf_counter;
-      return product(X, Y, D, M, N, K);
+      const int64_t u0 = leaf_counter;
+      leaf_counter += panels;
+      if (leaf_count < 0 || panels == 1) return product(X, Y, D, M, N, K);
+      // only this rank's contiguous row panels of the leaf: shift operand and destination rows
+      const int64_t lo = std::max(u0, leaf_first) - u0, hi = std::min(u0 + panels, leaf_first + leaf_count) - u0;
+      const int64_t pr = M / panels, r0 = lo * pr, rows = (hi - lo) * pr;
+      Lin Xs = X, Ds = D;
+      for (Blk& t : Xs) t.row += r0;
+      for (Blk& t : Ds) t.row += r0;
+      return product(Xs, Y, Ds, rows, N, K);
     }
     const int64_t hm = M / 2, hn = N / 2, hk = K / 2;
     for (int p = 0; p < co->nprod; ++p) {
@@ -690,6 +702,46 @@ struct Engine {
     return MK_OK;
   }
 
+  // Fewest groups of siblings with pairwise disjoint output quadrants (exhaustive over the
+  // <= 8^8 colourings is too many; backtracking with a colour bound finds the optimum at once
+  // for 7-8 products), most balanced among optima (larger launches fill the GPU evenly).
+  std::vector<std::vector<int>> colour_siblings() const {
+    const int np = co->nprod;
+    auto clash = [&](int p, int o) {
+      for (int q = 0; q < 4; ++q)
+        if (co->c[q][p] != 0 && co->c[q][o] != 0) return true;
+      return false;
+    };
+    std::vector<int> col(np, -1), best;
+    int best_k = np + 1, best_spread = 1 << 30;
+    std::function<void(int, int)> rec = [&](int p, int k) {
+      if (k > best_k) return;
+      if (p == np) {
+        std::vector<int> cnt(k, 0);
+        for (int c : col) ++cnt[c];
+        const int spread = *std::max_element(cnt.begin(), cnt.end()) - *std::min_element(cnt.begin(), cnt.end());
+        if (k < best_k || (k == best_k && spread < best_spread)) {
+          best_k = k;
+          best_spread = spread;
+          best = col;
+        }
+        return;
+      }
+      for (int c = 0; c <= k && c < np; ++c) {
+        bool ok = true;
+        for (int o = 0; o < p && ok; ++o) ok = !(col[o] == c && clash(p, o));
+        if (!ok) continue;
+        col[p] = c;
+        rec(p + 1, c == k ? k + 1 : k);
+        col[p] = -1;
+      }
+    };
+    rec(0, 0);
+    std::vector<std::vector<int>> groups(best_k);
+    for (int p = 0; p < np; ++p) groups[best[p]].push_back(p);
+    return groups;
+  }
+
   struct BNode {
     Blk x, y;          // operands: single signed blocks (views or materialised sums)
     int out = -1;      // output block base (inner nodes)
@@ -757,21 +809,7 @@ struct Engine {
     // order) so that each launch holds products with disjoint quadrants -- e.g. Winograd
     // {P1} {P2,P6} {P3,P7} {P4,P5}: 4 launches instead of 7, still race-free and deterministic
     // (per quadrant, contributions land in launch order; the first one stores).
-    std::vector<std::vector<int>> groups;
-    for (int p = 0; p < np; ++p) {
-      bool placed = false;
-      for (auto& gr : groups) {
-        bool clash = false;
-        for (int o : gr)
-          for (int q = 0; q < 4; ++q) clash |= co->c[q][p] != 0 && co->c[q][o] != 0;
-        if (!clash) {
-          gr.push_back(p);
-          placed = true;
-          break;
-        }
-      }
-      if (!placed) groups.push_back({p});
-    }
+    std::vector<std::vector<int>> groups = colour_siblings();
     if (L == 1) {  // one parent (the root): plain sequential launches
       groups.clear();
       for (int p = 0; p < np; ++p) groups.push_back({p});
@@ -1086,14 +1124,34 @@ int mk_product_count(int algo, int levels) {
   return (int)c;
 }
 
+size_t mk_partial_workspace_bytes(int algo, int64_t n, int levels) {
+  if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_WINOGRAD_KNUTH_8CALL || n < 1 || !is_pow2(n) || levels < 0 ||
+      (levels > 0 && (n >> levels) < 2))
+    return 0;
+  Engine e;
+  e.dry = true;
+  if (setup_square(e, algo, reinterpret_cast<double*>(0x100000), n, reinterpret_cast<double*>(0x200000), n,
+                   reinterpret_cast<double*>(0x300000), n, n, levels) != MK_OK)
+    return 0;
+  e.leaf_first = 0;
+  e.leaf_count = 1 << 30;  // every unit: the depth-first plan a partial product runs
+  e.set_state(BASE_C, 0, 0, n, n, 1);
+  if (run_square(e) != MK_OK) return 0;
+  return e.ws_peak;
+}
+
 int mk_strassen_partial(int algo, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
-                        int64_t ldc, int64_t n, int levels, int first, int count, void* ws, size_t ws_bytes,
-                        void* stream) {
+                        int64_t ldc, int64_t n, int levels, int first, int count, int panels, void* ws,
+                        size_t ws_bytes, void* stream) {
   g_last_error.clear();
   if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_WINOGRAD_KNUTH_8CALL)
     return fail(MK_ERR_ARG, "partial products support the fused algorithms only");
+  if (panels < 1 || ((n >> levels) % panels) != 0 || (((n >> levels) / panels) % 2) != 0)
+    return fail(MK_ERR_ARG, "panels must divide the leaf order into even row panels");
+  if (first < 0 || count < 0) return fail(MK_ERR_ARG, "negative shard range");
   Engine e;
   MK_TRY(setup_square(e, algo, const_cast<double*>(A), lda, const_cast<double*>(B), ldb, C, ldc, n, levels));
+  e.panels = panels;
   if (overlaps(C, ldc, n, n, A, lda, n, n) || overlaps(C, ldc, n, n, B, ldb, n, n))
     return fail(MK_ERR_ALIAS, "output view must not alias an input view");
   e.st = static_cast<cudaStream_t>(stream);

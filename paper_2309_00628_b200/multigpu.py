@@ -2,23 +2,26 @@
 GPUs of one node, partial C blocks sum-reduced over NVLink.
 
 Decomposition. An L-level product is a sum of 7^L leaf contributions (Kronecker powers of
-the one-level coefficients). Rank r of W computes a contiguous range of leaf indices in
-level-major order (``shard_range``), so leaves sharing an outer-level operand sum land on
-the same rank and that sum is materialised once there. Each rank accumulates its leaves
+the one-level coefficients); each leaf's output rows are independent, so the shard unit is a
+leaf row panel (``PANELS`` per leaf). Rank r of W computes a contiguous range of units in
+level-major order (``shard_range``): every rank gets the same amount of work, and leaves sharing
+an outer-level operand sum land on the same rank, where that sum is materialised once. Each rank accumulates its leaves
 into a zero-initialised partial C with the fused multi-destination epilogue
 (``mk_strassen_partial``); the partials are then summed with one collective
 (``torch.distributed.reduce``, NCCL on GPUs, gloo in the CPU tests). That reduce is the
 path's only exchange step: operands are replicated (inputs resident on every GPU, as
 BASELINE.json's multi-GPU config states) and nothing else crosses GPUs.
 
-Load balance: 7 leaves over 8 GPUs cap efficiency at 7/8; 49 over 8 at 49/56; 49 over 4
-at 49/52 -- bench.py uses two levels for N > 1.
+Load balance: with whole leaves 49 over 8 GPUs would cap efficiency at 49/56; in row-panel
+units (49 x 8 = 392) the split is exact.
 """
 from __future__ import annotations
 
 import ctypes
 
 from . import _lib
+
+PANELS = 8  # row panels per leaf (shard granularity)
 
 
 def shard_range(total: int, world: int, rank: int) -> tuple[int, int]:
@@ -38,8 +41,9 @@ def leaf_count(algo: str, levels: int) -> int:
     return n
 
 
-def partial_product(algo: str, a, b, c_partial, levels: int, first: int, count: int, stream=None, ws=None) -> int:
-    """c_partial += sum of leaves [first, first+count) of A B (all CUDA FP64, square order n).
+def partial_product(algo: str, a, b, c_partial, levels: int, first: int, count: int, stream=None, ws=None,
+                    panels: int = PANELS) -> int:
+    """c_partial += shard units [first, first+count) of A B (all CUDA FP64, square order n).
 
     ``c_partial`` must be zero-initialised (or hold earlier partial sums). Returns the
     workspace bytes used.
@@ -49,13 +53,13 @@ def partial_product(algo: str, a, b, c_partial, levels: int, first: int, count: 
     lib = _lib.load()
     n = a.shape[0]
     aid = _lib.ALGO_IDS[algo]
-    need = int(lib.mk_workspace_bytes(aid, n, levels))
+    need = int(lib.mk_partial_workspace_bytes(aid, n, levels))
     if ws is None or ws.numel() < need:
         ws = torch.empty(max(need, 16), dtype=torch.uint8, device=a.device)
     st = ctypes.c_void_p((stream or torch.cuda.current_stream()).cuda_stream)
     rc = lib.mk_strassen_partial(aid, ctypes.c_void_p(a.data_ptr()), a.stride(0), ctypes.c_void_p(b.data_ptr()),
                                  b.stride(0), ctypes.c_void_p(c_partial.data_ptr()), c_partial.stride(0), n, levels,
-                                 first, count, ctypes.c_void_p(ws.data_ptr()), need, st)
+                                 first, count, panels, ctypes.c_void_p(ws.data_ptr()), need, st)
     _lib.check(rc, "mk_strassen_partial")
     return need
 
@@ -84,7 +88,7 @@ def sharded_multiply(algo: str, a, b, levels: int, group=None, out=None, ws=None
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
-    total = leaf_count(algo, levels)
+    total = leaf_count(algo, levels) * PANELS
     first, count = shard_range(total, world, rank)
     if out is None:
         out = torch.zeros_like(a)

@@ -348,15 +348,16 @@ def test_sharded_partials_sum_to_product(levels, world):
     n = 1024
     a = torch.from_numpy(r.integers(-8, 9, (n, n)).astype(np.float64)).cuda()
     b = torch.from_numpy(r.integers(-8, 9, (n, n)).astype(np.float64)).cuda()
-    total = multigpu.leaf_count("winograd-block", levels)
-    acc = torch.zeros_like(a)
-    for rank in range(world):
-        first, count = multigpu.shard_range(total, world, rank)
-        part = torch.zeros_like(a)
-        if count:
-            multigpu.partial_product("winograd-block", a, b, part, levels, first, count)
-        acc += part
-    assert torch.equal(acc, a @ b)
+    for panels in (1, multigpu.PANELS):
+        total = multigpu.leaf_count("winograd-block", levels) * panels
+        acc = torch.zeros_like(a)
+        for rank in range(world):
+            first, count = multigpu.shard_range(total, world, rank)
+            part = torch.zeros_like(a)
+            if count:
+                multigpu.partial_product("winograd-block", a, b, part, levels, first, count, panels=panels)
+            acc += part
+        assert torch.equal(acc, a @ b), panels
 
 
 def test_device_resident_multiply_rect_and_presets(rng):

@@ -31,12 +31,13 @@ def test_leaf_decomposition_sums_to_the_product(kernel, levels):
     r = np.random.default_rng(5)
     n = 16
     a, b = r.integers(-8, 9, (n, n)), r.integers(-8, 9, (n, n))
-    total = len(o.one_level_coefficients(kernel)[0]) ** levels
-    acc = np.zeros((n, n), dtype=np.int64)
-    for w in range(3):
-        first, count = shard_range(total, 3, w)
-        acc += o.leaf_partial(kernel, a, b, levels, first, count)
-    assert np.array_equal(acc, a @ b)
+    for panels in (1, 4):
+        total = len(o.one_level_coefficients(kernel)[0]) ** levels * panels
+        acc = np.zeros((n, n), dtype=np.int64)
+        for w in range(3):
+            first, count = shard_range(total, 3, w)
+            acc += o.leaf_partial(kernel, a, b, levels, first, count, panels)
+        assert np.array_equal(acc, a @ b), panels
 
 
 def _free_port():
@@ -55,9 +56,10 @@ def _worker(rank, world, port, kernel, levels, q):
         r = np.random.default_rng(9)
         n = 32
         a, b = r.integers(-8, 9, (n, n)), r.integers(-8, 9, (n, n))
-        total = len(o.one_level_coefficients(kernel)[0]) ** levels
+        panels = 8
+        total = len(o.one_level_coefficients(kernel)[0]) ** levels * panels
         first, count = shard_range(total, world, rank)
-        part = torch.from_numpy(o.leaf_partial(kernel, a, b, levels, first, count))
+        part = torch.from_numpy(o.leaf_partial(kernel, a, b, levels, first, count, panels))
         out = assemble(part, dst_rank=0)
         if rank == 0:
             q.put(bool(np.array_equal(out.numpy(), a @ b)))
