@@ -280,6 +280,15 @@ static bool async_epilogue_enabled() {
   return v == 1;
 }
 
+static bool literal_bfs_tail() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MK_LITERAL_TAIL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static bool debug_sync() {
   static int v = -1;
   if (v < 0) {
@@ -615,6 +624,23 @@ struct Engine {
     set_state(D.base, D.row, D.col, s, s, 0);
     if (remaining == 0 || (remaining == 1 && fuse_preadds))
       return fused(remaining, Lin{X}, Lin{Y}, Lin{D}, s, s, s, L - remaining);
+    // Two-temp may use scratch: its last two levels run breadth-first (leaf products of the
+    // 7 sub-parents batched per launch) under the literal Table-2 levels above. In-place keeps
+    // the literal schedule to the leaves (zero workspace). MK_LITERAL_TAIL=0 disables this.
+    if (use_xy && remaining == 2 && !fuse_preadds && literal_bfs_tail()) {
+      const size_t mark = ws_used;
+      const int nb_mark = nbases;
+      MK_TRY(bfs(2, s, s, s, X, Y, D));
+      ws_used = mark;
+      while (nbases > nb_mark) {
+        --nbases;
+        written.pop_back();
+        cell_rows.pop_back();
+        cell_cols.pop_back();
+      }
+      set_state(D.base, D.row, D.col, s, s, 1);
+      return MK_OK;
+    }
     const int64_t h = s / 2;
     std::map<std::string, Blk> loc;
     static const char* qs[4] = {"11", "12", "21", "22"};
@@ -743,14 +769,16 @@ struct Engine {
   }
 
   struct BNode {
-    Blk x, y;          // operands: single signed blocks (views or materialised sums)
-    int out = -1;      // output block base (inner nodes)
+    Blk x, y;                     // operands: single signed blocks (views or materialised sums)
+    Blk o{-1, 0, 0, 1.0};         // output block (inner nodes; the root's is the caller's D)
   };
 
-  int bfs(int64_t M, int64_t N, int64_t K) {
+  // Breadth-first product of the root operands X (M x K), Y (K x N) into block D (store
+  // semantics: D is fully overwritten) with `L` levels.
+  int bfs(int L, int64_t M, int64_t N, int64_t K, Blk X, Blk Y, Blk D) {
     const int np = co->nprod;
     std::vector<std::vector<BNode>> lv(1);
-    lv[0].push_back(BNode{Blk{BASE_A, 0, 0, 1.0}, Blk{BASE_B, 0, 0, 1.0}, -1});
+    lv[0].push_back(BNode{X, Y, Blk{-1, 0, 0, 1.0}});
     // ---- operand sums, depth by depth ----
     for (int d = 0; d < L; ++d) {
       const int64_t hm = (M >> d) / 2, hn = (N >> d) / 2, hk = (K >> d) / 2;
@@ -799,9 +827,13 @@ struct Engine {
     std::vector<BNode>& par = lv[L - 1];
     const int64_t lm = M >> L, ln = N >> L, lk = K >> L;
     if (L == 1) {
-      par[0].out = BASE_C;
+      par[0].o = D;
     } else {
-      for (BNode& pn : par) MK_TRY(alloc_slot(2 * lm, 2 * ln, &pn.out));
+      for (BNode& pn : par) {
+        int sb;
+        MK_TRY(alloc_slot(2 * lm, 2 * ln, &sb));
+        pn.o = Blk{sb, 0, 0, 1.0};
+      }
     }
     const int slab = consumer_layout() == 16 ? 32 : 64;
     bool touched[4] = {false, false, false, false};
@@ -831,9 +863,10 @@ struct Engine {
       if (L == 1) {
         const int p = gr[0];
         const BNode& lf = lv[1][p];
-        Lin D;
-        for (int i = 0; i < dd[0].nd; ++i) D.push_back(Blk{BASE_C, dd[0].dt[i].row, dd[0].dt[i].col, dd[0].dt[i].sign});
-        MK_TRY(product(Lin{lf.x}, Lin{lf.y}, D, lm, ln, lk));
+        Lin Dl;
+        for (int i = 0; i < dd[0].nd; ++i)
+          Dl.push_back(Blk{D.base, D.row + dd[0].dt[i].row, D.col + dd[0].dt[i].col, dd[0].dt[i].sign});
+        MK_TRY(product(Lin{lf.x}, Lin{lf.y}, Dl, lm, ln, lk));
         continue;
       }
       bool async_ok = async_epilogue_enabled() && lm % slab == 0 && ln % 16 == 0;
@@ -851,14 +884,18 @@ struct Engine {
           e.prod.nd = dd[gi].nd;
           e.prod.a[0] = MkTerm{(int32_t)lf.x.row, (int32_t)lf.x.col, lf.x.sign};
           e.prod.b[0] = MkTerm{(int32_t)lf.y.row, (int32_t)lf.y.col, lf.y.sign};
-          for (int k = 0; k < dd[gi].nd; ++k) e.prod.d[k] = dd[gi].dt[k];
-          e.C = bases[par[i].out].ptr;
-          e.ldc = bases[par[i].out].ld;
-          vec_ok = vec_ok && e.ldc % 4 == 0 && reinterpret_cast<uintptr_t>(e.C) % 32 == 0;
+          for (int k = 0; k < dd[gi].nd; ++k) {
+            e.prod.d[k] = dd[gi].dt[k];
+            e.prod.d[k].row += par[i].o.row;
+            e.prod.d[k].col += par[i].o.col;
+          }
+          e.C = bases[par[i].o.base].ptr;
+          e.ldc = bases[par[i].o.base].ld;
+          vec_ok = vec_ok && e.ldc % 4 == 0 && reinterpret_cast<uintptr_t>(e.C) % 32 == 0 && par[i].o.col % 4 == 0;
           if (!dry) {
             MK_TRY(cached_map(lf.x.base, 0, &e.tmA));
             MK_TRY(cached_map(lf.y.base, 1, &e.tmB));
-            if (async_ok) MK_TRY(cached_map(par[i].out, slab == 64 ? 2 : 3, &e.tmC));
+            if (async_ok) MK_TRY(cached_map(par[i].o.base, slab == 64 ? 2 : 3, &e.tmC));
           }
         }
       }
@@ -901,20 +938,23 @@ struct Engine {
       const int64_t cm = M >> d, cn = N >> d;
       std::vector<MkXformJob> jobs;
       for (size_t j = 0; j < pa.size(); ++j) {
-        if (d - 1 == 0)
-          pa[j].out = BASE_C;
-        else
-          MK_TRY(alloc_slot(2 * cm, 2 * cn, &pa[j].out));
+        if (d - 1 == 0) {
+          pa[j].o = D;
+        } else {
+          int sb;
+          MK_TRY(alloc_slot(2 * cm, 2 * cn, &sb));
+          pa[j].o = Blk{sb, 0, 0, 1.0};
+        }
         MkXformJob job{};
         job.nsrc = np;
         for (int p = 0; p < np; ++p) {
-          job.src[p] = bases[ch[j * np + p].out].ptr;
-          job.lds[p] = bases[ch[j * np + p].out].ld;
+          job.src[p] = ptr_of(ch[j * np + p].o);
+          job.lds[p] = bases[ch[j * np + p].o.base].ld;
         }
         job.ndst = 4;
         for (int q = 0; q < 4; ++q) {
-          job.dst[q] = ptr_of(Blk{pa[j].out, (q >> 1) * cm, (q & 1) * cn, 1.0});
-          job.ldd[q] = bases[pa[j].out].ld;
+          job.dst[q] = ptr_of(Blk{pa[j].o.base, pa[j].o.row + (q >> 1) * cm, pa[j].o.col + (q & 1) * cn, 1.0});
+          job.ldd[q] = bases[pa[j].o.base].ld;
           for (int p = 0; p < np; ++p) job.coef[q][p] = (int8_t)co->c[q][p];
         }
         jobs.push_back(job);
@@ -970,7 +1010,8 @@ static bool use_bfs(const Engine& e, int64_t lm, int64_t ln) {
 
 static int run_square(Engine& e) {
   const int64_t n = e.n;
-  if (use_bfs(e, e.leaf_m, e.leaf_n)) return e.bfs(n, n, n);
+  if (use_bfs(e, e.leaf_m, e.leaf_n))
+    return e.bfs(e.L, n, n, n, Blk{BASE_A, 0, 0, 1.0}, Blk{BASE_B, 0, 0, 1.0}, Blk{BASE_C, 0, 0, 1.0});
   if (e.algo == MK_ALGO_TWO_TEMP)
     return e.literal(kTwoTemp, true, e.L, Blk{BASE_A, 0, 0, 1.0}, Blk{BASE_B, 0, 0, 1.0}, Blk{BASE_C, 0, 0, 1.0}, n);
   if (e.algo == MK_ALGO_IN_PLACE)
@@ -1215,7 +1256,7 @@ static int run_rect(int algo, const double* A, int64_t lda, const double* B, int
   e.ws = dry ? nullptr : static_cast<char*>(ws) + off;
   e.ws_bytes = dry ? 0 : ws_bytes - off;
   if (use_bfs(e, e.leaf_m, e.leaf_n))
-    MK_TRY(e.bfs(mp, np_, kp));
+    MK_TRY(e.bfs(levels, mp, np_, kp, Blk{BASE_A, 0, 0, 1.0}, Blk{BASE_B, 0, 0, 1.0}, Blk{BASE_C, 0, 0, 1.0}));
   else
     MK_TRY(e.fused(levels, Lin{Blk{BASE_A, 0, 0, 1.0}}, Lin{Blk{BASE_B, 0, 0, 1.0}}, Lin{Blk{BASE_C, 0, 0, 1.0}},
                    mp, np_, kp, 0));
