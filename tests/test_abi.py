@@ -73,8 +73,10 @@ def test_workspace_sizes(lib):
     assert ws("in-place", 1024, 1) == 0 and ws("in-place", 1024, 3) == 0
     assert ws("winograd-block", 1024, 1) == 2 * 512 * 512 * 8
     assert ws("two-temp", 1024, 1) == 2 * 512 * 512 * 8
-    # deeper: the two slots of every level (two-temp: sum of 2 (n/2^l)^2 over levels)
-    assert ws("two-temp", 1024, 3) == 2 * 8 * (512 ** 2 + 256 ** 2 + 128 ** 2)
+    # deeper: two-temp keeps its two (n/2)^2 slots at the literal top level; its last two levels
+    # run breadth-first (more scratch), still below the all-breadth-first plan
+    assert 2 * 8 * 512 ** 2 < ws("two-temp", 1024, 3) <= ws("winograd-block", 1024, 3)
+    assert ws("two-temp", 1024, 2) == ws("winograd-block", 1024, 2)
     assert ws("winograd-block", 16384, 1) == 2 * 8192 * 8192 * 8
     assert ws("winograd-block", 16, 5) == 0  # invalid (leaf order < 2)
     assert lib.mk_rect_workspace_bytes(_lib.ALGO_IDS["winograd-block"], 12000, 10000, 14000, 5) > 0
@@ -84,3 +86,20 @@ def test_product_counts(lib):
     assert lib.mk_product_count(_lib.ALGO_IDS["winograd-block"], 2) == 49
     assert lib.mk_product_count(_lib.ALGO_IDS["winograd-knuth-8call"], 1) == 8
     assert lib.mk_product_count(_lib.ALGO_IDS["two-temp"], 1) == -1
+
+
+def test_plain_c_consumer_links_and_runs(lib, tmp_path):
+    """include/mk_strassen.h is a usable C boundary: a C program links the .so (no Python)."""
+    import shutil
+    import subprocess
+
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    exe = tmp_path / "abi_check"
+    src = os.path.join(ROOT, "tests", "c", "abi_check.c")
+    libdir = os.path.dirname(_lib.LIB_PATH)
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), src, "-o", str(exe),
+                    "-L", libdir, "-lmk_strassen", f"-Wl,-rpath,{libdir}"], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "abi_check ok" in out.stdout
