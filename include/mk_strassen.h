@@ -109,6 +109,20 @@ int mk_multiply_rect(int algo, const double* A, int64_t lda, const double* B, in
                      int64_t ldc, int64_t m, int64_t n, int64_t k, int levels, void* ws, size_t ws_bytes,
                      void* stream);
 
+/* End-to-end product for HOST operands with transfers overlapped with compute (fused
+ * algorithms, levels >= 1). hA/hB/hC: host matrices (pinned for asynchronous DMA); dA/dB/dC:
+ * caller-owned device buffers of order n with even leading dimension ldd. Quadrants are
+ * uploaded on `copy_stream` in order of first use, the top-level products run on `stream` in
+ * the order mk_overlap_order reports (each waiting only for the quadrants it reads), and every
+ * C quadrant is downloaded as soon as its last contributor finishes. Synchronous: returns when
+ * hC holds the result. Workspace from mk_partial_workspace_bytes (depth-first plan). */
+int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, int64_t ldb, double* hC, int64_t ldc,
+                     int64_t n, int levels, double* dA, double* dB, double* dC, int64_t ldd, void* ws,
+                     size_t ws_bytes, void* stream, void* copy_stream);
+/* Top-level product order (order_out[nprod]) and quadrant upload order (uploads_out[8]: A11..A22
+ * = 0..3, B11..B22 = 4..7) of the overlapped host path; returns nprod. */
+int mk_overlap_order(int algo, int* order_out, int* uploads_out);
+
 /* dst = sum_i sign[i] * src_i over a rows x cols block (nsrc <= 8); dst may alias a
  * source exactly. Replaces block_add core.py:153-169 (np.add / np.subtract). */
 int mk_block_combine(double* dst, int64_t ldd, const double* const* src, const int64_t* lds,

@@ -554,66 +554,94 @@ struct Engine {
       for (Blk& t : Ds) t.row += r0;
       return product(Xs, Y, Ds, rows, N, K);
     }
+    for (int p = 0; p < co->nprod; ++p) MK_TRY(fused_child(remaining, p, X, Y, D, M, N, K, level));
+    return MK_OK;
+  }
+
+
+  // One child product p of a fused-plan node (operands X, Y, destinations D at this level).
+  int fused_child(int remaining, int p, const Lin& X, const Lin& Y, const Lin& D, int64_t M, int64_t N, int64_t K,
+                  int level) {
     const int64_t hm = M / 2, hn = N / 2, hk = K / 2;
-    for (int p = 0; p < co->nprod; ++p) {
-      Lin Xp = kron(X, co->a[p], hm, hk);
-      Lin Yp = kron(Y, co->b[p], hk, hn);
-      Lin Dp = kron_dest(D, p, hm, hn);
-      if (remaining == 1 && fuse_preadds) {
-        if ((int)Xp.size() > MK_MAX_TERMS || (int)Yp.size() > MK_MAX_TERMS)
-          return fail(MK_ERR_ARG, "internal: unmaterialised operand at fused level");
-        MK_TRY(fused(0, Xp, Yp, Dp, hm, hn, hk, level + 1));
-        continue;
+    Lin Xp = kron(X, co->a[p], hm, hk);
+    Lin Yp = kron(Y, co->b[p], hk, hn);
+    Lin Dp = kron_dest(D, p, hm, hn);
+    if (remaining == 1 && fuse_preadds) {
+      if ((int)Xp.size() > MK_MAX_TERMS || (int)Yp.size() > MK_MAX_TERMS)
+        return fail(MK_ERR_ARG, "internal: unmaterialised operand at fused level");
+      return fused(0, Xp, Yp, Dp, hm, hn, hk, level + 1);
+    }
+    // skip whole subtree if outside shard
+    const int64_t sub = leaves_below(remaining - 1);
+    if (leaf_count >= 0 && (leaf_counter + sub <= leaf_first || leaf_counter >= leaf_first + leaf_count)) {
+      leaf_counter += sub;
+      return MK_OK;
+    }
+    const size_t mark = ws_used;
+    const int nb_mark = nbases;
+    // materialise multi-term operands (two-temp style slots, freed after the subtree)
+    if (Xp.size() > 1) {
+      int sb;
+      MK_TRY(alloc_slot(hm, hk, &sb));
+      MK_TRY(combine(Blk{sb, 0, 0, 1.0}, Xp, hm, hk));
+      Xp = Lin{Blk{sb, 0, 0, 1.0}};
+    }
+    if (Yp.size() > 1) {
+      int sb;
+      MK_TRY(alloc_slot(hk, hn, &sb));
+      MK_TRY(combine(Blk{sb, 0, 0, 1.0}, Yp, hk, hn));
+      Yp = Lin{Blk{sb, 0, 0, 1.0}};
+    }
+    // destination fan-out below grows by <= 4 per level
+    int64_t worst = (int64_t)Dp.size();
+    for (int i = 1; i < remaining; ++i) worst *= 4;
+    if (worst > MK_MAX_DESTS) {
+      int pb;
+      MK_TRY(alloc_slot(hm, hn, &pb));
+      MK_TRY(fused(remaining - 1, Xp, Yp, Lin{Blk{pb, 0, 0, 1.0}}, hm, hn, hk, level + 1));
+      // post-add the materialised product into its destinations
+      for (const Blk& d : Dp) {
+        const int s = state(d.base, d.row, d.col, hm, hn);
+        if (s == 2) return fail(MK_ERR_ARG, "internal: partially written post-add destination");
+        Lin src;
+        if (s == 1) src.push_back(Blk{d.base, d.row, d.col, d.sign});  // keep existing (sign folded below)
+        src.push_back(Blk{pb, 0, 0, 1.0});
+        MK_TRY(combine(Blk{d.base, d.row, d.col, d.sign}, src, hm, hn));
+        set_state(d.base, d.row, d.col, hm, hn, 1);
       }
-      // skip whole subtree if outside shard
-      const int64_t sub = leaves_below(remaining - 1);
-      if (leaf_count >= 0 && (leaf_counter + sub <= leaf_first || leaf_counter >= leaf_first + leaf_count)) {
-        leaf_counter += sub;
-        continue;
+    } else {
+      MK_TRY(fused(remaining - 1, Xp, Yp, Dp, hm, hn, hk, level + 1));
+    }
+    // release slots allocated for this product
+    ws_used = mark;
+    while (nbases > nb_mark) {
+      --nbases;
+      written.pop_back();
+      cell_rows.pop_back();
+      cell_cols.pop_back();
+    }
+  
+    return MK_OK;
+  }
+
+  // Overlapped host run (mk_strassen_host): the top-level products run in `order`; before each
+  // one the compute stream waits for the input quadrants it reads (in_ev: A11..A22, B11..B22),
+  // after it every C quadrant whose last contributor it was is signalled (out_ev: C11..C22).
+  int fused_overlapped(const std::vector<int>& order, cudaEvent_t* in_ev, cudaEvent_t* out_ev, int64_t n) {
+    int last[4] = {-1, -1, -1, -1};
+    for (int i = 0; i < (int)order.size(); ++i)
+      for (int q = 0; q < 4; ++q)
+        if (co->c[q][order[i]]) last[q] = i;
+    for (int i = 0; i < (int)order.size(); ++i) {
+      const int p = order[i];
+      for (int q = 0; q < 4; ++q) {
+        if (co->a[p][q]) MK_CUDA_TRY(cudaStreamWaitEvent(st, in_ev[q], 0));
+        if (co->b[p][q]) MK_CUDA_TRY(cudaStreamWaitEvent(st, in_ev[4 + q], 0));
       }
-      const size_t mark = ws_used;
-      const int nb_mark = nbases;
-      // materialise multi-term operands (two-temp style slots, freed after the subtree)
-      if (Xp.size() > 1) {
-        int sb;
-        MK_TRY(alloc_slot(hm, hk, &sb));
-        MK_TRY(combine(Blk{sb, 0, 0, 1.0}, Xp, hm, hk));
-        Xp = Lin{Blk{sb, 0, 0, 1.0}};
-      }
-      if (Yp.size() > 1) {
-        int sb;
-        MK_TRY(alloc_slot(hk, hn, &sb));
-        MK_TRY(combine(Blk{sb, 0, 0, 1.0}, Yp, hk, hn));
-        Yp = Lin{Blk{sb, 0, 0, 1.0}};
-      }
-      // destination fan-out below grows by <= 4 per level
-      int64_t worst = (int64_t)Dp.size();
-      for (int i = 1; i < remaining; ++i) worst *= 4;
-      if (worst > MK_MAX_DESTS) {
-        int pb;
-        MK_TRY(alloc_slot(hm, hn, &pb));
-        MK_TRY(fused(remaining - 1, Xp, Yp, Lin{Blk{pb, 0, 0, 1.0}}, hm, hn, hk, level + 1));
-        // post-add the materialised product into its destinations
-        for (const Blk& d : Dp) {
-          const int s = state(d.base, d.row, d.col, hm, hn);
-          if (s == 2) return fail(MK_ERR_ARG, "internal: partially written post-add destination");
-          Lin src;
-          if (s == 1) src.push_back(Blk{d.base, d.row, d.col, d.sign});  // keep existing (sign folded below)
-          src.push_back(Blk{pb, 0, 0, 1.0});
-          MK_TRY(combine(Blk{d.base, d.row, d.col, d.sign}, src, hm, hn));
-          set_state(d.base, d.row, d.col, hm, hn, 1);
-        }
-      } else {
-        MK_TRY(fused(remaining - 1, Xp, Yp, Dp, hm, hn, hk, level + 1));
-      }
-      // release slots allocated for this product
-      ws_used = mark;
-      while (nbases > nb_mark) {
-        --nbases;
-        written.pop_back();
-        cell_rows.pop_back();
-        cell_cols.pop_back();
-      }
+      MK_TRY(fused_child(L, p, Lin{Blk{BASE_A, 0, 0, 1.0}}, Lin{Blk{BASE_B, 0, 0, 1.0}},
+                         Lin{Blk{BASE_C, 0, 0, 1.0}}, n, n, n, 0));
+      for (int q = 0; q < 4; ++q)
+        if (last[q] == i) MK_CUDA_TRY(cudaEventRecord(out_ev[q], st));
     }
     return MK_OK;
   }
@@ -1156,6 +1184,137 @@ int mk_strassen(int algo, double* A, int64_t lda, double* B, int64_t ldb, double
   e.ws = static_cast<char*>(ws);
   e.ws_bytes = ws ? ws_bytes : 0;
   return run_square(e);
+}
+
+// ---- overlapped host path -------------------------------------------------------------
+// Order of the top-level products for mk_strassen_host: simulate quadrant uploads (one unit
+// each, in order of first use), products (kProd units, each waiting for its input quadrants)
+// and downloads (one unit each, once a C quadrant's last contributor finished; the D2H
+// direction is independent of H2D), and keep the permutation that finishes first.
+// Winograd: P1 P2 P5 P6 P3 P7 P4 -- only A11, B11 before the first product, only C21 after the last.
+static std::vector<int> overlap_order(const Coeffs& co, std::vector<int>* uploads) {
+  const double kProd = 3.0;  // one top-level product ~ 3 quadrant transfers (n=16384, L=2, PCIe 5)
+  std::vector<int> perm(co.nprod), best;
+  for (int i = 0; i < co.nprod; ++i) perm[i] = i;
+  double best_t = 1e30;
+  do {
+    std::vector<int> up;
+    bool seen[8] = {false};
+    for (int p : perm)
+      for (int q = 0; q < 8; ++q) {
+        const int c = q < 4 ? co.a[p][q] : co.b[p][q - 4];
+        if (c && !seen[q]) {
+          seen[q] = true;
+          up.push_back(q);
+        }
+      }
+    double ready[8] = {0};
+    for (size_t i = 0; i < up.size(); ++i) ready[up[i]] = (double)(i + 1);
+    double tc = 0, done[4] = {0};
+    for (int p : perm) {
+      double start = tc;
+      for (int q = 0; q < 8; ++q)
+        if ((q < 4 ? co.a[p][q] : co.b[p][q - 4]) && ready[q] > start) start = ready[q];
+      tc = start + kProd;
+      for (int q = 0; q < 4; ++q)
+        if (co.c[q][p]) done[q] = tc;
+    }
+    std::vector<double> d(done, done + 4);
+    std::sort(d.begin(), d.end());
+    double td = 0;
+    for (double x : d) td = std::max(td, x) + 1.0;
+    if (td < best_t - 1e-9) {
+      best_t = td;
+      best = perm;
+      if (uploads) *uploads = up;
+    }
+  } while (std::next_permutation(perm.begin(), perm.end()));
+  return best;
+}
+
+int mk_overlap_order(int algo, int* order_out, int* uploads_out) {
+  g_last_error.clear();
+  if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_WINOGRAD_KNUTH_8CALL) return fail(MK_ERR_ARG, "fused algorithms only");
+  std::vector<int> up;
+  const std::vector<int> ord = overlap_order(coeffs_for(algo), &up);
+  for (size_t i = 0; i < ord.size(); ++i) order_out[i] = ord[i];
+  for (size_t i = 0; i < up.size(); ++i) uploads_out[i] = up[i];
+  return (int)ord.size();
+}
+
+int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, int64_t ldb, double* hC, int64_t ldc,
+                     int64_t n, int levels, double* dA, double* dB, double* dC, int64_t ldd, void* ws,
+                     size_t ws_bytes, void* stream, void* copy_stream) {
+  g_last_error.clear();
+  if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_WINOGRAD_KNUTH_8CALL)
+    return fail(MK_ERR_ARG, "the overlapped host path supports the fused algorithms");
+  if (levels < 1) return fail(MK_ERR_ARG, "the overlapped host path needs at least one level");
+  if (ldd < n || ldd % 2 || lda < n || ldb < n || ldc < n)
+    return fail(MK_ERR_DIMENSION, "leading dimension smaller than the order (device ld must be even)");
+  Engine e;
+  MK_TRY(setup_square(e, algo, dA, ldd, dB, ldd, dC, ldd, n, levels));
+  cudaStream_t st = static_cast<cudaStream_t>(stream), cp = static_cast<cudaStream_t>(copy_stream);
+  e.st = st;
+  e.ws = static_cast<char*>(ws);
+  e.ws_bytes = ws ? ws_bytes : 0;
+  std::vector<int> up;
+  static std::map<int, std::pair<std::vector<int>, std::vector<int>>> cache;
+  static std::mutex mu;
+  std::vector<int> order;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(algo);
+    if (it == cache.end()) {
+      order = overlap_order(coeffs_for(algo), &up);
+      cache[algo] = {order, up};
+    } else {
+      order = it->second.first;
+      up = it->second.second;
+    }
+  }
+  const int64_t h = n / 2;
+  cudaEvent_t ev[13];
+  for (int i = 0; i < 13; ++i) MK_CUDA_TRY(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+  cudaEvent_t *in_ev = ev, *out_ev = ev + 8, start = ev[12];
+  int rc = MK_OK;
+  auto quad_ptr = [&](double* base, int64_t ld, int q) { return base + ((q >> 1) * h) * ld + (q & 1) * h; };
+  // the copy stream starts after prior work on the compute stream (device buffers may be reused)
+  if (cudaEventRecord(start, st) != cudaSuccess || cudaStreamWaitEvent(cp, start, 0) != cudaSuccess)
+    rc = fail(MK_ERR_CUDA, "stream ordering failed");
+  for (size_t i = 0; rc == MK_OK && i < up.size(); ++i) {
+    const int q = up[i];
+    const bool isA = q < 4;
+    const double* src = isA ? quad_ptr(const_cast<double*>(hA), lda, q) : quad_ptr(const_cast<double*>(hB), ldb, q - 4);
+    double* dst = isA ? quad_ptr(dA, ldd, q) : quad_ptr(dB, ldd, q - 4);
+    cudaError_t ce = cudaMemcpy2DAsync(dst, ldd * 8, src, (isA ? lda : ldb) * 8, h * 8, h, cudaMemcpyHostToDevice, cp);
+    if (ce == cudaSuccess) ce = cudaEventRecord(in_ev[q], cp);
+    if (ce != cudaSuccess) rc = fail(MK_ERR_CUDA, std::string("upload: ") + cudaGetErrorString(ce));
+  }
+  if (rc == MK_OK) rc = e.fused_overlapped(order, in_ev, out_ev, n);
+  if (rc == MK_OK) {
+    // downloads in the order the quadrants complete
+    int last[4] = {-1, -1, -1, -1};
+    for (int i = 0; i < (int)order.size(); ++i)
+      for (int q = 0; q < 4; ++q)
+        if (e.co->c[q][order[i]]) last[q] = i;
+    int qs[4] = {0, 1, 2, 3};
+    std::sort(qs, qs + 4, [&](int x, int y) { return last[x] < last[y]; });
+    for (int q : qs) {
+      cudaError_t ce = cudaStreamWaitEvent(cp, out_ev[q], 0);
+      if (ce == cudaSuccess)
+        ce = cudaMemcpy2DAsync(quad_ptr(hC, ldc, q), ldc * 8, quad_ptr(dC, ldd, q), ldd * 8, h * 8, h,
+                               cudaMemcpyDeviceToHost, cp);
+      if (ce != cudaSuccess) {
+        rc = fail(MK_ERR_CUDA, std::string("download: ") + cudaGetErrorString(ce));
+        break;
+      }
+    }
+  }
+  cudaError_t se = cudaStreamSynchronize(cp);
+  if (rc == MK_OK && se == cudaSuccess) se = cudaStreamSynchronize(st);
+  if (rc == MK_OK && se != cudaSuccess) rc = fail(MK_ERR_CUDA, std::string("sync: ") + cudaGetErrorString(se));
+  for (int i = 0; i < 13; ++i) cudaEventDestroy(ev[i]);
+  return rc;
 }
 
 int mk_product_count(int algo, int levels) {

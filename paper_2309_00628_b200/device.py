@@ -253,88 +253,51 @@ _PIPE_ALGOS = ("strassen", "winograd-block", "winograd-knuth", "winograd-knuth-8
 _copy_stream = None
 
 
-def _pipeline_panels(a: MatrixView, b: MatrixView, c: MatrixView, levels: int, algo: str, dtype) -> int:
-    """Row panels for the overlapped host path, or 0 when it does not apply.
-
-    Applies to FP64 products whose operands and result live in *pinned* host memory (so the
-    copies are true async DMA), large enough for transfers to matter, on the fused algorithms.
-    MK_PIPELINE=0 disables it; MK_PIPELINE_PANELS sets the panel count (default 4).
-    """
+def _overlap_applies(a: MatrixView, b: MatrixView, c: MatrixView, levels: int, algo: str, dtype) -> bool:
+    """Whether the overlapped host path applies: FP64 operands and result in *pinned* host
+    memory (so the copies are true async DMA), large enough for transfers to matter, one of
+    the fused algorithms. MK_PIPELINE=0 disables it."""
     import os
 
     if os.environ.get("MK_PIPELINE", "1") == "0" or algo not in _PIPE_ALGOS or levels < 1:
-        return 0
+        return False
     if a.on_device or b.on_device or c.on_device or np.dtype(dtype) != np.float64:
-        return 0
-    if not (a.dtype == b.dtype == c.dtype == np.float64) or not c.arr.flags.writeable:
-        return 0
-    n = a.rows
-    if n < 4096:
-        return 0
+        return False
+    if not (a.dtype == b.dtype == c.dtype == np.float64) or not c.arr.flags.writeable or a.rows < 2048:
+        return False
+    if any(v.arr.strides[1] != 8 for v in (a, b, c)):
+        return False
     try:
-        if not (torch.from_numpy(a.arr).is_pinned() and torch.from_numpy(b.arr).is_pinned()
-                and torch.from_numpy(c.arr).is_pinned()):
-            return 0
+        return all(torch.from_numpy(v.arr).is_pinned() for v in (a, b, c))
     except Exception:
-        return 0
-    panels = int(os.environ.get("MK_PIPELINE_PANELS", "4"))
-    pm = n // max(panels, 1)
-    if panels < 2 or n % panels or pm % (2 << levels) or n % (4 << levels):
-        return 0
-    return panels
+        return False
 
 
-def _pipelined_host_product(algo: str, a: MatrixView, b: MatrixView, c: MatrixView, levels: int, panels: int,
-                            st: EngineStats) -> None:
-    """C = A B for pinned host operands with transfers overlapped with compute.
-
-    B and the row panels of A go up on a copy stream; C row panel r (= A panel r . B, the same
-    L-level Strassen-Winograd recursion on an (n/P) x n x n problem, operands used in place) is
-    computed as soon as A panel r has landed and downloaded while panel r+1 computes. Only the
-    upload of B + one A panel and the download of one C panel stay exposed.
-    """
+def _overlapped_host_product(algo: str, a: MatrixView, b: MatrixView, c: MatrixView, levels: int,
+                             st: EngineStats) -> None:
+    """C = A B for pinned host operands through mk_strassen_host: quadrants go up on a copy
+    stream in order of first use, each top-level product starts as soon as the quadrants it
+    reads have landed, each C quadrant comes back as soon as its last contributor is done."""
     global _copy_stream
     lib = require_engine()
     n = a.rows
-    pm = n // panels
-    comp = torch.cuda.current_stream()
     if _copy_stream is None:
         _copy_stream = torch.cuda.Stream()
-    cp = _copy_stream
-    ha, hb, hc = torch.from_numpy(a.arr), torch.from_numpy(b.arr), torch.from_numpy(c.arr)
-    dA = torch.empty((n, n), dtype=torch.float64, device="cuda")
-    dB = torch.empty((n, n), dtype=torch.float64, device="cuda")
-    dC = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    ld = _round_ld(n)
+    dA = torch.empty((n, ld), dtype=torch.float64, device="cuda")
+    dB = torch.empty((n, ld), dtype=torch.float64, device="cuda")
+    dC = torch.empty((n, ld), dtype=torch.float64, device="cuda")
     aid = _lib.ALGO_IDS[algo]
-    ws_bytes = int(lib.mk_rect_workspace_bytes(aid, pm, n, n, levels))
+    ws_bytes = int(lib.mk_partial_workspace_bytes(aid, n, levels))
     ws = workspace(ws_bytes)
     st.workspace_bytes = ws_bytes
-    ev_b, ev_a = torch.cuda.Event(), [torch.cuda.Event() for _ in range(panels)]
-    ev_c = [torch.cuda.Event() for _ in range(panels)]
-    cp.wait_stream(comp)  # buffers were allocated on the compute stream
-    with torch.cuda.stream(cp):
-        for r in range(panels):
-            dA[r * pm:(r + 1) * pm].copy_(ha[r * pm:(r + 1) * pm], non_blocking=True)
-            ev_a[r].record(cp)
-            if r == 0:
-                dB.copy_(hb, non_blocking=True)
-                ev_b.record(cp)
+    rc = lib.mk_strassen_host(aid, ctypes.c_void_p(a.arr.ctypes.data), a.arr.strides[0] // 8,
+                              ctypes.c_void_p(b.arr.ctypes.data), b.arr.strides[0] // 8,
+                              ctypes.c_void_p(c.arr.ctypes.data), c.arr.strides[0] // 8, n, levels, _vp(dA), _vp(dB),
+                              _vp(dC), ld, _vp(ws), ws_bytes, _stream(), ctypes.c_void_p(_copy_stream.cuda_stream))
+    _lib.check(rc, f"mk_strassen_host({algo})")
     st.h2d_bytes += 2 * n * n * 8
-    comp.wait_event(ev_b)
-    for r in range(panels):
-        comp.wait_event(ev_a[r])
-        rows = slice(r * pm, (r + 1) * pm)
-        rc = lib.mk_multiply_rect(aid, _vp(dA[rows]), n, _vp(dB), n, _vp(dC[rows]), n, pm, n, n, levels, _vp(ws),
-                                  ws_bytes, _stream())
-        _lib.check(rc, f"mk_multiply_rect({algo}) panel {r}")
-        ev_c[r].record(comp)
-        cp.wait_event(ev_c[r])
-        with torch.cuda.stream(cp):
-            hc[rows].copy_(dC[rows], non_blocking=True)
     st.d2h_bytes += n * n * 8
-    for t in (dA, dB, dC, ws):
-        t.record_stream(cp)
-    cp.synchronize()
 
 
 def device_square(algo: str, a: MatrixView, b: MatrixView, c: MatrixView, levels: int, dtype,
@@ -350,9 +313,8 @@ def device_square(algo: str, a: MatrixView, b: MatrixView, c: MatrixView, levels
     n = a.rows
     if _is_int(dtype):
         exactness_guard(a, b, n, levels)
-    panels = 0 if clobber_inputs else _pipeline_panels(a, b, c, levels, algo, dtype)
-    if panels:
-        _pipelined_host_product(algo, a, b, c, levels, panels, st)
+    if not clobber_inputs and _overlap_applies(a, b, c, levels, algo, dtype):
+        _overlapped_host_product(algo, a, b, c, levels, st)
         return
     A = stage_in(a, copy=clobber_inputs and a.on_device and not _zero_copy_ok(a.arr), stats=st)
     B = stage_in(b, copy=clobber_inputs and b.on_device and not _zero_copy_ok(b.arr), stats=st)

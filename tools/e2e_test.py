@@ -13,7 +13,7 @@ pk.winograd_block_mul(pk.Matrix(ha.cuda()), pk.Matrix(hb.cuda()), dC, pol)
 want = dC.arr.cpu()
 for mode in ("1", "0"):
     os.environ["MK_PIPELINE"] = mode
-    for panels in (["4", "8"] if mode == "1" else ["-"]):
+    for panels in (["-"]):
         os.environ["MK_PIPELINE_PANELS"] = panels if panels != "-" else "4"
         pk.winograd_block_mul(A, B, C, pol); torch.cuda.synchronize()
         t = []
