@@ -82,8 +82,9 @@ int mk_dgemm(const double* A, int64_t lda, const double* B, int64_t ldb, double*
 /* Levels the engine runs for an order-n problem under the reference's base policy
  * (BasePolicy kernels.py:26-57): kind 0 = "scalar", 1 = "unrolled" (param = order),
  * 2 = "naive-cutoff" (param = threshold). naive-cutoff is honoured exactly
- * (leaf when n <= threshold, kernels.py:276); scalar/unrolled recursion below the
- * engine's minimum leaf order is clamped (results identical for integer data). */
+ * (leaf when n <= threshold, kernels.py:276) down to the engine's limits: leaf order >= 32
+ * and at most 5 levels (7^5 leaves); deeper recursion (scalar / unrolled policies, tiny
+ * thresholds) is clamped -- results identical for integer data, within tolerance otherwise. */
 int mk_levels_for_policy(int64_t n, int kind, int64_t param, int algo, int* levels_out);
 
 /* Device workspace bytes mk_strassen needs for (algo, n, levels). 0 for the fully

@@ -1150,6 +1150,10 @@ int mk_levels_for_policy(int64_t n, int kind, int64_t param, int algo, int* leve
   // scalar/unrolled micro-kernels, kernels.py:279-287) is clamped: results are identical for
   // integer data and within tolerance otherwise; the modeled counts stay the policy's.
   while (L > 0 && (n >> L) < MK_MIN_LEAF) --L;
+  // ... and at MK_MAX_LEVELS (7^5 = 16807 leaves, the depth BASELINE cfg5's cutoff 512 needs):
+  // deeper recursions only multiply HBM-bound block additions and shrink leaves below a
+  // tensor-core tile; the modeled counters still describe the policy's full recursion.
+  if (L > MK_MAX_LEVELS) L = MK_MAX_LEVELS;
   // the paper's storage maps need at least one literal level to be observable
   if ((algo == MK_ALGO_IN_PLACE || algo == MK_ALGO_TWO_TEMP) && L == 0 && n >= 4 &&
       !(kind != 0 && n <= param))

@@ -17,7 +17,8 @@
 // CTA = warpgroup 0 (TMA producer / pre-add combiner) + 2 or 4 DMMA consumer warpgroups
 #define MK_TILE_BYTES (MK_BM * MK_BK * 8)  // 16 KiB: one operand term tile per stage
 #define MK_SMEM_BUDGET (224 * 1024)
-#define MK_MIN_LEAF 32  // smallest leaf order the level policy recurses to (scalar/unrolled clamp)
+#define MK_MIN_LEAF 32    // smallest leaf order the level policy recurses to
+#define MK_MAX_LEVELS 5   // deepest recursion the level policy plans (7^5 leaves)
 
 struct MkTerm {
   int32_t row, col;  // offset of the term block inside the operand base matrix

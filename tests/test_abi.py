@@ -61,6 +61,9 @@ def test_levels_follow_reference_recursion(lib):
     assert levels(lib, 256, 0, 1, "strassen") == 3
     assert levels(lib, 16, 0, 1, "strassen") == 0
     assert levels(lib, 64, 1, 8, "winograd-block") == 1
+    # at most 5 levels whatever the policy asks for
+    assert levels(lib, 16384, 0, 1, "strassen") == 5
+    assert levels(lib, 16384, 2, 32, "winograd-block") == 5
     # the storage maps of the memory-lean schedules stay observable on small orders
     assert levels(lib, 16, 0, 1, "in-place") == 1
     assert levels(lib, 2, 0, 1, "in-place") == 0
