@@ -100,8 +100,21 @@ def _zero_copy_ok(t) -> bool:
             and t.data_ptr() % 16 == 0 and t.stride(0) >= t.shape[1])
 
 
+_SUPPORTED_KINDS = ("f", "i", "u", "b")
+
+
+def check_dtype(*views) -> None:
+    """The engine computes in FP64: real floating point and integer (exactness-guarded) operands
+    only. Complex or object data raise TypeError (no silent truncation, no CPU fallback)."""
+    for v in views:
+        kind = np.dtype(v.dtype).kind
+        if kind not in _SUPPORTED_KINDS:
+            raise TypeError(f"unsupported operand dtype {v.dtype} for the FP64 engine (real or integer data only)")
+
+
 def stage_in(view: MatrixView, *, copy: bool = False, stats: EngineStats | None = None) -> Operand:
     """Resolve a (host or device) view to an FP64 device operand."""
+    check_dtype(view)
     rows, cols = view.rows, view.cols
     if view.on_device:
         t = view.arr
@@ -227,6 +240,7 @@ def workspace(nbytes: int):
 def device_gemm(a: MatrixView, b: MatrixView, c: MatrixView, dtype) -> None:
     """C = A B on the DMMA kernel (mk_dgemm); replaces _naive_arrays kernels.py:258-266."""
     lib = require_engine()
+    check_dtype(a, b, c)
     st = _new_stats(algo="naive")
     if _is_int(dtype):
         exactness_guard(a, b, a.cols, 0)
@@ -309,6 +323,7 @@ def device_square(algo: str, a: MatrixView, b: MatrixView, c: MatrixView, levels
     views, so host callers observe the same "inputs destroyed" contract as the reference.
     """
     lib = require_engine()
+    check_dtype(a, b, c)
     st = _new_stats(algo=algo, levels=levels)
     n = a.rows
     if _is_int(dtype):
@@ -352,6 +367,7 @@ def _write_back(view: MatrixView, t) -> None:
 def device_rect(algo: str, a: MatrixView, b: MatrixView, c: MatrixView, levels: int, dtype) -> None:
     """Rectangular product with even-quadrant padding (mk_multiply_rect)."""
     lib = require_engine()
+    check_dtype(a, b, c)
     st = _new_stats(algo=algo, levels=levels)
     m, k, n = a.rows, a.cols, b.cols
     if _is_int(dtype):

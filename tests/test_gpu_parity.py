@@ -309,6 +309,14 @@ def test_int64_exactness_guard_and_dtypes(rng):
     big = pk.Matrix(np.full((64, 64), 2 ** 40, dtype=np.int64))
     with pytest.raises(pk.ExactnessError):
         pk.winograd_block_mul(big, big.copy(), pk.Matrix.zeros(64, 64, np.int64), pk.BasePolicy.naive_cutoff(16))
+    cplx = pk.Matrix(np.ones((8, 8), dtype=np.complex128))
+    with pytest.raises(TypeError):
+        pk.naive_mul(cplx, cplx.copy(), pk.Matrix(np.zeros((8, 8), dtype=np.complex128)))
+    # bool and small integer dtypes follow numpy's result type
+    bb = pk.Matrix(np.eye(8, dtype=np.int16))
+    c16 = pk.Matrix.zeros(8, 8, np.int16)
+    pk.strassen_mul(bb, bb.copy(), c16)
+    assert c16.arr.dtype == np.int16 and np.array_equal(c16.arr, np.eye(8, dtype=np.int16))
     a32 = rng.uniform(-1, 1, (64, 64)).astype(np.float32)
     c = pk.Matrix.zeros(64, 64, np.float32)
     pk.strassen_mul(pk.Matrix(a32), pk.Matrix(a32.copy()), c, pk.BasePolicy.naive_cutoff(16))
