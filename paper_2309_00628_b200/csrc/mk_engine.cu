@@ -627,23 +627,96 @@ struct Engine {
   // Overlapped host run (mk_strassen_host): the top-level products run in `order`; before each
   // one the compute stream waits for the input quadrants it reads (in_ev: A11..A22, B11..B22),
   // after it every C quadrant whose last contributor it was is signalled (out_ev: C11..C22).
-  int fused_overlapped(const std::vector<int>& order, cudaEvent_t* in_ev, cudaEvent_t* out_ev, int64_t n) {
+  // With L >= 2 the first and last products are split one level further (their children run in
+  // `order` too): sub_in (8 events, may be null) then gates each child of the first product on
+  // the sub-blocks of its single-term operand quadrants only, and sub_out[4q+s] signals sub-block
+  // s of each C quadrant q the last product finishes -- the pipeline's head waits for 1/4 of a
+  // quadrant per operand instead of a whole one, its tail downloads 1/4 of a quadrant.
+  int fused_overlapped(const std::vector<int>& order, cudaEvent_t* in_ev, cudaEvent_t* out_ev, int64_t n,
+                       cudaEvent_t* sub_in, cudaEvent_t* sub_out, bool* tail_split) {
     int last[4] = {-1, -1, -1, -1};
-    for (int i = 0; i < (int)order.size(); ++i)
+    const int np = (int)order.size();
+    for (int i = 0; i < np; ++i)
       for (int q = 0; q < 4; ++q)
         if (co->c[q][order[i]]) last[q] = i;
-    for (int i = 0; i < (int)order.size(); ++i) {
+    const int64_t h = n / 2;
+    const Lin A0{Blk{BASE_A, 0, 0, 1.0}}, B0{Blk{BASE_B, 0, 0, 1.0}}, C0{Blk{BASE_C, 0, 0, 1.0}};
+    for (int q = 0; q < 4; ++q) tail_split[q] = false;
+    for (int i = 0; i < np; ++i) {
       const int p = order[i];
+      const bool head = i == 0 && sub_in != nullptr && L >= 2;
+      const bool tail = i == np - 1 && sub_out != nullptr && L >= 2 && split_fits(p);
       for (int q = 0; q < 4; ++q) {
+        if (head) break;  // the first product waits per child on sub-blocks (below)
         if (co->a[p][q]) MK_CUDA_TRY(cudaStreamWaitEvent(st, in_ev[q], 0));
         if (co->b[p][q]) MK_CUDA_TRY(cudaStreamWaitEvent(st, in_ev[4 + q], 0));
       }
-      MK_TRY(fused_child(L, p, Lin{Blk{BASE_A, 0, 0, 1.0}}, Lin{Blk{BASE_B, 0, 0, 1.0}},
-                         Lin{Blk{BASE_C, 0, 0, 1.0}}, n, n, n, 0));
+      if (!head && !tail) {
+        MK_TRY(fused_child(L, p, A0, B0, C0, n, n, n, 0));
+      } else {
+        // the top-level part of fused_child, then the children one by one
+        Lin Xp = kron(A0, co->a[p], h, h), Yp = kron(B0, co->b[p], h, h), Dp = kron_dest(C0, p, h, h);
+        const size_t mark = ws_used;
+        const int nb_mark = nbases;
+        for (int side = 0; side < 2; ++side) {
+          Lin& T = side == 0 ? Xp : Yp;
+          if (T.size() == 1) continue;
+          int sb;
+          MK_TRY(alloc_slot(h, h, &sb));
+          MK_TRY(combine(Blk{sb, 0, 0, 1.0}, T, h, h));
+          T = Lin{Blk{sb, 0, 0, 1.0}};
+        }
+        int child_last[4] = {-1, -1, -1, -1};
+        for (int j = 0; j < np; ++j)
+          for (int s = 0; s < 4; ++s)
+            if (co->c[s][order[j]]) child_last[s] = j;
+        for (int j = 0; j < np; ++j) {
+          const int pc = order[j];
+          if (head)
+            for (int s = 0; s < 4; ++s) {
+              if (co->a[pc][s]) MK_CUDA_TRY(cudaStreamWaitEvent(st, sub_in[s], 0));
+              if (co->b[pc][s]) MK_CUDA_TRY(cudaStreamWaitEvent(st, sub_in[4 + s], 0));
+            }
+          MK_TRY(fused_child(L - 1, pc, Xp, Yp, Dp, h, h, h, 1));
+          if (tail)
+            for (int q = 0; q < 4; ++q)
+              if (last[q] == i)
+                for (int s = 0; s < 4; ++s)
+                  if (child_last[s] == j) MK_CUDA_TRY(cudaEventRecord(sub_out[4 * q + s], st));
+        }
+        ws_used = mark;
+        while (nbases > nb_mark) {
+          --nbases;
+          written.pop_back();
+          cell_rows.pop_back();
+          cell_cols.pop_back();
+        }
+        if (tail)
+          for (int q = 0; q < 4; ++q)
+            if (last[q] == i) tail_split[q] = true;
+      }
       for (int q = 0; q < 4; ++q)
         if (last[q] == i) MK_CUDA_TRY(cudaEventRecord(out_ev[q], st));
     }
     return MK_OK;
+  }
+  // A top-level product can run child by child when its destination fan-out fits the epilogue
+  // without a materialised product (fused_child's own test).
+  bool split_fits(int p) const {
+    int64_t worst = 0;
+    for (int q = 0; q < 4; ++q) worst += co->c[q][p] != 0;
+    for (int i = 1; i < L; ++i) worst *= 4;
+    return worst <= MK_MAX_DESTS;
+  }
+  // Whether the first product qualifies for sub-block uploads: single-term operands and a
+  // fan-out that fits.
+  bool head_split_ok(int p) const {
+    int ta = 0, tb = 0;
+    for (int q = 0; q < 4; ++q) {
+      ta += co->a[p][q] != 0;
+      tb += co->b[p][q] != 0;
+    }
+    return L >= 2 && ta == 1 && tb == 1 && split_fits(p);
   }
 
   // ---- literal schedule plan (two-temp / in-place) ----
@@ -1276,48 +1349,96 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
       up = it->second.second;
     }
   }
-  const int64_t h = n / 2;
-  cudaEvent_t ev[13];
-  for (int i = 0; i < 13; ++i) MK_CUDA_TRY(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
-  cudaEvent_t *in_ev = ev, *out_ev = ev + 8, start = ev[12];
+  const int64_t h = n / 2, hh = h / 2;
+  // events: 8 quadrant uploads, 4 quadrant completions, start, 8 sub-block uploads, 16 sub-block completions
+  constexpr int kEv = 37;
+  cudaEvent_t ev[kEv];
+  for (int i = 0; i < kEv; ++i) MK_CUDA_TRY(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+  cudaEvent_t *in_ev = ev, *out_ev = ev + 8, start = ev[12], *sub_in = ev + 13, *sub_out = ev + 21;
   int rc = MK_OK;
   auto quad_ptr = [&](double* base, int64_t ld, int q) { return base + ((q >> 1) * h) * ld + (q & 1) * h; };
+  auto sub_ptr = [&](double* base, int64_t ld, int q, int s) {
+    return quad_ptr(base, ld, q) + ((s >> 1) * hh) * ld + (s & 1) * hh;
+  };
+  auto copy = [&](double* dst, int64_t dld, const double* src, int64_t sld, int64_t r, cudaMemcpyKind kind,
+                  cudaEvent_t done, const char* what) {
+    if (rc != MK_OK) return;
+    cudaError_t ce = cudaMemcpy2DAsync(dst, dld * 8, src, sld * 8, r * 8, r, kind, cp);
+    if (ce == cudaSuccess && done) ce = cudaEventRecord(done, cp);
+    if (ce != cudaSuccess) rc = fail(MK_ERR_CUDA, std::string(what) + cudaGetErrorString(ce));
+  };
   // the copy stream starts after prior work on the compute stream (device buffers may be reused)
   if (cudaEventRecord(start, st) != cudaSuccess || cudaStreamWaitEvent(cp, start, 0) != cudaSuccess)
     rc = fail(MK_ERR_CUDA, "stream ordering failed");
-  for (size_t i = 0; rc == MK_OK && i < up.size(); ++i) {
+  const bool head = (h % 2 == 0) && e.head_split_ok(order[0]);
+  int qa = -1, qb = -1;
+  if (head) {
+    for (int q = 0; q < 4; ++q) {
+      if (e.co->a[order[0]][q]) qa = q;
+      if (e.co->b[order[0]][q]) qb = q;
+    }
+    // sub-blocks of the first product's two operand quadrants, in the children's order of first use
+    for (int u : up) {
+      const bool isA = u < 4;
+      const int s = u & 3, q = isA ? qa : qb;
+      if (isA)
+        copy(sub_ptr(dA, ldd, q, s), ldd, sub_ptr(const_cast<double*>(hA), lda, q, s), lda, hh,
+             cudaMemcpyHostToDevice, sub_in[s], "upload: ");
+      else
+        copy(sub_ptr(dB, ldd, q, s), ldd, sub_ptr(const_cast<double*>(hB), ldb, q, s), ldb, hh,
+             cudaMemcpyHostToDevice, sub_in[4 + s], "upload: ");
+    }
+    if (rc == MK_OK && (cudaEventRecord(in_ev[qa], cp) != cudaSuccess || cudaEventRecord(in_ev[4 + qb], cp) != cudaSuccess))
+      rc = fail(MK_ERR_CUDA, "event record failed");
+  }
+  for (size_t i = 0; i < up.size(); ++i) {
     const int q = up[i];
     const bool isA = q < 4;
-    const double* src = isA ? quad_ptr(const_cast<double*>(hA), lda, q) : quad_ptr(const_cast<double*>(hB), ldb, q - 4);
-    double* dst = isA ? quad_ptr(dA, ldd, q) : quad_ptr(dB, ldd, q - 4);
-    cudaError_t ce = cudaMemcpy2DAsync(dst, ldd * 8, src, (isA ? lda : ldb) * 8, h * 8, h, cudaMemcpyHostToDevice, cp);
-    if (ce == cudaSuccess) ce = cudaEventRecord(in_ev[q], cp);
-    if (ce != cudaSuccess) rc = fail(MK_ERR_CUDA, std::string("upload: ") + cudaGetErrorString(ce));
+    if ((isA && q == qa) || (!isA && q - 4 == qb)) continue;  // already uploaded by sub-blocks
+    if (isA)
+      copy(quad_ptr(dA, ldd, q), ldd, quad_ptr(const_cast<double*>(hA), lda, q), lda, h, cudaMemcpyHostToDevice,
+           in_ev[q], "upload: ");
+    else
+      copy(quad_ptr(dB, ldd, q - 4), ldd, quad_ptr(const_cast<double*>(hB), ldb, q - 4), ldb, h,
+           cudaMemcpyHostToDevice, in_ev[q], "upload: ");
   }
-  if (rc == MK_OK) rc = e.fused_overlapped(order, in_ev, out_ev, n);
+  bool tail_split[4] = {false, false, false, false};
+  if (rc == MK_OK)
+    rc = e.fused_overlapped(order, in_ev, out_ev, n, head ? sub_in : nullptr, (h % 2 == 0) ? sub_out : nullptr,
+                            tail_split);
   if (rc == MK_OK) {
-    // downloads in the order the quadrants complete
+    // downloads in the order the quadrants (or, for the last product's, their sub-blocks) complete
     int last[4] = {-1, -1, -1, -1};
     for (int i = 0; i < (int)order.size(); ++i)
       for (int q = 0; q < 4; ++q)
         if (e.co->c[q][order[i]]) last[q] = i;
     int qs[4] = {0, 1, 2, 3};
     std::sort(qs, qs + 4, [&](int x, int y) { return last[x] < last[y]; });
+    int child_last[4] = {-1, -1, -1, -1};
+    for (int j = 0; j < (int)order.size(); ++j)
+      for (int s = 0; s < 4; ++s)
+        if (e.co->c[s][order[j]]) child_last[s] = j;
+    int ss[4] = {0, 1, 2, 3};
+    std::sort(ss, ss + 4, [&](int x, int y) { return child_last[x] < child_last[y]; });
     for (int q : qs) {
-      cudaError_t ce = cudaStreamWaitEvent(cp, out_ev[q], 0);
-      if (ce == cudaSuccess)
-        ce = cudaMemcpy2DAsync(quad_ptr(hC, ldc, q), ldc * 8, quad_ptr(dC, ldd, q), ldd * 8, h * 8, h,
-                               cudaMemcpyDeviceToHost, cp);
-      if (ce != cudaSuccess) {
-        rc = fail(MK_ERR_CUDA, std::string("download: ") + cudaGetErrorString(ce));
-        break;
+      if (rc != MK_OK) break;
+      if (!tail_split[q]) {
+        if (cudaStreamWaitEvent(cp, out_ev[q], 0) != cudaSuccess) rc = fail(MK_ERR_CUDA, "stream wait failed");
+        copy(quad_ptr(hC, ldc, q), ldc, quad_ptr(dC, ldd, q), ldd, h, cudaMemcpyDeviceToHost, nullptr, "download: ");
+        continue;
+      }
+      for (int s : ss) {
+        if (rc == MK_OK && cudaStreamWaitEvent(cp, sub_out[4 * q + s], 0) != cudaSuccess)
+          rc = fail(MK_ERR_CUDA, "stream wait failed");
+        copy(sub_ptr(hC, ldc, q, s), ldc, sub_ptr(dC, ldd, q, s), ldd, hh, cudaMemcpyDeviceToHost, nullptr,
+             "download: ");
       }
     }
   }
   cudaError_t se = cudaStreamSynchronize(cp);
   if (rc == MK_OK && se == cudaSuccess) se = cudaStreamSynchronize(st);
   if (rc == MK_OK && se != cudaSuccess) rc = fail(MK_ERR_CUDA, std::string("sync: ") + cudaGetErrorString(se));
-  for (int i = 0; i < 13; ++i) cudaEventDestroy(ev[i]);
+  for (int i = 0; i < kEv; ++i) cudaEventDestroy(ev[i]);
   return rc;
 }
 

@@ -305,6 +305,7 @@ def _overlapped_host_product(algo: str, a: MatrixView, b: MatrixView, c: MatrixV
     ws_bytes = int(lib.mk_partial_workspace_bytes(aid, n, levels))
     ws = workspace(ws_bytes)
     st.workspace_bytes = ws_bytes
+    st.path = "overlapped-host"
     rc = lib.mk_strassen_host(aid, ctypes.c_void_p(a.arr.ctypes.data), a.arr.strides[0] // 8,
                               ctypes.c_void_p(b.arr.ctypes.data), b.arr.strides[0] // 8,
                               ctypes.c_void_p(c.arr.ctypes.data), c.arr.strides[0] // 8, n, levels, _vp(dA), _vp(dB),

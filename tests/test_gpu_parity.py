@@ -418,11 +418,29 @@ def test_pipelined_host_path_matches_device_path():
     pol = pk.BasePolicy.naive_cutoff(1024)
     pk.winograd_block_mul(pk.Matrix(ha.numpy()), pk.Matrix(hb.numpy()), pk.Matrix(hc.numpy()), pol)
     st = pk.last_stats()
-    assert st.h2d_bytes == 2 * n * n * 8 and st.d2h_bytes == n * n * 8
+    assert st.h2d_bytes == 2 * n * n * 8 and st.d2h_bytes == n * n * 8 and st.path == "overlapped-host"
     dc = pk.Matrix.zeros(n, n, device="cuda")
     pk.winograd_block_mul(pk.Matrix(ha.cuda()), pk.Matrix(hb.cuda()), dc, pol)
     err = float((hc - dc.arr.cpu()).abs().max())
     assert err <= tol(n, ha.numpy(), hb.numpy()) and err < 1e-11, err
+
+
+@pytest.mark.parametrize("algo", ["strassen", "winograd-block", "winograd-knuth", "winograd-knuth-8call"])
+@pytest.mark.parametrize("cut", [512, 256])
+def test_pipelined_host_path_exact(algo, cut):
+    """Overlapped host path (quadrant uploads, first/last products split into sub-block
+    transfers) on integer-valued pinned operands: bit-exact, and the result lands in place."""
+    import torch
+
+    n = 2048
+    r = np.random.default_rng(9)
+    a = r.integers(-8, 9, (n, n)).astype(np.float64)
+    b = r.integers(-8, 9, (n, n)).astype(np.float64)
+    ha, hb = torch.from_numpy(a).pin_memory(), torch.from_numpy(b).pin_memory()
+    hc = torch.full((n, n), float("nan"), dtype=torch.float64).pin_memory()
+    CALL[algo](pk.Matrix(ha.numpy()), pk.Matrix(hb.numpy()), pk.Matrix(hc.numpy()), pk.BasePolicy.naive_cutoff(cut))
+    assert pk.last_stats().h2d_bytes == 2 * n * n * 8 and pk.last_stats().path == "overlapped-host"
+    assert np.array_equal(hc.numpy(), a @ b)
 
 
 @pytest.mark.parametrize("algo", ["strassen", "winograd-block", "winograd-knuth", "winograd-knuth-8call",
