@@ -132,4 +132,9 @@ __device__ __forceinline__ void stg256(double* p, double a, double b, double c, 
                : "memory");
 }
 
+// Fire-and-forget FP64 add at L2 (REDG.ADD.F64): the accumulate half of the direct epilogue.
+__device__ __forceinline__ void red_add(double* p, double v) {
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
 }  // namespace mk

@@ -94,6 +94,25 @@ struct Regs<4, true> {  // 61440 >= 128 x 40 + 512 x 104
   static constexpr int kProducer = 40, kConsumer = 104;
 };
 
+#ifdef MK_TRACE
+// Per-CTA timeline (trace builds only, tools/tile_trace.py): smid, entry, first stage ready,
+// main loop done, epilogue done (%globaltimer ns), stamped by consumer warp 0.
+__device__ unsigned long long mk_trace_buf[5 * 65536];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define MK_STAMP(slot)                                                                  \
+  do {                                                                                  \
+    if (warp == 4 && lane == 0 && blockIdx.x < 65536) mk_trace_buf[5 * blockIdx.x + (slot)] = gtimer(); \
+  } while (0)
+#else
+#define MK_STAMP(slot) \
+  do {                 \
+  } while (0)
+#endif
+
 // CA / CB: the A / B operand has more than one term and goes through the combiner.
 template <bool CA, bool CB, int MT>
 __global__ void __launch_bounds__(Layout<MT>::kThreads, 1)
@@ -119,6 +138,14 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const __grid
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+#ifdef MK_TRACE
+  if (warp == 4 && lane == 0 && blockIdx.x < 65536) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    mk_trace_buf[5 * blockIdx.x] = smid;
+    mk_trace_buf[5 * blockIdx.x + 1] = gtimer();
+  }
+#endif
   const int na = prod.na, nb = prod.nb;
   const int S = args.stages;    // operand stages
   const int D = args.raw_sets;  // raw term sets in flight (0 when nothing is combined)
@@ -332,6 +359,7 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const __grid
   for (int kt = 0; kt < KT; ++kt) {
     const int s = kt % S;
     mbar_wait(&full_bar[s], (kt / S) & 1);
+    if (kt == 0) MK_STAMP(2);
     const uint8_t* sA = smem_gen + (size_t)s * kOpStageBytes;
     const uint8_t* sB = sA + MK_TILE_BYTES;
     if (kt == KT - 1 && krem_last < MK_BK)
@@ -363,6 +391,7 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const __grid
     if (cw == 0) tmem_dealloc(tmem_base_sh, 256);
   }
 
+  MK_STAMP(3);
   // ============================ multi-destination epilogue ============================
   // Lane owns, per (i, j): row m0 + warp_m*8*MT + 8i + prow, cols n0 + warp_n*32 + 16j + 4q .. +3
   // holding {acc[i][2j][0], acc[i][2j+1][0], acc[i][2j][1], acc[i][2j+1][1]}.
@@ -430,6 +459,7 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const __grid
     }
     if (lane == 0) bulk_wait_read_all();  // smem must stay valid until the TMA unit has read it
     __syncwarp();
+    MK_STAMP(4);
     return;
   }
   for (int d = 0; d < nd; ++d) {
@@ -449,10 +479,11 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const __grid
         if (args.vec_ok) {
           if (col >= args.N) continue;
           double* p = crow + col;
-          if (dst.accumulate) {
-            double c0, c1, c2, c3;
-            ldg256(p, c0, c1, c2, c3);
-            stg256(p, fma(sg, v0, c0), fma(sg, v1, c1), fma(sg, v2, c2), fma(sg, v3, c3));
+          if (dst.accumulate) {  // one contribution per element per launch: deterministic
+            red_add(p, sg * v0);
+            red_add(p + 1, sg * v1);
+            red_add(p + 2, sg * v2);
+            red_add(p + 3, sg * v3);
           } else {
             stg256(p, sg * v0, sg * v1, sg * v2, sg * v3);
           }
@@ -462,7 +493,10 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const __grid
           for (int u = 0; u < 4; ++u) {
             if (col + u < args.N) {
               double* p = crow + col + u;
-              *p = dst.accumulate ? fma(sg, v[u], *p) : sg * v[u];
+              if (dst.accumulate)
+                red_add(p, sg * v[u]);
+              else
+                *p = sg * v[u];
             }
           }
         }
@@ -470,6 +504,12 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const __grid
     }
   }
 }
+
+#ifdef MK_TRACE
+extern "C" __attribute__((visibility("default"))) int mk_trace_read(unsigned long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, mk_trace_buf, sizeof(unsigned long long) * 5 * n);
+}
+#endif
 
 // ------------------------------------------------------------------------------------
 // Host-side launcher (called by the planner).
