@@ -347,7 +347,7 @@ def main():
     roofline = {
         "bound": "tensor", "achieved": round(achieved, 3) if achieved else None, "peak": round(peak_tflops, 3),
         "unit": "TFLOP/s", "frac": round(achieved / peak_tflops, 4) if achieved else None, "traffic": traffic,
-        "kernel": "mk::fused_product_kernel (DMMA leaf product, K1/K3)",
+        "kernel": "mk::persistent_product_kernel (DMMA leaf product, K1/K3)",
         "launches_timed": kcnt.value // max(args.steps, 1) if kcnt.value else 0,
         "peak_source": "measured in this run: DMMA-only microbenchmark on all SMs (mk_fp64_peak); "
                        "MEASURED_PEAKS.json has no FP64 figure",

@@ -505,6 +505,338 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const __grid
   }
 }
 
+
+// =====================================================================================
+// Persistent plain product (single-term operands on both sides -- every leaf of the
+// materialised plans and mk_dgemm). One CTA per SM walks the launch's tiles
+// t = blockIdx.x + i*gridDim.x (product-major over a batch, rasterised as above). The TMA
+// thread streams k-stages across tile boundaries, so the next tile's first stages land while
+// the consumers run the current tile's epilogue; the epilogue stages each warp's fragment one
+// 16-column box at a time in a dedicated area (not the ring), and the TMA unit's reads of the
+// last box overlap the next tile's main loop. Removes the per-tile pipeline fill, CTA launch
+// gap and epilogue drain (~5 us per tile measured by tools/tile_trace.py).
+// =====================================================================================
+template <int MT>
+__global__ void __launch_bounds__(Layout<MT>::kThreads, 1)
+persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const __grid_constant__ CUtensorMap tmB_param,
+                          const __grid_constant__ CUtensorMap tmC_param, const MkGemmArgs args,
+                          const __grid_constant__ MkProduct prod_param) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[kMaxStages];
+  __shared__ __align__(8) uint64_t empty_bar[kMaxStages];
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int S = args.stages;
+  const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  uint8_t* smem_gen = smem_raw + (smem_base - smem_u32(smem_raw));
+  uint8_t* box_area = smem_gen + (size_t)S * kOpStageBytes;  // epilogue boxes, one per consumer warp
+  const int tiles_per = args.tiles_m * args.tiles_n;
+  const int total = tiles_per * (args.batch ? args.nprod : 1);
+  const int KT = (args.K + MK_BK - 1) / MK_BK;
+
+  auto tile_of = [&](int t, int& pi, int& m0, int& n0) {
+    pi = t / tiles_per;
+    const int bid = t - pi * tiles_per;
+    const int per_group = args.group_m * args.tiles_n;
+    const int g = bid / per_group;
+    const int first_m = g * args.group_m;
+    const int gsz = min(args.tiles_m - first_m, args.group_m);
+    const int r = bid - g * per_group;
+    m0 = (first_m + r % gsz) * MK_BM;
+    n0 = (r / gsz) * MK_BN;
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], Layout<MT>::kConsumerWarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp < 4) {
+    // ============================ TMA producer (one thread) ============================
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(Regs<MT, false>::kProducer));
+    if (threadIdx.x != 0) return;
+    int s = 0;            // ring slot of the next stage (carried across tiles)
+    uint32_t eph = 0;     // parity of the empty-barrier phase to wait for (first lap: no wait)
+    bool first_lap = true;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      int pi, m0, n0;
+      tile_of(t, pi, m0, n0);
+      const MkBatchEntry* ent = args.batch ? args.batch + pi : nullptr;
+      const MkProduct& prod = ent ? ent->prod : prod_param;
+      const CUtensorMap* tmA = ent ? &ent->tmA : &tmA_param;
+      const CUtensorMap* tmB = ent ? &ent->tmB : &tmB_param;
+      const int ar = m0 + prod.a[0].row, ac = prod.a[0].col;
+      const int br = prod.b[0].row, bc = n0 + prod.b[0].col;
+      for (int k = 0; k < KT; ++k) {
+        if (!first_lap) mbar_wait(&empty_bar[s], eph);
+        uint8_t* opA = smem_gen + (size_t)s * kOpStageBytes;
+        uint8_t* opB = opA + MK_TILE_BYTES;
+        const int k0 = k * MK_BK;
+        mbar_arrive_expect_tx(&full_bar[s], 2 * MK_TILE_BYTES);
+        tma_load_2d(opA, tmA, k0 + ac, ar, &full_bar[s]);
+#pragma unroll
+        for (int bj = 0; bj < 8; ++bj) tma_load_2d(opB + bj * 2048, tmB, bc + bj * 16, k0 + br, &full_bar[s]);
+        if (++s == S) {
+          s = 0;
+          if (first_lap)
+            first_lap = false;
+          else
+            eph ^= 1u;
+        }
+      }
+    }
+    return;
+  }
+
+  // ================================ DMMA consumers ================================
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(Regs<MT, false>::kConsumer));
+  const int cw = warp - 4;
+  const int warp_m = cw >> 2;
+  const int warp_n = cw & 3;
+  const int q = lane & 3, g = lane >> 2;
+  const int prow = (g >> 1) + 4 * (g & 1);
+  const uint32_t a_lane = (uint32_t)(warp_m * (8 * MT) + prow) * 128u;
+  const uint32_t a_chunk0 = (uint32_t)(((q + 0) ^ prow) << 4);
+  const uint32_t a_chunk1 = (uint32_t)(((q + 4) ^ prow) << 4);
+  const uint32_t b_lane = (uint32_t)(warp_n * 2) * 2048u;
+  uint32_t b_off[2][2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int k = 2 * q + 8 * t + e;
+      b_off[t][e] = b_lane + (uint32_t)k * 128u + (uint32_t)((g ^ ((2 * q + e) & 7)) << 4);
+    }
+
+  double acc[MT][4][2];
+  auto stage = [&](const uint8_t* sA, const uint8_t* sB, const int krem, auto tail_tag) {
+    constexpr bool TAIL = decltype(tail_tag)::value;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const uint32_t a_chunk = t ? a_chunk1 : a_chunk0;
+      double a0[MT], a1[MT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) lds128(a0[i], a1[i], sA + a_lane + i * 1024u + a_chunk);
+      if (TAIL) {
+        const int kk = 2 * q + 8 * t;
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+          a0[i] = kk < krem ? a0[i] : 0.0;
+          a1[i] = kk + 1 < krem ? a1[i] : 0.0;
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double b[4];
+        lds128(b[0], b[1], sB + b_off[t][e]);
+        lds128(b[2], b[3], sB + b_off[t][e] + 2048u);
+        if (TAIL) {
+          const bool live = 2 * q + 8 * t + e < krem;
+#pragma unroll
+          for (int f = 0; f < 4; ++f) b[f] = live ? b[f] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+          for (int f = 0; f < 4; ++f) dmma(acc[i][f][0], acc[i][f][1], e ? a1[i] : a0[i], b[f]);
+      }
+    }
+  };
+
+  // two-level accumulation (see fused_product_kernel); TMEM is allocated once per CTA
+  const int chunk = (args.chunk_stages > 0 && KT > args.chunk_stages) ? args.chunk_stages : 0;
+  constexpr int kWords = 16 * MT;
+  constexpr int kPieces = kWords / 16;
+  uint32_t taddr = 0;
+  if (chunk) {
+    if (cw == 0) tmem_alloc(&tmem_base_sh, 256);
+    tmem_fence_before();
+    named_bar_sync(3, 32 * Layout<MT>::kConsumerWarps);
+    tmem_fence_after();
+    taddr = tmem_base_sh + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((cw >> 2) * kWords);
+  }
+  bool master_live = false;
+  auto fold_to_tmem = [&]() {
+#pragma unroll
+    for (int pc = 0; pc < kPieces; pc += 2) {
+      uint32_t w[2][16];
+      if (master_live) {
+        tmem_ld16(taddr + pc * 16, w[0]);
+        tmem_ld16(taddr + pc * 16 + 16, w[1]);
+        tmem_wait_ld();
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = (pc + h) * 8 + u;
+          double& a = acc[e >> 3][(e >> 1) & 3][e & 1];
+          const double m = master_live ? __hiloint2double((int)w[h][2 * u + 1], (int)w[h][2 * u]) + a : a;
+          w[h][2 * u] = (uint32_t)__double2loint(m);
+          w[h][2 * u + 1] = (uint32_t)__double2hiint(m);
+          a = 0.0;
+        }
+      tmem_st16(taddr + pc * 16, w[0]);
+      tmem_st16(taddr + pc * 16 + 16, w[1]);
+    }
+    tmem_wait_st();
+    master_live = true;
+  };
+
+  constexpr int kBoxRows = 8 * MT;
+  uint8_t* box = box_area + (size_t)cw * (kBoxRows * 128);
+  const int c_first = (g & 1) ? 1 : 0;
+  bool reads_pending = false;  // TMA reads of this warp's box still in flight
+  const int krem_last = args.K - (KT - 1) * MK_BK;
+  int rs = 0;         // ring slot of the next stage (carried across tiles)
+  uint32_t fph = 0;   // parity of the full-barrier phase to wait for
+
+  for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    int pi, m0, n0;
+    tile_of(t, pi, m0, n0);
+    const MkBatchEntry* ent = args.batch ? args.batch + pi : nullptr;
+    const MkProduct& prod = ent ? ent->prod : prod_param;
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int f = 0; f < 4; ++f) acc[i][f][0] = acc[i][f][1] = 0.0;
+    master_live = false;
+    for (int kt = 0; kt < KT; ++kt) {
+      mbar_wait(&full_bar[rs], fph);
+      const uint8_t* sA = smem_gen + (size_t)rs * kOpStageBytes;
+      const uint8_t* sB = sA + MK_TILE_BYTES;
+      if (kt == KT - 1 && krem_last < MK_BK)
+        stage(sA, sB, krem_last, std::true_type{});
+      else
+        stage(sA, sB, MK_BK, std::false_type{});
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[rs]);
+      if (++rs == S) {
+        rs = 0;
+        fph ^= 1u;
+      }
+      if (chunk && (kt + 1) % chunk == 0 && kt + 1 < KT) fold_to_tmem();
+    }
+    if (chunk && master_live) {
+#pragma unroll
+      for (int pc = 0; pc < kPieces; ++pc) {
+        uint32_t w[16];
+        tmem_ld16(taddr + pc * 16, w);
+        tmem_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = pc * 8 + u;
+          double& a = acc[e >> 3][(e >> 1) & 3][e & 1];
+          a = __hiloint2double((int)w[2 * u + 1], (int)w[2 * u]) + a;
+        }
+      }
+    }
+
+    // ---- epilogue: every destination of the product, signs grouped into two passes ----
+    const double out_sign = prod.a[0].sign * prod.b[0].sign;
+    const int nd = prod.nd;
+    if (args.async_epi) {
+      const CUtensorMap* tmC = ent ? &ent->tmC : &tmC_param;
+      const int row0 = m0 + warp_m * kBoxRows;
+      const int col0 = n0 + warp_n * 32;
+      const bool slab_live = row0 < args.M && col0 < args.N;
+      for (int pass = 0; pass < 2; ++pass) {
+        const double want = pass == 0 ? 1.0 : -1.0;
+        bool any = false;
+        for (int d = 0; d < nd; ++d) any |= (prod.d[d].sign * out_sign) == want;
+        if (!any) continue;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          if (reads_pending) {  // the box's previous contents must have been read by the TMA unit
+            if (lane == 0) bulk_wait_read_all();
+            __syncwarp();
+          }
+#pragma unroll
+          for (int i = 0; i < MT; ++i) {
+            const int r = 8 * i + prow;
+            uint8_t* rowp = box + r * 128;
+            const double v0 = want * acc[i][2 * j][0], v1 = want * acc[i][2 * j + 1][0];
+            const double v2 = want * acc[i][2 * j][1], v3 = want * acc[i][2 * j + 1][1];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int c = 2 * q + (h ^ c_first);
+              double2 v = (c & 1) ? make_double2(v2, v3) : make_double2(v0, v1);
+              *reinterpret_cast<double2*>(rowp + ((c ^ prow) << 4)) = v;
+            }
+          }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0 && slab_live && col0 + 16 * j < args.N) {
+            for (int d = 0; d < nd; ++d) {
+              const MkDest dst = prod.d[d];
+              if ((dst.sign * out_sign) != want) continue;
+              const int cc = (int)dst.col + col0 + 16 * j, rr = (int)dst.row + row0;
+              if (dst.accumulate)
+                tma_reduce_add_2d(tmC, cc, rr, box);
+              else
+                tma_store_2d(tmC, cc, rr, box);
+            }
+            bulk_commit();
+          }
+          reads_pending = true;
+        }
+      }
+    } else {
+      double* const Cbase = ent ? ent->C : args.C;
+      const int64_t ldc = ent ? ent->ldc : args.ldc;
+      for (int d = 0; d < nd; ++d) {
+        const MkDest dst = prod.d[d];
+        const double sg = dst.sign * out_sign;
+        double* Cd = Cbase + dst.row * ldc + dst.col;
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+          const int row = m0 + warp_m * (8 * MT) + 8 * i + prow;
+          if (row >= args.M) continue;
+          double* crow = Cd + (int64_t)row * ldc;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int col = n0 + warp_n * 32 + 16 * j + 4 * q;
+            const double v[4] = {acc[i][2 * j][0], acc[i][2 * j + 1][0], acc[i][2 * j][1], acc[i][2 * j + 1][1]};
+            if (args.vec_ok) {
+              if (col >= args.N) continue;
+              double* p = crow + col;
+              if (dst.accumulate) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) red_add(p + u, sg * v[u]);
+              } else {
+                stg256(p, sg * v[0], sg * v[1], sg * v[2], sg * v[3]);
+              }
+            } else {
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (col + u < args.N) {
+                  if (dst.accumulate)
+                    red_add(crow + col + u, sg * v[u]);
+                  else
+                    crow[col + u] = sg * v[u];
+                }
+            }
+          }
+        }
+      }
+    }
+  }
+  if (lane == 0) bulk_wait_read_all();  // the boxes must stay valid until the TMA unit has read them
+  __syncwarp();
+  if (chunk) {
+    tmem_fence_before();
+    named_bar_sync(3, 32 * Layout<MT>::kConsumerWarps);
+    tmem_fence_after();
+    if (cw == 0) tmem_dealloc(tmem_base_sh, 256);
+  }
+}
+
 #ifdef MK_TRACE
 extern "C" __attribute__((visibility("default"))) int mk_trace_read(unsigned long long* out, int n) {
   return (int)cudaMemcpyFromSymbol(out, mk_trace_buf, sizeof(unsigned long long) * 5 * n);
@@ -537,11 +869,58 @@ int accumulate_chunk_stages() {
   return g_chunk;
 }
 
+// Persistent plain-product kernel (env MK_PERSISTENT=0 selects the one-CTA-per-tile kernel).
+static int g_persistent = -1;
+bool persistent_enabled() {
+  if (g_persistent < 0) {
+    const char* e = getenv("MK_PERSISTENT");
+    g_persistent = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_persistent == 1;
+}
+static int sm_count() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (cache[dev] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
+// One CTA per SM over `total` tiles; the ring keeps S = (budget - boxes) / stage stages.
+static cudaError_t launch_persistent(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
+                                     MkGemmArgs args, const MkProduct& prod, int total, cudaStream_t stream) {
+  constexpr size_t kBoxBytes = 64 * 1024;  // 8 warps x 64 rows or 16 warps x 32 rows, 128 B each
+  args.stages = (int)((MK_SMEM_BUDGET - kBoxBytes) / kOpStageBytes);
+  if (args.stages > kMaxStages) args.stages = kMaxStages;
+  args.raw_sets = 0;
+  args.chunk_stages = accumulate_chunk_stages();
+  const size_t smem = (size_t)args.stages * kOpStageBytes + kBoxBytes + 1024;
+  const bool wide = consumer_layout() == 16;
+  auto fn = wide ? persistent_product_kernel<4> : persistent_product_kernel<8>;
+  const int threads = wide ? Layout<4>::kThreads : Layout<8>::kThreads;
+  cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
+  const int grid = total < sm_count() ? total : sm_count();
+  fn<<<grid, threads, smem, stream>>>(tmA, tmB, tmC, args, prod);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fused_product(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
                                  const MkGemmArgs& args_in, const MkProduct& prod, cudaStream_t stream) {
   if (prod.na < 1 || prod.na > MK_MAX_TERMS || prod.nb < 1 || prod.nb > MK_MAX_TERMS) return cudaErrorInvalidValue;
   MkGemmArgs args = args_in;
   const bool ca = prod.na > 1, cb = prod.nb > 1;
+  if (!ca && !cb && persistent_enabled()) {
+    const int total = args.tiles_m * args.tiles_n;
+    if (total == 0) return cudaSuccess;
+    args.batch = nullptr;
+    args.nprod = 1;
+    args.tiles_per_prod = total;
+    return launch_persistent(tmA, tmB, tmC, args, prod, total, stream);
+  }
   const int raw_tiles = (ca ? prod.na : 0) + (cb ? prod.nb : 0);
   const size_t raw_set = (size_t)raw_tiles * MK_TILE_BYTES;
   const size_t budget = MK_SMEM_BUDGET;
@@ -591,6 +970,13 @@ cudaError_t launch_product_batch(const MkBatchEntry* entries_dev, int nprod, con
   args.chunk_stages = accumulate_chunk_stages();
   args.tiles_per_prod = tiles;
   args.batch = entries_dev;
+  args.nprod = nprod;
+  if (persistent_enabled()) {
+    CUtensorMap z{};
+    MkProduct zp{};
+    zp.na = zp.nb = 1;
+    return launch_persistent(z, z, z, args, zp, tiles * nprod, stream);
+  }
   const size_t smem = (size_t)args.stages * kOpStageBytes + 1024;
   const bool wide = consumer_layout() == 16;
   auto fn = wide ? fused_product_kernel<false, false, 4> : fused_product_kernel<false, false, 8>;

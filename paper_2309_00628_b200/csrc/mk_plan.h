@@ -54,5 +54,6 @@ struct MkGemmArgs {
   int32_t async_epi;     // TMA store / reduce-add epilogue (tile-aligned leaf, tmC valid)
   int32_t chunk_stages;               // >0: two-level accumulation, flush registers to TMEM every N stages
   int32_t tiles_per_prod;             // batched launch: CTAs per product
+  int32_t nprod;                      // batched launch: products in the batch (persistent kernel)
   const MkBatchEntry* batch;          // batched launch: per-product maps/descriptors (nullptr: single)
 };

@@ -18,7 +18,7 @@ def sample():
 
 
 SM = torch.cuda.get_device_properties(0).multi_processor_count
-M, N = SM * 128, 4 * 128
+M, N = SM * 128, int(os.environ.get("WAVES", "4")) * 128
 res = {}
 th = threading.Thread(target=sample); th.start()
 for K in (8192, 16384):
