@@ -663,16 +663,20 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
   }
   bool master_live = false;
   auto fold_to_tmem = [&]() {
+#ifndef MK_FOLD_GROUP
+#define MK_FOLD_GROUP 2
+#endif
+    constexpr int kGrp = MK_FOLD_GROUP < kPieces ? MK_FOLD_GROUP : kPieces;  // pieces per tcgen05.ld round trip
 #pragma unroll
-    for (int pc = 0; pc < kPieces; pc += 2) {
-      uint32_t w[2][16];
+    for (int pc = 0; pc < kPieces; pc += kGrp) {
+      uint32_t w[kGrp][16];
       if (master_live) {
-        tmem_ld16(taddr + pc * 16, w[0]);
-        tmem_ld16(taddr + pc * 16 + 16, w[1]);
+#pragma unroll
+        for (int h = 0; h < kGrp; ++h) tmem_ld16(taddr + (pc + h) * 16, w[h]);
         tmem_wait_ld();
       }
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
+      for (int h = 0; h < kGrp; ++h)
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int e = (pc + h) * 8 + u;
@@ -682,8 +686,8 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
           w[h][2 * u + 1] = (uint32_t)__double2hiint(m);
           a = 0.0;
         }
-      tmem_st16(taddr + pc * 16, w[0]);
-      tmem_st16(taddr + pc * 16 + 16, w[1]);
+#pragma unroll
+      for (int h = 0; h < kGrp; ++h) tmem_st16(taddr + (pc + h) * 16, w[h]);
     }
     tmem_wait_st();
     master_live = true;

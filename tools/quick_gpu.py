@@ -12,7 +12,7 @@ import time
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-lib = ctypes.CDLL(os.path.join(HERE, "..", "paper_2309_00628_b200", "libmk_strassen.so"))
+lib = ctypes.CDLL(os.environ.get("MK_LIB") or os.path.join(HERE, "..", "paper_2309_00628_b200", "libmk_strassen.so"))
 lib.mk_last_error.restype = ctypes.c_char_p
 lib.mk_workspace_bytes.restype = ctypes.c_size_t
 lib.mk_rect_workspace_bytes.restype = ctypes.c_size_t
