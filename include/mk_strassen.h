@@ -110,13 +110,19 @@ int mk_multiply_rect(int algo, const double* A, int64_t lda, const double* B, in
                      int64_t ldc, int64_t m, int64_t n, int64_t k, int levels, void* ws, size_t ws_bytes,
                      void* stream);
 
+/* Workspace bytes mk_strassen_host needs for (algo, n, levels) (0 on invalid input): the
+ * depth-first plan's for L <= 2, a breadth-first plan per top-level product for L >= 3. */
+size_t mk_host_workspace_bytes(int algo, int64_t n, int levels);
+
 /* End-to-end product for HOST operands with transfers overlapped with compute (fused
  * algorithms, levels >= 1). hA/hB/hC: host matrices (pinned for asynchronous DMA); dA/dB/dC:
- * caller-owned device buffers of order n with even leading dimension ldd. Quadrants are
- * uploaded on `copy_stream` in order of first use, the top-level products run on `stream` in
- * the order mk_overlap_order reports (each waiting only for the quadrants it reads), and every
- * C quadrant is downloaded as soon as its last contributor finishes. Synchronous: returns when
- * hC holds the result. Workspace from mk_partial_workspace_bytes (depth-first plan). */
+ * caller-owned device buffers of order n with even leading dimension ldd. Operands are
+ * uploaded on `copy_stream` (quadrants for L = 1; for L = 2, quarter-quadrant sub-blocks in the
+ * order the compute first needs them, each top-level product running child by child and
+ * waiting only for the sub-blocks it reads), the top-level products run on `stream` in the
+ * order mk_overlap_order reports, and every C quadrant is downloaded as soon as its last
+ * contributor finishes (the last one by sub-blocks). Synchronous: returns when hC holds the
+ * result. Workspace from mk_host_workspace_bytes. */
 int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, int64_t ldb, double* hC, int64_t ldc,
                      int64_t n, int levels, double* dA, double* dB, double* dC, int64_t ldd, void* ws,
                      size_t ws_bytes, void* stream, void* copy_stream);

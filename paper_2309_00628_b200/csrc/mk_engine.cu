@@ -624,14 +624,18 @@ struct Engine {
     return MK_OK;
   }
 
-  // Overlapped host run (mk_strassen_host): the top-level products run in `order`; before each
-  // one the compute stream waits for the input quadrants it reads (in_ev: A11..A22, B11..B22),
-  // after it every C quadrant whose last contributor it was is signalled (out_ev: C11..C22).
-  // With L >= 2 the first and last products are split one level further (their children run in
-  // `order` too): sub_in (8 events, may be null) then gates each child of the first product on
-  // the sub-blocks of its single-term operand quadrants only, and sub_out[4q+s] signals sub-block
-  // s of each C quadrant q the last product finishes -- the pipeline's head waits for 1/4 of a
-  // quadrant per operand instead of a whole one, its tail downloads 1/4 of a quadrant.
+  // Overlapped host run (mk_strassen_host): the top-level products run in `order`. Quadrant
+  // mode (sub_in == nullptr): before each product the compute stream waits for the input
+  // quadrants it reads (in_ev: A11..A22, B11..B22). Sub-block mode (L = 2): every product whose
+  // fan-out fits runs child by child (children in `order` too); before each child the stream
+  // waits only for the sub-blocks (sub_in[4q+s]) its operands read, and a multi-term top-level
+  // operand sum is formed one sub-block at a time, right before the first child that reads it,
+  // so the compute stream follows the uploads at 1/4-quadrant granularity instead of stalling
+  // until whole quadrants have landed. L >= 3: each top-level product runs breadth-first below
+  // the top level (top_product_bfs). After a product, every C quadrant whose last contributor
+  // it was is signalled (out_ev); in sub-block mode the last product also signals each C
+  // sub-block as soon as its last child is done (sub_out[4q+s]) so the tail downloads 1/4 of a
+  // quadrant.
   int fused_overlapped(const std::vector<int>& order, cudaEvent_t* in_ev, cudaEvent_t* out_ev, int64_t n,
                        cudaEvent_t* sub_in, cudaEvent_t* sub_out, bool* tail_split) {
     int last[4] = {-1, -1, -1, -1};
@@ -639,50 +643,71 @@ struct Engine {
     for (int i = 0; i < np; ++i)
       for (int q = 0; q < 4; ++q)
         if (co->c[q][order[i]]) last[q] = i;
-    const int64_t h = n / 2;
+    const int64_t h = n / 2, hh = h / 2;
     const Lin A0{Blk{BASE_A, 0, 0, 1.0}}, B0{Blk{BASE_B, 0, 0, 1.0}}, C0{Blk{BASE_C, 0, 0, 1.0}};
+    int child_last[4] = {-1, -1, -1, -1};
+    for (int j = 0; j < np; ++j)
+      for (int s = 0; s < 4; ++s)
+        if (co->c[s][order[j]]) child_last[s] = j;
     for (int q = 0; q < 4; ++q) tail_split[q] = false;
+    auto wait_ev = [&](cudaEvent_t ev) -> int {
+      if (!dry && ev) MK_CUDA_TRY(cudaStreamWaitEvent(st, ev, 0));
+      return MK_OK;
+    };
+    auto record_ev = [&](cudaEvent_t ev) -> int {
+      if (!dry && ev) MK_CUDA_TRY(cudaEventRecord(ev, st));
+      return MK_OK;
+    };
+    const bool inner_bfs = L >= 3 && !fuse_preadds;
     for (int i = 0; i < np; ++i) {
       const int p = order[i];
-      const bool head = i == 0 && sub_in != nullptr && L >= 2;
-      const bool tail = i == np - 1 && sub_out != nullptr && L >= 2 && split_fits(p);
-      for (int q = 0; q < 4; ++q) {
-        if (head) break;  // the first product waits per child on sub-blocks (below)
-        if (co->a[p][q]) MK_CUDA_TRY(cudaStreamWaitEvent(st, in_ev[q], 0));
-        if (co->b[p][q]) MK_CUDA_TRY(cudaStreamWaitEvent(st, in_ev[4 + q], 0));
-      }
-      if (!head && !tail) {
-        MK_TRY(fused_child(L, p, A0, B0, C0, n, n, n, 0));
+      const bool split = !inner_bfs && sub_in != nullptr && L >= 2 && split_fits(p);
+      const bool tail = split && i == np - 1 && sub_out != nullptr;
+      if (!split) {
+        for (int q = 0; q < 4; ++q) {
+          if (co->a[p][q]) MK_TRY(wait_ev(in_ev[q]));
+          if (co->b[p][q]) MK_TRY(wait_ev(in_ev[4 + q]));
+        }
+        if (inner_bfs)
+          MK_TRY(top_product_bfs(p, A0, B0, C0, h));
+        else
+          MK_TRY(fused_child(L, p, A0, B0, C0, n, n, n, 0));
       } else {
-        // the top-level part of fused_child, then the children one by one
-        Lin Xp = kron(A0, co->a[p], h, h), Yp = kron(B0, co->b[p], h, h), Dp = kron_dest(C0, p, h, h);
+        const Lin T[2] = {kron(A0, co->a[p], h, h), kron(B0, co->b[p], h, h)};
+        const Lin Dp = kron_dest(C0, p, h, h);
+        Lin Op[2] = {T[0], T[1]};
+        int slot[2] = {-1, -1};
         const size_t mark = ws_used;
         const int nb_mark = nbases;
-        for (int side = 0; side < 2; ++side) {
-          Lin& T = side == 0 ? Xp : Yp;
-          if (T.size() == 1) continue;
-          int sb;
-          MK_TRY(alloc_slot(h, h, &sb));
-          MK_TRY(combine(Blk{sb, 0, 0, 1.0}, T, h, h));
-          T = Lin{Blk{sb, 0, 0, 1.0}};
-        }
-        int child_last[4] = {-1, -1, -1, -1};
-        for (int j = 0; j < np; ++j)
-          for (int s = 0; s < 4; ++s)
-            if (co->c[s][order[j]]) child_last[s] = j;
+        for (int side = 0; side < 2; ++side)
+          if (T[side].size() > 1) {
+            MK_TRY(alloc_slot(h, h, &slot[side]));
+            Op[side] = Lin{Blk{slot[side], 0, 0, 1.0}};
+          }
+        bool formed[2][4] = {{false}};
         for (int j = 0; j < np; ++j) {
           const int pc = order[j];
-          if (head)
-            for (int s = 0; s < 4; ++s) {
-              if (co->a[pc][s]) MK_CUDA_TRY(cudaStreamWaitEvent(st, sub_in[s], 0));
-              if (co->b[pc][s]) MK_CUDA_TRY(cudaStreamWaitEvent(st, sub_in[4 + s], 0));
+          for (int side = 0; side < 2; ++side) {
+            const int* cf = side == 0 ? co->a[pc] : co->b[pc];
+            for (int sb = 0; sb < 4; ++sb) {
+              if (!cf[sb] || formed[side][sb]) continue;
+              Lin src;
+              for (const Blk& t : T[side]) {
+                const int q = (int)(t.row / h) * 2 + (int)(t.col / h) + 4 * side;
+                MK_TRY(wait_ev(sub_in[4 * q + sb]));
+                src.push_back(Blk{t.base, t.row + (sb >> 1) * hh, t.col + (sb & 1) * hh, t.sign});
+              }
+              if (slot[side] >= 0)
+                MK_TRY(combine(Blk{slot[side], (sb >> 1) * hh, (sb & 1) * hh, 1.0}, src, hh, hh));
+              formed[side][sb] = true;
             }
-          MK_TRY(fused_child(L - 1, pc, Xp, Yp, Dp, h, h, h, 1));
+          }
+          MK_TRY(fused_child(L - 1, pc, Op[0], Op[1], Dp, h, h, h, 1));
           if (tail)
             for (int q = 0; q < 4; ++q)
               if (last[q] == i)
-                for (int s = 0; s < 4; ++s)
-                  if (child_last[s] == j) MK_CUDA_TRY(cudaEventRecord(sub_out[4 * q + s], st));
+                for (int sb = 0; sb < 4; ++sb)
+                  if (child_last[sb] == j) MK_TRY(record_ev(sub_out[4 * q + sb]));
         }
         ws_used = mark;
         while (nbases > nb_mark) {
@@ -696,7 +721,49 @@ struct Engine {
             if (last[q] == i) tail_split[q] = true;
       }
       for (int q = 0; q < 4; ++q)
-        if (last[q] == i) MK_CUDA_TRY(cudaEventRecord(out_ev[q], st));
+        if (last[q] == i) MK_TRY(record_ev(out_ev[q]));
+    }
+    return MK_OK;
+  }
+  // Top-level product p with a breadth-first plan below it: operand sums materialised, the
+  // (n/2)^2 product formed by bfs(L-1) in a slot, then added with its signs into every C quadrant
+  // it feeds (store for the first writer).
+  int top_product_bfs(int p, const Lin& A0, const Lin& B0, const Lin& C0, int64_t h) {
+    Lin X = kron(A0, co->a[p], h, h), Y = kron(B0, co->b[p], h, h);
+    const Lin Dp = kron_dest(C0, p, h, h);
+    const size_t mark = ws_used;
+    const int nb_mark = nbases;
+    Blk Xb = X[0], Yb = Y[0];  // single terms stay views (bfs carries their sign)
+    if (X.size() > 1) {
+      int sb;
+      MK_TRY(alloc_slot(h, h, &sb));
+      MK_TRY(combine(Blk{sb, 0, 0, 1.0}, X, h, h));
+      Xb = Blk{sb, 0, 0, 1.0};
+    }
+    if (Y.size() > 1) {
+      int sb;
+      MK_TRY(alloc_slot(h, h, &sb));
+      MK_TRY(combine(Blk{sb, 0, 0, 1.0}, Y, h, h));
+      Yb = Blk{sb, 0, 0, 1.0};
+    }
+    int pb;
+    MK_TRY(alloc_slot(h, h, &pb));
+    MK_TRY(bfs(L - 1, h, h, h, Xb, Yb, Blk{pb, 0, 0, 1.0}));
+    for (const Blk& d : Dp) {
+      const int s = state(d.base, d.row, d.col, h, h);
+      if (s == 2) return fail(MK_ERR_ARG, "internal: partially written post-add destination");
+      Lin src;
+      if (s == 1) src.push_back(Blk{d.base, d.row, d.col, d.sign});
+      src.push_back(Blk{pb, 0, 0, 1.0});
+      MK_TRY(combine(Blk{d.base, d.row, d.col, d.sign}, src, h, h));
+      set_state(d.base, d.row, d.col, h, h, 1);
+    }
+    ws_used = mark;
+    while (nbases > nb_mark) {
+      --nbases;
+      written.pop_back();
+      cell_rows.pop_back();
+      cell_cols.pop_back();
     }
     return MK_OK;
   }
@@ -708,15 +775,33 @@ struct Engine {
     for (int i = 1; i < L; ++i) worst *= 4;
     return worst <= MK_MAX_DESTS;
   }
-  // Whether the first product qualifies for sub-block uploads: single-term operands and a
-  // fan-out that fits.
-  bool head_split_ok(int p) const {
-    int ta = 0, tb = 0;
-    for (int q = 0; q < 4; ++q) {
-      ta += co->a[p][q] != 0;
-      tb += co->b[p][q] != 0;
+  // Sub-block upload order: (quadrant 0..7, sub-block 0..3) pairs in the order fused_overlapped
+  // first waits for them.
+  std::vector<std::pair<int, int>> sub_upload_order(const std::vector<int>& order) const {
+    std::vector<std::pair<int, int>> ups;
+    bool seen[8][4] = {{false}};
+    auto add = [&](int q, int sb) {
+      if (!seen[q][sb]) {
+        seen[q][sb] = true;
+        ups.emplace_back(q, sb);
+      }
+    };
+    for (int p : order) {
+      const bool split = split_fits(p) && L < 3;  // fused_overlapped splits at L = 2 only
+      for (int pc : order) {
+        for (int side = 0; side < 2; ++side) {
+          const int* cf = side == 0 ? co->a[pc] : co->b[pc];
+          const int* tp = side == 0 ? co->a[p] : co->b[p];
+          for (int sb = 0; sb < 4; ++sb)
+            for (int q = 0; q < 4; ++q)
+              if (tp[q] && (!split || cf[sb])) add(q + 4 * side, sb);
+        }
+        if (!split) break;
+      }
     }
-    return L >= 2 && ta == 1 && tb == 1 && split_fits(p);
+    for (int q = 0; q < 8; ++q)
+      for (int sb = 0; sb < 4; ++sb) add(q, sb);
+    return ups;
   }
 
   // ---- literal schedule plan (two-temp / in-place) ----
@@ -1319,6 +1404,25 @@ int mk_overlap_order(int algo, int* order_out, int* uploads_out) {
   return (int)ord.size();
 }
 
+size_t mk_host_workspace_bytes(int algo, int64_t n, int levels) {
+  if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_WINOGRAD_KNUTH_8CALL || n < 2 || !is_pow2(n) || levels < 1 ||
+      (n >> levels) < 2)
+    return 0;
+  Engine e;
+  e.dry = true;
+  if (setup_square(e, algo, reinterpret_cast<double*>(0x100000), n, reinterpret_cast<double*>(0x200000), n,
+                   reinterpret_cast<double*>(0x300000), n, n, levels) != MK_OK)
+    return 0;
+  const std::vector<int> order = overlap_order(*e.co, nullptr);
+  cudaEvent_t none[61] = {nullptr};
+  bool tail_split[4];
+  const bool sub = levels == 2 && (n / 2) % 2 == 0;
+  if (e.fused_overlapped(order, none, none + 8, n, sub ? none + 13 : nullptr, sub ? none + 45 : nullptr,
+                         tail_split) != MK_OK)
+    return 0;
+  return e.ws_peak;
+}
+
 int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, int64_t ldb, double* hC, int64_t ldc,
                      int64_t n, int levels, double* dA, double* dB, double* dC, int64_t ldd, void* ws,
                      size_t ws_bytes, void* stream, void* copy_stream) {
@@ -1350,11 +1454,11 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
     }
   }
   const int64_t h = n / 2, hh = h / 2;
-  // events: 8 quadrant uploads, 4 quadrant completions, start, 8 sub-block uploads, 16 sub-block completions
-  constexpr int kEv = 37;
+  // events: 8 quadrant uploads, 4 quadrant completions, start, 32 sub-block uploads, 16 sub-block completions
+  constexpr int kEv = 61;
   cudaEvent_t ev[kEv];
   for (int i = 0; i < kEv; ++i) MK_CUDA_TRY(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
-  cudaEvent_t *in_ev = ev, *out_ev = ev + 8, start = ev[12], *sub_in = ev + 13, *sub_out = ev + 21;
+  cudaEvent_t *in_ev = ev, *out_ev = ev + 8, start = ev[12], *sub_in = ev + 13, *sub_out = ev + 45;
   int rc = MK_OK;
   auto quad_ptr = [&](double* base, int64_t ld, int q) { return base + ((q >> 1) * h) * ld + (q & 1) * h; };
   auto sub_ptr = [&](double* base, int64_t ld, int q, int s) {
@@ -1370,42 +1474,28 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
   // the copy stream starts after prior work on the compute stream (device buffers may be reused)
   if (cudaEventRecord(start, st) != cudaSuccess || cudaStreamWaitEvent(cp, start, 0) != cudaSuccess)
     rc = fail(MK_ERR_CUDA, "stream ordering failed");
-  const bool head = (h % 2 == 0) && e.head_split_ok(order[0]);
-  int qa = -1, qb = -1;
-  if (head) {
-    for (int q = 0; q < 4; ++q) {
-      if (e.co->a[order[0]][q]) qa = q;
-      if (e.co->b[order[0]][q]) qb = q;
+  // sub-block mode (L = 2): the 32 operand sub-blocks go up in the order the compute stream
+  // first waits for them; otherwise the 8 quadrants in order of first use
+  const bool sub = levels == 2 && h % 2 == 0;
+  if (sub) {
+    int done_subs[8] = {0};
+    for (const auto& qs : e.sub_upload_order(order)) {
+      const int q = qs.first, sb = qs.second;
+      double* dst = q < 4 ? sub_ptr(dA, ldd, q, sb) : sub_ptr(dB, ldd, q - 4, sb);
+      const double* src = q < 4 ? sub_ptr(const_cast<double*>(hA), lda, q, sb) : sub_ptr(const_cast<double*>(hB), ldb, q - 4, sb);
+      copy(dst, ldd, src, q < 4 ? lda : ldb, hh, cudaMemcpyHostToDevice, sub_in[4 * q + sb], "upload: ");
+      if (++done_subs[q] == 4 && rc == MK_OK && cudaEventRecord(in_ev[q], cp) != cudaSuccess)
+        rc = fail(MK_ERR_CUDA, "event record failed");
     }
-    // sub-blocks of the first product's two operand quadrants, in the children's order of first use
-    for (int u : up) {
-      const bool isA = u < 4;
-      const int s = u & 3, q = isA ? qa : qb;
-      if (isA)
-        copy(sub_ptr(dA, ldd, q, s), ldd, sub_ptr(const_cast<double*>(hA), lda, q, s), lda, hh,
-             cudaMemcpyHostToDevice, sub_in[s], "upload: ");
-      else
-        copy(sub_ptr(dB, ldd, q, s), ldd, sub_ptr(const_cast<double*>(hB), ldb, q, s), ldb, hh,
-             cudaMemcpyHostToDevice, sub_in[4 + s], "upload: ");
-    }
-    if (rc == MK_OK && (cudaEventRecord(in_ev[qa], cp) != cudaSuccess || cudaEventRecord(in_ev[4 + qb], cp) != cudaSuccess))
-      rc = fail(MK_ERR_CUDA, "event record failed");
-  }
-  for (size_t i = 0; i < up.size(); ++i) {
-    const int q = up[i];
-    const bool isA = q < 4;
-    if ((isA && q == qa) || (!isA && q - 4 == qb)) continue;  // already uploaded by sub-blocks
-    if (isA)
-      copy(quad_ptr(dA, ldd, q), ldd, quad_ptr(const_cast<double*>(hA), lda, q), lda, h, cudaMemcpyHostToDevice,
-           in_ev[q], "upload: ");
-    else
-      copy(quad_ptr(dB, ldd, q - 4), ldd, quad_ptr(const_cast<double*>(hB), ldb, q - 4), ldb, h,
-           cudaMemcpyHostToDevice, in_ev[q], "upload: ");
+  } else {
+    for (int q : up)
+      copy(q < 4 ? quad_ptr(dA, ldd, q) : quad_ptr(dB, ldd, q - 4), ldd,
+           q < 4 ? quad_ptr(const_cast<double*>(hA), lda, q) : quad_ptr(const_cast<double*>(hB), ldb, q - 4),
+           q < 4 ? lda : ldb, h, cudaMemcpyHostToDevice, in_ev[q], "upload: ");
   }
   bool tail_split[4] = {false, false, false, false};
   if (rc == MK_OK)
-    rc = e.fused_overlapped(order, in_ev, out_ev, n, head ? sub_in : nullptr, (h % 2 == 0) ? sub_out : nullptr,
-                            tail_split);
+    rc = e.fused_overlapped(order, in_ev, out_ev, n, sub ? sub_in : nullptr, sub ? sub_out : nullptr, tail_split);
   if (rc == MK_OK) {
     // downloads in the order the quadrants (or, for the last product's, their sub-blocks) complete
     int last[4] = {-1, -1, -1, -1};

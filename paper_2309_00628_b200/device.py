@@ -302,7 +302,7 @@ def _overlapped_host_product(algo: str, a: MatrixView, b: MatrixView, c: MatrixV
     dB = torch.empty((n, ld), dtype=torch.float64, device="cuda")
     dC = torch.empty((n, ld), dtype=torch.float64, device="cuda")
     aid = _lib.ALGO_IDS[algo]
-    ws_bytes = int(lib.mk_partial_workspace_bytes(aid, n, levels))
+    ws_bytes = int(lib.mk_host_workspace_bytes(aid, n, levels))
     ws = workspace(ws_bytes)
     st.workspace_bytes = ws_bytes
     st.path = "overlapped-host"
