@@ -324,6 +324,16 @@ struct Engine {
   char* ws = nullptr;
   size_t ws_bytes = 0, ws_used = 0;
   bool dry = false;  // sizing pass: no launches
+  // Plan-table record/replay (mk_strassen_host): a launch-free pass records every table into
+  // tbl_host at its offset in the device arena tbl_dev (tbl_mode 1); the caller uploads the
+  // arena once, before any bulk transfer is queued, and the replay pass (tbl_mode 2) launches
+  // with the same pointers. Otherwise (tbl_mode 0) tables are copied as they are built -- on
+  // the host path those copies would queue behind the operand transfers on the copy engines.
+  bool no_launch = false;
+  int tbl_mode = 0;
+  char* tbl_dev = nullptr;
+  size_t tbl_pos = 0, table_bytes = 0;
+  std::vector<char>* tbl_host = nullptr;
   size_t ws_peak = 0;
   // leaf-range filter (multi-GPU sharding)
   // Shard filter in units of leaf row panels: leaf i covers units [i*panels, (i+1)*panels);
@@ -404,7 +414,7 @@ struct Engine {
 
   // ---- block combine: dst := dst.sign * sum_i src_i.sign * src_i (chained past 8 sources) ----
   int combine(const Blk& dst, const Lin& src, int64_t rows, int64_t cols) {
-    if (dry) return MK_OK;
+    if (dry || no_launch) return MK_OK;
     double* dp = bases[dst.base].ptr + dst.row * bases[dst.base].ld + dst.col;
     const int64_t ldd = bases[dst.base].ld;
     size_t i = 0;
@@ -466,7 +476,7 @@ struct Engine {
       set_state(bd, D[i].row, D[i].col, M, N, 1);
     }
     ++launches;
-    if (dry) return MK_OK;
+    if (dry || no_launch) return MK_OK;
     CUtensorMap tmA, tmB, tmC;
     MK_TRY(cached_map(bx, 0, &tmA));
     MK_TRY(cached_map(by, 1, &tmB));
@@ -651,11 +661,11 @@ struct Engine {
         if (co->c[s][order[j]]) child_last[s] = j;
     for (int q = 0; q < 4; ++q) tail_split[q] = false;
     auto wait_ev = [&](cudaEvent_t ev) -> int {
-      if (!dry && ev) MK_CUDA_TRY(cudaStreamWaitEvent(st, ev, 0));
+      if (!dry && !no_launch && ev) MK_CUDA_TRY(cudaStreamWaitEvent(st, ev, 0));
       return MK_OK;
     };
     auto record_ev = [&](cudaEvent_t ev) -> int {
-      if (!dry && ev) MK_CUDA_TRY(cudaEventRecord(ev, st));
+      if (!dry && !no_launch && ev) MK_CUDA_TRY(cudaEventRecord(ev, st));
       return MK_OK;
     };
     const bool inner_bfs = L >= 3 && !fuse_preadds;
@@ -884,6 +894,16 @@ struct Engine {
   int upload(const void* host, size_t bytes, void** dev_out) {
     const size_t al = (bytes + 1023) / 1024 * 1024;
     *dev_out = nullptr;
+    table_bytes += al;
+    if (tbl_mode != 0) {
+      *dev_out = tbl_dev + tbl_pos;
+      if (tbl_mode == 1) {
+        if (tbl_host->size() < tbl_pos + al) tbl_host->resize(tbl_pos + al);
+        std::memcpy(tbl_host->data() + tbl_pos, host, bytes);
+      }
+      tbl_pos += al;
+      return MK_OK;
+    }
     if (!dry) {
       if (ws_used + al > ws_bytes)
         return fail(MK_ERR_WORKSPACE, "workspace too small for device plan tables");
@@ -908,7 +928,7 @@ struct Engine {
     }
     void* dev = nullptr;
     MK_TRY(upload(jobs.data(), jobs.size() * sizeof(MkXformJob), &dev));
-    if (dry) return MK_OK;
+    if (dry || no_launch) return MK_OK;
     MK_CUDA_TRY(launch_xform_batch(static_cast<const MkXformJob*>(dev), (int)jobs.size(), rows, cols, vec, st));
     ++g_launch_count;
     return MK_OK;
@@ -1089,7 +1109,7 @@ struct Engine {
       void* dev = nullptr;
       MK_TRY(upload(ents.data(), ents.size() * sizeof(MkBatchEntry), &dev));
       launches += nprod_launch;
-      if (dry) continue;
+      if (dry || no_launch) continue;
       MkGemmArgs g{};
       g.M = (int32_t)lm;
       g.N = (int32_t)ln;
@@ -1404,6 +1424,10 @@ int mk_overlap_order(int algo, int* order_out, int* uploads_out) {
   return (int)ord.size();
 }
 
+// Top-level product / quadrant upload order of the overlapped host path, per algorithm.
+static std::map<int, std::pair<std::vector<int>, std::vector<int>>> g_order_cache;
+static std::mutex g_order_mu;
+
 size_t mk_host_workspace_bytes(int algo, int64_t n, int levels) {
   if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_WINOGRAD_KNUTH_8CALL || n < 2 || !is_pow2(n) || levels < 1 ||
       (n >> levels) < 2)
@@ -1420,7 +1444,7 @@ size_t mk_host_workspace_bytes(int algo, int64_t n, int levels) {
   if (e.fused_overlapped(order, none, none + 8, n, sub ? none + 13 : nullptr, sub ? none + 45 : nullptr,
                          tail_split) != MK_OK)
     return 0;
-  return e.ws_peak;
+  return e.ws_peak + e.table_bytes;  // slots (+ tables, conservatively) and the table arena
 }
 
 int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, int64_t ldb, double* hC, int64_t ldc,
@@ -1432,26 +1456,65 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
   if (levels < 1) return fail(MK_ERR_ARG, "the overlapped host path needs at least one level");
   if (ldd < n || ldd % 2 || lda < n || ldb < n || ldc < n)
     return fail(MK_ERR_DIMENSION, "leading dimension smaller than the order (device ld must be even)");
+  cudaStream_t st = static_cast<cudaStream_t>(stream), cp = static_cast<cudaStream_t>(copy_stream);
+  std::vector<int> order0;
+  {
+    std::lock_guard<std::mutex> lk(g_order_mu);
+    auto it = g_order_cache.find(algo);
+    if (it == g_order_cache.end()) {
+      std::vector<int> up0;
+      order0 = overlap_order(coeffs_for(algo), &up0);
+      g_order_cache[algo] = {order0, up0};
+    } else {
+      order0 = it->second.first;
+    }
+  }
+  const bool sub = levels == 2 && (n / 2) % 2 == 0;
+  cudaEvent_t none[61] = {nullptr};
+  bool ts0[4];
+  // plan tables: sized by a dry run, recorded by a launch-free pass into a device arena at the top
+  // of the workspace, uploaded once on the compute stream before any operand transfer is queued
+  size_t tbl_total = 0;
+  {
+    Engine d;
+    d.dry = true;
+    MK_TRY(setup_square(d, algo, dA, ldd, dB, ldd, dC, ldd, n, levels));
+    MK_TRY(d.fused_overlapped(order0, none, none + 8, n, sub ? none + 13 : nullptr, sub ? none + 45 : nullptr, ts0));
+    tbl_total = d.table_bytes;
+  }
+  if (!ws && tbl_total) return fail(MK_ERR_WORKSPACE, "workspace required for plan tables");
+  if (tbl_total > ws_bytes) return fail(MK_ERR_WORKSPACE, "workspace too small for plan tables");
+  const size_t tbl_off = (ws_bytes - tbl_total) & ~(size_t)1023;
+  char* const tbl_dev = static_cast<char*>(ws) + tbl_off;
+  std::vector<char> tbl_host;
+  if (tbl_total) {
+    Engine r;
+    MK_TRY(setup_square(r, algo, dA, ldd, dB, ldd, dC, ldd, n, levels));
+    r.st = st;
+    r.ws = static_cast<char*>(ws);
+    r.ws_bytes = tbl_off;
+    r.no_launch = true;
+    r.tbl_mode = 1;
+    r.tbl_dev = tbl_dev;
+    r.tbl_host = &tbl_host;
+    MK_TRY(r.fused_overlapped(order0, none, none + 8, n, sub ? none + 13 : nullptr, sub ? none + 45 : nullptr, ts0));
+    if (!tbl_host.empty())
+      MK_CUDA_TRY(cudaMemcpyAsync(tbl_dev, tbl_host.data(), tbl_host.size(), cudaMemcpyHostToDevice, st));
+  }
   Engine e;
   MK_TRY(setup_square(e, algo, dA, ldd, dB, ldd, dC, ldd, n, levels));
-  cudaStream_t st = static_cast<cudaStream_t>(stream), cp = static_cast<cudaStream_t>(copy_stream);
   e.st = st;
   e.ws = static_cast<char*>(ws);
-  e.ws_bytes = ws ? ws_bytes : 0;
-  std::vector<int> up;
-  static std::map<int, std::pair<std::vector<int>, std::vector<int>>> cache;
-  static std::mutex mu;
-  std::vector<int> order;
+  e.ws_bytes = ws ? tbl_off : 0;
+  if (tbl_total) {
+    e.tbl_mode = 2;
+    e.tbl_dev = tbl_dev;
+  }
+  std::vector<int> order, up;
   {
-    std::lock_guard<std::mutex> lk(mu);
-    auto it = cache.find(algo);
-    if (it == cache.end()) {
-      order = overlap_order(coeffs_for(algo), &up);
-      cache[algo] = {order, up};
-    } else {
-      order = it->second.first;
-      up = it->second.second;
-    }
+    std::lock_guard<std::mutex> lk(g_order_mu);
+    order = g_order_cache[algo].first;
+    up = g_order_cache[algo].second;
   }
   const int64_t h = n / 2, hh = h / 2;
   // events: 8 quadrant uploads, 4 quadrant completions, start, 32 sub-block uploads, 16 sub-block completions
@@ -1476,7 +1539,6 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
     rc = fail(MK_ERR_CUDA, "stream ordering failed");
   // sub-block mode (L = 2): the 32 operand sub-blocks go up in the order the compute stream
   // first waits for them; otherwise the 8 quadrants in order of first use
-  const bool sub = levels == 2 && h % 2 == 0;
   if (sub) {
     int done_subs[8] = {0};
     for (const auto& qs : e.sub_upload_order(order)) {
