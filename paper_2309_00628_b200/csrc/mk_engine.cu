@@ -307,6 +307,32 @@ using Lin = std::vector<Blk>;
 
 enum { BASE_A = 0, BASE_B = 1, BASE_C = 2, BASE_WS0 = 3 };
 
+// MK_HOST_TRACE=1: mk_strassen_host prints a timeline (ms from the first upload) of its uploads,
+// top-level products / children and downloads to stderr (dev aid).
+static bool host_trace_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MK_HOST_TRACE");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+static std::vector<std::string> g_host_trace;
+static unsigned long long* g_trace_dev = nullptr;
+constexpr int kTraceMax = 4096;
+__global__ void trace_stamp_kernel(unsigned long long* slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  *slot = t;
+}
+static void host_trace(const std::string& label, cudaStream_t s) {
+  if (!host_trace_on()) return;
+  if (!g_trace_dev && cudaMalloc(&g_trace_dev, kTraceMax * sizeof(unsigned long long)) != cudaSuccess) return;
+  if ((int)g_host_trace.size() >= kTraceMax) return;
+  trace_stamp_kernel<<<1, 1, 0, s>>>(g_trace_dev + g_host_trace.size());
+  g_host_trace.push_back(label);
+}
+
 struct Engine {
   int algo = 0;
   const Coeffs* co = nullptr;
@@ -330,6 +356,7 @@ struct Engine {
   // with the same pointers. Otherwise (tbl_mode 0) tables are copied as they are built -- on
   // the host path those copies would queue behind the operand transfers on the copy engines.
   bool no_launch = false;
+  std::vector<int> head_children;  // child order of the first top-level product (sub-block mode)
   int tbl_mode = 0;
   char* tbl_dev = nullptr;
   size_t tbl_pos = 0, table_bytes = 0;
@@ -672,7 +699,7 @@ struct Engine {
     for (int i = 0; i < np; ++i) {
       const int p = order[i];
       const bool split = !inner_bfs && sub_in != nullptr && L >= 2 && split_fits(p);
-      const bool tail = split && i == np - 1 && sub_out != nullptr;
+      const bool tail = split && i == np - 1 && i != 0 && sub_out != nullptr;
       if (!split) {
         for (int q = 0; q < 4; ++q) {
           if (co->a[p][q]) MK_TRY(wait_ev(in_ev[q]));
@@ -695,8 +722,9 @@ struct Engine {
             Op[side] = Lin{Blk{slot[side], 0, 0, 1.0}};
           }
         bool formed[2][4] = {{false}};
+        const std::vector<int>& kids = (i == 0 && !head_children.empty()) ? head_children : order;
         for (int j = 0; j < np; ++j) {
-          const int pc = order[j];
+          const int pc = kids[j];
           for (int side = 0; side < 2; ++side) {
             const int* cf = side == 0 ? co->a[pc] : co->b[pc];
             for (int sb = 0; sb < 4; ++sb) {
@@ -713,6 +741,7 @@ struct Engine {
             }
           }
           MK_TRY(fused_child(L - 1, pc, Op[0], Op[1], Dp, h, h, h, 1));
+          if (!dry && !no_launch) host_trace("P" + std::to_string(p + 1) + "." + std::to_string(pc + 1) + " done", st);
           if (tail)
             for (int q = 0; q < 4; ++q)
               if (last[q] == i)
@@ -730,6 +759,7 @@ struct Engine {
           for (int q = 0; q < 4; ++q)
             if (last[q] == i) tail_split[q] = true;
       }
+      if (!dry && !no_launch) host_trace("P" + std::to_string(p + 1) + " done", st);
       for (int q = 0; q < 4; ++q)
         if (last[q] == i) MK_TRY(record_ev(out_ev[q]));
     }
@@ -798,7 +828,8 @@ struct Engine {
     };
     for (int p : order) {
       const bool split = split_fits(p) && L < 3;  // fused_overlapped splits at L = 2 only
-      for (int pc : order) {
+      const std::vector<int>& kids = (p == order[0] && !head_children.empty()) ? head_children : order;
+      for (int pc : kids) {
         for (int side = 0; side < 2; ++side) {
           const int* cf = side == 0 ? co->a[pc] : co->b[pc];
           const int* tp = side == 0 ? co->a[p] : co->b[p];
@@ -1414,6 +1445,48 @@ static std::vector<int> overlap_order(const Coeffs& co, std::vector<int>* upload
   return best;
 }
 
+// Child order of the first top-level product in sub-block mode (single-term operands): its
+// operand sub-blocks go up one unit each in the children's order of first use and gate the
+// children (kChild units each: a 4096^3 leaf vs a 128 MiB upload at n = 16384); keep the
+// permutation whose last child finishes first (ties: table order).
+static std::vector<int> head_child_order(const Coeffs& co, int p0) {
+  const double kChild = 1.7;
+  std::vector<int> perm(co.nprod), best;
+  for (int i = 0; i < co.nprod; ++i) perm[i] = i;
+  double best_t = 1e30;
+  do {
+    double ready[8][4];
+    bool have[8][4] = {{false}};
+    double t_up = 0, t = 0;
+    for (int pc : perm) {
+      double need = 0;
+      for (int side = 0; side < 2; ++side) {
+        const int* cf = side == 0 ? co.a[pc] : co.b[pc];
+        const int* tp = side == 0 ? co.a[p0] : co.b[p0];
+        for (int sb = 0; sb < 4; ++sb) {
+          if (!cf[sb]) continue;
+          for (int q = 0; q < 4; ++q) {
+            if (!tp[q]) continue;
+            const int k = q + 4 * side;
+            if (!have[k][sb]) {
+              have[k][sb] = true;
+              t_up += 1.0;
+              ready[k][sb] = t_up;
+            }
+            need = std::max(need, ready[k][sb]);
+          }
+        }
+      }
+      t = std::max(t, need) + kChild;
+    }
+    if (t < best_t - 1e-9) {
+      best_t = t;
+      best = perm;
+    }
+  } while (std::next_permutation(perm.begin(), perm.end()));
+  return best;
+}
+
 int mk_overlap_order(int algo, int* order_out, int* uploads_out) {
   g_last_error.clear();
   if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_WINOGRAD_KNUTH_8CALL) return fail(MK_ERR_ARG, "fused algorithms only");
@@ -1424,9 +1497,18 @@ int mk_overlap_order(int algo, int* order_out, int* uploads_out) {
   return (int)ord.size();
 }
 
-// Top-level product / quadrant upload order of the overlapped host path, per algorithm.
+// Top-level product / quadrant upload order of the overlapped host path, per algorithm, and the
+// child order of its first product (head_child_order).
 static std::map<int, std::pair<std::vector<int>, std::vector<int>>> g_order_cache;
+static std::map<int, std::vector<int>> g_head_cache;
 static std::mutex g_order_mu;
+static std::vector<int> head_child_order(const Coeffs& co, int p0);
+static std::vector<int> cached_head_children(int algo, int p0) {
+  std::lock_guard<std::mutex> lk(g_order_mu);
+  auto it = g_head_cache.find(algo);
+  if (it != g_head_cache.end()) return it->second;
+  return g_head_cache[algo] = head_child_order(coeffs_for(algo), p0);
+}
 
 size_t mk_host_workspace_bytes(int algo, int64_t n, int levels) {
   if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_WINOGRAD_KNUTH_8CALL || n < 2 || !is_pow2(n) || levels < 1 ||
@@ -1441,6 +1523,7 @@ size_t mk_host_workspace_bytes(int algo, int64_t n, int levels) {
   cudaEvent_t none[61] = {nullptr};
   bool tail_split[4];
   const bool sub = levels == 2 && (n / 2) % 2 == 0;
+  if (sub) e.head_children = cached_head_children(algo, order[0]);
   if (e.fused_overlapped(order, none, none + 8, n, sub ? none + 13 : nullptr, sub ? none + 45 : nullptr,
                          tail_split) != MK_OK)
     return 0;
@@ -1470,6 +1553,7 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
     }
   }
   const bool sub = levels == 2 && (n / 2) % 2 == 0;
+  const std::vector<int> kids0 = sub ? cached_head_children(algo, order0[0]) : std::vector<int>();
   cudaEvent_t none[61] = {nullptr};
   bool ts0[4];
   // plan tables: sized by a dry run, recorded by a launch-free pass into a device arena at the top
@@ -1479,6 +1563,7 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
     Engine d;
     d.dry = true;
     MK_TRY(setup_square(d, algo, dA, ldd, dB, ldd, dC, ldd, n, levels));
+    d.head_children = kids0;
     MK_TRY(d.fused_overlapped(order0, none, none + 8, n, sub ? none + 13 : nullptr, sub ? none + 45 : nullptr, ts0));
     tbl_total = d.table_bytes;
   }
@@ -1497,6 +1582,7 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
     r.tbl_mode = 1;
     r.tbl_dev = tbl_dev;
     r.tbl_host = &tbl_host;
+    r.head_children = kids0;
     MK_TRY(r.fused_overlapped(order0, none, none + 8, n, sub ? none + 13 : nullptr, sub ? none + 45 : nullptr, ts0));
     if (!tbl_host.empty())
       MK_CUDA_TRY(cudaMemcpyAsync(tbl_dev, tbl_host.data(), tbl_host.size(), cudaMemcpyHostToDevice, st));
@@ -1506,6 +1592,7 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
   e.st = st;
   e.ws = static_cast<char*>(ws);
   e.ws_bytes = ws ? tbl_off : 0;
+  e.head_children = kids0;
   if (tbl_total) {
     e.tbl_mode = 2;
     e.tbl_dev = tbl_dev;
@@ -1546,6 +1633,7 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
       double* dst = q < 4 ? sub_ptr(dA, ldd, q, sb) : sub_ptr(dB, ldd, q - 4, sb);
       const double* src = q < 4 ? sub_ptr(const_cast<double*>(hA), lda, q, sb) : sub_ptr(const_cast<double*>(hB), ldb, q - 4, sb);
       copy(dst, ldd, src, q < 4 ? lda : ldb, hh, cudaMemcpyHostToDevice, sub_in[4 * q + sb], "upload: ");
+      host_trace(std::string(q < 4 ? "A" : "B") + "q" + std::to_string(q & 3) + "s" + std::to_string(sb) + " up", cp);
       if (++done_subs[q] == 4 && rc == MK_OK && cudaEventRecord(in_ev[q], cp) != cudaSuccess)
         rc = fail(MK_ERR_CUDA, "event record failed");
     }
@@ -1587,9 +1675,17 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
       }
     }
   }
+  host_trace("downloads done", cp);
   cudaError_t se = cudaStreamSynchronize(cp);
   if (rc == MK_OK && se == cudaSuccess) se = cudaStreamSynchronize(st);
   if (rc == MK_OK && se != cudaSuccess) rc = fail(MK_ERR_CUDA, std::string("sync: ") + cudaGetErrorString(se));
+  if (host_trace_on() && !g_host_trace.empty()) {
+    std::vector<unsigned long long> t(g_host_trace.size());
+    cudaMemcpy(t.data(), g_trace_dev, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    for (size_t i = 0; i < t.size(); ++i)
+      fprintf(stderr, "[host-trace] %8.2f ms  %s\n", (double)(t[i] - t[0]) * 1e-6, g_host_trace[i].c_str());
+    g_host_trace.clear();
+  }
   for (int i = 0; i < kEv; ++i) cudaEventDestroy(ev[i]);
   return rc;
 }
