@@ -30,6 +30,7 @@
 
 #include "../../include/mk_strassen.h"
 #include "mk_blockops.h"
+#include "mk_hoststage.h"
 #include "mk_plan.h"
 
 namespace mk {
@@ -1614,16 +1615,31 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
   auto sub_ptr = [&](double* base, int64_t ld, int q, int s) {
     return quad_ptr(base, ld, q) + ((s >> 1) * hh) * ld + (s & 1) * hh;
   };
-  auto copy = [&](double* dst, int64_t dld, const double* src, int64_t sld, int64_t r, cudaMemcpyKind kind,
-                  cudaEvent_t done, const char* what) {
-    if (rc != MK_OK) return;
-    cudaError_t ce = cudaMemcpy2DAsync(dst, dld * 8, src, sld * 8, r * 8, r, kind, cp);
-    if (ce == cudaSuccess && done) ce = cudaEventRecord(done, cp);
-    if (ce != cudaSuccess) rc = fail(MK_ERR_CUDA, std::string(what) + cudaGetErrorString(ce));
-  };
   // the copy stream starts after prior work on the compute stream (device buffers may be reused)
   if (cudaEventRecord(start, st) != cudaSuccess || cudaStreamWaitEvent(cp, start, 0) != cudaSuccess)
     rc = fail(MK_ERR_CUDA, "stream ordering failed");
+  // pageable operands (plain host arrays) go through the pinned bounce slots of a Stager
+  const bool page_a = is_pageable(hA), page_b = is_pageable(hB), page_c = is_pageable(hC);
+  Stager stg;
+  const bool staged = rc == MK_OK && (page_a || page_b || page_c) && stg.prepare(cp);
+  // H2D of an r x r block (ready -> event `done`), or D2H once `ready` has completed
+  auto copy = [&](double* dst, int64_t dld, const double* src, int64_t sld, int64_t r, cudaMemcpyKind kind,
+                  cudaEvent_t done, const char* what, cudaEvent_t ready = nullptr) {
+    if (rc != MK_OK) return;
+    const bool up = kind == cudaMemcpyHostToDevice;
+    const bool via = staged && (up ? ((src >= hA && page_a && (src < hA + (size_t)lda * n)) ||
+                                      (src >= hB && page_b && (src < hB + (size_t)ldb * n)))
+                                   : page_c);
+    cudaError_t ce = cudaSuccess;
+    if (via) {
+      ce = up ? stg.upload(dst, dld, src, sld, r, r, done) : stg.download(dst, dld, src, sld, r, r, ready);
+    } else {
+      if (ready) ce = cudaStreamWaitEvent(cp, ready, 0);
+      if (ce == cudaSuccess) ce = cudaMemcpy2DAsync(dst, dld * 8, src, sld * 8, r * 8, r, kind, cp);
+      if (ce == cudaSuccess && done) ce = cudaEventRecord(done, cp);
+    }
+    if (ce != cudaSuccess) rc = fail(MK_ERR_CUDA, std::string(what) + cudaGetErrorString(ce));
+  };
   // sub-block mode (L = 2): the 32 operand sub-blocks go up in the order the compute stream
   // first waits for them; otherwise the 8 quadrants in order of first use
   if (sub) {
@@ -1663,20 +1679,19 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
     for (int q : qs) {
       if (rc != MK_OK) break;
       if (!tail_split[q]) {
-        if (cudaStreamWaitEvent(cp, out_ev[q], 0) != cudaSuccess) rc = fail(MK_ERR_CUDA, "stream wait failed");
-        copy(quad_ptr(hC, ldc, q), ldc, quad_ptr(dC, ldd, q), ldd, h, cudaMemcpyDeviceToHost, nullptr, "download: ");
+        copy(quad_ptr(hC, ldc, q), ldc, quad_ptr(dC, ldd, q), ldd, h, cudaMemcpyDeviceToHost, nullptr, "download: ",
+             out_ev[q]);
         continue;
       }
-      for (int s : ss) {
-        if (rc == MK_OK && cudaStreamWaitEvent(cp, sub_out[4 * q + s], 0) != cudaSuccess)
-          rc = fail(MK_ERR_CUDA, "stream wait failed");
+      for (int s : ss)
         copy(sub_ptr(hC, ldc, q, s), ldc, sub_ptr(dC, ldd, q, s), ldd, hh, cudaMemcpyDeviceToHost, nullptr,
-             "download: ");
-      }
+             "download: ", sub_out[4 * q + s]);
     }
   }
   host_trace("downloads done", cp);
+  const cudaError_t fe = stg.finish();  // both staging streams (no-op when nothing was staged)
   cudaError_t se = cudaStreamSynchronize(cp);
+  if (se == cudaSuccess) se = fe;
   if (rc == MK_OK && se == cudaSuccess) se = cudaStreamSynchronize(st);
   if (rc == MK_OK && se != cudaSuccess) rc = fail(MK_ERR_CUDA, std::string("sync: ") + cudaGetErrorString(se));
   if (host_trace_on() && !g_host_trace.empty()) {

@@ -268,9 +268,10 @@ _copy_stream = None
 
 
 def _overlap_applies(a: MatrixView, b: MatrixView, c: MatrixView, levels: int, algo: str, dtype) -> bool:
-    """Whether the overlapped host path applies: FP64 operands and result in *pinned* host
-    memory (so the copies are true async DMA), large enough for transfers to matter, one of
-    the fused algorithms. MK_PIPELINE=0 disables it."""
+    """Whether the overlapped host path applies: FP64 host operands and result with unit column
+    stride (pinned memory is copied by DMA directly; pageable arrays go through the engine's
+    pinned bounce slots), large enough for transfers to matter, one of the fused algorithms.
+    MK_PIPELINE=0 disables it."""
     import os
 
     if os.environ.get("MK_PIPELINE", "1") == "0" or algo not in _PIPE_ALGOS or levels < 1:
@@ -279,19 +280,16 @@ def _overlap_applies(a: MatrixView, b: MatrixView, c: MatrixView, levels: int, a
         return False
     if not (a.dtype == b.dtype == c.dtype == np.float64) or not c.arr.flags.writeable or a.rows < 2048:
         return False
-    if any(v.arr.strides[1] != 8 for v in (a, b, c)):
-        return False
-    try:
-        return all(torch.from_numpy(v.arr).is_pinned() for v in (a, b, c))
-    except Exception:
-        return False
+    return all(v.arr.strides[1] == 8 and v.arr.strides[0] % 8 == 0 for v in (a, b, c))
 
 
 def _overlapped_host_product(algo: str, a: MatrixView, b: MatrixView, c: MatrixView, levels: int,
                              st: EngineStats) -> None:
-    """C = A B for pinned host operands through mk_strassen_host: quadrants go up on a copy
-    stream in order of first use, each top-level product starts as soon as the quadrants it
-    reads have landed, each C quadrant comes back as soon as its last contributor is done."""
+    """C = A B for host operands through mk_strassen_host: operand blocks go up on copy
+    streams in the order the compute first needs them, each top-level product (or child)
+    starts as soon as the blocks it reads have landed, each C block comes back as soon as its
+    last contributor is done. Pageable arrays are staged through pinned bounce slots by the
+    engine's host thread pool."""
     global _copy_stream
     lib = require_engine()
     n = a.rows

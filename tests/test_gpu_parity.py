@@ -426,21 +426,28 @@ def test_pipelined_host_path_matches_device_path():
 
 
 @pytest.mark.parametrize("algo", ["strassen", "winograd-block", "winograd-knuth", "winograd-knuth-8call"])
-@pytest.mark.parametrize("cut", [512, 256])
-def test_pipelined_host_path_exact(algo, cut):
-    """Overlapped host path (quadrant uploads, first/last products split into sub-block
-    transfers) on integer-valued pinned operands: bit-exact, and the result lands in place."""
+@pytest.mark.parametrize("cut", [1024, 512, 256])
+@pytest.mark.parametrize("pinned", [True, False])
+def test_pipelined_host_path_exact(algo, cut, pinned):
+    """Overlapped host path (L=1 quadrant uploads, L=2 sub-block uploads with child-by-child
+    products, L=3 breadth-first under each top-level product) on integer-valued host operands,
+    pinned (direct DMA) or plain pageable numpy arrays (pinned bounce slots + host thread pool):
+    bit-exact, the result lands in place, and the operand views are left intact."""
     import torch
 
     n = 2048
     r = np.random.default_rng(9)
     a = r.integers(-8, 9, (n, n)).astype(np.float64)
     b = r.integers(-8, 9, (n, n)).astype(np.float64)
-    ha, hb = torch.from_numpy(a).pin_memory(), torch.from_numpy(b).pin_memory()
-    hc = torch.full((n, n), float("nan"), dtype=torch.float64).pin_memory()
-    CALL[algo](pk.Matrix(ha.numpy()), pk.Matrix(hb.numpy()), pk.Matrix(hc.numpy()), pk.BasePolicy.naive_cutoff(cut))
+    if pinned:
+        ha, hb = torch.from_numpy(a.copy()).pin_memory().numpy(), torch.from_numpy(b.copy()).pin_memory().numpy()
+        hc = torch.full((n, n), float("nan"), dtype=torch.float64).pin_memory().numpy()
+    else:
+        ha, hb, hc = a.copy(), b.copy(), np.full((n, n), np.nan)
+    CALL[algo](pk.Matrix(ha), pk.Matrix(hb), pk.Matrix(hc), pk.BasePolicy.naive_cutoff(cut))
     assert pk.last_stats().h2d_bytes == 2 * n * n * 8 and pk.last_stats().path == "overlapped-host"
-    assert np.array_equal(hc.numpy(), a @ b)
+    assert np.array_equal(hc, a @ b)
+    assert np.array_equal(ha, a) and np.array_equal(hb, b)
 
 
 @pytest.mark.parametrize("algo", ["strassen", "winograd-block", "winograd-knuth", "winograd-knuth-8call",
