@@ -82,54 +82,83 @@ cudaError_t launch_combine(double* dst, int64_t ldd, const double* const* src, c
 }
 
 // Batched quadrant transform: blockIdx.y = job, grid-stride over the job's elements. Each
-// thread reads every source once (16-byte vectors when VEC) and writes every destination.
-template <bool VEC>
+// thread reads every source once (W consecutive doubles: 8, 16 or 32-byte accesses) and
+// writes every destination.
+template <int W>
+struct Vec {
+  double v[W];
+};
+template <int W>
+__device__ __forceinline__ Vec<W> ld_vec(const double* p) {
+  Vec<W> r;
+  if constexpr (W == 4) {
+    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3])
+                 : "l"(p));
+  } else if constexpr (W == 2) {
+    const double2 t = __ldg(reinterpret_cast<const double2*>(p));
+    r.v[0] = t.x;
+    r.v[1] = t.y;
+  } else {
+    r.v[0] = __ldg(p);
+  }
+  return r;
+}
+template <int W>
+__device__ __forceinline__ void st_vec(double* p, const Vec<W>& r) {
+  if constexpr (W == 4) {
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(r.v[0]), "d"(r.v[1]), "d"(r.v[2]),
+                 "d"(r.v[3])
+                 : "memory");
+  } else if constexpr (W == 2) {
+    *reinterpret_cast<double2*>(p) = make_double2(r.v[0], r.v[1]);
+  } else {
+    *p = r.v[0];
+  }
+}
+
+template <int W>
 __global__ void __launch_bounds__(256) xform_kernel(const MkXformJob* __restrict__ jobs, int64_t rows, int64_t cols) {
   const MkXformJob& jb = jobs[blockIdx.y];
   const int ns = jb.nsrc, nd = jb.ndst;
-  const int64_t cv = VEC ? (cols >> 1) : cols;
+  const int64_t cv = cols / W;
   // rows x cv < 2^32 for every block the planner forms (checked by the launcher)
   const uint32_t total = (uint32_t)(rows * cv), ucv = (uint32_t)cv;
   for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
     const uint32_t r = idx / ucv;
-    const int64_t c = (int64_t)(idx - r * ucv) * (VEC ? 2 : 1);
-    double2 v[MK_XFORM_MAX];
+    const int64_t c = (int64_t)(idx - r * ucv) * W;
+    Vec<W> v[MK_XFORM_MAX];
 #pragma unroll
-    for (int i = 0; i < MK_XFORM_MAX; ++i) {
-      if (i < ns) {
-        const double* p = jb.src[i] + r * jb.lds[i] + c;
-        v[i] = VEC ? __ldg(reinterpret_cast<const double2*>(p)) : make_double2(__ldg(p), 0.0);
-      }
-    }
+    for (int i = 0; i < MK_XFORM_MAX; ++i)
+      if (i < ns) v[i] = ld_vec<W>(jb.src[i] + r * jb.lds[i] + c);
 #pragma unroll
     for (int j = 0; j < MK_XFORM_MAX; ++j) {
       if (j < nd) {
-        double2 acc = make_double2(0.0, 0.0);
+        Vec<W> acc;
+#pragma unroll
+        for (int u = 0; u < W; ++u) acc.v[u] = 0.0;
 #pragma unroll
         for (int i = 0; i < MK_XFORM_MAX; ++i) {
           const int cf = i < ns ? jb.coef[j][i] : 0;  // job-uniform: zero terms are skipped,
           if (cf > 0) {                               // so an inf elsewhere cannot become NaN
-            acc.x += v[i].x;
-            acc.y += v[i].y;
+#pragma unroll
+            for (int u = 0; u < W; ++u) acc.v[u] += v[i].v[u];
           } else if (cf < 0) {
-            acc.x -= v[i].x;
-            acc.y -= v[i].y;
+#pragma unroll
+            for (int u = 0; u < W; ++u) acc.v[u] -= v[i].v[u];
           }
         }
-        double* q = jb.dst[j] + r * jb.ldd[j] + c;
-        if (VEC)
-          *reinterpret_cast<double2*>(q) = acc;
-        else
-          *q = acc.x;
+        st_vec<W>(jb.dst[j] + r * jb.ldd[j] + c, acc);
       }
     }
   }
 }
 
-cudaError_t launch_xform_batch(const MkXformJob* jobs_dev, int njobs, int64_t rows, int64_t cols, bool vec,
+cudaError_t launch_xform_batch(const MkXformJob* jobs_dev, int njobs, int64_t rows, int64_t cols, int width,
                                cudaStream_t stream) {
   if (njobs <= 0 || rows <= 0 || cols <= 0) return cudaSuccess;
-  const int64_t work = rows * (vec ? cols / 2 : cols);
+  if (width != 4 && width != 2) width = 1;
+  const int64_t work = rows * (cols / width);
   if (work >= (int64_t)1 << 32) return cudaErrorInvalidValue;
   int64_t bx = (work + 255) / 256;
   const int64_t cap = (148 * 8 + njobs - 1) / njobs;  // ~8 resident CTAs per SM across all jobs
@@ -138,10 +167,12 @@ cudaError_t launch_xform_batch(const MkXformJob* jobs_dev, int njobs, int64_t ro
   for (int j0 = 0; j0 < njobs; j0 += 65535) {
     const int nj = njobs - j0 < 65535 ? njobs - j0 : 65535;
     dim3 grid((unsigned)bx, (unsigned)nj);
-    if (vec)
-      xform_kernel<true><<<grid, 256, 0, stream>>>(jobs_dev + j0, rows, cols);
+    if (width == 4)
+      xform_kernel<4><<<grid, 256, 0, stream>>>(jobs_dev + j0, rows, cols);
+    else if (width == 2)
+      xform_kernel<2><<<grid, 256, 0, stream>>>(jobs_dev + j0, rows, cols);
     else
-      xform_kernel<false><<<grid, 256, 0, stream>>>(jobs_dev + j0, rows, cols);
+      xform_kernel<1><<<grid, 256, 0, stream>>>(jobs_dev + j0, rows, cols);
   }
   return cudaGetLastError();
 }

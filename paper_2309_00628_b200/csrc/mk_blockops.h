@@ -39,7 +39,7 @@ cudaError_t launch_absmax_f64(const double* src, int64_t lds, int64_t rows, int6
 cudaError_t launch_absmax_i64(const int64_t* src, int64_t lds, int64_t rows, int64_t cols,
                               unsigned long long* out, cudaStream_t stream);
 // jobs_dev: device array of njobs jobs (identical rows x cols).
-cudaError_t launch_xform_batch(const MkXformJob* jobs_dev, int njobs, int64_t rows, int64_t cols, bool vec,
+cudaError_t launch_xform_batch(const MkXformJob* jobs_dev, int njobs, int64_t rows, int64_t cols, int width,
                                cudaStream_t stream);
 cudaError_t measure_dmma_peak(double* tflops_out, cudaStream_t st);
 cudaError_t launch_fused_product(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,

@@ -272,6 +272,17 @@ static bool fuse_preadds_default() {
   return g_fuse_preadds == 1;
 }
 
+// Widest batched-transform access in doubles (env MK_XFORM_WIDTH: 1, 2 or 4; default 4).
+static int xform_max_width() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MK_XFORM_WIDTH");
+    v = e ? atoi(e) : 4;
+    if (v != 1 && v != 2) v = 4;
+  }
+  return v;
+}
+
 static bool async_epilogue_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -951,17 +962,22 @@ struct Engine {
 
   int xform_batch(std::vector<MkXformJob>& jobs, int64_t rows, int64_t cols) {
     if (jobs.empty()) return MK_OK;
-    bool vec = cols % 2 == 0;
-    for (const MkXformJob& j : jobs) {
-      for (int i = 0; i < j.nsrc; ++i)
-        vec = vec && j.lds[i] % 2 == 0 && reinterpret_cast<uintptr_t>(j.src[i]) % 16 == 0;
-      for (int i = 0; i < j.ndst; ++i)
-        vec = vec && j.ldd[i] % 2 == 0 && reinterpret_cast<uintptr_t>(j.dst[i]) % 16 == 0;
+    // widest access (4, 2 or 1 doubles) every source and destination row allows
+    int width = xform_max_width();
+    while (width > 1) {
+      bool ok = cols % width == 0;
+      const uintptr_t al = (uintptr_t)width * 8;
+      for (const MkXformJob& j : jobs) {
+        for (int i = 0; i < j.nsrc; ++i) ok = ok && j.lds[i] % width == 0 && reinterpret_cast<uintptr_t>(j.src[i]) % al == 0;
+        for (int i = 0; i < j.ndst; ++i) ok = ok && j.ldd[i] % width == 0 && reinterpret_cast<uintptr_t>(j.dst[i]) % al == 0;
+      }
+      if (ok) break;
+      width /= 2;
     }
     void* dev = nullptr;
     MK_TRY(upload(jobs.data(), jobs.size() * sizeof(MkXformJob), &dev));
     if (dry || no_launch) return MK_OK;
-    MK_CUDA_TRY(launch_xform_batch(static_cast<const MkXformJob*>(dev), (int)jobs.size(), rows, cols, vec, st));
+    MK_CUDA_TRY(launch_xform_batch(static_cast<const MkXformJob*>(dev), (int)jobs.size(), rows, cols, width, st));
     ++g_launch_count;
     return MK_OK;
   }
