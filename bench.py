@@ -384,6 +384,39 @@ def main():
                          "actual_tflops": round(actual_flops(n, lv, args.algo) / (ams * 1e-3) / 1e12, 4),
                          "workspace_bytes": int(lib.mk_workspace_bytes(_lib.ALGO_IDS[args.algo], n, lv))})
         line["alt_cutoffs"] = alts
+    if world == 1 and args.alt:
+        # peak-workspace trade-off at the bench config: the memory-lean plans, same inputs
+        def timed(fn, reps=2):
+            fn()
+            torch.cuda.synchronize()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            for _ in range(reps):
+                fn()
+            g1.record(stream)
+            torch.cuda.synchronize()
+            return g0.elapsed_time(g1) / reps
+
+        lean = []
+        try:
+            pk.set_plan("depth-first", two_temp_tail=False)
+            ms_dfs = timed(lambda: pk.winograd_block_mul(A, B, C, policy))
+            lean.append({"variant": "winograd-block, depth-first plan (P_i accumulated into C by the epilogue)",
+                         "ms_per_step": round(ms_dfs, 3), "value": round(2.0 * n ** 3 / (ms_dfs * 1e-3) / 1e12, 4),
+                         "workspace_bytes": int(lib.mk_workspace_bytes(_lib.ALGO_IDS[args.algo], n, levels))})
+            ms_tt = timed(lambda: pk.two_temp_winograd(A, B, C, policy))
+            lean.append({"variant": "two-temp, literal Table-2 schedule to the leaves",
+                         "ms_per_step": round(ms_tt, 3), "value": round(2.0 * n ** 3 / (ms_tt * 1e-3) / 1e12, 4),
+                         "workspace_bytes": int(lib.mk_workspace_bytes(_lib.ALGO_IDS["two-temp"], n, levels))})
+        finally:
+            pk.set_plan()
+        a2, b2 = da.clone(), db.clone()
+        ms_ip = timed(lambda: pk.in_place_winograd(pk.Matrix(a2), pk.Matrix(b2), C, policy))
+        lean.append({"variant": "in-place, literal Table-3 schedule (inputs clobbered)",
+                     "ms_per_step": round(ms_ip, 3), "value": round(2.0 * n ** 3 / (ms_ip * 1e-3) / 1e12, 4),
+                     "workspace_bytes": int(lib.mk_workspace_bytes(_lib.ALGO_IDS["in-place"], n, levels))})
+        del a2, b2
+        line["memory_lean"] = lean
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, levels)
     print(json.dumps(line), flush=True)

@@ -53,10 +53,17 @@ enum mk_algo {
 /* Engine version: (major << 16) | minor. */
 int mk_version(void);
 
-/* Engine options (process-wide). MK_OPT_FUSE_PREADDS: 1 = form the last level's operand
- * sums inside the DMMA kernel (K2 combiner), 0 = materialise them with HBM-bound block
- * kernels first (default; measured faster on B200). */
-enum mk_option { MK_OPT_FUSE_PREADDS = 1 };
+/* Engine options (process-wide).
+ * MK_OPT_FUSE_PREADDS: 1 = form the last level's operand sums inside the DMMA kernel (K2
+ *   combiner), 0 = materialise them with HBM-bound block kernels first (default; measured
+ *   faster on B200).
+ * MK_OPT_PLAN (strassen / winograd kinds, L >= 2): 0 = breadth-first (default: batched leaves,
+ *   fastest, largest workspace), 1 = depth-first (workspace-minimal: operand sums only, P_i
+ *   accumulated straight into C by the epilogue).
+ * MK_OPT_LITERAL_TAIL (two-temp): 1 = run the last two levels breadth-first under the literal
+ *   Table-2 levels (default), 0 = the literal schedule down to the leaves (2 (n/2)^2-style
+ *   scratch only, the paper's memory bound). */
+enum mk_option { MK_OPT_FUSE_PREADDS = 1, MK_OPT_PLAN = 2, MK_OPT_LITERAL_TAIL = 3 };
 int mk_set_option(int key, int value);
 
 /* Instrumentation (bench.py). mk_launch_count: kernels this thread has launched so far.

@@ -292,13 +292,14 @@ static bool async_epilogue_enabled() {
   return v == 1;
 }
 
+// MK_OPT_LITERAL_TAIL / MK_OPT_PLAN (mk_set_option); -1 = take the environment default
+static int g_literal_tail = -1, g_plan_dfs = -1;
 static bool literal_bfs_tail() {
-  static int v = -1;
-  if (v < 0) {
+  if (g_literal_tail < 0) {
     const char* e = getenv("MK_LITERAL_TAIL");
-    v = (e && e[0] == '0') ? 0 : 1;
+    g_literal_tail = (e && e[0] == '0') ? 0 : 1;
   }
-  return v == 1;
+  return g_literal_tail == 1;
 }
 
 static bool debug_sync() {
@@ -1258,8 +1259,11 @@ static bool use_bfs(const Engine& e, int64_t lm, int64_t ln) {
   (void)ln;
   if (e.fuse_preadds || e.leaf_count >= 0 || e.L < 2) return false;
   if (e.algo < MK_ALGO_STRASSEN || e.algo > MK_ALGO_WINOGRAD_KNUTH_8CALL) return false;
-  const char* env = getenv("MK_PLAN");
-  return !(env && std::string(env) == "dfs");
+  if (g_plan_dfs < 0) {
+    const char* env = getenv("MK_PLAN");
+    g_plan_dfs = (env && std::string(env) == "dfs") ? 1 : 0;
+  }
+  return g_plan_dfs == 0;
 }
 
 static int run_square(Engine& e) {
@@ -1332,6 +1336,15 @@ int mk_set_option(int key, int value) {
   g_last_error.clear();
   if (key == MK_OPT_FUSE_PREADDS) {
     g_fuse_preadds = value ? 1 : 0;
+    return MK_OK;
+  }
+  if (key == MK_OPT_PLAN) {
+    if (value != 0 && value != 1) return fail(MK_ERR_ARG, "MK_OPT_PLAN takes 0 (breadth-first) or 1 (depth-first)");
+    g_plan_dfs = value;
+    return MK_OK;
+  }
+  if (key == MK_OPT_LITERAL_TAIL) {
+    g_literal_tail = value ? 1 : 0;
     return MK_OK;
   }
   return fail(MK_ERR_ARG, "unknown option key");

@@ -53,6 +53,23 @@ def require_engine():
     return _lib.load(required=True)
 
 
+def set_plan(plan: str = "breadth-first", two_temp_tail: bool = True) -> None:
+    """Process-wide engine plan (B200 addition; the reference has no counterpart).
+
+    ``plan``: "breadth-first" (default for >= 2 levels: batched leaf launches, fastest, largest
+    workspace) or "depth-first" (workspace-minimal: operand sums only, each P_i accumulated
+    straight into C by the leaf epilogue). ``two_temp_tail``: two_temp_winograd runs its last two
+    levels breadth-first (default) or the literal Table-2 schedule down to the leaves (the paper's
+    2 x (n/2)^2-per-level scratch bound). Results are unchanged on integer data; float results
+    differ only in summation order. Modeled OpCounter values never change.
+    """
+    if plan not in ("breadth-first", "depth-first"):
+        raise ValueError(f"plan must be 'breadth-first' or 'depth-first', got {plan!r}")
+    lib = _lib.load(required=True)
+    _lib.check(lib.mk_set_option(_lib.MK_OPT_PLAN, 1 if plan == "depth-first" else 0), "mk_set_option")
+    _lib.check(lib.mk_set_option(_lib.MK_OPT_LITERAL_TAIL, 1 if two_temp_tail else 0), "mk_set_option")
+
+
 def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 

@@ -85,6 +85,21 @@ def test_workspace_sizes(lib):
     assert lib.mk_rect_workspace_bytes(_lib.ALGO_IDS["winograd-block"], 12000, 10000, 14000, 5) > 0
 
 
+def test_plan_options_change_workspace_not_counts(lib):
+    ws = lambda algo, n, L: lib.mk_workspace_bytes(_lib.ALGO_IDS[algo], n, L)  # noqa: E731
+    try:
+        assert lib.mk_set_option(_lib.MK_OPT_PLAN, 1) == 0  # depth-first: operand sums only
+        assert ws("winograd-block", 16384, 2) == (2 * 8192 ** 2 + 2 * 4096 ** 2) * 8
+        assert lib.mk_set_option(_lib.MK_OPT_PLAN, 0) == 0
+        assert ws("winograd-block", 16384, 2) > 7 * 16384 ** 2 * 8  # breadth-first: every depth
+        assert lib.mk_set_option(_lib.MK_OPT_LITERAL_TAIL, 0) == 0  # two-temp literal to the leaves
+        assert ws("two-temp", 16384, 2) == (2 * 8192 ** 2 + 2 * 4096 ** 2) * 8
+        assert lib.mk_set_option(_lib.MK_OPT_PLAN, 7) == _lib.MK_ERR_ARG
+    finally:
+        lib.mk_set_option(_lib.MK_OPT_PLAN, 0)
+        lib.mk_set_option(_lib.MK_OPT_LITERAL_TAIL, 1)
+
+
 def test_product_counts(lib):
     assert lib.mk_product_count(_lib.ALGO_IDS["winograd-block"], 2) == 49
     assert lib.mk_product_count(_lib.ALGO_IDS["winograd-knuth-8call"], 1) == 8

@@ -425,6 +425,35 @@ def test_pipelined_host_path_matches_device_path():
     assert err <= tol(n, ha.numpy(), hb.numpy()) and err < 1e-11, err
 
 
+@pytest.mark.parametrize("plan,tail", [("depth-first", True), ("breadth-first", False)])
+def test_memory_lean_plans_exact(plan, tail):
+    """set_plan: the workspace-minimal depth-first plan and the literal two-temp schedule give
+    bit-exact integer results, smaller workspaces, unchanged modeled counters."""
+    n = 512
+    r = np.random.default_rng(21)
+    a = r.integers(-8, 9, (n, n)).astype(np.float64)
+    b = r.integers(-8, 9, (n, n)).astype(np.float64)
+    want = a @ b
+    pol = pk.BasePolicy.naive_cutoff(32)  # 4 levels
+    base = {}
+    for algo in ("strassen", "winograd-block", "two-temp"):
+        c = pk.Matrix.zeros(n, n)
+        ctr = CALL[algo](pk.Matrix(a), pk.Matrix(b), c, pol)
+        base[algo] = (ctr.snapshot(), pk.last_stats().workspace_bytes)
+    try:
+        pk.set_plan(plan, two_temp_tail=tail)
+        for algo in ("strassen", "winograd-block", "two-temp"):
+            c = pk.Matrix.zeros(n, n)
+            ctr = CALL[algo](pk.Matrix(a), pk.Matrix(b), c, pol)
+            assert np.array_equal(c.arr, want), (plan, algo)
+            assert ctr.snapshot() == base[algo][0]
+            lean = (plan == "depth-first") if algo != "two-temp" else (not tail)
+            if lean:
+                assert pk.last_stats().workspace_bytes < base[algo][1], (plan, algo)
+    finally:
+        pk.set_plan()
+
+
 @pytest.mark.parametrize("algo", ["strassen", "winograd-block", "winograd-knuth", "winograd-knuth-8call"])
 @pytest.mark.parametrize("cut", [1024, 512, 256])
 @pytest.mark.parametrize("pinned", [True, False])
