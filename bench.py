@@ -152,6 +152,19 @@ def cpu_sample_seconds(n_sample, cutoff_sample, algo):
     return time.perf_counter() - t0
 
 
+def all_host_threads():
+    """Context raising the BLAS pool to every host core: torchrun exports OMP_NUM_THREADS=1 to
+    its ranks, and the reference's CPU path should still use the whole host."""
+    try:
+        from threadpoolctl import threadpool_limits
+
+        return threadpool_limits(limits=os.cpu_count() or 1, user_api="blas")
+    except Exception:  # pragma: no cover
+        import contextlib
+
+        return contextlib.nullcontext()
+
+
 def blas_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -164,14 +177,16 @@ def blas_threads():
 def cpu_baseline(args, levels):
     n_s = args.n // 2
     cut_s = n_s >> levels
-    # warm numpy/OpenBLAS once on a small case
-    cpu_sample_seconds(512, 128, args.algo)
-    t = cpu_sample_seconds(n_s, cut_s, args.algo)
+    with all_host_threads():
+        # warm numpy/OpenBLAS once on a small case
+        cpu_sample_seconds(512, 128, args.algo)
+        t = cpu_sample_seconds(n_s, cut_s, args.algo)
+        cores = blas_threads()
     return {
-        "value": round(2.0 * n_s ** 3 / t / 1e12, 4), "unit": UNIT, "cores": blas_threads(), "kind": "port",
+        "value": round(2.0 * n_s ** 3 / t / 1e12, 4), "unit": UNIT, "cores": cores, "kind": "port",
         "sample": f"oracle (numpy restatement of matmulkit, bit-identical) {args.algo} n={n_s} "
                   f"naive_cutoff({cut_s}) = same {levels}-level recursion at 1/8 the flops; "
-                  f"OpenBLAS leaves on {blas_threads()} threads, block adds single-threaded; {t:.2f} s",
+                  f"OpenBLAS leaves on {cores} threads, block adds single-threaded; {t:.2f} s",
         "seconds": round(t, 3),
     }
 
@@ -183,10 +198,12 @@ def run_reference(args):
         return
     n_s = args.n // 2
     cut_s = n_s >> levels
-    cpu_sample_seconds(512, 128, args.algo)
-    for _ in range(args.warmup):
-        cpu_sample_seconds(n_s, cut_s, args.algo)
-    ts = [cpu_sample_seconds(n_s, cut_s, args.algo) for _ in range(args.steps)]
+    with all_host_threads():
+        cpu_sample_seconds(512, 128, args.algo)
+        for _ in range(args.warmup):
+            cpu_sample_seconds(n_s, cut_s, args.algo)
+        ts = [cpu_sample_seconds(n_s, cut_s, args.algo) for _ in range(args.steps)]
+        cores = blas_threads()
     ms = 1e3 * sum(ts) / len(ts)
     value = 2.0 * n_s ** 3 / (ms * 1e-3) / 1e12
     line = {
@@ -194,7 +211,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 2), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded standard normal)",
         "config": config(args, levels),
-        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": blas_threads(), "kind": "port",
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"oracle {args.algo} n={n_s} naive_cutoff({cut_s}) per step (bounded sample of "
                                    f"the n={args.n} workload, same recursion depth); host cores only"},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -360,7 +377,8 @@ def main():
         "config": config(args, levels),
         "actual_tflops": round(f_act / (ms * 1e-3) / 1e12, 4),
         "frac_of_fp64_peak_actual": round(f_act / (ms * 1e-3) / 1e12 / peak_tflops, 4),
-        "workspace_bytes": int(lib.mk_workspace_bytes(_lib.ALGO_IDS[args.algo], n, levels)),
+        "workspace_bytes": int(lib.mk_workspace_bytes(_lib.ALGO_IDS[args.algo], n, levels) if world == 1
+                               else lib.mk_partial_workspace_bytes(_lib.ALGO_IDS[args.algo], n, levels)),
         "peak_mem_delta_bytes": int(peak_mem),
         "roofline": roofline, "clocks": clocks, "gpu_launches": int(launches), "e2e": e2e,
     }
