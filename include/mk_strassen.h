@@ -65,6 +65,7 @@ int mk_version(void);
  *   scratch only, the paper's memory bound). */
 enum mk_option { MK_OPT_FUSE_PREADDS = 1, MK_OPT_PLAN = 2, MK_OPT_LITERAL_TAIL = 3 };
 int mk_set_option(int key, int value);
+int mk_get_option(int key, int* value);
 
 /* Instrumentation (bench.py). mk_launch_count: kernels this thread has launched so far.
  * mk_timing_begin / mk_timing_end: bracket engine calls; every leaf-product (DMMA) launch in

@@ -42,6 +42,7 @@ SIGNATURES = {
     "mk_timing_end": (_INT, [_DP, ctypes.POINTER(_INT), _DP]),
     "mk_fp64_peak": (_INT, [_DP, _VP]),
     "mk_set_option": (_INT, [_INT, _INT]),
+    "mk_get_option": (_INT, [_INT, ctypes.POINTER(ctypes.c_int)]),
     "mk_last_error": (ctypes.c_char_p, []),
     "mk_dgemm": (_INT, [_VP, _I64, _VP, _I64, _VP, _I64, _I64, _I64, _I64, _VP]),
     "mk_levels_for_policy": (_INT, [_I64, _INT, _I64, _INT, ctypes.POINTER(_INT)]),

@@ -301,6 +301,13 @@ static bool literal_bfs_tail() {
   }
   return g_literal_tail == 1;
 }
+static bool plan_dfs() {
+  if (g_plan_dfs < 0) {
+    const char* env = getenv("MK_PLAN");
+    g_plan_dfs = (env && std::string(env) == "dfs") ? 1 : 0;
+  }
+  return g_plan_dfs == 1;
+}
 
 static bool debug_sync() {
   static int v = -1;
@@ -708,7 +715,7 @@ struct Engine {
       if (!dry && !no_launch && ev) MK_CUDA_TRY(cudaEventRecord(ev, st));
       return MK_OK;
     };
-    const bool inner_bfs = L >= 3 && !fuse_preadds;
+    const bool inner_bfs = L >= 3 && !fuse_preadds && !plan_dfs();  // depth-first on request
     for (int i = 0; i < np; ++i) {
       const int p = order[i];
       const bool split = !inner_bfs && sub_in != nullptr && L >= 2 && split_fits(p);
@@ -1259,11 +1266,7 @@ static bool use_bfs(const Engine& e, int64_t lm, int64_t ln) {
   (void)ln;
   if (e.fuse_preadds || e.leaf_count >= 0 || e.L < 2) return false;
   if (e.algo < MK_ALGO_STRASSEN || e.algo > MK_ALGO_WINOGRAD_KNUTH_8CALL) return false;
-  if (g_plan_dfs < 0) {
-    const char* env = getenv("MK_PLAN");
-    g_plan_dfs = (env && std::string(env) == "dfs") ? 1 : 0;
-  }
-  return g_plan_dfs == 0;
+  return !plan_dfs();
 }
 
 static int run_square(Engine& e) {
@@ -1348,6 +1351,21 @@ int mk_set_option(int key, int value) {
     return MK_OK;
   }
   return fail(MK_ERR_ARG, "unknown option key");
+}
+
+int mk_get_option(int key, int* value) {
+  g_last_error.clear();
+  if (!value) return fail(MK_ERR_ARG, "null output");
+  if (key == MK_OPT_FUSE_PREADDS) {
+    *value = fuse_preadds_default() ? 1 : 0;
+  } else if (key == MK_OPT_PLAN) {
+    *value = plan_dfs() ? 1 : 0;
+  } else if (key == MK_OPT_LITERAL_TAIL) {
+    *value = literal_bfs_tail() ? 1 : 0;
+  } else {
+    return fail(MK_ERR_ARG, "unknown option key");
+  }
+  return MK_OK;
 }
 
 const char* mk_last_error(void) { return g_last_error.c_str(); }

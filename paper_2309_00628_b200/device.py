@@ -17,6 +17,7 @@ torch CUDA stream, and results are written back to wherever the caller's output 
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import threading
 
@@ -250,6 +251,43 @@ def workspace(nbytes: int):
     return torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device="cuda")
 
 
+_plan_lock = threading.Lock()
+_WS_MARGIN = 256 << 20
+
+
+def _fits(nbytes: int) -> bool:
+    """Whether a workspace of nbytes can be allocated now (free device memory plus what torch's
+    caching allocator holds unused)."""
+    free, _ = torch.cuda.mem_get_info()
+    slack = torch.cuda.memory_reserved() - torch.cuda.memory_allocated()
+    return nbytes + _WS_MARGIN <= free + slack
+
+
+@contextlib.contextmanager
+def _memory_aware_plan(size_of):
+    """Yield the workspace size for this call. When the configured plan's workspace does not fit
+    in device memory, the call runs with the workspace-minimal options instead (depth-first plan,
+    literal two-temp schedule; same results on integer data) and the options are restored."""
+    need = int(size_of())
+    if _fits(need):
+        yield need
+        return
+    lib = _lib.load(required=True)
+    with _plan_lock:
+        old = []
+        for key in (_lib.MK_OPT_PLAN, _lib.MK_OPT_LITERAL_TAIL):
+            v = ctypes.c_int(0)
+            _lib.check(lib.mk_get_option(key, ctypes.byref(v)), "mk_get_option")
+            old.append((key, v.value))
+        try:
+            lib.mk_set_option(_lib.MK_OPT_PLAN, 1)
+            lib.mk_set_option(_lib.MK_OPT_LITERAL_TAIL, 0)
+            yield int(size_of())
+        finally:
+            for key, v in old:
+                lib.mk_set_option(key, v)
+
+
 # ---------------------------------------------------------------------------------
 # Engine calls
 # ---------------------------------------------------------------------------------
@@ -317,17 +355,21 @@ def _overlapped_host_product(algo: str, a: MatrixView, b: MatrixView, c: MatrixV
     dB = torch.empty((n, ld), dtype=torch.float64, device="cuda")
     dC = torch.empty((n, ld), dtype=torch.float64, device="cuda")
     aid = _lib.ALGO_IDS[algo]
-    ws_bytes = int(lib.mk_host_workspace_bytes(aid, n, levels))
-    ws = workspace(ws_bytes)
-    st.workspace_bytes = ws_bytes
-    st.path = "overlapped-host"
-    rc = lib.mk_strassen_host(aid, ctypes.c_void_p(a.arr.ctypes.data), a.arr.strides[0] // 8,
-                              ctypes.c_void_p(b.arr.ctypes.data), b.arr.strides[0] // 8,
-                              ctypes.c_void_p(c.arr.ctypes.data), c.arr.strides[0] // 8, n, levels, _vp(dA), _vp(dB),
-                              _vp(dC), ld, _vp(ws), ws_bytes, _stream(), ctypes.c_void_p(_copy_stream.cuda_stream))
+    with _memory_aware_plan(lambda: lib.mk_host_workspace_bytes(aid, n, levels)) as ws_bytes:
+        ws = workspace(ws_bytes)
+        st.workspace_bytes = ws_bytes
+        st.path = "overlapped-host"
+        rc = _call_host(lib, aid, a, b, c, n, levels, dA, dB, dC, ld, ws, ws_bytes)
     _lib.check(rc, f"mk_strassen_host({algo})")
     st.h2d_bytes += 2 * n * n * 8
     st.d2h_bytes += n * n * 8
+
+
+def _call_host(lib, aid, a, b, c, n, levels, dA, dB, dC, ld, ws, ws_bytes):
+    return lib.mk_strassen_host(aid, ctypes.c_void_p(a.arr.ctypes.data), a.arr.strides[0] // 8,
+                                ctypes.c_void_p(b.arr.ctypes.data), b.arr.strides[0] // 8,
+                                ctypes.c_void_p(c.arr.ctypes.data), c.arr.strides[0] // 8, n, levels, _vp(dA), _vp(dB),
+                                _vp(dC), ld, _vp(ws), ws_bytes, _stream(), ctypes.c_void_p(_copy_stream.cuda_stream))
 
 
 def device_square(algo: str, a: MatrixView, b: MatrixView, c: MatrixView, levels: int, dtype,
@@ -352,10 +394,10 @@ def device_square(algo: str, a: MatrixView, b: MatrixView, c: MatrixView, levels
     out = Output(c, dtype, st)
     C = out.op
     aid = _lib.ALGO_IDS[algo]
-    ws_bytes = int(lib.mk_workspace_bytes(aid, n, levels))
-    st.workspace_bytes = ws_bytes
-    ws = workspace(ws_bytes)
-    rc = lib.mk_strassen(aid, A.ptr, A.ld, B.ptr, B.ld, C.ptr, C.ld, n, levels, _vp(ws), ws_bytes, _stream())
+    with _memory_aware_plan(lambda: lib.mk_workspace_bytes(aid, n, levels)) as ws_bytes:
+        st.workspace_bytes = ws_bytes
+        ws = workspace(ws_bytes)
+        rc = lib.mk_strassen(aid, A.ptr, A.ld, B.ptr, B.ld, C.ptr, C.ld, n, levels, _vp(ws), ws_bytes, _stream())
     _lib.check(rc, f"mk_strassen({algo})")
     out.finish()
     if clobber_inputs:
@@ -392,11 +434,11 @@ def device_rect(algo: str, a: MatrixView, b: MatrixView, c: MatrixView, levels: 
     out = Output(c, dtype, st)
     C = out.op
     aid = _lib.ALGO_IDS[algo]
-    ws_bytes = int(lib.mk_rect_workspace_bytes(aid, m, n, k, levels))
-    st.workspace_bytes = ws_bytes
-    ws = workspace(ws_bytes)
-    rc = lib.mk_multiply_rect(aid, A.ptr, A.ld, B.ptr, B.ld, C.ptr, C.ld, m, n, k, levels, _vp(ws), ws_bytes,
-                              _stream())
+    with _memory_aware_plan(lambda: lib.mk_rect_workspace_bytes(aid, m, n, k, levels)) as ws_bytes:
+        st.workspace_bytes = ws_bytes
+        ws = workspace(ws_bytes)
+        rc = lib.mk_multiply_rect(aid, A.ptr, A.ld, B.ptr, B.ld, C.ptr, C.ld, m, n, k, levels, _vp(ws), ws_bytes,
+                                  _stream())
     _lib.check(rc, f"mk_multiply_rect({algo})")
     out.finish()
 

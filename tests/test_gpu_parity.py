@@ -425,6 +425,32 @@ def test_pipelined_host_path_matches_device_path():
     assert err <= tol(n, ha.numpy(), hb.numpy()) and err < 1e-11, err
 
 
+def test_memory_aware_plan_fallback(monkeypatch):
+    """When the breadth-first workspace does not fit in free device memory the call runs with the
+    workspace-minimal plan (bit-exact on integer data) and the process-wide options are restored."""
+    import ctypes
+
+    from paper_2309_00628_b200 import _lib, device
+
+    n = 1024
+    r = np.random.default_rng(5)
+    a = r.integers(-8, 9, (n, n)).astype(np.float64)
+    b = r.integers(-8, 9, (n, n)).astype(np.float64)
+    lib = _lib.load()
+    lean = lib.mk_set_option(_lib.MK_OPT_PLAN, 1) or lib.mk_workspace_bytes(_lib.ALGO_IDS["winograd-block"], n, 4)
+    lib.mk_set_option(_lib.MK_OPT_PLAN, 0)
+    full = lib.mk_workspace_bytes(_lib.ALGO_IDS["winograd-block"], n, 4)
+    assert lean < full
+    monkeypatch.setattr(device, "_fits", lambda nbytes: nbytes <= lean)
+    c = pk.Matrix.zeros(n, n)
+    pk.winograd_block_mul(pk.Matrix(a), pk.Matrix(b), c, pk.BasePolicy.naive_cutoff(64))
+    assert pk.last_stats().workspace_bytes == lean
+    assert np.array_equal(c.arr, a @ b)
+    v = ctypes.c_int(-1)
+    assert lib.mk_get_option(_lib.MK_OPT_PLAN, ctypes.byref(v)) == 0 and v.value == 0
+    assert lib.mk_get_option(_lib.MK_OPT_LITERAL_TAIL, ctypes.byref(v)) == 0 and v.value == 1
+
+
 @pytest.mark.parametrize("plan,tail", [("depth-first", True), ("breadth-first", False)])
 def test_memory_lean_plans_exact(plan, tail):
     """set_plan: the workspace-minimal depth-first plan and the literal two-temp schedule give
