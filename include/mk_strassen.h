@@ -118,6 +118,15 @@ int mk_multiply_rect(int algo, const double* A, int64_t lda, const double* B, in
                      int64_t ldc, int64_t m, int64_t n, int64_t k, int levels, void* ws, size_t ws_bytes,
                      void* stream);
 
+/* Synchronous block copies of 8-byte elements (rows x cols, leading dimensions in elements)
+ * between host and device, ordered after prior work on `stream`. Pageable host memory is
+ * staged through pinned bounce slots with parallel host copies on two streams (several times
+ * the driver's pageable path); pinned memory is copied directly. */
+int mk_copy_to_device(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows, int64_t cols,
+                      void* stream);
+int mk_copy_to_host(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows, int64_t cols,
+                    void* stream);
+
 /* Workspace bytes mk_strassen_host needs for (algo, n, levels) (0 on invalid input): the
  * depth-first plan's for L <= 2, a breadth-first plan per top-level product for L >= 3. */
 size_t mk_host_workspace_bytes(int algo, int64_t n, int levels);

@@ -58,6 +58,8 @@ SIGNATURES = {
     "mk_product_count": (_INT, [_INT, _INT]),
     "mk_partial_workspace_bytes": (_SZ, [_INT, _I64, _INT]),
     "mk_host_workspace_bytes": (_SZ, [_INT, _I64, _INT]),
+    "mk_copy_to_device": (_INT, [_VP, _I64, _VP, _I64, _I64, _I64, _VP]),
+    "mk_copy_to_host": (_INT, [_VP, _I64, _VP, _I64, _I64, _I64, _VP]),
     "mk_strassen_host": (_INT, [_INT, _VP, _I64, _VP, _I64, _VP, _I64, _I64, _INT, _VP, _VP, _VP, _I64, _VP, _SZ,
                                 _VP, _VP]),
     "mk_overlap_order": (_INT, [_INT, ctypes.POINTER(_INT), ctypes.POINTER(_INT)]),

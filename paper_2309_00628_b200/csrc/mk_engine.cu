@@ -1558,6 +1558,45 @@ static std::vector<int> cached_head_children(int algo, int p0) {
   return g_head_cache[algo] = head_child_order(coeffs_for(algo), p0);
 }
 
+// Synchronous host <-> device block copies for the staging of operands and results: pageable
+// host memory goes through the Stager (pinned bounce slots, parallel host copies, two streams),
+// pinned memory is copied directly. Ordered after prior work on `stream`.
+static int host_copy(bool up, double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows, int64_t cols,
+                     void* stream) {
+  g_last_error.clear();
+  if (rows < 0 || cols < 0) return fail(MK_ERR_DIMENSION, "negative extents");
+  if (rows == 0 || cols == 0) return MK_OK;
+  if (ldd < cols || lds < cols) return fail(MK_ERR_DIMENSION, "leading dimension smaller than the column count");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const void* host = up ? static_cast<const void*>(src) : static_cast<const void*>(dst);
+  if (is_pageable(host)) {
+    Stager stg;
+    if (stg.prepare(st)) {
+      cudaError_t e = up ? stg.upload(dst, ldd, src, lds, rows, cols, nullptr)
+                         : stg.download(dst, ldd, src, lds, rows, cols, nullptr);
+      const cudaError_t f = stg.finish();
+      if (e == cudaSuccess) e = f;
+      if (e != cudaSuccess) return fail(MK_ERR_CUDA, std::string("staged copy: ") + cudaGetErrorString(e));
+      return MK_OK;
+    }
+  }
+  cudaError_t e = cudaMemcpy2DAsync(dst, ldd * 8, src, lds * 8, cols * 8, rows,
+                                    up ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return fail(MK_ERR_CUDA, std::string("copy: ") + cudaGetErrorString(e));
+  return MK_OK;
+}
+
+int mk_copy_to_device(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows, int64_t cols,
+                      void* stream) {
+  return host_copy(true, dst, ldd, src, lds, rows, cols, stream);
+}
+
+int mk_copy_to_host(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows, int64_t cols,
+                    void* stream) {
+  return host_copy(false, dst, ldd, src, lds, rows, cols, stream);
+}
+
 size_t mk_host_workspace_bytes(int algo, int64_t n, int levels) {
   if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_WINOGRAD_KNUTH_8CALL || n < 2 || !is_pow2(n) || levels < 1 ||
       (n >> levels) < 2)

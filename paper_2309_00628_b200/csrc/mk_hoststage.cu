@@ -142,11 +142,13 @@ bool Stager::prepare(cudaStream_t s0) {
     sh.call_mu.unlock();
     return false;
   }
-  s_[0] = s0;
+  s_[0] = s0;  // may be the legacy default stream (0)
   s_[1] = sh.second;
+  active_ = true;
   // the second stream starts where the first one is
   cudaEvent_t e;
   if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+    active_ = false;
     sh.call_mu.unlock();
     return false;
   }
@@ -212,7 +214,7 @@ cudaError_t Stager::download(double* host, int64_t hld, const double* dev, int64
 
 cudaError_t Stager::finish() {
   cudaError_t e = cudaSuccess;
-  if (s_[0]) {
+  if (active_) {
     const cudaError_t e0 = cudaStreamSynchronize(s_[0]);
     const cudaError_t e1 = cudaStreamSynchronize(s_[1]);
     e = e0 != cudaSuccess ? e0 : e1;
@@ -220,6 +222,7 @@ cudaError_t Stager::finish() {
     temps_.clear();
     jobs_.clear();
     s_[0] = s_[1] = nullptr;
+    active_ = false;
     shared().call_mu.unlock();
   }
   return e;

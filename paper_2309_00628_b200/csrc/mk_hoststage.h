@@ -46,6 +46,7 @@ class Stager {
 
  private:
   cudaStream_t s_[2] = {nullptr, nullptr};
+  bool active_ = false;  // between a successful prepare() and finish()
   int next_ = 0;  // stream / slot of the next chunk
   std::vector<std::unique_ptr<Job>> jobs_;
   std::vector<cudaEvent_t> temps_;

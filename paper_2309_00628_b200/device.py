@@ -150,6 +150,19 @@ def stage_in(view: MatrixView, *, copy: bool = False, stats: EngineStats | None 
     src = torch.from_numpy(view.arr)  # strided host window; pinned if its storage is
     if stats is not None:
         stats.h2d_bytes += src.numel() * src.element_size()
+    if _staged_ok(view.arr):  # large 8-byte rows: the engine's staged copy (bounce slots)
+        lib = require_engine()
+        if src.dtype == torch.float64:
+            out = _fresh(rows, cols)
+            _lib.check(lib.mk_copy_to_device(_vp(out), out.stride(0), ctypes.c_void_p(view.arr.ctypes.data),
+                                             view.arr.strides[0] // 8, rows, cols, _stream()), "mk_copy_to_device")
+            return Operand(out, rows, cols)
+        dev = torch.empty((rows, cols), dtype=torch.int64, device="cuda")
+        _lib.check(lib.mk_copy_to_device(_vp(dev), dev.stride(0), ctypes.c_void_p(view.arr.ctypes.data),
+                                         view.arr.strides[0] // 8, rows, cols, _stream()), "mk_copy_to_device")
+        out = _fresh(rows, cols)
+        _convert_int_dev(dev, out)
+        return Operand(out, rows, cols, keep=dev)
     if src.dtype == torch.float64:
         out = _fresh(rows, cols)
         out.copy_(src, non_blocking=src.is_pinned())
@@ -162,6 +175,16 @@ def stage_in(view: MatrixView, *, copy: bool = False, stats: EngineStats | None 
     out = _fresh(rows, cols)
     _convert_int_dev(dev, out)
     return Operand(out, rows, cols, keep=dev)
+
+
+_STAGED_MIN_BYTES = 8 << 20
+
+
+def _staged_ok(arr) -> bool:
+    """Large host blocks of 8-byte elements with unit column stride go through the engine's
+    staged copies (mk_copy_to_device / mk_copy_to_host)."""
+    return (arr.dtype.itemsize == 8 and arr.dtype.kind in "fi" and arr.ndim == 2 and arr.strides[1] == 8
+            and arr.strides[0] % 8 == 0 and arr.strides[0] >= 8 * arr.shape[1] and arr.nbytes >= _STAGED_MIN_BYTES)
 
 
 def _convert_int_dev(t, out) -> None:
@@ -233,12 +256,16 @@ class Output:
         host = self.view.arr
         if self.stats is not None:
             self.stats.d2h_bytes += res.shape[0] * res.shape[1] * res.element_size()
-        tgt = torch.from_numpy(host) if host.flags.writeable else None
-        if tgt is None:
+        if not host.flags.writeable:
             raise ValueError("output view is read-only")
         want = getattr(torch, self.dtype.name)
         src = res if res.dtype == want else res.to(want)
-        tgt.copy_(src)
+        if _staged_ok(host) and src.stride(1) == 1:
+            lib = require_engine()
+            _lib.check(lib.mk_copy_to_host(ctypes.c_void_p(host.ctypes.data), host.strides[0] // 8, _vp(src),
+                                           src.stride(0), src.shape[0], src.shape[1], _stream()), "mk_copy_to_host")
+            return
+        torch.from_numpy(host).copy_(src)
 
 
 def check_disjoint(a: MatrixView, b: MatrixView, c: MatrixView) -> None:

@@ -425,6 +425,33 @@ def test_pipelined_host_path_matches_device_path():
     assert err <= tol(n, ha.numpy(), hb.numpy()) and err < 1e-11, err
 
 
+def test_staged_host_copies():
+    """Large host blocks travel through the engine's staged copies (mk_copy_to_device /
+    mk_copy_to_host): rectangular float64 and int64 operands, and strided windows of larger host
+    arrays as operands and as the output, give exact results and leave everything else intact."""
+    r = np.random.default_rng(17)
+    a = r.integers(-8, 9, (1500, 1700)).astype(np.float64)
+    b = r.integers(-8, 9, (1700, 1300)).astype(np.float64)
+    c = pk.multiply(pk.Matrix(a), pk.Matrix(b), pk.get_variant("winograd-mod2", cutoff=256))
+    assert np.array_equal(c.arr, a @ b)
+    ai, bi = a.astype(np.int64), b.astype(np.int64)
+    ci = pk.multiply(pk.Matrix(ai), pk.Matrix(bi), pk.get_variant("strassen-mod2", cutoff=256))
+    assert ci.arr.dtype == np.int64 and np.array_equal(ci.arr, ai @ bi)
+    n, pad = 1024, 48
+    big_a = r.integers(-8, 9, (n + 2 * pad, n + 3 * pad)).astype(np.float64)
+    big_b = r.integers(-8, 9, (n + 2 * pad, n + 3 * pad)).astype(np.float64)
+    big_c = np.full((n + 2 * pad, n + 3 * pad), np.nan)
+    va = pk.MatrixView(pk.Matrix(big_a), pad, 2 * pad, n, n)
+    vb = pk.MatrixView(pk.Matrix(big_b), pad, 2 * pad, n, n)
+    vc = pk.MatrixView(pk.Matrix(big_c), pad, 2 * pad, n, n)
+    pk.winograd_block_mul(va, vb, vc, pk.BasePolicy.naive_cutoff(128))
+    inner = (slice(pad, pad + n), slice(2 * pad, 2 * pad + n))
+    assert np.array_equal(big_c[inner], big_a[inner] @ big_b[inner])
+    mask = np.ones_like(big_c, dtype=bool)
+    mask[inner] = False
+    assert np.isnan(big_c[mask]).all()
+
+
 def test_memory_aware_plan_fallback(monkeypatch):
     """When the breadth-first workspace does not fit in free device memory the call runs with the
     workspace-minimal plan (bit-exact on integer data) and the process-wide options are restored."""
