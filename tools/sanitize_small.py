@@ -39,3 +39,18 @@ for (m, k, nn, L) in [(300, 517, 129, 2), (256, 256, 512, 2)]:
     torch.cuda.synchronize()
     assert torch.equal(c, a @ b)
 print("sanitize workload ok")
+# host paths: overlapped (pinned and pageable) and staged copies, n = 2048 (L = 1, 2, 3)
+import numpy as np
+import paper_2309_00628_b200 as pk
+r = np.random.default_rng(3)
+n = 2048
+ah = r.integers(-8, 9, (n, n)).astype(np.float64)
+bh = r.integers(-8, 9, (n, n)).astype(np.float64)
+want = ah @ bh
+for cut in (1024, 512, 256):
+    ch = np.zeros((n, n))
+    pk.winograd_block_mul(pk.Matrix(ah), pk.Matrix(bh), pk.Matrix(ch), pk.BasePolicy.naive_cutoff(cut))
+    assert np.array_equal(ch, want) and pk.last_stats().path == "overlapped-host", cut
+cr = pk.multiply(pk.Matrix(ah[:1500, :1700]), pk.Matrix(bh[:1700, :1300]), pk.get_variant("winograd-mod2", cutoff=256))
+assert np.array_equal(cr.arr, ah[:1500, :1700] @ bh[:1700, :1300])
+print("sanitize_small ok")
