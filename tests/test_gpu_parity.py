@@ -452,6 +452,23 @@ def test_staged_host_copies():
     assert np.isnan(big_c[mask]).all()
 
 
+def test_overlapped_host_path_on_windows():
+    """The overlapped host path on windows of larger (pageable) host arrays: leading dimensions
+    larger than the order for A, B and C, sentinels around the output window intact."""
+    r = np.random.default_rng(23)
+    n, pad = 2048, 40
+    big = [r.integers(-8, 9, (n + 2 * pad, n + 3 * pad)).astype(np.float64) for _ in range(2)]
+    big_c = np.full((n + 2 * pad, n + 3 * pad), np.nan)
+    views = [pk.MatrixView(pk.Matrix(x), pad, 2 * pad, n, n) for x in (*big, big_c)]
+    pk.winograd_block_mul(*views, pk.BasePolicy.naive_cutoff(512))
+    assert pk.last_stats().path == "overlapped-host"
+    inner = (slice(pad, pad + n), slice(2 * pad, 2 * pad + n))
+    assert np.array_equal(big_c[inner], big[0][inner] @ big[1][inner])
+    mask = np.ones_like(big_c, dtype=bool)
+    mask[inner] = False
+    assert np.isnan(big_c[mask]).all()
+
+
 def test_memory_aware_plan_fallback(monkeypatch):
     """When the breadth-first workspace does not fit in free device memory the call runs with the
     workspace-minimal plan (bit-exact on integer data) and the process-wide options are restored."""
