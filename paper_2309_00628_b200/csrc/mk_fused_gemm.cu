@@ -516,8 +516,23 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const __grid
 // last box overlap the next tile's main loop. Removes the per-tile pipeline fill, CTA launch
 // gap and epilogue drain (~5 us per tile measured by tools/tile_trace.py).
 // =====================================================================================
-template <int MT>
-__global__ void __launch_bounds__(Layout<MT>::kThreads, 1)
+// Persistent layouts: MT m-fragments (8 rows each) per warp, BN tile columns; warps of
+// 8*MT x 32 cover the 128 x BN tile. (8, 128): 8 warps of 64x32 (default); (4, 128): 16 warps of
+// 32x32 (MK_CONSUMER_WARPS=16); (4, 64): 8 warps of 32x32 for narrow leaves (BN = 64 halves the
+// column padding of leaves whose width is not a multiple of 128, e.g. cfg5's 316).
+template <int MT, int BN>
+struct PLayout {
+  static constexpr int kWarpsN = BN / 32;
+  static constexpr int kConsumerWarps = (MK_BM / (8 * MT)) * kWarpsN;
+  static constexpr int kThreads = 128 + 32 * kConsumerWarps;
+  static constexpr int kStageBytes = MK_TILE_BYTES + BN * MK_BK * 8;
+  static constexpr int kBoxBytes = kConsumerWarps * 8 * MT * 128;  // one 16-column box per warp
+  static constexpr int kProducerRegs = kThreads == 384 ? 56 : 32;
+  static constexpr int kConsumerRegs = kThreads == 384 ? 224 : 112;
+};
+
+template <int MT, int BN>
+__global__ void __launch_bounds__(PLayout<MT, BN>::kThreads, 1)
 persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const __grid_constant__ CUtensorMap tmB_param,
                           const __grid_constant__ CUtensorMap tmC_param, const MkGemmArgs args,
                           const __grid_constant__ MkProduct prod_param) {
@@ -531,7 +546,8 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
   const int S = args.stages;
   const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* smem_gen = smem_raw + (smem_base - smem_u32(smem_raw));
-  uint8_t* box_area = smem_gen + (size_t)S * kOpStageBytes;  // epilogue boxes, one per consumer warp
+  using PL = PLayout<MT, BN>;
+  uint8_t* box_area = smem_gen + (size_t)S * PL::kStageBytes;  // epilogue boxes, one per consumer warp
   const int tiles_per = args.tiles_m * args.tiles_n;
   const int total = tiles_per * (args.batch ? args.nprod : 1);
   const int KT = (args.K + MK_BK - 1) / MK_BK;
@@ -545,13 +561,13 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
     const int gsz = min(args.tiles_m - first_m, args.group_m);
     const int r = bid - g * per_group;
     m0 = (first_m + r % gsz) * MK_BM;
-    n0 = (r / gsz) * MK_BN;
+    n0 = (r / gsz) * BN;
   };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], Layout<MT>::kConsumerWarps);
+      mbar_init(&empty_bar[s], PL::kConsumerWarps);
     }
     fence_barrier_init();
   }
@@ -559,7 +575,7 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
 
   if (warp < 4) {
     // ============================ TMA producer (one thread) ============================
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(Regs<MT, false>::kProducer));
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PL::kProducerRegs));
     if (threadIdx.x != 0) return;
     int s = 0;            // ring slot of the next stage (carried across tiles)
     uint32_t eph = 0;     // parity of the empty-barrier phase to wait for (first lap: no wait)
@@ -575,13 +591,13 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
       const int br = prod.b[0].row, bc = n0 + prod.b[0].col;
       for (int k = 0; k < KT; ++k) {
         if (!first_lap) mbar_wait(&empty_bar[s], eph);
-        uint8_t* opA = smem_gen + (size_t)s * kOpStageBytes;
+        uint8_t* opA = smem_gen + (size_t)s * PL::kStageBytes;
         uint8_t* opB = opA + MK_TILE_BYTES;
         const int k0 = k * MK_BK;
-        mbar_arrive_expect_tx(&full_bar[s], 2 * MK_TILE_BYTES);
+        mbar_arrive_expect_tx(&full_bar[s], PL::kStageBytes);
         tma_load_2d(opA, tmA, k0 + ac, ar, &full_bar[s]);
 #pragma unroll
-        for (int bj = 0; bj < 8; ++bj) tma_load_2d(opB + bj * 2048, tmB, bc + bj * 16, k0 + br, &full_bar[s]);
+        for (int bj = 0; bj < BN / 16; ++bj) tma_load_2d(opB + bj * 2048, tmB, bc + bj * 16, k0 + br, &full_bar[s]);
         if (++s == S) {
           s = 0;
           if (first_lap)
@@ -595,10 +611,10 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
   }
 
   // ================================ DMMA consumers ================================
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(Regs<MT, false>::kConsumer));
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(PL::kConsumerRegs));
   const int cw = warp - 4;
-  const int warp_m = cw >> 2;
-  const int warp_n = cw & 3;
+  const int warp_m = cw / PL::kWarpsN;
+  const int warp_n = cw % PL::kWarpsN;
   const int q = lane & 3, g = lane >> 2;
   const int prow = (g >> 1) + 4 * (g & 1);
   const uint32_t a_lane = (uint32_t)(warp_m * (8 * MT) + prow) * 128u;
@@ -657,7 +673,7 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
   if (chunk) {
     if (cw == 0) tmem_alloc(&tmem_base_sh, 256);
     tmem_fence_before();
-    named_bar_sync(3, 32 * Layout<MT>::kConsumerWarps);
+    named_bar_sync(3, 32 * PL::kConsumerWarps);
     tmem_fence_after();
     taddr = tmem_base_sh + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((cw >> 2) * kWords);
   }
@@ -713,7 +729,7 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
     master_live = false;
     for (int kt = 0; kt < KT; ++kt) {
       mbar_wait(&full_bar[rs], fph);
-      const uint8_t* sA = smem_gen + (size_t)rs * kOpStageBytes;
+      const uint8_t* sA = smem_gen + (size_t)rs * PL::kStageBytes;
       const uint8_t* sB = sA + MK_TILE_BYTES;
       if (kt == KT - 1 && krem_last < MK_BK)
         stage(sA, sB, krem_last, std::true_type{});
@@ -835,7 +851,7 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
   __syncwarp();
   if (chunk) {
     tmem_fence_before();
-    named_bar_sync(3, 32 * Layout<MT>::kConsumerWarps);
+    named_bar_sync(3, 32 * PL::kConsumerWarps);
     tmem_fence_after();
     if (cw == 0) tmem_dealloc(tmem_base_sh, 256);
   }
@@ -893,23 +909,50 @@ static int sm_count() {
   }
   return cache[dev];
 }
-// One CTA per SM over `total` tiles; the ring keeps S = (budget - boxes) / stage stages.
-static cudaError_t launch_persistent(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
-                                     MkGemmArgs args, const MkProduct& prod, int total, cudaStream_t stream) {
-  constexpr size_t kBoxBytes = 64 * 1024;  // 8 warps x 64 rows or 16 warps x 32 rows, 128 B each
-  args.stages = (int)((MK_SMEM_BUDGET - kBoxBytes) / kOpStageBytes);
+// Tile width of the persistent kernel: 64 when it cuts the column padding of the leaf by more
+// than 10% (only with the synchronous epilogue: the TMA epilogue's C maps are built for the
+// default box shape), else 128. Env MK_NARROW=0 disables narrow tiles.
+static int persistent_bn(const MkGemmArgs& a) {
+  static int narrow = -1;
+  if (narrow < 0) {
+    const char* e = getenv("MK_NARROW");
+    narrow = (e && e[0] == '0') ? 0 : 1;
+  }
+  if (!narrow || a.async_epi) return 128;
+  const int64_t w128 = (a.N + 127) / 128 * 128, w64 = (a.N + 63) / 64 * 64;
+  return (w64 * 10 < w128 * 9) ? 64 : 128;
+}
+
+// One CTA per SM over the launch's tiles; the ring keeps S = (budget - boxes) / stage stages.
+template <int MT, int BN>
+static cudaError_t launch_persistent_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
+                                       MkGemmArgs args, const MkProduct& prod, int nprod, cudaStream_t stream) {
+  using PL = PLayout<MT, BN>;
+  args.tiles_n = (args.N + BN - 1) / BN;
+  const int tiles = args.tiles_m * args.tiles_n;
+  if (tiles == 0) return cudaSuccess;
+  if ((int64_t)tiles * nprod > 0x7fffffff) return cudaErrorInvalidValue;
+  args.tiles_per_prod = tiles;
+  args.nprod = nprod;
+  args.stages = (int)((MK_SMEM_BUDGET - PL::kBoxBytes) / PL::kStageBytes);
   if (args.stages > kMaxStages) args.stages = kMaxStages;
   args.raw_sets = 0;
   args.chunk_stages = accumulate_chunk_stages();
-  const size_t smem = (size_t)args.stages * kOpStageBytes + kBoxBytes + 1024;
-  const bool wide = consumer_layout() == 16;
-  auto fn = wide ? persistent_product_kernel<4> : persistent_product_kernel<8>;
-  const int threads = wide ? Layout<4>::kThreads : Layout<8>::kThreads;
+  const size_t smem = (size_t)args.stages * PL::kStageBytes + PL::kBoxBytes + 1024;
+  auto fn = persistent_product_kernel<MT, BN>;
   cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
+  const int total = tiles * nprod;
   const int grid = total < sm_count() ? total : sm_count();
-  fn<<<grid, threads, smem, stream>>>(tmA, tmB, tmC, args, prod);
+  fn<<<grid, PL::kThreads, smem, stream>>>(tmA, tmB, tmC, args, prod);
   return cudaGetLastError();
+}
+
+static cudaError_t launch_persistent(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
+                                     MkGemmArgs args, const MkProduct& prod, int nprod, cudaStream_t stream) {
+  if (persistent_bn(args) == 64) return launch_persistent_t<4, 64>(tmA, tmB, tmC, args, prod, nprod, stream);
+  if (consumer_layout() == 16) return launch_persistent_t<4, 128>(tmA, tmB, tmC, args, prod, nprod, stream);
+  return launch_persistent_t<8, 128>(tmA, tmB, tmC, args, prod, nprod, stream);
 }
 
 cudaError_t launch_fused_product(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
@@ -918,12 +961,8 @@ cudaError_t launch_fused_product(const CUtensorMap& tmA, const CUtensorMap& tmB,
   MkGemmArgs args = args_in;
   const bool ca = prod.na > 1, cb = prod.nb > 1;
   if (!ca && !cb && persistent_enabled()) {
-    const int total = args.tiles_m * args.tiles_n;
-    if (total == 0) return cudaSuccess;
     args.batch = nullptr;
-    args.nprod = 1;
-    args.tiles_per_prod = total;
-    return launch_persistent(tmA, tmB, tmC, args, prod, total, stream);
+    return launch_persistent(tmA, tmB, tmC, args, prod, 1, stream);
   }
   const int raw_tiles = (ca ? prod.na : 0) + (cb ? prod.nb : 0);
   const size_t raw_set = (size_t)raw_tiles * MK_TILE_BYTES;
@@ -979,7 +1018,7 @@ cudaError_t launch_product_batch(const MkBatchEntry* entries_dev, int nprod, con
     CUtensorMap z{};
     MkProduct zp{};
     zp.na = zp.nb = 1;
-    return launch_persistent(z, z, z, args, zp, tiles * nprod, stream);
+    return launch_persistent(z, z, z, args, zp, nprod, stream);
   }
   const size_t smem = (size_t)args.stages * kOpStageBytes + 1024;
   const bool wide = consumer_layout() == 16;
