@@ -346,7 +346,14 @@ def levels_for(n: int, policy, algo: str) -> int:
 
 
 _PIPE_ALGOS = ("strassen", "winograd-block", "winograd-knuth", "winograd-knuth-8call")
-_copy_stream = None
+_copy_streams: dict = {}  # device index -> copy stream of the overlapped host path
+
+
+def _copy_stream():
+    dev = torch.cuda.current_device()
+    if dev not in _copy_streams:
+        _copy_streams[dev] = torch.cuda.Stream(device=dev)
+    return _copy_streams[dev]
 
 
 def _overlap_applies(a: MatrixView, b: MatrixView, c: MatrixView, levels: int, algo: str, dtype) -> bool:
@@ -372,11 +379,8 @@ def _overlapped_host_product(algo: str, a: MatrixView, b: MatrixView, c: MatrixV
     starts as soon as the blocks it reads have landed, each C block comes back as soon as its
     last contributor is done. Pageable arrays are staged through pinned bounce slots by the
     engine's host thread pool."""
-    global _copy_stream
     lib = require_engine()
     n = a.rows
-    if _copy_stream is None:
-        _copy_stream = torch.cuda.Stream()
     ld = _round_ld(n)
     dA = torch.empty((n, ld), dtype=torch.float64, device="cuda")
     dB = torch.empty((n, ld), dtype=torch.float64, device="cuda")
@@ -396,7 +400,7 @@ def _call_host(lib, aid, a, b, c, n, levels, dA, dB, dC, ld, ws, ws_bytes):
     return lib.mk_strassen_host(aid, ctypes.c_void_p(a.arr.ctypes.data), a.arr.strides[0] // 8,
                                 ctypes.c_void_p(b.arr.ctypes.data), b.arr.strides[0] // 8,
                                 ctypes.c_void_p(c.arr.ctypes.data), c.arr.strides[0] // 8, n, levels, _vp(dA), _vp(dB),
-                                _vp(dC), ld, _vp(ws), ws_bytes, _stream(), ctypes.c_void_p(_copy_stream.cuda_stream))
+                                _vp(dC), ld, _vp(ws), ws_bytes, _stream(), ctypes.c_void_p(_copy_stream().cuda_stream))
 
 
 def device_square(algo: str, a: MatrixView, b: MatrixView, c: MatrixView, levels: int, dtype,

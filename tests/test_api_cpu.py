@@ -177,3 +177,26 @@ def test_core_views_quadrants_padding_text(tmp_path):
     with pytest.raises(ValueError):
         pk.read_matrix(__import__("io").StringIO("2 2\n1 2 3"))
     assert pk.max_abs_diff(pk.Matrix(np.ones((2, 2))), pk.Matrix(np.zeros((2, 2)))) == 1.0
+
+
+def test_set_plan_validates_and_round_trips():
+    """set_plan (B200 addition): bad names raise ValueError; the options reach the engine's
+    planner (workspace sizes change) and can be restored. Host-only: no GPU needed."""
+    import ctypes
+
+    from paper_2309_00628_b200 import _lib
+
+    with pytest.raises(ValueError):
+        pk.set_plan("sideways")
+    lib = _lib.load()
+    v = ctypes.c_int(-1)
+    try:
+        pk.set_plan("depth-first", two_temp_tail=False)
+        assert lib.mk_get_option(_lib.MK_OPT_PLAN, ctypes.byref(v)) == 0 and v.value == 1
+        assert lib.mk_get_option(_lib.MK_OPT_LITERAL_TAIL, ctypes.byref(v)) == 0 and v.value == 0
+        lean = lib.mk_workspace_bytes(_lib.ALGO_IDS["winograd-block"], 4096, 3)
+    finally:
+        pk.set_plan()
+    assert lib.mk_get_option(_lib.MK_OPT_PLAN, ctypes.byref(v)) == 0 and v.value == 0
+    assert lib.mk_workspace_bytes(_lib.ALGO_IDS["winograd-block"], 4096, 3) > lean
+    assert lib.mk_get_option(99, ctypes.byref(v)) == _lib.MK_ERR_ARG
