@@ -186,6 +186,12 @@ def test_set_plan_validates_and_round_trips():
 
     from paper_2309_00628_b200 import _lib
 
+    import os
+
+    if not os.path.exists(_lib.LIB_PATH):
+        import __graft_entry__
+
+        __graft_entry__.build()
     with pytest.raises(ValueError):
         pk.set_plan("sideways")
     lib = _lib.load()
