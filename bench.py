@@ -316,15 +316,15 @@ def main():
     e2e = None
     if not args.no_e2e:
         host_c = torch.empty((n, n), dtype=torch.float64).pin_memory()
+        moved = [2 * n * n * 8]  # H2D bytes of this rank per step
         hA, hB, hC = pk.Matrix(host_a.numpy()), pk.Matrix(host_b.numpy()), pk.Matrix(host_c.numpy())
 
         def e2e_step():
             if world == 1:
                 pk.winograd_block_mul(hA, hB, hC, policy)
-            else:
-                ta = host_a.to(dev, non_blocking=True)
-                tb = host_b.to(dev, non_blocking=True)
-                multigpu.sharded_multiply(args.algo, ta, tb, levels, out=dc, ws=ws)
+            else:  # each rank uploads only the operand quadrants its shard reads
+                moved[0] = multigpu.upload_operands(args.algo, levels, host_a, host_b, da, db)
+                multigpu.sharded_multiply(args.algo, da, db, levels, out=dc, ws=ws)
                 if rank == 0:
                     host_c.copy_(dc, non_blocking=True)
                 torch.cuda.current_stream().synchronize()
@@ -344,8 +344,13 @@ def main():
             t = torch.tensor([ems], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
+        h2d = moved[0]
+        if world > 1:
+            t = torch.tensor([h2d], device=dev, dtype=torch.int64)
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            h2d = int(t.item())
         e2e = {"value": round(2.0 * n ** 3 / (ems * 1e-3) / 1e12, 4), "unit": UNIT,
-               "h2d_bytes_per_step": 2 * n * n * 8 * world, "d2h_bytes_per_step": n * n * 8,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": n * n * 8,
                "ms_per_step": round(ems, 2)}
 
     if rank != 0:

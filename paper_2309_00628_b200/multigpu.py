@@ -19,9 +19,32 @@ from __future__ import annotations
 
 import ctypes
 
-from . import _lib
+from . import _lib, tables
 
 PANELS = 8  # row panels per leaf (shard granularity)
+
+_STEPS = {
+    "strassen": tables.STRASSEN_STEPS,
+    "winograd-block": tables.WINOGRAD_BLOCK_STEPS,
+    "winograd-knuth": tables.WINOGRAD_KNUTH_STEPS,
+    "winograd-knuth-8call": tables.WINOGRAD_KNUTH_8CALL_STEPS,
+}
+
+
+def operand_quadrants(algo: str, levels: int, first: int, count: int, panels: int = PANELS):
+    """Top-level quadrants of A and B (0..3 = 11, 12, 21, 22) that shard units
+    [first, first+count) read: the units of one top-level product read only the quadrants in
+    its operand sums, so a rank needs only those uploaded (the rest of its A/B buffers is never
+    touched)."""
+    if levels < 1 or count <= 0:
+        return (set(range(4)), set(range(4))) if count > 0 else (set(), set())
+    a, b, _ = tables.coefficients(_STEPS[algo])
+    per_parent = len(a) ** (levels - 1) * panels
+    qa, qb = set(), set()
+    for p in range(first // per_parent, (first + count - 1) // per_parent + 1):
+        qa |= {q for q in range(4) if a[p][q]}
+        qb |= {q for q in range(4) if b[p][q]}
+    return qa, qb
 
 
 def shard_range(total: int, world: int, rank: int) -> tuple[int, int]:
@@ -76,6 +99,40 @@ def assemble(partial, dst_rank: int = 0, group=None):
         else:
             dist.reduce(partial, dst=dst_rank, op=dist.ReduceOp.SUM, group=group)
     return partial
+
+
+def my_shard(algo: str, levels: int, group=None) -> tuple[int, int]:
+    """This rank's [first, first+count) shard units."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    return shard_range(leaf_count(algo, levels) * PANELS, world, rank)
+
+
+def upload_operands(algo: str, levels: int, host_a, host_b, dev_a, dev_b, group=None, stream=None) -> int:
+    """Copy to this rank's device buffers only the operand quadrants its shard reads (pinned or
+    pageable host tensors/arrays of order n; the engine's staged copies). Returns the bytes."""
+    import numpy as np
+    import torch
+
+    lib = _lib.load()
+    first, count = my_shard(algo, levels, group)
+    qa, qb = operand_quadrants(algo, levels, first, count)
+    n = dev_a.shape[0]
+    h = n // 2 if levels >= 1 else n
+    st = ctypes.c_void_p((stream or torch.cuda.current_stream()).cuda_stream)
+    moved = 0
+    for quads, src, dst in ((qa, host_a, dev_a), (qb, host_b, dev_b)):
+        arr = src.numpy() if isinstance(src, torch.Tensor) else np.asarray(src)
+        for q in sorted(quads) if levels >= 1 else [0]:
+            r0, c0 = (q >> 1) * h, (q & 1) * h
+            hp = arr.ctypes.data + (r0 * arr.strides[0] + c0 * 8)
+            dp = dst.data_ptr() + (r0 * dst.stride(0) + c0) * 8
+            _lib.check(lib.mk_copy_to_device(ctypes.c_void_p(dp), dst.stride(0), ctypes.c_void_p(hp),
+                                             arr.strides[0] // 8, h, h, st), "mk_copy_to_device")
+            moved += h * h * 8
+    return moved
 
 
 def sharded_multiply(algo: str, a, b, levels: int, group=None, out=None, ws=None):

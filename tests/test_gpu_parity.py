@@ -356,6 +356,7 @@ def test_sharded_partials_sum_to_product(levels, world):
     n = 1024
     a = torch.from_numpy(r.integers(-8, 9, (n, n)).astype(np.float64)).cuda()
     b = torch.from_numpy(r.integers(-8, 9, (n, n)).astype(np.float64)).cuda()
+    h = n // 2
     for panels in (1, multigpu.PANELS):
         total = multigpu.leaf_count("winograd-block", levels) * panels
         acc = torch.zeros_like(a)
@@ -363,7 +364,17 @@ def test_sharded_partials_sum_to_product(levels, world):
             first, count = multigpu.shard_range(total, world, rank)
             part = torch.zeros_like(a)
             if count:
-                multigpu.partial_product("winograd-block", a, b, part, levels, first, count, panels=panels)
+                # a rank reads only the quadrants operand_quadrants names: the others hold NaN
+                qa, qb = multigpu.operand_quadrants("winograd-block", levels, first, count, panels)
+                ra, rb = torch.full_like(a, float("nan")), torch.full_like(b, float("nan"))
+                for q in qa:
+                    sl = (slice((q >> 1) * h, (q >> 1) * h + h), slice((q & 1) * h, (q & 1) * h + h))
+                    ra[sl] = a[sl]
+                for q in qb:
+                    sl = (slice((q >> 1) * h, (q >> 1) * h + h), slice((q & 1) * h, (q & 1) * h + h))
+                    rb[sl] = b[sl]
+                multigpu.partial_product("winograd-block", ra, rb, part, levels, first, count, panels=panels)
+                assert not torch.isnan(part).any(), (panels, rank)
             acc += part
         assert torch.equal(acc, a @ b), panels
 

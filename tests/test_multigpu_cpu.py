@@ -9,7 +9,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2309_00628_b200.multigpu import assemble, shard_range
+from paper_2309_00628_b200.multigpu import assemble, operand_quadrants, shard_range
 from oracle import strassen_oracle as o
 
 
@@ -38,6 +38,32 @@ def test_leaf_decomposition_sums_to_the_product(kernel, levels):
             first, count = shard_range(total, 3, w)
             acc += o.leaf_partial(kernel, a, b, levels, first, count, panels)
         assert np.array_equal(acc, a @ b), panels
+
+
+@pytest.mark.parametrize("kernel", ["strassen", "winograd-block", "winograd-knuth", "winograd-knuth-8call"])
+@pytest.mark.parametrize("levels", [1, 2])
+def test_operand_quadrants_cover_what_a_shard_reads(kernel, levels):
+    """A shard's partial (oracle leaf decomposition) depends only on the quadrants
+    operand_quadrants names: NaN elsewhere in A and B never reaches it."""
+    r = np.random.default_rng(8)
+    n, h = 16, 8
+    a, b = r.integers(-8, 9, (n, n)).astype(np.float64), r.integers(-8, 9, (n, n)).astype(np.float64)
+    panels = 2
+    total = len(o.one_level_coefficients(kernel)[0]) ** levels * panels
+    for world in (2, 4, 8):
+        for w in range(world):
+            first, count = shard_range(total, world, w)
+            if not count:
+                continue
+            qa, qb = operand_quadrants(kernel, levels, first, count, panels)
+            ra, rb = np.full_like(a, np.nan), np.full_like(b, np.nan)
+            for q in qa:
+                ra[(q >> 1) * h:(q >> 1) * h + h, (q & 1) * h:(q & 1) * h + h] = a[(q >> 1) * h:(q >> 1) * h + h, (q & 1) * h:(q & 1) * h + h]
+            for q in qb:
+                rb[(q >> 1) * h:(q >> 1) * h + h, (q & 1) * h:(q & 1) * h + h] = b[(q >> 1) * h:(q >> 1) * h + h, (q & 1) * h:(q & 1) * h + h]
+            want = o.leaf_partial(kernel, a, b, levels, first, count, panels)
+            got = o.leaf_partial(kernel, ra, rb, levels, first, count, panels)
+            assert np.array_equal(got, want), (kernel, levels, world, w)
 
 
 def _free_port():
