@@ -1551,6 +1551,19 @@ static std::map<int, std::pair<std::vector<int>, std::vector<int>>> g_order_cach
 static std::map<int, std::vector<int>> g_head_cache;
 static std::mutex g_order_mu;
 static std::vector<int> head_child_order(const Coeffs& co, int p0);
+static std::vector<int> overlap_order(const Coeffs& co, std::vector<int>* uploads);
+// overlap_order is a search over all product permutations (~1.6 ms): computed once per algorithm
+static std::vector<int> cached_order(int algo, std::vector<int>* uploads) {
+  std::lock_guard<std::mutex> lk(g_order_mu);
+  auto it = g_order_cache.find(algo);
+  if (it == g_order_cache.end()) {
+    std::vector<int> up;
+    std::vector<int> ord = overlap_order(coeffs_for(algo), &up);
+    it = g_order_cache.emplace(algo, std::make_pair(ord, up)).first;
+  }
+  if (uploads) *uploads = it->second.second;
+  return it->second.first;
+}
 static std::vector<int> cached_head_children(int algo, int p0) {
   std::lock_guard<std::mutex> lk(g_order_mu);
   auto it = g_head_cache.find(algo);
@@ -1606,7 +1619,7 @@ size_t mk_host_workspace_bytes(int algo, int64_t n, int levels) {
   if (setup_square(e, algo, reinterpret_cast<double*>(0x100000), n, reinterpret_cast<double*>(0x200000), n,
                    reinterpret_cast<double*>(0x300000), n, n, levels) != MK_OK)
     return 0;
-  const std::vector<int> order = overlap_order(*e.co, nullptr);
+  const std::vector<int> order = cached_order(algo, nullptr);
   cudaEvent_t none[61] = {nullptr};
   bool tail_split[4];
   const bool sub = levels == 2 && (n / 2) % 2 == 0;
@@ -1627,18 +1640,7 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
   if (ldd < n || ldd % 2 || lda < n || ldb < n || ldc < n)
     return fail(MK_ERR_DIMENSION, "leading dimension smaller than the order (device ld must be even)");
   cudaStream_t st = static_cast<cudaStream_t>(stream), cp = static_cast<cudaStream_t>(copy_stream);
-  std::vector<int> order0;
-  {
-    std::lock_guard<std::mutex> lk(g_order_mu);
-    auto it = g_order_cache.find(algo);
-    if (it == g_order_cache.end()) {
-      std::vector<int> up0;
-      order0 = overlap_order(coeffs_for(algo), &up0);
-      g_order_cache[algo] = {order0, up0};
-    } else {
-      order0 = it->second.first;
-    }
-  }
+  const std::vector<int> order0 = cached_order(algo, nullptr);
   const bool sub = levels == 2 && (n / 2) % 2 == 0;
   const std::vector<int> kids0 = sub ? cached_head_children(algo, order0[0]) : std::vector<int>();
   cudaEvent_t none[61] = {nullptr};
@@ -1684,12 +1686,8 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
     e.tbl_mode = 2;
     e.tbl_dev = tbl_dev;
   }
-  std::vector<int> order, up;
-  {
-    std::lock_guard<std::mutex> lk(g_order_mu);
-    order = g_order_cache[algo].first;
-    up = g_order_cache[algo].second;
-  }
+  std::vector<int> up;
+  const std::vector<int> order = cached_order(algo, &up);
   const int64_t h = n / 2, hh = h / 2;
   // events: 8 quadrant uploads, 4 quadrant completions, start, 32 sub-block uploads, 16 sub-block completions
   constexpr int kEv = 61;
