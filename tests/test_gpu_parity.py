@@ -225,6 +225,34 @@ def test_known_answers_and_counts():
     assert ctr.mults == 8
 
 
+def test_reference_edge_semantics(rng):
+    """Edge semantics the reference's tests pin: order-1 schedules (no buffers, in-place leaves its
+    inputs alone, test_schedules.py order-1 cases), identity products, Knuth and block forms agree
+    exactly, in-place rejects A overlapping B (AliasError)."""
+    a1, b1 = pk.Matrix(np.array([[3]])), pk.Matrix(np.array([[5]]))
+    c1 = pk.Matrix.zeros(1, 1, np.int64)
+    ctr = pk.in_place_winograd(a1, b1, c1)
+    assert c1[0, 0] == 15 and a1[0, 0] == 3 and b1[0, 0] == 5 and ctr.temp_buffers == 0
+    c1 = pk.Matrix.zeros(1, 1, np.int64)
+    ctr = pk.two_temp_winograd(a1, b1, c1)
+    assert c1[0, 0] == 15 and ctr.temp_buffers == 0
+    eye = pk.Matrix(np.eye(64, dtype=np.int64))
+    x = rng.integers(-8, 9, (64, 64), dtype=np.int64)
+    for fn in (pk.strassen_mul, pk.winograd_block_mul, pk.winograd_knuth_mul):
+        c = pk.Matrix.zeros(64, 64, np.int64)
+        fn(eye, pk.Matrix(x), c, pk.BasePolicy.naive_cutoff(8))
+        assert np.array_equal(c.arr, x)
+    y = rng.integers(-8, 9, (64, 64), dtype=np.int64)
+    ck, cb = pk.Matrix.zeros(64, 64, np.int64), pk.Matrix.zeros(64, 64, np.int64)
+    pk.winograd_knuth_mul(pk.Matrix(x), pk.Matrix(y), ck)
+    pk.winograd_block_mul(pk.Matrix(x), pk.Matrix(y), cb)
+    assert np.array_equal(ck.arr, cb.arr)
+    big = pk.Matrix(rng.integers(-8, 9, (64, 96), dtype=np.int64))
+    va, vb = pk.MatrixView(big, 0, 0, 64, 64), pk.MatrixView(big, 0, 32, 64, 64)  # A and B overlap
+    with pytest.raises(pk.AliasError):
+        pk.in_place_winograd(va, vb, pk.Matrix.zeros(64, 64, np.int64))
+
+
 def test_naive_rectangular_ragged(rng):
     for (m, k, n) in ((3, 2, 4), (1, 1, 1), (130, 3, 17), (1000, 777, 555), (7, 1025, 3)):
         a = rng.integers(-8, 9, (m, k), dtype=np.int64)
