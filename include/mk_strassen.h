@@ -59,7 +59,8 @@ int mk_version(void);
  *   faster on B200).
  * MK_OPT_PLAN (strassen / winograd kinds, L >= 2): 0 = breadth-first (default: batched leaves,
  *   fastest, largest workspace), 1 = depth-first (workspace-minimal: operand sums only, P_i
- *   accumulated straight into C by the epilogue).
+ *   accumulated straight into C by the epilogue), 2 = hybrid (top level depth-first, each
+ *   top-level product breadth-first below it: about 1/7 of the breadth-first workspace).
  * MK_OPT_LITERAL_TAIL (two-temp): 1 = run the last two levels breadth-first under the literal
  *   Table-2 levels (default), 0 = the literal schedule down to the leaves (2 (n/2)^2-style
  *   scratch only, the paper's memory bound). */

@@ -30,7 +30,7 @@ ALGO_IDS = {
     "in-place": 6,
 }
 MK_OPT_FUSE_PREADDS = 1
-MK_OPT_PLAN = 2  # 0 breadth-first (default), 1 depth-first (workspace-minimal)
+MK_OPT_PLAN = 2  # 0 breadth-first (default), 1 depth-first (workspace-minimal), 2 hybrid
 MK_OPT_LITERAL_TAIL = 3  # two-temp: 1 breadth-first last two levels (default), 0 literal to the leaves
 
 # every exported symbol with (restype, argtypes)

@@ -301,13 +301,16 @@ static bool literal_bfs_tail() {
   }
   return g_literal_tail == 1;
 }
-static bool plan_dfs() {
+// MK_OPT_PLAN: 0 breadth-first, 1 depth-first, 2 top-level depth-first with a breadth-first plan
+// under each top-level product (env MK_PLAN=dfs / hybrid)
+static int plan_kind() {
   if (g_plan_dfs < 0) {
     const char* env = getenv("MK_PLAN");
-    g_plan_dfs = (env && std::string(env) == "dfs") ? 1 : 0;
+    g_plan_dfs = (env && std::string(env) == "dfs") ? 1 : (env && std::string(env) == "hybrid") ? 2 : 0;
   }
-  return g_plan_dfs == 1;
+  return g_plan_dfs;
 }
+static bool plan_dfs() { return plan_kind() == 1; }
 
 static bool debug_sync() {
   static int v = -1;
@@ -789,34 +792,37 @@ struct Engine {
   // (n/2)^2 product formed by bfs(L-1) in a slot, then added with its signs into every C quadrant
   // it feeds (store for the first writer).
   int top_product_bfs(int p, const Lin& A0, const Lin& B0, const Lin& C0, int64_t h) {
-    Lin X = kron(A0, co->a[p], h, h), Y = kron(B0, co->b[p], h, h);
-    const Lin Dp = kron_dest(C0, p, h, h);
+    return top_product_bfs(p, A0, B0, C0, h, h, h);
+  }
+  int top_product_bfs(int p, const Lin& A0, const Lin& B0, const Lin& C0, int64_t hm, int64_t hn, int64_t hk) {
+    Lin X = kron(A0, co->a[p], hm, hk), Y = kron(B0, co->b[p], hk, hn);
+    const Lin Dp = kron_dest(C0, p, hm, hn);
     const size_t mark = ws_used;
     const int nb_mark = nbases;
     Blk Xb = X[0], Yb = Y[0];  // single terms stay views (bfs carries their sign)
     if (X.size() > 1) {
       int sb;
-      MK_TRY(alloc_slot(h, h, &sb));
-      MK_TRY(combine(Blk{sb, 0, 0, 1.0}, X, h, h));
+      MK_TRY(alloc_slot(hm, hk, &sb));
+      MK_TRY(combine(Blk{sb, 0, 0, 1.0}, X, hm, hk));
       Xb = Blk{sb, 0, 0, 1.0};
     }
     if (Y.size() > 1) {
       int sb;
-      MK_TRY(alloc_slot(h, h, &sb));
-      MK_TRY(combine(Blk{sb, 0, 0, 1.0}, Y, h, h));
+      MK_TRY(alloc_slot(hk, hn, &sb));
+      MK_TRY(combine(Blk{sb, 0, 0, 1.0}, Y, hk, hn));
       Yb = Blk{sb, 0, 0, 1.0};
     }
     int pb;
-    MK_TRY(alloc_slot(h, h, &pb));
-    MK_TRY(bfs(L - 1, h, h, h, Xb, Yb, Blk{pb, 0, 0, 1.0}));
+    MK_TRY(alloc_slot(hm, hn, &pb));
+    MK_TRY(bfs(L - 1, hm, hn, hk, Xb, Yb, Blk{pb, 0, 0, 1.0}));
     for (const Blk& d : Dp) {
-      const int s = state(d.base, d.row, d.col, h, h);
+      const int s = state(d.base, d.row, d.col, hm, hn);
       if (s == 2) return fail(MK_ERR_ARG, "internal: partially written post-add destination");
       Lin src;
       if (s == 1) src.push_back(Blk{d.base, d.row, d.col, d.sign});
       src.push_back(Blk{pb, 0, 0, 1.0});
-      MK_TRY(combine(Blk{d.base, d.row, d.col, d.sign}, src, h, h));
-      set_state(d.base, d.row, d.col, h, h, 1);
+      MK_TRY(combine(Blk{d.base, d.row, d.col, d.sign}, src, hm, hn));
+      set_state(d.base, d.row, d.col, hm, hn, 1);
     }
     ws_used = mark;
     while (nbases > nb_mark) {
@@ -1266,11 +1272,19 @@ static bool use_bfs(const Engine& e, int64_t lm, int64_t ln) {
   (void)ln;
   if (e.fuse_preadds || e.leaf_count >= 0 || e.L < 2) return false;
   if (e.algo < MK_ALGO_STRASSEN || e.algo > MK_ALGO_WINOGRAD_KNUTH_8CALL) return false;
-  return !plan_dfs();
+  return plan_kind() == 0;
 }
 
 static int run_square(Engine& e) {
   const int64_t n = e.n;
+  if (plan_kind() == 2 && !e.fuse_preadds && e.leaf_count < 0 && e.L >= 2 && e.algo >= MK_ALGO_STRASSEN &&
+      e.algo <= MK_ALGO_WINOGRAD_KNUTH_8CALL) {
+    // hybrid: the top level depth-first, each top-level product breadth-first below it (1/7 of
+    // the breadth-first workspace plus three (n/2)^2 slots)
+    const Lin A0{Blk{BASE_A, 0, 0, 1.0}}, B0{Blk{BASE_B, 0, 0, 1.0}}, C0{Blk{BASE_C, 0, 0, 1.0}};
+    for (int p = 0; p < e.co->nprod; ++p) MK_TRY(e.top_product_bfs(p, A0, B0, C0, n / 2));
+    return MK_OK;
+  }
   if (use_bfs(e, e.leaf_m, e.leaf_n))
     return e.bfs(e.L, n, n, n, Blk{BASE_A, 0, 0, 1.0}, Blk{BASE_B, 0, 0, 1.0}, Blk{BASE_C, 0, 0, 1.0});
   if (e.algo == MK_ALGO_TWO_TEMP)
@@ -1342,7 +1356,8 @@ int mk_set_option(int key, int value) {
     return MK_OK;
   }
   if (key == MK_OPT_PLAN) {
-    if (value != 0 && value != 1) return fail(MK_ERR_ARG, "MK_OPT_PLAN takes 0 (breadth-first) or 1 (depth-first)");
+    if (value < 0 || value > 2)
+      return fail(MK_ERR_ARG, "MK_OPT_PLAN takes 0 (breadth-first), 1 (depth-first) or 2 (hybrid)");
     g_plan_dfs = value;
     return MK_OK;
   }
@@ -1359,7 +1374,7 @@ int mk_get_option(int key, int* value) {
   if (key == MK_OPT_FUSE_PREADDS) {
     *value = fuse_preadds_default() ? 1 : 0;
   } else if (key == MK_OPT_PLAN) {
-    *value = plan_dfs() ? 1 : 0;
+    *value = plan_kind();
   } else if (key == MK_OPT_LITERAL_TAIL) {
     *value = literal_bfs_tail() ? 1 : 0;
   } else {
@@ -1886,7 +1901,11 @@ static int run_rect(int algo, const double* A, int64_t lda, const double* B, int
   e.add_base(Cp, ldcp, mp, np_, e.leaf_m, e.leaf_n);
   e.ws = dry ? nullptr : static_cast<char*>(ws) + off;
   e.ws_bytes = dry ? 0 : ws_bytes - off;
-  if (use_bfs(e, e.leaf_m, e.leaf_n))
+  if (plan_kind() == 2 && levels >= 2 && !e.fuse_preadds && algo >= MK_ALGO_STRASSEN &&
+      algo <= MK_ALGO_WINOGRAD_KNUTH_8CALL) {  // hybrid (see run_square)
+    const Lin A0{Blk{BASE_A, 0, 0, 1.0}}, B0{Blk{BASE_B, 0, 0, 1.0}}, C0{Blk{BASE_C, 0, 0, 1.0}};
+    for (int p = 0; p < e.co->nprod; ++p) MK_TRY(e.top_product_bfs(p, A0, B0, C0, mp / 2, np_ / 2, kp / 2));
+  } else if (use_bfs(e, e.leaf_m, e.leaf_n))
     MK_TRY(e.bfs(levels, mp, np_, kp, Blk{BASE_A, 0, 0, 1.0}, Blk{BASE_B, 0, 0, 1.0}, Blk{BASE_C, 0, 0, 1.0}));
   else
     MK_TRY(e.fused(levels, Lin{Blk{BASE_A, 0, 0, 1.0}}, Lin{Blk{BASE_B, 0, 0, 1.0}}, Lin{Blk{BASE_C, 0, 0, 1.0}},

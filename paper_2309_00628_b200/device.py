@@ -58,16 +58,18 @@ def set_plan(plan: str = "breadth-first", two_temp_tail: bool = True) -> None:
     """Process-wide engine plan (B200 addition; the reference has no counterpart).
 
     ``plan``: "breadth-first" (default for >= 2 levels: batched leaf launches, fastest, largest
-    workspace) or "depth-first" (workspace-minimal: operand sums only, each P_i accumulated
-    straight into C by the leaf epilogue). ``two_temp_tail``: two_temp_winograd runs its last two
+    workspace), "hybrid" (top level depth-first, each top-level product breadth-first below it:
+    about 1/7 of the breadth-first workspace) or "depth-first" (workspace-minimal: operand sums
+    only, each P_i accumulated straight into C by the leaf epilogue). ``two_temp_tail``: two_temp_winograd runs its last two
     levels breadth-first (default) or the literal Table-2 schedule down to the leaves (the paper's
     2 x (n/2)^2-per-level scratch bound). Results are unchanged on integer data; float results
     differ only in summation order. Modeled OpCounter values never change.
     """
-    if plan not in ("breadth-first", "depth-first"):
-        raise ValueError(f"plan must be 'breadth-first' or 'depth-first', got {plan!r}")
+    kinds = {"breadth-first": 0, "depth-first": 1, "hybrid": 2}
+    if plan not in kinds:
+        raise ValueError(f"plan must be one of {sorted(kinds)}, got {plan!r}")
     lib = _lib.load(required=True)
-    _lib.check(lib.mk_set_option(_lib.MK_OPT_PLAN, 1 if plan == "depth-first" else 0), "mk_set_option")
+    _lib.check(lib.mk_set_option(_lib.MK_OPT_PLAN, kinds[plan]), "mk_set_option")
     _lib.check(lib.mk_set_option(_lib.MK_OPT_LITERAL_TAIL, 1 if two_temp_tail else 0), "mk_set_option")
 
 
@@ -307,9 +309,13 @@ def _memory_aware_plan(size_of):
             _lib.check(lib.mk_get_option(key, ctypes.byref(v)), "mk_get_option")
             old.append((key, v.value))
         try:
-            lib.mk_set_option(_lib.MK_OPT_PLAN, 1)
             lib.mk_set_option(_lib.MK_OPT_LITERAL_TAIL, 0)
-            yield int(size_of())
+            lib.mk_set_option(_lib.MK_OPT_PLAN, 2)  # hybrid first: breadth-first speed, ~1/7 memory
+            need = int(size_of())
+            if not _fits(need):
+                lib.mk_set_option(_lib.MK_OPT_PLAN, 1)  # depth-first: operand sums only
+                need = int(size_of())
+            yield need
         finally:
             for key, v in old:
                 lib.mk_set_option(key, v)

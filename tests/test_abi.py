@@ -90,8 +90,11 @@ def test_plan_options_change_workspace_not_counts(lib):
     try:
         assert lib.mk_set_option(_lib.MK_OPT_PLAN, 1) == 0  # depth-first: operand sums only
         assert ws("winograd-block", 16384, 2) == (2 * 8192 ** 2 + 2 * 4096 ** 2) * 8
+        assert lib.mk_set_option(_lib.MK_OPT_PLAN, 2) == 0  # hybrid: one top-level subtree at a time
+        hybrid = ws("winograd-block", 16384, 3)
         assert lib.mk_set_option(_lib.MK_OPT_PLAN, 0) == 0
         assert ws("winograd-block", 16384, 2) > 7 * 16384 ** 2 * 8  # breadth-first: every depth
+        assert hybrid * 4 < ws("winograd-block", 16384, 3)
         assert lib.mk_set_option(_lib.MK_OPT_LITERAL_TAIL, 0) == 0  # two-temp literal to the leaves
         assert ws("two-temp", 16384, 2) == (2 * 8192 ** 2 + 2 * 4096 ** 2) * 8
         assert lib.mk_set_option(_lib.MK_OPT_PLAN, 7) == _lib.MK_ERR_ARG

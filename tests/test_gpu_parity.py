@@ -534,7 +534,7 @@ def test_memory_aware_plan_fallback(monkeypatch):
     assert lib.mk_get_option(_lib.MK_OPT_LITERAL_TAIL, ctypes.byref(v)) == 0 and v.value == 1
 
 
-@pytest.mark.parametrize("plan,tail", [("depth-first", True), ("breadth-first", False)])
+@pytest.mark.parametrize("plan,tail", [("depth-first", True), ("hybrid", True), ("breadth-first", False)])
 def test_memory_lean_plans_exact(plan, tail):
     """set_plan: the workspace-minimal depth-first plan and the literal two-temp schedule give
     bit-exact integer results, smaller workspaces, unchanged modeled counters."""
@@ -556,9 +556,14 @@ def test_memory_lean_plans_exact(plan, tail):
             ctr = CALL[algo](pk.Matrix(a), pk.Matrix(b), c, pol)
             assert np.array_equal(c.arr, want), (plan, algo)
             assert ctr.snapshot() == base[algo][0]
-            lean = (plan == "depth-first") if algo != "two-temp" else (not tail)
+            lean = (plan in ("depth-first", "hybrid")) if algo != "two-temp" else (not tail)
             if lean:
                 assert pk.last_stats().workspace_bytes < base[algo][1], (plan, algo)
+        # rectangular driver under the same plan (even-quadrant padding, 3 levels)
+        ar = r.integers(-8, 9, (300, 517)).astype(np.float64)
+        br = r.integers(-8, 9, (517, 260)).astype(np.float64)
+        cr = pk.multiply(pk.Matrix(ar), pk.Matrix(br), pk.get_variant("winograd-mod2", cutoff=64))
+        assert np.array_equal(cr.arr, ar @ br), plan
     finally:
         pk.set_plan()
 
