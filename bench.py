@@ -422,6 +422,11 @@ def main():
 
         lean = []
         try:
+            pk.set_plan("hybrid", two_temp_tail=False)
+            ms_hy = timed(lambda: pk.winograd_block_mul(A, B, C, policy))
+            lean.append({"variant": "winograd-block, hybrid plan (top level depth-first, breadth-first below)",
+                         "ms_per_step": round(ms_hy, 3), "value": round(2.0 * n ** 3 / (ms_hy * 1e-3) / 1e12, 4),
+                         "workspace_bytes": int(lib.mk_workspace_bytes(_lib.ALGO_IDS[args.algo], n, levels))})
             pk.set_plan("depth-first", two_temp_tail=False)
             ms_dfs = timed(lambda: pk.winograd_block_mul(A, B, C, policy))
             lean.append({"variant": "winograd-block, depth-first plan (P_i accumulated into C by the epilogue)",
