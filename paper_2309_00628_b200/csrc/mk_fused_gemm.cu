@@ -912,13 +912,20 @@ static int sm_count() {
 // Tile width of the persistent kernel: 64 when it cuts the column padding of the leaf by more
 // than 10% (only with the synchronous epilogue: the TMA epilogue's C maps are built for the
 // default box shape), else 128. Env MK_NARROW=0 disables narrow tiles.
-static int persistent_bn(const MkGemmArgs& a) {
+// Also narrow when 128-column tiles would leave most SMs idle (a launch of fewer than 60% of the
+// SM count in tiles, e.g. one 1024^2 leaf of a literal schedule: 64 tiles -> 128); such launches
+// switch to the synchronous epilogue.
+static int sm_count();
+static int persistent_bn(const MkGemmArgs& a, int nprod) {
   static int narrow = -1;
   if (narrow < 0) {
     const char* e = getenv("MK_NARROW");
     narrow = (e && e[0] == '0') ? 0 : 1;
   }
-  if (!narrow || a.async_epi) return 128;
+  if (!narrow) return 128;
+  const int64_t tiles128 = (int64_t)a.tiles_m * ((a.N + 127) / 128) * nprod;
+  if (tiles128 * 10 < (int64_t)sm_count() * 6) return 64;
+  if (a.async_epi) return 128;
   const int64_t w128 = (a.N + 127) / 128 * 128, w64 = (a.N + 63) / 64 * 64;
   return (w64 * 10 < w128 * 9) ? 64 : 128;
 }
@@ -950,7 +957,10 @@ static cudaError_t launch_persistent_t(const CUtensorMap& tmA, const CUtensorMap
 
 static cudaError_t launch_persistent(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
                                      MkGemmArgs args, const MkProduct& prod, int nprod, cudaStream_t stream) {
-  if (persistent_bn(args) == 64) return launch_persistent_t<4, 64>(tmA, tmB, tmC, args, prod, nprod, stream);
+  if (persistent_bn(args, nprod) == 64) {
+    args.async_epi = 0;  // the TMA epilogue's C maps are built for the 128-column layouts' boxes
+    return launch_persistent_t<4, 64>(tmA, tmB, tmC, args, prod, nprod, stream);
+  }
   if (consumer_layout() == 16) return launch_persistent_t<4, 128>(tmA, tmB, tmC, args, prod, nprod, stream);
   return launch_persistent_t<8, 128>(tmA, tmB, tmC, args, prod, nprod, stream);
 }
