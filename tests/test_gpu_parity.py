@@ -622,3 +622,25 @@ def test_guard_bands_no_out_of_bounds_writes(algo):
             assert bool(torch.isnan(G[mask]).all()), (algo, cut, "write outside the view")
         if algo != "in-place":
             assert np.array_equal(GA[inner].cpu().numpy(), a) and np.array_equal(GB[inner].cpu().numpy(), b)
+
+
+def test_randomized_shapes_and_presets():
+    """Randomised sweep (fixed seed): rectangular shapes 1..700, every preset, random cutoffs,
+    host and device operands, integer data bit-exact against numpy."""
+    import torch
+
+    r = np.random.default_rng(2024)
+    presets = pk.preset_names()
+    for case in range(48):
+        m, k, n = (int(x) for x in r.integers(1, 700, 3))
+        name = presets[case % len(presets)]
+        spec = pk.get_variant(name, cutoff=int(r.choice([8, 16, 32, 64, 100, 128])))
+        a = r.integers(-8, 9, (m, k)).astype(np.float64)
+        b = r.integers(-8, 9, (k, n)).astype(np.float64)
+        if case % 3 == 2:
+            A, B = pk.Matrix(torch.from_numpy(a).cuda()), pk.Matrix(torch.from_numpy(b).cuda())
+        else:
+            A, B = pk.Matrix(a), pk.Matrix(b)
+        c = pk.multiply(A, B, spec)
+        got = c.numpy() if hasattr(c, "numpy") else np.asarray(c.arr)
+        assert np.array_equal(got, a @ b), (case, name, m, k, n)
