@@ -293,10 +293,11 @@ def _fits(nbytes: int) -> bool:
 
 
 @contextlib.contextmanager
-def _memory_aware_plan(size_of):
+def _memory_aware_plan(size_of, levels: int = 3):
     """Yield the workspace size for this call. When the configured plan's workspace does not fit
-    in device memory, the call runs with the workspace-minimal options instead (depth-first plan,
-    literal two-temp schedule; same results on integer data) and the options are restored."""
+    in device memory, the call runs with leaner options instead -- the hybrid plan first for
+    deep recursions (breadth-first speed at ~1/7 of the memory), else the depth-first plan and the
+    literal two-temp schedule (same results on integer data) -- and the options are restored."""
     need = int(size_of())
     if _fits(need):
         yield need
@@ -310,9 +311,11 @@ def _memory_aware_plan(size_of):
             old.append((key, v.value))
         try:
             lib.mk_set_option(_lib.MK_OPT_LITERAL_TAIL, 0)
-            lib.mk_set_option(_lib.MK_OPT_PLAN, 2)  # hybrid first: breadth-first speed, ~1/7 memory
-            need = int(size_of())
-            if not _fits(need):
+            need = -1
+            if levels >= 3:  # at <= 2 levels depth-first is as fast and smaller
+                lib.mk_set_option(_lib.MK_OPT_PLAN, 2)  # hybrid: breadth-first speed, ~1/7 memory
+                need = int(size_of())
+            if need < 0 or not _fits(need):
                 lib.mk_set_option(_lib.MK_OPT_PLAN, 1)  # depth-first: operand sums only
                 need = int(size_of())
             yield need
@@ -392,7 +395,7 @@ def _overlapped_host_product(algo: str, a: MatrixView, b: MatrixView, c: MatrixV
     dB = torch.empty((n, ld), dtype=torch.float64, device="cuda")
     dC = torch.empty((n, ld), dtype=torch.float64, device="cuda")
     aid = _lib.ALGO_IDS[algo]
-    with _memory_aware_plan(lambda: lib.mk_host_workspace_bytes(aid, n, levels)) as ws_bytes:
+    with _memory_aware_plan(lambda: lib.mk_host_workspace_bytes(aid, n, levels), levels) as ws_bytes:
         ws = workspace(ws_bytes)
         st.workspace_bytes = ws_bytes
         st.path = "overlapped-host"
@@ -431,7 +434,7 @@ def device_square(algo: str, a: MatrixView, b: MatrixView, c: MatrixView, levels
     out = Output(c, dtype, st)
     C = out.op
     aid = _lib.ALGO_IDS[algo]
-    with _memory_aware_plan(lambda: lib.mk_workspace_bytes(aid, n, levels)) as ws_bytes:
+    with _memory_aware_plan(lambda: lib.mk_workspace_bytes(aid, n, levels), levels) as ws_bytes:
         st.workspace_bytes = ws_bytes
         ws = workspace(ws_bytes)
         rc = lib.mk_strassen(aid, A.ptr, A.ld, B.ptr, B.ld, C.ptr, C.ld, n, levels, _vp(ws), ws_bytes, _stream())
@@ -471,7 +474,7 @@ def device_rect(algo: str, a: MatrixView, b: MatrixView, c: MatrixView, levels: 
     out = Output(c, dtype, st)
     C = out.op
     aid = _lib.ALGO_IDS[algo]
-    with _memory_aware_plan(lambda: lib.mk_rect_workspace_bytes(aid, m, n, k, levels)) as ws_bytes:
+    with _memory_aware_plan(lambda: lib.mk_rect_workspace_bytes(aid, m, n, k, levels), levels) as ws_bytes:
         st.workspace_bytes = ws_bytes
         ws = workspace(ws_bytes)
         rc = lib.mk_multiply_rect(aid, A.ptr, A.ld, B.ptr, B.ld, C.ptr, C.ld, m, n, k, levels, _vp(ws), ws_bytes,
