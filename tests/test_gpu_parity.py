@@ -141,7 +141,8 @@ def test_cfg3_n8192_winograd_three_levels(levels_cut):
     err = float((c.arr - cn.arr).abs().max())
     # reference CPU Winograd error vs naive on these inputs: 3.5e-12
     print(f"cfg3: max|C - C_naive| = {err:.3e} (reference CPU 3.5e-12)")
-    assert err <= tol(8192, a, b) and err <= 4 * 3.5e-12, err
+    # at least as accurate as the reference itself (256-k two-level accumulation: 2.9e-12)
+    assert err <= tol(8192, a, b) and err <= 3.5e-12, err
     r = np.random.default_rng(3)
     res_s = _freivalds(c.arr.cpu().numpy(), a, b, r)
     res_n = _freivalds(cn.arr.cpu().numpy(), a, b, np.random.default_rng(3))
@@ -163,9 +164,9 @@ def test_cfg4_n16384_winograd(cut, ref_err):
     err = float((c.arr - cn.arr).abs().max())
     # reference CPU Winograd error vs naive on these inputs: ref_err
     print(f"cfg4 cutoff {cut}: max|C - C_naive| = {err:.3e} (reference CPU {ref_err:.1e})")
-    # gate: the stated bound; sanity: within 4x the reference's own error (two-level register +
-    # TMEM accumulation keeps the DMMA error at the OpenBLAS level -- DESIGN.md, accuracy)
-    assert err <= tol(16384, a, b) and err <= 4 * ref_err, err
+    # gate: the stated bound; and at least as accurate as the reference's own Winograd (two-level
+    # register + TMEM accumulation every 256 k: 1.5e-12 / 4.0e-12 -- DESIGN.md, accuracy)
+    assert err <= tol(16384, a, b) and err <= ref_err, err
     del c, cn, da, db
     torch.cuda.empty_cache()
 
