@@ -313,7 +313,8 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const __grid
   // so each output is a short register sum of <= 16*chunk products plus a sum of K/(16*chunk)
   // chunk totals -- the error growth of OpenBLAS-style K blocking, with the DMMA pipe idle for
   // only ~0.2% of the time. Disabled (chunk = 0) when K fits in one chunk.
-  const int chunk = (args.chunk_stages > 0 && KT > args.chunk_stages) ? args.chunk_stages : 0;
+  // leaves with K <= 512 keep a single register sum (<= 512 terms): folding them buys little
+  const int chunk = (args.chunk_stages > 0 && KT > 32 && KT > args.chunk_stages) ? args.chunk_stages : 0;
   constexpr int kWords = 16 * MT;  // 32-bit words of accumulator per thread
   uint32_t taddr = 0;
   if (chunk) {
@@ -666,7 +667,8 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
   };
 
   // two-level accumulation (see fused_product_kernel); TMEM is allocated once per CTA
-  const int chunk = (args.chunk_stages > 0 && KT > args.chunk_stages) ? args.chunk_stages : 0;
+  // leaves with K <= 512 keep a single register sum (<= 512 terms): folding them buys little
+  const int chunk = (args.chunk_stages > 0 && KT > 32 && KT > args.chunk_stages) ? args.chunk_stages : 0;
   constexpr int kWords = 16 * MT;
   constexpr int kPieces = kWords / 16;
   uint32_t taddr = 0;
