@@ -291,9 +291,12 @@ def main():
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         _lib.check(lib.mk_timing_begin(), "mk_timing_begin")
+        marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps - 1)]
         e0.record(stream)
-        for _ in range(args.steps):
+        for i in range(args.steps):
             step()
+            if i < args.steps - 1:
+                marks[i].record(stream)  # per-step boundaries (median / best below)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -302,6 +305,8 @@ def main():
                                  __import__("ctypes").byref(kfl)), "mk_timing_end")
     launches = lib.mk_launch_count() - launches0
     ms = e0.elapsed_time(e1) / args.steps
+    bounds = [e0] + marks + [e1]
+    step_ms = [bounds[i].elapsed_time(bounds[i + 1]) for i in range(args.steps)]
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -378,6 +383,8 @@ def main():
     line = {
         "metric": METRIC.format(n=n), "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 3), "higher_is_better": True,
+        "step_ms": {"median": round(statistics.median(step_ms), 3), "best": round(min(step_ms), 3),
+                    "worst": round(max(step_ms), 3)},
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded standard normal)",
         "config": config(args, levels),
         "actual_tflops": round(f_act / (ms * 1e-3) / 1e12, 4),
