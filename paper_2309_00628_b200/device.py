@@ -282,6 +282,7 @@ def workspace(nbytes: int):
 
 _plan_lock = threading.Lock()
 _WS_MARGIN = 256 << 20
+_WS_QUERY_MIN = 1 << 30  # workspaces below 1 GiB are allocated without asking the driver first
 
 
 def _fits(nbytes: int) -> bool:
@@ -299,7 +300,7 @@ def _memory_aware_plan(size_of, levels: int = 3):
     deep recursions (breadth-first speed at ~1/7 of the memory), else the depth-first plan and the
     literal two-temp schedule (same results on integer data) -- and the options are restored."""
     need = int(size_of())
-    if _fits(need):
+    if need < _WS_QUERY_MIN or _fits(need):  # small workspaces: skip the (~0.7 ms) memory query
         yield need
         return
     lib = _lib.load(required=True)

@@ -526,6 +526,7 @@ def test_memory_aware_plan_fallback(monkeypatch):
     full = lib.mk_workspace_bytes(_lib.ALGO_IDS["winograd-block"], n, 4)
     assert lean < full
     monkeypatch.setattr(device, "_fits", lambda nbytes: nbytes <= lean)
+    monkeypatch.setattr(device, "_WS_QUERY_MIN", 0)
     c = pk.Matrix.zeros(n, n)
     pk.winograd_block_mul(pk.Matrix(a), pk.Matrix(b), c, pk.BasePolicy.naive_cutoff(64))
     assert pk.last_stats().workspace_bytes == lean
