@@ -1053,6 +1053,23 @@ struct Engine {
       const std::vector<BNode>& cur = lv[d];
       std::vector<BNode> next(cur.size() * np);
       std::vector<MkXformJob> ja, jb;
+      // every materialised sum of this depth lives in one arena per side (row-stacked blocks of
+      // equal shape): one tensor map per arena instead of one per block -- deep recursions plan
+      // thousands of blocks. Tiles that run past a block's rows or K extent read the next block,
+      // which the kernel's row masking and K-tail zeroing already ignore.
+      int arena[2] = {-1, -1};
+      int64_t arena_next[2] = {0, 0};
+      for (int side = 0; side < 2; ++side) {
+        int64_t count = 0;
+        for (int p = 0; p < np; ++p) {
+          const int* cf = side == 0 ? co->a[p] : co->b[p];
+          int terms = 0;
+          for (int q = 0; q < 4; ++q) terms += cf[q] != 0;
+          if (terms > 1) count += (int64_t)cur.size();
+        }
+        const int64_t hr = side == 0 ? hm : hk, hc = side == 0 ? hk : hn;
+        if (count) MK_TRY(alloc_slot(count * hr, hc, &arena[side]));
+      }
       for (size_t i = 0; i < cur.size(); ++i) {
         for (int side = 0; side < 2; ++side) {
           const Blk& src = side == 0 ? cur[i].x : cur[i].y;
@@ -1076,12 +1093,11 @@ struct Engine {
               tgt = Blk{src.base, src.row + (q1 >> 1) * hr, src.col + (q1 & 1) * hc, src.sign * cf[q1]};
               continue;
             }
-            int sb;
-            MK_TRY(alloc_slot(hr, hc, &sb));
-            tgt = Blk{sb, 0, 0, 1.0};
+            tgt = Blk{arena[side], arena_next[side], 0, 1.0};
+            arena_next[side] += hr;
             const int j = job.ndst++;
-            job.dst[j] = bases[sb].ptr;
-            job.ldd[j] = bases[sb].ld;
+            job.dst[j] = ptr_of(tgt);
+            job.ldd[j] = bases[arena[side]].ld;
             for (int q = 0; q < 4; ++q) job.coef[j][q] = (int8_t)(cf[q] * (src.sign < 0 ? -1 : 1));
           }
           if (job.ndst) (side == 0 ? ja : jb).push_back(job);
@@ -1096,12 +1112,10 @@ struct Engine {
     const int64_t lm = M >> L, ln = N >> L, lk = K >> L;
     if (L == 1) {
       par[0].o = D;
-    } else {
-      for (BNode& pn : par) {
-        int sb;
-        MK_TRY(alloc_slot(2 * lm, 2 * ln, &sb));
-        pn.o = Blk{sb, 0, 0, 1.0};
-      }
+    } else {  // parents' outputs row-stacked in one arena
+      int ob;
+      MK_TRY(alloc_slot((int64_t)par.size() * 2 * lm, 2 * ln, &ob));
+      for (size_t i = 0; i < par.size(); ++i) par[i].o = Blk{ob, (int64_t)i * 2 * lm, 0, 1.0};
     }
     const int slab = consumer_layout() == 16 ? 32 : 64;
     bool touched[4] = {false, false, false, false};
@@ -1205,13 +1219,13 @@ struct Engine {
       std::vector<BNode>& pa = lv[d - 1];
       const int64_t cm = M >> d, cn = N >> d;
       std::vector<MkXformJob> jobs;
+      int pb_arena = -1;
+      if (d - 1 != 0) MK_TRY(alloc_slot((int64_t)pa.size() * 2 * cm, 2 * cn, &pb_arena));
       for (size_t j = 0; j < pa.size(); ++j) {
         if (d - 1 == 0) {
           pa[j].o = D;
         } else {
-          int sb;
-          MK_TRY(alloc_slot(2 * cm, 2 * cn, &sb));
-          pa[j].o = Blk{sb, 0, 0, 1.0};
+          pa[j].o = Blk{pb_arena, (int64_t)j * 2 * cm, 0, 1.0};
         }
         MkXformJob job{};
         job.nsrc = np;
