@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <atomic>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -263,7 +264,7 @@ struct ProductTiming {
 };
 static thread_local ProductTiming g_timing;
 
-static int g_fuse_preadds = -1;  // -1: unset (env MK_FUSE_PREADDS), 0/1 explicit
+static std::atomic<int> g_fuse_preadds{-1};  // -1: unset (env MK_FUSE_PREADDS), 0/1 explicit
 static bool fuse_preadds_default() {
   if (g_fuse_preadds < 0) {
     const char* e = getenv("MK_FUSE_PREADDS");
@@ -274,7 +275,7 @@ static bool fuse_preadds_default() {
 
 // Widest batched-transform access in doubles (env MK_XFORM_WIDTH: 1, 2 or 4; default 4).
 static int xform_max_width() {
-  static int v = -1;
+  static std::atomic<int> v{-1};
   if (v < 0) {
     const char* e = getenv("MK_XFORM_WIDTH");
     v = e ? atoi(e) : 4;
@@ -284,7 +285,7 @@ static int xform_max_width() {
 }
 
 static bool async_epilogue_enabled() {
-  static int v = -1;
+  static std::atomic<int> v{-1};
   if (v < 0) {
     const char* e = getenv("MK_ASYNC_EPI");
     v = (e && e[0] == '0') ? 0 : 1;
@@ -293,7 +294,7 @@ static bool async_epilogue_enabled() {
 }
 
 // MK_OPT_LITERAL_TAIL / MK_OPT_PLAN (mk_set_option); -1 = take the environment default
-static int g_literal_tail = -1, g_plan_dfs = -1;
+static std::atomic<int> g_literal_tail{-1}, g_plan_dfs{-1};  // process-wide options
 static bool literal_bfs_tail() {
   if (g_literal_tail < 0) {
     const char* e = getenv("MK_LITERAL_TAIL");
@@ -313,7 +314,7 @@ static int plan_kind() {
 static bool plan_dfs() { return plan_kind() == 1; }
 
 static bool debug_sync() {
-  static int v = -1;
+  static std::atomic<int> v{-1};
   if (v < 0) {
     const char* e = getenv("MK_DEBUG_SYNC");
     v = (e && e[0] == '1') ? 1 : 0;
@@ -333,7 +334,7 @@ enum { BASE_A = 0, BASE_B = 1, BASE_C = 2, BASE_WS0 = 3 };
 // MK_HOST_TRACE=1: mk_strassen_host prints a timeline (ms from the first upload) of its uploads,
 // top-level products / children and downloads to stderr (dev aid).
 static bool host_trace_on() {
-  static int v = -1;
+  static std::atomic<int> v{-1};
   if (v < 0) {
     const char* e = getenv("MK_HOST_TRACE");
     v = (e && e[0] == '1') ? 1 : 0;

@@ -23,6 +23,7 @@
 // (g>>1) + 4*(g&1).  A lane reads one 16B chunk of a B row holding columns 2g, 2g+1, which
 // feeds two n-fragments per LDS.128; the k order (2q+8t+e) matches A's.
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdlib>
 #include <type_traits>
 #include "mk_device.cuh"
@@ -869,7 +870,7 @@ extern "C" __attribute__((visibility("default"))) int mk_trace_read(unsigned lon
 // Host-side launcher (called by the planner).
 // ------------------------------------------------------------------------------------
 // Consumer warps per CTA: 8 (MT=8, default) or 16 (MT=4); env MK_CONSUMER_WARPS overrides.
-static int g_consumer_layout = 0;
+static std::atomic<int> g_consumer_layout{0};
 int consumer_layout() {
   if (g_consumer_layout == 0) {
     const char* e = getenv("MK_CONSUMER_WARPS");
@@ -882,7 +883,7 @@ void set_consumer_layout(int warps) { g_consumer_layout = (warps == 8) ? 8 : 16;
 // Stages per register chunk of the two-level (register + TMEM) accumulation; 0 disables it.
 // Default 16 stages = 256 k (errors below the reference CPU's on every config, for ~0.7% of the main
 // loop; 32 stages: 1.3x the reference's errors). Env MK_ACC_CHUNK overrides (0 = single-level).
-static int g_chunk = -1;
+static std::atomic<int> g_chunk{-1};
 int accumulate_chunk_stages() {
   if (g_chunk < 0) {
     const char* e = getenv("MK_ACC_CHUNK");
@@ -893,7 +894,7 @@ int accumulate_chunk_stages() {
 }
 
 // Persistent plain-product kernel (env MK_PERSISTENT=0 selects the one-CTA-per-tile kernel).
-static int g_persistent = -1;
+static std::atomic<int> g_persistent{-1};
 bool persistent_enabled() {
   if (g_persistent < 0) {
     const char* e = getenv("MK_PERSISTENT");
@@ -902,7 +903,7 @@ bool persistent_enabled() {
   return g_persistent == 1;
 }
 static int sm_count() {
-  static int cache[64] = {0};
+  static std::atomic<int> cache[64] = {};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
   if (cache[dev] == 0) {
@@ -920,7 +921,7 @@ static int sm_count() {
 // switch to the synchronous epilogue.
 static int sm_count();
 static int persistent_bn(const MkGemmArgs& a, int nprod) {
-  static int narrow = -1;
+  static std::atomic<int> narrow{-1};
   if (narrow < 0) {
     const char* e = getenv("MK_NARROW");
     narrow = (e && e[0] == '0') ? 0 : 1;
