@@ -646,3 +646,45 @@ def test_randomized_shapes_and_presets():
         c = pk.multiply(A, B, spec)
         got = c.numpy() if hasattr(c, "numpy") else np.asarray(c.arr)
         assert np.array_equal(got, a @ b), (case, name, m, k, n)
+
+
+def test_concurrent_calls_from_threads():
+    """The engine is reentrant per stream: two host threads, each on its own CUDA stream, run
+    products (device-resident, breadth-first and depth-first plans, and the host path) at once."""
+    import threading
+
+    import torch
+
+    errors = []
+
+    def worker(seed, n, cut, host):
+        try:
+            r = np.random.default_rng(seed)
+            a = r.integers(-8, 9, (n, n)).astype(np.float64)
+            b = r.integers(-8, 9, (n, n)).astype(np.float64)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(3):
+                    if host:
+                        c = np.zeros((n, n))
+                        pk.winograd_block_mul(pk.Matrix(a), pk.Matrix(b), pk.Matrix(c), pk.BasePolicy.naive_cutoff(cut))
+                        got = c
+                    else:
+                        ca = pk.Matrix.zeros(n, n, device="cuda")
+                        pk.strassen_mul(pk.Matrix(torch.from_numpy(a).cuda()), pk.Matrix(torch.from_numpy(b).cuda()),
+                                        ca, pk.BasePolicy.naive_cutoff(cut))
+                        s.synchronize()
+                        got = ca.numpy()
+                    if not np.array_equal(got, a @ b):
+                        errors.append((seed, n, cut, host))
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+
+    threads = [threading.Thread(target=worker, args=(1, 1024, 128, False)),
+               threading.Thread(target=worker, args=(2, 512, 64, False)),
+               threading.Thread(target=worker, args=(3, 2048, 512, True))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
