@@ -688,3 +688,33 @@ def test_concurrent_calls_from_threads():
     for t in threads:
         t.join()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("algo", ["winograd-block", "two-temp"])
+def test_workspace_too_small_fails_cleanly(algo):
+    """A workspace one byte short returns MK_ERR_WORKSPACE with a message, leaves C untouched, and
+    the engine keeps working afterwards."""
+    import ctypes
+
+    import torch
+
+    from paper_2309_00628_b200 import _lib
+
+    lib = _lib.load()
+    n, L = 1024, 3
+    a = torch.randint(-8, 9, (n, n), device="cuda").double()
+    b = torch.randint(-8, 9, (n, n), device="cuda").double()
+    c = torch.full((n, n), float("nan"), dtype=torch.float64, device="cuda")
+    aid = _lib.ALGO_IDS[algo]
+    need = int(lib.mk_workspace_bytes(aid, n, L))
+    ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    args = (aid, ctypes.c_void_p(a.data_ptr()), n, ctypes.c_void_p(b.data_ptr()), n, ctypes.c_void_p(c.data_ptr()), n,
+            n, L, ctypes.c_void_p(ws.data_ptr()))
+    rc = lib.mk_strassen(*args, need - 1, st)
+    torch.cuda.synchronize()
+    assert rc == _lib.MK_ERR_WORKSPACE and b"workspace" in lib.mk_last_error()
+    assert bool(torch.isnan(c).all())
+    assert lib.mk_strassen(*args, need, st) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(c, a @ b)
