@@ -23,6 +23,7 @@ N > 1     = strong scaling of one product: the 49 leaves, split into 8 row panel
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -248,9 +249,9 @@ def main():
     policy = pk.BasePolicy.naive_cutoff(args.cutoff)
     dev = torch.device("cuda", local)
 
-    peak = __import__("ctypes").c_double(0.0)
-    _lib.check(lib.mk_fp64_peak(__import__("ctypes").byref(peak),
-                                __import__("ctypes").c_void_p(torch.cuda.current_stream().cuda_stream)), "mk_fp64_peak")
+    peak = ctypes.c_double(0.0)
+    _lib.check(lib.mk_fp64_peak(ctypes.byref(peak), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
+               "mk_fp64_peak")
     peak_tflops = float(peak.value)
 
     from oracle import strassen_oracle as o  # seeded inputs identical to the oracle's (cfg4 generator)
@@ -300,9 +301,8 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
-    kms, kcnt, kfl = __import__("ctypes").c_double(), __import__("ctypes").c_int(), __import__("ctypes").c_double()
-    _lib.check(lib.mk_timing_end(__import__("ctypes").byref(kms), __import__("ctypes").byref(kcnt),
-                                 __import__("ctypes").byref(kfl)), "mk_timing_end")
+    kms, kcnt, kfl = ctypes.c_double(), ctypes.c_int(), ctypes.c_double()
+    _lib.check(lib.mk_timing_end(ctypes.byref(kms), ctypes.byref(kcnt), ctypes.byref(kfl)), "mk_timing_end")
     launches = lib.mk_launch_count() - launches0
     ms = e0.elapsed_time(e1) / args.steps
     bounds = [e0] + marks + [e1]
