@@ -100,6 +100,12 @@ class ClockSampler:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=self.fh, stderr=subprocess.DEVNULL)
+            # let nvidia-smi finish starting up (NVML init) before the timed region begins: its
+            # start-up must not land inside a timed step
+            t0 = time.time()
+            while time.time() - t0 < 3.0 and os.path.getsize(self.path) == 0:
+                time.sleep(0.05)
+            time.sleep(0.3)
         except Exception:
             self.proc = None
         return self
