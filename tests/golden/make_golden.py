@@ -163,6 +163,20 @@ def main() -> None:
     meta["model_cost_8call"] = [[1 << e, list(rk.model_cost("winograd-knuth-8call", mk.BasePolicy.scalar_only(), 1 << e))]
                                 for e in range(0, 10)]
 
+    # 5. the reference CLI's `count` report (stdout, exit code) for a few presets
+    import contextlib
+    import io
+
+    from matmulkit import cli as rcli
+
+    cli_count = {}
+    for preset in ("winograd-mod2", "strassen-mod", "two-temp", "in-place-mod", "winograd-knuth"):
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            rc = rcli.main(["count", "--algo", preset, "--orders", "2..256"])
+        cli_count[preset] = {"rc": rc, "stdout": buf.getvalue()}
+    meta["cli_count"] = cli_count
+
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(meta, f, indent=0, sort_keys=True)
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)

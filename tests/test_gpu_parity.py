@@ -718,3 +718,15 @@ def test_workspace_too_small_fails_cleanly(algo):
     assert lib.mk_strassen(*args, need, st) == 0
     torch.cuda.synchronize()
     assert torch.equal(c, a @ b)
+
+
+@pytest.mark.parametrize("preset", ["winograd-mod2", "strassen-mod", "two-temp", "in-place-mod", "winograd-knuth"])
+def test_cli_count_output_matches_reference(golden, preset, capsys):
+    """`count` through the engine prints exactly the reference CLI's report (golden, produced by
+    running the reference's own cli.main) and returns the same exit code."""
+    from paper_2309_00628_b200 import cli
+
+    want = golden[0]["cli_count"][preset]
+    rc = cli.main(["count", "--algo", preset, "--orders", "2..256"])
+    assert rc == want["rc"]
+    assert capsys.readouterr().out == want["stdout"]
