@@ -176,6 +176,11 @@ def main() -> None:
             rc = rcli.main(["count", "--algo", preset, "--orders", "2..256"])
         cli_count[preset] = {"rc": rc, "stdout": buf.getvalue()}
     meta["cli_count"] = cli_count
+    buf = io.StringIO()
+    with contextlib.redirect_stdout(buf):
+        rc = rcli.main(["verify", "--orders", "1..32", "--seeds", "2", "--cutoff", "4"])
+    meta["cli_verify"] = {"args": ["verify", "--orders", "1..32", "--seeds", "2", "--cutoff", "4"], "rc": rc,
+                          "stdout": buf.getvalue()}
 
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(meta, f, indent=0, sort_keys=True)

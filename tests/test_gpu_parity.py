@@ -730,3 +730,12 @@ def test_cli_count_output_matches_reference(golden, preset, capsys):
     rc = cli.main(["count", "--algo", preset, "--orders", "2..256"])
     assert rc == want["rc"]
     assert capsys.readouterr().out == want["stdout"]
+
+
+def test_cli_verify_output_matches_reference(golden, capsys):
+    """`verify` through the engine prints the reference CLI's report (golden) byte for byte."""
+    from paper_2309_00628_b200 import cli
+
+    want = golden[0]["cli_verify"]
+    assert cli.main(want["args"]) == want["rc"]
+    assert capsys.readouterr().out == want["stdout"]
