@@ -181,6 +181,24 @@ def main() -> None:
         rc = rcli.main(["verify", "--orders", "1..32", "--seeds", "2", "--cutoff", "4"])
     meta["cli_verify"] = {"args": ["verify", "--orders", "1..32", "--seeds", "2", "--cutoff", "4"], "rc": rc,
                           "stdout": buf.getvalue()}
+    # `multiply --trace` on text files (integer entries, non-square shapes, every schedule preset)
+    import tempfile
+
+    rng = np.random.default_rng(SEED + 77)
+    a = rng.integers(-8, 9, (13, 22))
+    b = rng.integers(-8, 9, (22, 9))
+    cli_mul = {"a": a.tolist(), "b": b.tolist(), "runs": {}}
+    with tempfile.TemporaryDirectory() as td:
+        fa, fb, fc = (os.path.join(td, x) for x in ("a.txt", "b.txt", "c.txt"))
+        mk.write_matrix(mk.Matrix(a), fa)
+        mk.write_matrix(mk.Matrix(b), fb)
+        for preset in ("two-temp-mod", "in-place-mod", "winograd-mod2", "naive"):
+            buf = io.StringIO()
+            args = ["multiply", fa, fb, "--algo", preset, "--cutoff", "4", "-o", fc, "--trace"]
+            with contextlib.redirect_stdout(buf):
+                rc = rcli.main(args)
+            cli_mul["runs"][preset] = {"rc": rc, "stdout": buf.getvalue(), "out": open(fc).read()}
+    meta["cli_multiply"] = cli_mul
 
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(meta, f, indent=0, sort_keys=True)

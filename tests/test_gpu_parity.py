@@ -739,3 +739,20 @@ def test_cli_verify_output_matches_reference(golden, capsys):
     want = golden[0]["cli_verify"]
     assert cli.main(want["args"]) == want["rc"]
     assert capsys.readouterr().out == want["stdout"]
+
+
+@pytest.mark.parametrize("preset", ["two-temp-mod", "in-place-mod", "winograd-mod2", "naive"])
+def test_cli_multiply_files_and_trace_match_reference(golden, preset, tmp_path, capsys):
+    """`multiply --trace` on matrix text files: same trace lines, same output file, same exit code
+    as the reference CLI (golden)."""
+    from paper_2309_00628_b200 import cli
+
+    g = golden[0]["cli_multiply"]
+    fa, fb, fc = (str(tmp_path / x) for x in ("a.txt", "b.txt", "c.txt"))
+    pk.write_matrix(pk.Matrix(np.array(g["a"], dtype=np.int64)), fa)
+    pk.write_matrix(pk.Matrix(np.array(g["b"], dtype=np.int64)), fb)
+    want = g["runs"][preset]
+    rc = cli.main(["multiply", fa, fb, "--algo", preset, "--cutoff", "4", "-o", fc, "--trace"])
+    assert rc == want["rc"]
+    assert capsys.readouterr().out == want["stdout"]
+    assert open(fc).read() == want["out"]
