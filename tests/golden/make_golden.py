@@ -199,6 +199,16 @@ def main() -> None:
                 rc = rcli.main(args)
             cli_mul["runs"][preset] = {"rc": rc, "stdout": buf.getvalue(), "out": open(fc).read()}
     meta["cli_multiply"] = cli_mul
+    # metrics.bench_run records (everything but the times)
+    bench = []
+    for preset in ("winograd-mod2", "two-temp-mod", "in-place", "naive"):
+        for exact in (True, False):
+            for rec in mk.bench_run(preset, [1, 2, 8, 32, 64], 2, SEED, exact=exact, cutoff=8):
+                bench.append({"algo": rec.algo, "order": rec.order, "reps": rec.reps, "mults": rec.mults,
+                              "adds": rec.adds, "temp_buffers": rec.temp_buffers,
+                              "peak_live_elements": rec.peak_live_elements, "seed": rec.seed, "exact": exact})
+    meta["bench_run"] = bench
+    meta["bench_csv_header"] = mk.BenchRecord.CSV_HEADER
 
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(meta, f, indent=0, sort_keys=True)

@@ -756,3 +756,19 @@ def test_cli_multiply_files_and_trace_match_reference(golden, preset, tmp_path, 
     assert rc == want["rc"]
     assert capsys.readouterr().out == want["stdout"]
     assert open(fc).read() == want["out"]
+
+
+def test_bench_run_records_match_reference(golden):
+    """metrics.bench_run through the engine: the records' counters, seeds and CSV header are the
+    reference's (golden); only the times differ."""
+    g = golden[0]
+    assert pk.BenchRecord.CSV_HEADER == g["bench_csv_header"]
+    got = []
+    for preset in ("winograd-mod2", "two-temp-mod", "in-place", "naive"):
+        for exact in (True, False):
+            for rec in pk.bench_run(preset, [1, 2, 8, 32, 64], 2, 20240901, exact=exact, cutoff=8):
+                got.append({"algo": rec.algo, "order": rec.order, "reps": rec.reps, "mults": rec.mults,
+                            "adds": rec.adds, "temp_buffers": rec.temp_buffers,
+                            "peak_live_elements": rec.peak_live_elements, "seed": rec.seed, "exact": exact})
+                assert rec.min_time > 0 and rec.median_time >= rec.min_time
+    assert got == g["bench_run"]
