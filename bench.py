@@ -344,13 +344,18 @@ def main():
         torch.cuda.synchronize()
         barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        fmarks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps - 1)]
         f0.record(stream)
-        for _ in range(args.steps):
+        for i in range(args.steps):
             e2e_step()
+            if i < args.steps - 1:
+                fmarks[i].record(stream)
         f1.record(stream)
         torch.cuda.synchronize()
         barrier()
         ems = f0.elapsed_time(f1) / args.steps
+        fb = [f0] + fmarks + [f1]
+        e2e_steps = [fb[i].elapsed_time(fb[i + 1]) for i in range(args.steps)]
         if world > 1:
             t = torch.tensor([ems], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -362,6 +367,8 @@ def main():
             h2d = int(t.item())
         e2e = {"value": round(2.0 * n ** 3 / (ems * 1e-3) / 1e12, 4), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": n * n * 8,
+               "step_ms": {"median": round(statistics.median(e2e_steps), 3), "best": round(min(e2e_steps), 3),
+                           "worst": round(max(e2e_steps), 3)},
                "ms_per_step": round(ems, 2)}
 
     if rank != 0:
