@@ -161,7 +161,10 @@ cudaError_t launch_xform_batch(const MkXformJob* jobs_dev, int njobs, int64_t ro
   const int64_t work = rows * (cols / width);
   if (work >= (int64_t)1 << 32) return cudaErrorInvalidValue;
   int64_t bx = (work + 255) / 256;
-  const int64_t cap = (148 * 8 + njobs - 1) / njobs;  // ~8 resident CTAs per SM across all jobs
+#ifndef MK_XFORM_CTAS_PER_SM
+#define MK_XFORM_CTAS_PER_SM 32
+#endif
+  const int64_t cap = (148 * MK_XFORM_CTAS_PER_SM + njobs - 1) / njobs;  // resident CTAs per SM, all jobs
   if (bx > cap) bx = cap;
   if (bx < 1) bx = 1;
   for (int j0 = 0; j0 < njobs; j0 += 65535) {
