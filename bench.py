@@ -93,6 +93,7 @@ class ClockSampler:
         self.gpu = gpu_index
         self.proc = None
         self.path = os.path.join("/tmp", f"mk_clocks_{os.getpid()}.csv")
+        self.skip = 0
 
     def __enter__(self):
         try:
@@ -120,12 +121,21 @@ class ClockSampler:
                 self.proc.kill()
             self.fh.close()
 
+    def mark(self):
+        """Start of the timed region: samples written before this are not summarised."""
+        if self.proc is not None:
+            self.fh.flush()
+            self.skip = os.path.getsize(self.path)
+
     def summary(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         sms, maxes, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
+        with open(self.path) as fh:
+            fh.seek(self.skip)
+            lines = fh.read().splitlines()
+        for line in lines:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) < 7:
                 continue
@@ -286,17 +296,19 @@ def main():
 
     torch.cuda.reset_peak_memory_stats(dev)
     mem0 = torch.cuda.memory_allocated(dev)
-    for _ in range(max(args.warmup, 3)):
-        step()
-    torch.cuda.synchronize()
-    peak_mem = torch.cuda.max_memory_allocated(dev) - mem0
-
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = lib.mk_launch_count()
-    barrier()
-    torch.cuda.synchronize()
+    # the clock sampler starts before the warm-up steps so that nvidia-smi's own start-up work
+    # is over before the timed region; only samples taken after mark() are summarised
     with ClockSampler(local) as clk:
+        for _ in range(max(args.warmup, 3)):
+            step()
+        torch.cuda.synchronize()
+        peak_mem = torch.cuda.max_memory_allocated(dev) - mem0
+        launches0 = lib.mk_launch_count()
+        barrier()
+        torch.cuda.synchronize()
+        clk.mark()
         _lib.check(lib.mk_timing_begin(), "mk_timing_begin")
         marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps - 1)]
         e0.record(stream)
@@ -313,6 +325,8 @@ def main():
     ms = e0.elapsed_time(e1) / args.steps
     bounds = [e0] + marks + [e1]
     step_ms = [bounds[i].elapsed_time(bounds[i + 1]) for i in range(args.steps)]
+    if os.environ.get("MK_BENCH_VERBOSE"):
+        print("step_ms", [round(x, 3) for x in step_ms], file=sys.stderr)
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
