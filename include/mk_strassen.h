@@ -88,6 +88,20 @@ const char* mk_last_error(void);
 int mk_dgemm(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
              int64_t m, int64_t n, int64_t k, void* stream);
 
+/* C[m x n] = A[m x k] * B[k x n] with FP64 operands multiplied on the INT8 tensor cores
+ * (Ozaki scheme I: each row of A / column of B split into `slices` signed 7-bit digits under a
+ * power-of-two scale, the slices*(slices+1)/2 digit-pair products accumulated exactly in int32
+ * by tcgen05.mma kind::i8, recombined in FP64). Same operand/alias rules as mk_dgemm; an
+ * opt-in alternative to the DMMA leaf (mk_set_option(MK_OPT_LEAF_SLICES, s)). slices in [4, 8];
+ * k <= 2^31 / (slices * 127^2). ws: mk_ozaki_workspace_bytes(m, n, k, slices) bytes of device
+ * memory, 256-byte aligned. Integer-valued data with <= 7*slices significant bits relative to
+ * each row / column maximum is reproduced exactly; otherwise the per-term error is
+ * <= (slices + 2) * 2^(-7 slices) * 2^(e_i + f_j) (e_i, f_j: row / column max exponents).
+ * Replaces the same call sites as mk_dgemm (kernels.py:258-266). */
+size_t mk_ozaki_workspace_bytes(int64_t m, int64_t n, int64_t k, int slices);
+int mk_ozaki_dgemm(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                   int64_t m, int64_t n, int64_t k, int slices, void* ws, size_t ws_bytes, void* stream);
+
 /* Levels the engine runs for an order-n problem under the reference's base policy
  * (BasePolicy kernels.py:26-57): kind 0 = "scalar", 1 = "unrolled" (param = order),
  * 2 = "naive-cutoff" (param = threshold). naive-cutoff is honoured exactly

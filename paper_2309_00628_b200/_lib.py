@@ -45,6 +45,8 @@ SIGNATURES = {
     "mk_get_option": (_INT, [_INT, ctypes.POINTER(ctypes.c_int)]),
     "mk_last_error": (ctypes.c_char_p, []),
     "mk_dgemm": (_INT, [_VP, _I64, _VP, _I64, _VP, _I64, _I64, _I64, _I64, _VP]),
+    "mk_ozaki_workspace_bytes": (_SZ, [_I64, _I64, _I64, _INT]),
+    "mk_ozaki_dgemm": (_INT, [_VP, _I64, _VP, _I64, _VP, _I64, _I64, _I64, _I64, _INT, _VP, _SZ, _VP]),
     "mk_levels_for_policy": (_INT, [_I64, _INT, _I64, _INT, ctypes.POINTER(_INT)]),
     "mk_workspace_bytes": (_SZ, [_INT, _I64, _INT]),
     "mk_strassen": (_INT, [_INT, _VP, _I64, _VP, _I64, _VP, _I64, _I64, _INT, _VP, _SZ, _VP]),

@@ -32,6 +32,7 @@
 #include "../../include/mk_strassen.h"
 #include "mk_blockops.h"
 #include "mk_hoststage.h"
+#include "mk_ozaki.h"
 #include "mk_plan.h"
 
 namespace mk {
@@ -1484,6 +1485,26 @@ int mk_dgemm(const double* A, int64_t lda, const double* B, int64_t ldb, double*
   e.add_base(const_cast<double*>(B), ldb, k, n, k, n);
   e.add_base(C, ldc, m, n, m, n);
   return e.product(Lin{Blk{BASE_A, 0, 0, 1.0}}, Lin{Blk{BASE_B, 0, 0, 1.0}}, Lin{Blk{BASE_C, 0, 0, 1.0}}, m, n, k);
+}
+
+size_t mk_ozaki_workspace_bytes(int64_t m, int64_t n, int64_t k, int slices) {
+  if (m < 1 || n < 1 || k < 1 || slices < kOzMinSlices || slices > kOzMaxSlices) return 0;
+  return ozaki_workspace_bytes(m, n, k, slices);
+}
+
+int mk_ozaki_dgemm(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int64_t m,
+                   int64_t n, int64_t k, int slices, void* ws, size_t ws_bytes, void* stream) {
+  g_last_error.clear();
+  if (m < 1 || n < 1 || k < 1) return fail(MK_ERR_DIMENSION, "extents must be positive");
+  if (lda < k || ldb < n || ldc < n) return fail(MK_ERR_DIMENSION, "leading dimension smaller than the extent");
+  if (overlaps(C, ldc, m, n, A, lda, m, k) || overlaps(C, ldc, m, n, B, ldb, k, n))
+    return fail(MK_ERR_ALIAS, "output view must not alias an input view");
+  std::string err;
+  const int rc = ozaki_product(A, lda, B, ldb, C, ldc, m, n, k, slices, 0, 1.0, ws, ws_bytes,
+                               static_cast<cudaStream_t>(stream), &err);
+  if (rc != MK_OK) return fail(rc, err);
+  g_launch_count += 5;
+  return MK_OK;
 }
 
 int mk_levels_for_policy(int64_t n, int kind, int64_t param, int algo, int* levels_out) {
