@@ -63,8 +63,12 @@ int mk_version(void);
  *   top-level product breadth-first below it: about 1/7 of the breadth-first workspace).
  * MK_OPT_LITERAL_TAIL (two-temp): 1 = run the last two levels breadth-first under the literal
  *   Table-2 levels (default), 0 = the literal schedule down to the leaves (2 (n/2)^2-style
- *   scratch only, the paper's memory bound). */
-enum mk_option { MK_OPT_FUSE_PREADDS = 1, MK_OPT_PLAN = 2, MK_OPT_LITERAL_TAIL = 3 };
+ *   scratch only, the paper's memory bound).
+ * MK_OPT_LEAF_SLICES: 0 = leaf products on the FP64 tensor cores (DMMA, default); 4..8 = on the
+ *   INT8 tensor cores (tcgen05 kind::i8, Ozaki scheme I) with that many 7-bit digit slices per
+ *   operand (see mk_ozaki_dgemm; 8 is as accurate as the DMMA leaf, fewer trade accuracy for speed).
+ *   Applies to every product of the engine with single-block operands. */
+enum mk_option { MK_OPT_FUSE_PREADDS = 1, MK_OPT_PLAN = 2, MK_OPT_LITERAL_TAIL = 3, MK_OPT_LEAF_SLICES = 4 };
 int mk_set_option(int key, int value);
 int mk_get_option(int key, int* value);
 

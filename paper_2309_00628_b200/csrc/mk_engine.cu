@@ -314,6 +314,18 @@ static int plan_kind() {
 }
 static bool plan_dfs() { return plan_kind() == 1; }
 
+// MK_OPT_LEAF_SLICES: 0 = leaf products on the FP64 tensor cores (DMMA, default); 4..8 = on the
+// INT8 tensor cores with that many Ozaki digit slices (env MK_LEAF_SLICES)
+static std::atomic<int> g_leaf_slices{-1};
+static int leaf_slices() {
+  if (g_leaf_slices < 0) {
+    const char* e = getenv("MK_LEAF_SLICES");
+    const int v = e ? atoi(e) : 0;
+    g_leaf_slices = (v >= kOzMinSlices && v <= kOzMaxSlices) ? v : 0;
+  }
+  return g_leaf_slices;
+}
+
 static bool debug_sync() {
   static std::atomic<int> v{-1};
   if (v < 0) {
@@ -557,6 +569,41 @@ struct Engine {
   }
 
   // ---- one leaf product launch ----
+  // Leaf product on the INT8 tensor cores (mk_ozaki.cu), timed like the DMMA launches.
+  OzOperand oz_operand(const Lin& T) const {
+    OzOperand o{};
+    o.n = (int)T.size();
+    o.ld = bases[T[0].base].ld;
+    for (int i = 0; i < o.n; ++i) {
+      o.p[i] = ptr_of(T[i]);
+      o.s[i] = T[i].sign;
+    }
+    return o;
+  }
+  int ozaki_leaf(const OzOperand& x, const OzOperand& y, double* c, int64_t ldc, int64_t M, int64_t N, int64_t K,
+                 const OzDest* od, int nd) {
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    if (g_timing.on) {
+      MK_CUDA_TRY(cudaEventCreate(&t0));
+      MK_CUDA_TRY(cudaEventCreate(&t1));
+      MK_CUDA_TRY(cudaEventRecord(t0, st));
+    }
+    std::string err;
+    const int rc = ozaki_product_multi(x, y, c, ldc, M, N, K, leaf_slices(), od, nd, st, &err);
+    if (rc != MK_OK) return fail(rc, err);
+    g_launch_count += 5;
+    if (g_timing.on) {
+      MK_CUDA_TRY(cudaEventRecord(t1, st));
+      g_timing.ev.emplace_back(t0, t1);
+      g_timing.flops.push_back(2.0 * (double)M * (double)N * (double)K);
+    }
+    if (debug_sync()) {
+      cudaError_t e2 = cudaStreamSynchronize(st);
+      if (e2 != cudaSuccess) return fail(MK_ERR_CUDA, std::string("Ozaki leaf: ") + cudaGetErrorString(e2));
+    }
+    return MK_OK;
+  }
+
   int product(const Lin& X, const Lin& Y, const Lin& D, int64_t M, int64_t N, int64_t K) {
     if ((int)X.size() > MK_MAX_TERMS || (int)Y.size() > MK_MAX_TERMS || (int)D.size() > MK_MAX_DESTS ||
         X.empty() || Y.empty() || D.empty())
@@ -590,6 +637,11 @@ struct Engine {
     }
     ++launches;
     if (dry || no_launch) return MK_OK;
+    if (leaf_slices() > 0) {  // INT8 tensor-core leaf; multi-term operands summed as they are split
+      std::vector<OzDest> od(p.nd);
+      for (int i = 0; i < p.nd; ++i) od[i] = OzDest{p.d[i].row, p.d[i].col, p.d[i].sign, p.d[i].accumulate, 0};
+      return ozaki_leaf(oz_operand(X), oz_operand(Y), bases[bd].ptr, bases[bd].ld, M, N, K, od.data(), p.nd);
+    }
     CUtensorMap tmA, tmB, tmC;
     MK_TRY(cached_map(bx, 0, &tmA));
     MK_TRY(cached_map(by, 1, &tmB));
@@ -1250,6 +1302,21 @@ struct Engine {
           }
         }
       }
+      if (leaf_slices() > 0) {  // INT8 tensor-core leaves: one Ozaki product per entry
+        launches += (int)ents.size();
+        if (dry || no_launch) continue;
+        for (size_t gi = 0; gi < gr.size(); ++gi) {
+          for (size_t i = 0; i < par.size(); ++i) {
+            const BNode& lf = lv[L][i * np + gr[gi]];
+            const MkBatchEntry& e = ents[gi * par.size() + i];
+            OzDest od[MK_MAX_DESTS];
+            for (int k = 0; k < e.prod.nd; ++k)
+              od[k] = OzDest{e.prod.d[k].row, e.prod.d[k].col, e.prod.d[k].sign, e.prod.d[k].accumulate, 0};
+            MK_TRY(ozaki_leaf(oz_operand(Lin{lf.x}), oz_operand(Lin{lf.y}), e.C, e.ldc, lm, ln, lk, od, e.prod.nd));
+          }
+        }
+        continue;
+      }
       const int nprod_launch = (int)ents.size();
       void* dev = nullptr;
       MK_TRY(upload(ents.data(), ents.size() * sizeof(MkBatchEntry), &dev));
@@ -1448,6 +1515,12 @@ int mk_set_option(int key, int value) {
     g_literal_tail = value ? 1 : 0;
     return MK_OK;
   }
+  if (key == MK_OPT_LEAF_SLICES) {
+    if (value != 0 && (value < kOzMinSlices || value > kOzMaxSlices))
+      return fail(MK_ERR_ARG, "MK_OPT_LEAF_SLICES takes 0 (DMMA leaves) or 4..8 (INT8 Ozaki slices)");
+    g_leaf_slices = value;
+    return MK_OK;
+  }
   return fail(MK_ERR_ARG, "unknown option key");
 }
 
@@ -1460,6 +1533,8 @@ int mk_get_option(int key, int* value) {
     *value = plan_kind();
   } else if (key == MK_OPT_LITERAL_TAIL) {
     *value = literal_bfs_tail() ? 1 : 0;
+  } else if (key == MK_OPT_LEAF_SLICES) {
+    *value = leaf_slices();
   } else {
     return fail(MK_ERR_ARG, "unknown option key");
   }
@@ -1499,6 +1574,7 @@ int mk_ozaki_dgemm(const double* A, int64_t lda, const double* B, int64_t ldb, d
   if (lda < k || ldb < n || ldc < n) return fail(MK_ERR_DIMENSION, "leading dimension smaller than the extent");
   if (overlaps(C, ldc, m, n, A, lda, m, k) || overlaps(C, ldc, m, n, B, ldb, k, n))
     return fail(MK_ERR_ALIAS, "output view must not alias an input view");
+  if (slices < kOzMinSlices || slices > kOzMaxSlices) return fail(MK_ERR_ARG, "slices must be in [4, 8]");
   std::string err;
   const int rc = ozaki_product(A, lda, B, ldb, C, ldc, m, n, k, slices, 0, 1.0, ws, ws_bytes,
                                static_cast<cudaStream_t>(stream), &err);

@@ -73,6 +73,33 @@ def set_plan(plan: str = "breadth-first", two_temp_tail: bool = True) -> None:
     _lib.check(lib.mk_set_option(_lib.MK_OPT_LITERAL_TAIL, 1 if two_temp_tail else 0), "mk_set_option")
 
 
+def set_leaf(kind: str = "dmma", slices: int = 8) -> None:
+    """Process-wide leaf arithmetic (B200 addition; the reference's leaf is np.matmul, kernels.py:261).
+
+    ``"dmma"`` (default): every leaf product on the FP64 tensor cores (mma.sync f64 -> DMMA).
+    ``"ozaki"``: on the INT8 tensor cores (tcgen05.mma kind::i8, Ozaki scheme I): each operand
+    row / column is split into ``slices`` (4..8) signed 7-bit digits under a power-of-two scale,
+    the digit-pair products are exact int32 sums in tensor memory and are recombined in FP64.
+    With 8 slices the leaf error is at or below the DMMA leaf's (56 digit bits vs 53); integer
+    data is exact either way. Fewer slices trade accuracy for speed. Modeled OpCounter values
+    never change.
+    """
+    if kind not in ("dmma", "ozaki"):
+        raise ValueError(f"leaf must be 'dmma' or 'ozaki', got {kind!r}")
+    if kind == "ozaki" and not (4 <= int(slices) <= 8):
+        raise ValueError(f"slices must be in [4, 8], got {slices!r}")
+    lib = _lib.load(required=True)
+    _lib.check(lib.mk_set_option(_lib.MK_OPT_LEAF_SLICES, int(slices) if kind == "ozaki" else 0), "mk_set_option")
+
+
+def get_leaf() -> tuple:
+    """(kind, slices) of the current leaf arithmetic (see set_leaf)."""
+    lib = _lib.load(required=True)
+    v = ctypes.c_int(0)
+    _lib.check(lib.mk_get_option(_lib.MK_OPT_LEAF_SLICES, ctypes.byref(v)), "mk_get_option")
+    return ("ozaki", v.value) if v.value else ("dmma", 0)
+
+
 def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
