@@ -21,12 +21,15 @@ constexpr int BN = 64;       // tile columns = TMEM columns per anti-diagonal ac
 constexpr int BK = 32;       // int8 k per stage = one UMMA K step (32 bytes = the 32B swizzle span)
 constexpr int STAGES = 4;
 constexpr int NTHREADS = 192;  // warp 0 TMA, warp 1 MMA issuer + TMEM owner, warps 2-5 epilogue
-constexpr int KPAD = 16;       // digit-plane row pitch granularity (TMA stride alignment)
+constexpr int KPAD = BK;       // K padding: whole 32-byte k-blocks
 constexpr int EXP_NONFINITE = INT_MIN;
 
 struct Args {
+  const uint8_t* px;  // X digit tiles [tiles_m][nkb][S][128 rows x 32 B] (smem images, 32B swizzle)
+  const uint8_t* py;  // Y digit tiles [tiles_n][nkb][S][64 rows x 32 B]
   const int32_t* ex;  // row exponents of X (m)
   const int32_t* fy;  // column exponents of Y (n)
+  const int32_t* rs;  // [S][m] row sums of the X digit planes (offset correction of Y's plane 0)
   double* C;
   int64_t ldc;
   int32_t M, N, K, tiles_n;
@@ -70,12 +73,21 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, int c0, int c1, int c2, uint64_t* bar) {
+// Contiguous global -> shared bulk copy (one large request stream instead of one 32-byte
+// request per tile row), completes on `bar`.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// Byte offset of (row r, byte c) in a K-major tile of 32-byte rows under the 32B swizzle
+// (CuTe Swizzle<1,4,3>: address bit 7 flips bit 4 -- the 16-byte halves of rows 4..7 of each
+// 8-row group swap), i.e. the image the UMMA descriptor's SWIZZLE_32B layout reads.
+__host__ __device__ __forceinline__ uint32_t swz32(uint32_t r, uint32_t c) {
+  const uint32_t o = r * 32 + c;
+  return o ^ ((o >> 3) & 0x10);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -86,7 +98,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, int
 // ---------------------------------------------------------------------------------------------
 template <int S>
 __global__ void __launch_bounds__(NTHREADS, 1)
-    ozaki_product_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY, Args a) {
+    ozaki_product_kernel(const __grid_constant__ Args a) {
   constexpr int A_TILE = BM * BK;
   constexpr int B_TILE = BN * BK;
   constexpr int STAGE_BYTES = S * (A_TILE + B_TILE);
@@ -102,8 +114,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int nkb = (a.K + BK - 1) / BK;
 
   if (threadIdx.x == 0) {
-    tma_prefetch_desc(&tmX);
-    tma_prefetch_desc(&tmY);
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
@@ -124,8 +134,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (kb >= STAGES) mbar_wait(&empty[st], ((kb / STAGES) - 1) & 1);
         uint8_t* sa = smem + st * STAGE_BYTES;
         mbar_arrive_expect_tx(&full[st], STAGE_BYTES);
-        tma_load_3d(sa, &tmX, kb * BK, tm * BM, 0, &full[st]);
-        tma_load_3d(sa + S * A_TILE, &tmY, kb * BK, tn * BN, 0, &full[st]);
+        bulk_load(sa, a.px + ((int64_t)tm * nkb + kb) * (S * A_TILE), S * A_TILE, &full[st]);
+        bulk_load(sa + S * A_TILE, a.py + ((int64_t)tn * nkb + kb) * (S * B_TILE), S * B_TILE, &full[st]);
       }
     }
   } else if (warp == 1) {
@@ -137,17 +147,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const uint8_t* sa = smem + st * STAGE_BYTES;
         const uint8_t* sb = sa + S * A_TILE;
         // X digit plane s meets Y planes t = 0..S-1-s. The Y planes are consecutive 64-row
-        // blocks of one K-major operand and their accumulators (anti-diagonals s+t) are
-        // consecutive 64-column TMEM blocks, so one MMA with N = 64 * #planes (<= 256) covers
-        // several pairs of one signedness: plane 0 (signed) alone, planes 1.. (unsigned) in
-        // groups of 4 -- S(S+1)/2 pairs in sum_s (1 + ceil((S-1-s)/4)) MMAs.
+        // blocks of one K-major operand (all unsigned: plane 0 carries a +128 offset) and their
+        // accumulators (anti-diagonals s+t) are consecutive 64-column TMEM blocks, so one MMA
+        // with N = 64 * #planes (<= 256) covers up to 4 pairs: S(S+1)/2 pairs in
+        // sum_s ceil((S-s)/4) MMAs, each reading its X plane once.
 #pragma unroll
         for (int s = 0; s < S; ++s) {
           const uint64_t da = smem_desc_sw32(sa + s * A_TILE);
           const uint32_t acc = (kb > 0 || s > 0) ? 1u : 0u;
-          mma_i8(tmem + (uint32_t)(s * BN), da, smem_desc_sw32(sb), idesc_i8(BN, s == 0, true), acc);
 #pragma unroll
-          for (int t0 = 1; t0 < S - s; t0 += 4) {
+          for (int t0 = 0; t0 < S - s; t0 += 4) {
             const int cnt = (S - s - t0) < 4 ? (S - s - t0) : 4;
             mma_i8(tmem + (uint32_t)((s + t0) * BN), da, smem_desc_sw32(sb + t0 * B_TILE),
                    idesc_i8(cnt * BN, s == 0, false), acc);
@@ -166,6 +175,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
     const bool row_ok = row < a.M;
     const int e = row_ok ? a.ex[row] : 0;
+    // diagonal d holds (a_d . (b_0 + 128)) + ...: subtract 128 * rowsum(a_d)
+    double corr[S];
+#pragma unroll
+    for (int d = 0; d < S; ++d) corr[d] = row_ok ? 128.0 * (double)a.rs[(int64_t)d * a.M + row] : 0.0;
     double* crow = a.C + (int64_t)row * a.ldc;
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 16) {
@@ -178,9 +191,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       for (int j = 0; j < 16; ++j) {
         const int col = tn * BN + c0 + j;
         if (col >= a.N) break;
-        double v = (double)(int32_t)r[S - 1][j];
+        double v = (double)(int32_t)r[S - 1][j] - corr[S - 1];  // exact (integers < 2^40)
 #pragma unroll
-        for (int d = S - 2; d >= 0; --d) v = fma(v, 0.00390625, (double)(int32_t)r[d][j]);
+        for (int d = S - 2; d >= 0; --d) v = fma(v, 0.00390625, (double)(int32_t)r[d][j] - corr[d]);
         const int f = a.fy[col];
         double p;
         if (e == EXP_NONFINITE || f == EXP_NONFINITE)
@@ -214,22 +227,29 @@ __device__ __forceinline__ int row_exponent(double mx) {
 // x * scale = y in (-1, 1) is written as 2^-7 * sum_s d_s 2^(-8s): d_0 = floor(128 y) in
 // [-128, 127] (signed plane), then d_s = floor(256 r) in [0, 255] of the remainder r in [0, 1)
 // (unsigned planes, 8 bits each): 7 + 8 (S - 1) bits. Every step is exact in FP64.
-template <int S>
-__device__ __forceinline__ void digits4(const double x[4], double scale, uint32_t out[S]) {
+// OFFSET: plane 0 stored as d_0 + 128 in [0, 255] (the Y side: every Y plane unsigned, so one MMA
+// can span several planes); the product kernel subtracts 128 * rowsum(X plane) per diagonal.
+// dsum (may be null): per-plane sums of the 4 digits (signed plane 0), for those row sums.
+template <int S, bool OFFSET>
+__device__ __forceinline__ void digits4(const double x[4], double scale, uint32_t out[S], int* dsum) {
   double y[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) y[i] = x[i] * scale;  // |y| < 1, exact (power-of-two scaling)
 #pragma unroll
   for (int s = 0; s < S; ++s) {
     uint32_t w = 0;
+    int sum = 0;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const double z = y[i] * (s == 0 ? 128.0 : 256.0);  // exact
       const double dg = floor(z);
       y[i] = z - dg;  // exact remainder in [0, 1)
-      w |= ((uint32_t)(s == 0 ? (uint8_t)(int8_t)(int)dg : (uint8_t)(int)dg)) << (8 * i);
+      const int di = (int)dg;
+      sum += di;
+      w |= ((uint32_t)(s == 0 ? (uint8_t)(OFFSET ? di + 128 : di) : (uint8_t)di)) << (8 * i);
     }
     out[s] = w;
+    if (dsum) dsum[s] += sum;
   }
 }
 
@@ -242,36 +262,51 @@ __device__ __forceinline__ double term_sum(const OzOperand& o, int64_t r, int64_
   return v;
 }
 
-// X rows -> exponents + S digit planes [S][rows][kp]: one warp per row, each lane 4 consecutive
-// k per iteration (one 32-bit store per plane).
+// X rows -> exponents, digit row sums and S digit planes in the product kernel's tile images
+// ([tile_m][kb][S][128 x 32 B], swizzled): one warp per row (rows up to the padded tile edge
+// write zeros), each lane 4 consecutive k per iteration (one 32-bit store per plane).
 template <int S>
-__global__ void split_rows_kernel(const OzOperand X, int rows, int K, int kp, int32_t* __restrict__ ex,
-                                  uint8_t* __restrict__ planes) {
+__global__ void split_rows_kernel(const OzOperand X, int rows, int rows_pad, int K, int nkb, int32_t* __restrict__ ex,
+                                  int32_t* __restrict__ rs, uint8_t* __restrict__ planes) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (warp >= rows) return;
+  if (warp >= rows_pad) return;
+  const bool live = warp < rows;
   double mx = 0.0;
   bool bad = false;  // inf / nan (fmax alone would drop a NaN)
-  for (int k = lane; k < K; k += 32) {
-    const double v = fabs(term_sum(X, warp, k));
-    bad |= !(v <= 1.7976931348623157e308);
-    mx = fmax(mx, v);
-  }
+  if (live)
+    for (int k = lane; k < K; k += 32) {
+      const double v = fabs(term_sum(X, warp, k));
+      bad |= !(v <= 1.7976931348623157e308);
+      mx = fmax(mx, v);
+    }
 #pragma unroll
   for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   bad = __any_sync(0xffffffffu, bad);
   const int e = bad ? EXP_NONFINITE : row_exponent(mx);
-  if (lane == 0) ex[warp] = e;
+  if (lane == 0 && live) ex[warp] = e;
   const double scale = (e == EXP_NONFINITE) ? 0.0 : ldexp(1.0, -e);
-  const int64_t plane = (int64_t)rows * kp;
-  uint8_t* pr = planes + (int64_t)warp * kp;
+  const int tmi = warp / BM, r = warp % BM;
+  uint8_t* base = planes + (int64_t)tmi * nkb * (S * BM * BK);
+  int dsum[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) dsum[s] = 0;
+  const int kp = nkb * BK;
   for (int k0 = 4 * lane; k0 < kp; k0 += 128) {
     double x[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) x[i] = (k0 + i < K && e != EXP_NONFINITE) ? term_sum(X, warp, k0 + i) : 0.0;
+    for (int i = 0; i < 4; ++i) x[i] = (live && k0 + i < K && e != EXP_NONFINITE) ? term_sum(X, warp, k0 + i) : 0.0;
     uint32_t w[S];
-    digits4<S>(x, scale, w);
+    digits4<S, false>(x, scale, w, dsum);
+    uint8_t* t = base + (int64_t)(k0 / BK) * (S * BM * BK) + swz32(r, k0 % BK);
 #pragma unroll
-    for (int s = 0; s < S; ++s) *reinterpret_cast<uint32_t*>(pr + s * plane + k0) = w[s];
+    for (int s = 0; s < S; ++s) *reinterpret_cast<uint32_t*>(t + s * (BM * BK)) = w[s];
+  }
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    int v = dsum[s];  // |sum| <= K * 255 < 2^31
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0 && live) rs[(int64_t)s * rows + warp] = v;
   }
 }
 
@@ -297,10 +332,11 @@ __global__ void colexp_kernel(const unsigned long long* __restrict__ cmax, int N
   fy[col] = row_exponent(__longlong_as_double((long long)cmax[col]));
 }
 
-// Y (k x n, row-major) -> S planes of Y^T [S][n][kp] (K-major for the B operand), 32 x 32 tiles
-// through shared memory. Block (32, 8).
+// Y (k x n, row-major) -> S digit planes of Y^T in the product kernel's tile images
+// ([tile_n][kb][S][64 x 32 B], swizzled; K-major for the B operand), 32 x 32 tiles through shared
+// memory. Block (32, 8); the grid covers the padded tile edges (zeros).
 template <int S>
-__global__ void split_cols_kernel(const OzOperand Y, int K, int N, int kp, const int32_t* __restrict__ fy,
+__global__ void split_cols_kernel(const OzOperand Y, int K, int N, int nkb, const int32_t* __restrict__ fy,
                                   uint8_t* __restrict__ planes) {
   __shared__ uint32_t sm[S][32][9];  // [plane][col][k/4] (+1 pad)
   const int n0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
@@ -316,55 +352,43 @@ __global__ void split_cols_kernel(const OzOperand Y, int K, int N, int kp, const
     x[i] = (col < N && k < K && scale != 0.0) ? term_sum(Y, k, col) : 0.0;
   }
   uint32_t w[S];
-  digits4<S>(x, scale, w);
+  digits4<S, true>(x, scale, w, nullptr);
+  if (col >= N) {  // padded columns: zero digits (not the +128 offset)
+#pragma unroll
+    for (int s = 0; s < S; ++s) w[s] = 0;
+  }
 #pragma unroll
   for (int s = 0; s < S; ++s) sm[s][tx][ty] = w[s];
   __syncthreads();
-  // write: plane s, rows n0..n0+31, bytes k0..k0+31 -> 32 rows x 8 words; 256 threads, one word each
+  // write: 32 rows (n) x 8 words (k) of each plane; 256 threads, one word each
   const int t = ty * 32 + tx;
   const int r = t >> 3, wi = t & 7;
-  const int n = n0 + r, k = k0 + 4 * wi;
-  if (n < N && k < kp) {
-    const int64_t plane = (int64_t)N * kp;
+  const int n = n0 + r;
+  uint8_t* dst = planes + ((int64_t)(n / BN) * nkb + k0 / BK) * (S * BN * BK) + swz32(n % BN, 4 * wi);
 #pragma unroll
-    for (int s = 0; s < S; ++s) *reinterpret_cast<uint32_t*>(planes + s * plane + (int64_t)n * kp + k) = sm[s][r][wi];
-  }
+  for (int s = 0; s < S; ++s) *reinterpret_cast<uint32_t*>(dst + s * (BN * BK)) = sm[s][r][wi];
 }
 
 // ---------------------------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------------------------
-typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-static PFN_encodeTiled get_encode() {
-  static PFN_encodeTiled fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_encodeTiled>(p);
-  });
-  return fn;
-}
-
 static int64_t kpad(int64_t k) { return (k + KPAD - 1) / KPAD * KPAD; }
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t planes_x, planes_y, ex, fy, cmax, total;
+  size_t planes_x, planes_y, ex, fy, cmax, rs, total;
 };
 static Layout layout(int64_t m, int64_t n, int64_t k, int S) {
   Layout L;
   const int64_t kp = kpad(k);
+  const int64_t mp = (m + BM - 1) / BM * BM, np = (n + BN - 1) / BN * BN;
   L.planes_x = 0;
-  L.planes_y = align256(L.planes_x + (size_t)S * m * kp);
-  L.ex = align256(L.planes_y + (size_t)S * n * kp);
+  L.planes_y = align256(L.planes_x + (size_t)S * mp * kp);
+  L.ex = align256(L.planes_y + (size_t)S * np * kp);
   L.fy = align256(L.ex + 4 * (size_t)m);
   L.cmax = align256(L.fy + 4 * (size_t)n);
-  L.total = align256(L.cmax + 8 * (size_t)n);
+  L.rs = align256(L.cmax + 8 * (size_t)n);
+  L.total = align256(L.rs + 4 * (size_t)S * m);
   return L;
 }
 
@@ -373,26 +397,6 @@ static int64_t chunk_k(int64_t k, int S) {
   const int64_t mx = ozaki_max_k(S) / KPAD * KPAD;
   const int64_t nc = (k + mx - 1) / mx;
   return std::min(mx, kpad((k + nc - 1) / nc));
-}
-
-static int encode_planes(CUtensorMap* tm, uint8_t* planes, int64_t rows, int64_t kp, int S, uint32_t box_rows,
-                         std::string* err) {
-  PFN_encodeTiled enc = get_encode();
-  if (!enc) {
-    *err = "cuTensorMapEncodeTiled unavailable";
-    return MK_ERR_CUDA;
-  }
-  cuuint64_t dims[3] = {(cuuint64_t)kp, (cuuint64_t)rows, (cuuint64_t)S};
-  cuuint64_t strides[2] = {(cuuint64_t)kp, (cuuint64_t)(rows * kp)};
-  cuuint32_t box[3] = {BK, box_rows, (cuuint32_t)S};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, planes, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) {
-    *err = "cuTensorMapEncodeTiled (digit planes) failed: " + std::to_string((int)r);
-    return MK_ERR_CUDA;
-  }
-  return MK_OK;
 }
 
 template <int S>
@@ -405,27 +409,30 @@ template <int S>
 static int run(const OzOperand& X, const OzOperand& Y, double* C, int64_t ldc, int64_t m, int64_t n, int64_t k,
                const OzDest* d, int nd, uint8_t* ws, cudaStream_t st, std::string* err) {
   const Layout L = layout(m, n, k, S);
-  const int64_t kp = kpad(k);
+  const int64_t kp = kpad(k), nkb = kp / BK;
+  const int64_t tiles_m = (m + BM - 1) / BM, tiles_n = (n + BN - 1) / BN;
   uint8_t* px = ws + L.planes_x;
   uint8_t* py = ws + L.planes_y;
   int32_t* ex = reinterpret_cast<int32_t*>(ws + L.ex);
   int32_t* fy = reinterpret_cast<int32_t*>(ws + L.fy);
   auto* cmax = reinterpret_cast<unsigned long long*>(ws + L.cmax);
+  int32_t* rs = reinterpret_cast<int32_t*>(ws + L.rs);
 
-  split_rows_kernel<S><<<(unsigned)((m * 32 + 255) / 256), 256, 0, st>>>(X, (int)m, (int)k, (int)kp, ex, px);
+  split_rows_kernel<S><<<(unsigned)((tiles_m * BM * 32 + 255) / 256), 256, 0, st>>>(X, (int)m, (int)(tiles_m * BM),
+                                                                                 (int)k, (int)nkb, ex, rs, px);
   cudaMemsetAsync(cmax, 0, 8 * (size_t)n, st);
   colmax_kernel<<<dim3((unsigned)((n + 255) / 256), (unsigned)((k + 255) / 256)), 256, 0, st>>>(Y, (int)k, (int)n,
                                                                                                 cmax);
   colexp_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(cmax, (int)n, fy);
-  split_cols_kernel<S><<<dim3((unsigned)((n + 31) / 32), (unsigned)((kp + 31) / 32)), dim3(32, 8), 0, st>>>(
-      Y, (int)k, (int)n, (int)kp, fy, py);
+  split_cols_kernel<S><<<dim3((unsigned)(tiles_n * BN / 32), (unsigned)nkb), dim3(32, 8), 0, st>>>(
+      Y, (int)k, (int)n, (int)nkb, fy, py);
 
-  CUtensorMap tmX, tmY;
-  if (int rc = encode_planes(&tmX, px, m, kp, S, BM, err)) return rc;
-  if (int rc = encode_planes(&tmY, py, n, kp, S, BN, err)) return rc;
   Args a;
+  a.px = px;
+  a.py = py;
   a.ex = ex;
   a.fy = fy;
+  a.rs = rs;
   a.C = C;
   a.ldc = ldc;
   a.M = (int)m;
@@ -441,7 +448,7 @@ static int run(const OzOperand& X, const OzOperand& Y, double* C, int64_t ldc, i
   std::call_once(attr_once, [&] {
     cudaFuncSetAttribute(ozaki_product_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   });
-  ozaki_product_kernel<S><<<tiles, NTHREADS, smem, st>>>(tmX, tmY, a);
+  ozaki_product_kernel<S><<<tiles, NTHREADS, smem, st>>>(a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("ozaki_product_kernel launch: ") + cudaGetErrorString(e);
@@ -478,9 +485,10 @@ static int product_chunks(const OzOperand& X, const OzOperand& Y, double* C, int
 }  // namespace oz
 
 int64_t ozaki_max_k(int slices) {
-  // anti-diagonal d = S-1 sums 2 signed x unsigned pairs (|.| <= 128 * 255) and S-2 unsigned
-  // pairs (<= 255^2) per k; the int32 accumulator must hold K of them
-  const int64_t worst = 2 * 128 * 255 + (int64_t)(slices - 2) * 255 * 255;
+  // anti-diagonal d = S-1 sums per k one signed x unsigned pair (|.| <= 128 * 255) and S-1
+  // unsigned x unsigned pairs (<= 255^2, Y's plane 0 offset included); the int32 accumulator
+  // must hold K of them
+  const int64_t worst = 128 * 255 + (int64_t)(slices - 1) * 255 * 255;
   return 2147483647ll / worst;
 }
 
