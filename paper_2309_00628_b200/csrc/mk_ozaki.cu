@@ -7,7 +7,11 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
+#include <type_traits>
+#include <vector>
 
 #include "../../include/mk_strassen.h"
 #include "mk_device.cuh"
@@ -20,7 +24,8 @@ constexpr int BM = 128;      // tile rows = TMEM lanes
 constexpr int BN = 64;       // tile columns = TMEM columns per anti-diagonal accumulator
 constexpr int BK = 32;       // int8 k per stage = one UMMA K step (32 bytes = the 32B swizzle span)
 constexpr int STAGES = 4;
-constexpr int NTHREADS = 192;  // warp 0 TMA, warp 1 MMA issuer + TMEM owner, warps 2-5 epilogue
+constexpr int NTHREADS = 256;  // warp 0 TMA, warp 1 MMA issuer + TMEM owner; then all 8 warps run the epilogue
+                               // (2 per TMEM lane quarter; 8 warps = 2 per SM sub-partition: up to 255 registers)
 constexpr int KPAD = BK;       // K padding: whole 32-byte k-blocks
 constexpr int EXP_NONFINITE = INT_MIN;
 
@@ -34,6 +39,7 @@ struct Args {
   int64_t ldc;
   int32_t M, N, K, tiles_n;
   int32_t nd, pad_;
+  unsigned long long* trace;  // debug (MK_OZ_TRACE=1): 7 %globaltimer stamps per tile
   OzDest d[kOzMaxDests];  // destinations: C[d.row + i][d.col + j] (+)= d.sign * P_ij
 };
 
@@ -68,6 +74,25 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(da), "l"(db), "r"(idesc), "r"(acc)
       : "memory");
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(256);
+  }
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -112,6 +137,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tm = blockIdx.x / a.tiles_n, tn = blockIdx.x % a.tiles_n;
   const int nkb = (a.K + BK - 1) / BK;
+  unsigned long long* tr = a.trace ? a.trace + 10 * (size_t)blockIdx.x : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = gtimer();
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
@@ -126,6 +153,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   tmem_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (tr && threadIdx.x == 0) tr[1] = gtimer();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -144,6 +172,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int st = kb % STAGES;
         mbar_wait(&full[st], (kb / STAGES) & 1);
         tmem_fence_after();
+        if (tr && kb == 0) tr[2] = gtimer();
         const uint8_t* sa = smem + st * STAGE_BYTES;
         const uint8_t* sb = sa + S * A_TILE;
         // X digit plane s meets Y planes t = 0..S-1-s. The Y planes are consecutive 64-row
@@ -165,51 +194,128 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         mma_commit(&empty[st]);  // frees the stage once these MMAs have read it
       }
       mma_commit(tmem_full);
+      if (tr) tr[3] = gtimer();
     }
-  } else {
-    // epilogue: warp w reads TMEM lanes 32*(w%4)..+31 (one output row per thread)
-    const int q = warp & 3;
+  }
+  __syncwarp();
+  {
+    // epilogue (all 8 warps): warp w reads TMEM lanes 32*(w%4)..+31 (one output row per thread)
+    // and column half w/4, forms 16 columns at a time, stages them in shared memory (the
+    // operand ring is idle once every MMA has completed) and writes them back
+    // row-contiguously: 4 rows of 128 bytes per warp instruction.
+    const int q = warp & 3, half = warp >> 2;
     const int row = tm * BM + q * 32 + lane;
-    mbar_wait(tmem_full, 0);
+    mbar_wait_sleep(tmem_full, 0);  // the whole main loop: back off, leave issue slots to the MMA / TMA warps
     tmem_fence_after();
+    if (tr && warp == 2 && lane == 0) tr[4] = gtimer();
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
     const bool row_ok = row < a.M;
     const int e = row_ok ? a.ex[row] : 0;
-    // diagonal d holds (a_d . (b_0 + 128)) + ...: subtract 128 * rowsum(a_d)
-    double corr[S];
+    // Exact integer recombination: with acc'_d = acc_d - 128 * rowsum(a_d) (the +128 offset of
+    // Y's plane 0 taken back out), v = sum_d acc'_d 2^(-8d) = 2^-24 (hi + 2^-32 lo) where
+    // hi = sum_{d<4} acc'_d 2^(8(3-d)) and lo = sum_{d>=4} acc'_d 2^(8(7-d)) are exact int64
+    // (|acc'| < 2^32: < 2^57); two int64 -> FP64 conversions and one FMA instead of a serial
+    // S-step FP64 Horner chain per element.
+    long long chi = 0, clo = 0;
 #pragma unroll
-    for (int d = 0; d < S; ++d) corr[d] = row_ok ? 128.0 * (double)a.rs[(int64_t)d * a.M + row] : 0.0;
-    double* crow = a.C + (int64_t)row * a.ldc;
+    for (int d = 0; d < S; ++d) {
+      const long long c = row_ok ? 128ll * a.rs[(int64_t)d * a.M + row] : 0ll;
+      if (d < 4) chi += c << (8 * (3 - d));
+      else clo += c << (8 * (7 - d));
+    }
+    // P = 2^-24 (hi + 2^-32 lo) * 2^(e - 7) * 2^(f - 7): exact power-of-two scaling while normal
+    const bool e_fast = e > -900 && e < 900;
+    const double escale = e_fast ? __longlong_as_double((long long)(e - 7 - 24 + 1023) << 52) : 0.0;
+    double* stage = reinterpret_cast<double*>(smem) + warp * (32 * 18);  // [32 rows][18] doubles per warp
+    // column exponents of this warp's 32 columns: one coalesced load, shuffled out per element
+    const int mycol = tn * BN + half * (BN / 2) + lane;
+    const int fl = mycol < a.N ? a.fy[mycol] : 0;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      uint32_t r[S][16];
+    for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 16) {
+      // diagonals two at a time (bounded registers): hi/lo accumulate in int64
+      long long hi[16], lo[16];
 #pragma unroll
-      for (int d = 0; d < S; ++d) tmem_ld16(tl + (uint32_t)(d * BN + c0), r[d]);
-      tmem_wait_ld();
-      if (!row_ok) continue;
+      for (int j = 0; j < 16; ++j) hi[j] = lo[j] = 0;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int col = tn * BN + c0 + j;
-        if (col >= a.N) break;
-        double v = (double)(int32_t)r[S - 1][j] - corr[S - 1];  // exact (integers < 2^40)
+      for (int d0 = 0; d0 < S; d0 += 2) {
+        uint32_t r[2][16];
+        tmem_ld16(tl + (uint32_t)(d0 * BN + c0), r[0]);
+        if (d0 + 1 < S) tmem_ld16(tl + (uint32_t)((d0 + 1) * BN + c0), r[1]);
+        tmem_wait_ld();
 #pragma unroll
-        for (int d = S - 2; d >= 0; --d) v = fma(v, 0.00390625, (double)(int32_t)r[d][j] - corr[d]);
-        const int f = a.fy[col];
-        double p;
-        if (e == EXP_NONFINITE || f == EXP_NONFINITE)
-          p = __longlong_as_double(0x7ff8000000000000ll);
-        else
-          p = ldexp(v, e + f - 14);
-        for (int t = 0; t < a.nd; ++t) {
-          double* dst = crow + a.d[t].row * a.ldc + a.d[t].col + col;
-          *dst = a.d[t].accumulate ? fma(a.d[t].sign, p, *dst) : a.d[t].sign * p;
+        for (int dd = 0; dd < 2; ++dd) {
+          const int d = d0 + dd;
+          if (d >= S) break;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const long long x = (long long)(int32_t)r[dd][j];
+            if (d < 4) hi[j] += x << (8 * (3 - d));
+            else lo[j] += x << (8 * (7 - d));
+          }
         }
       }
+      if (tr && warp == 2 && lane == 0 && c0 == 0) tr[7] = gtimer();
+      double p[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const double v = fma((double)(lo[j] - clo), 2.3283064365386963e-10 /* 2^-32 */, (double)(hi[j] - chi));
+        const int f = __shfl_sync(0xffffffffu, fl, (c0 & 16) + j);
+        const bool fast = e_fast && f > -900 && f < 900;
+        p[j] = (v * escale) * __longlong_as_double((long long)((fast ? f : 0) - 7 + 1023) << 52);
+        if (!fast)  // rare: extreme exponents (exact ldexp) or non-finite operands (NaN)
+          p[j] = (e == EXP_NONFINITE || f == EXP_NONFINITE) ? __longlong_as_double(0x7ff8000000000000ll)
+                                                              : ldexp(v, e + f - 38);
+      }
+      // stage: lane = row, 16 doubles as 8 x 16-byte stores (row pitch 144 B: conflict-free)
+#pragma unroll
+      for (int j = 0; j < 16; j += 2)
+        *reinterpret_cast<double2*>(stage + lane * 18 + j) = make_double2(p[j], p[j + 1]);
+      __syncwarp();
+      if (tr && warp == 2 && lane == 0 && c0 == 0) tr[8] = gtimer();
+      // write back: lanes 8*i + c -> row rr + i, columns c0 + 2c, c0 + 2c + 1
+      const int cc = 2 * (lane & 7), col = tn * BN + c0 + cc;
+      double2 v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = *reinterpret_cast<const double2*>(stage + (4 * i + (lane >> 3)) * 18 + cc);
+      const int64_t r0 = tm * BM + q * 32 + (lane >> 3);
+      for (int t = 0; t < a.nd; ++t) {
+        const OzDest dd = a.d[t];
+        double* base = a.C + (r0 + dd.row) * a.ldc + dd.col + col;
+        const bool vec = col + 1 < a.N && ((reinterpret_cast<uintptr_t>(base) | (uintptr_t)(a.ldc * 8)) & 15) == 0;
+        if (vec && dd.accumulate) {
+          double2 c[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (r0 + 4 * i < a.M) c[i] = *reinterpret_cast<const double2*>(base + 4 * i * a.ldc);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (r0 + 4 * i < a.M)
+              *reinterpret_cast<double2*>(base + 4 * i * a.ldc) =
+                  make_double2(fma(dd.sign, v[i].x, c[i].x), fma(dd.sign, v[i].y, c[i].y));
+        } else if (vec) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (r0 + 4 * i < a.M)
+              *reinterpret_cast<double2*>(base + 4 * i * a.ldc) = make_double2(dd.sign * v[i].x, dd.sign * v[i].y);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (r0 + 4 * i >= a.M) continue;
+            double* d0 = base + 4 * i * a.ldc;
+            if (col < a.N) d0[0] = dd.accumulate ? fma(dd.sign, v[i].x, d0[0]) : dd.sign * v[i].x;
+            if (col + 1 < a.N) d0[1] = dd.accumulate ? fma(dd.sign, v[i].y, d0[1]) : dd.sign * v[i].y;
+          }
+        }
+      }
+      __syncwarp();
+      if (tr && warp == 2 && lane == 0 && c0 == 0) tr[9] = gtimer();
     }
   }
+  if (tr && warp == 2 && lane == 0) tr[5] = gtimer();
   tmem_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, 512);
+  if (tr && threadIdx.x == 0) tr[6] = gtimer();
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -255,46 +361,70 @@ __device__ __forceinline__ void digits4(const double x[4], double scale, uint32_
 
 // Operand value at (r, c): the signed sum of up to 4 blocks of one base (the Strassen / Winograd
 // pre-addition, formed on load instead of materialised), in table order.
+// NT = o.n as a template parameter: the term loop unrolls, so unrolled element loops keep several
+// independent loads in flight.
+template <int NT>
 __device__ __forceinline__ double term_sum(const OzOperand& o, int64_t r, int64_t c) {
   const int64_t off = r * o.ld + c;
   double v = o.s[0] * o.p[0][off];
-  for (int i = 1; i < o.n; ++i) v = fma(o.s[i], o.p[i][off], v);
+#pragma unroll
+  for (int i = 1; i < NT; ++i) v = fma(o.s[i], o.p[i][off], v);
   return v;
+}
+
+// Row maxima of X as IEEE bit patterns (monotone for |x|; inf / nan -> +inf): one warp per
+// (row, 1024-wide k chunk), 8 independent loads in flight per lane, one atomicMax per warp.
+template <int NT>
+__global__ void rowmax_kernel(const OzOperand X, int rows, int K, unsigned long long* __restrict__ rmax) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const int k0 = blockIdx.y * 1024, k1 = min(K, k0 + 1024);
+  double m[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) m[i] = 0.0;
+  bool bad = false;
+  for (int k = k0 + lane; k < k1; k += 256) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int kk = k + 32 * i;
+      const double v = kk < k1 ? fabs(term_sum<NT>(X, warp, kk)) : 0.0;
+      bad |= !(v <= 1.7976931348623157e308);
+      m[i] = fmax(m[i], v);
+    }
+  }
+  double mx = fmax(fmax(fmax(m[0], m[1]), fmax(m[2], m[3])), fmax(fmax(m[4], m[5]), fmax(m[6], m[7])));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  bad = __any_sync(0xffffffffu, bad);
+  if (lane == 0)
+    atomicMax(&rmax[warp], bad ? 0x7ff0000000000000ull : (unsigned long long)__double_as_longlong(mx));
 }
 
 // X rows -> exponents, digit row sums and S digit planes in the product kernel's tile images
 // ([tile_m][kb][S][128 x 32 B], swizzled): one warp per row (rows up to the padded tile edge
-// write zeros), each lane 4 consecutive k per iteration (one 32-bit store per plane).
-template <int S>
-__global__ void split_rows_kernel(const OzOperand X, int rows, int rows_pad, int K, int nkb, int32_t* __restrict__ ex,
+// write zeros), each lane 4 consecutive k per step, 4 steps in flight.
+template <int S, int NT>
+__global__ void split_rows_kernel(const OzOperand X, int rows, int rows_pad, int K, int nkb,
+                                  const unsigned long long* __restrict__ rmax, int32_t* __restrict__ ex,
                                   int32_t* __restrict__ rs, uint8_t* __restrict__ planes) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= rows_pad) return;
   const bool live = warp < rows;
-  double mx = 0.0;
-  bool bad = false;  // inf / nan (fmax alone would drop a NaN)
-  if (live)
-    for (int k = lane; k < K; k += 32) {
-      const double v = fabs(term_sum(X, warp, k));
-      bad |= !(v <= 1.7976931348623157e308);
-      mx = fmax(mx, v);
-    }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  bad = __any_sync(0xffffffffu, bad);
-  const int e = bad ? EXP_NONFINITE : row_exponent(mx);
+  const int e = live ? row_exponent(__longlong_as_double((long long)rmax[warp])) : 0;
   if (lane == 0 && live) ex[warp] = e;
   const double scale = (e == EXP_NONFINITE) ? 0.0 : ldexp(1.0, -e);
+  const bool load = live && e != EXP_NONFINITE;
   const int tmi = warp / BM, r = warp % BM;
   uint8_t* base = planes + (int64_t)tmi * nkb * (S * BM * BK);
   int dsum[S];
 #pragma unroll
   for (int s = 0; s < S; ++s) dsum[s] = 0;
   const int kp = nkb * BK;
+#pragma unroll 4
   for (int k0 = 4 * lane; k0 < kp; k0 += 128) {
     double x[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) x[i] = (live && k0 + i < K && e != EXP_NONFINITE) ? term_sum(X, warp, k0 + i) : 0.0;
+    for (int i = 0; i < 4; ++i) x[i] = (load && k0 + i < K) ? term_sum<NT>(X, warp, k0 + i) : 0.0;
     uint32_t w[S];
     digits4<S, false>(x, scale, w, dsum);
     uint8_t* t = base + (int64_t)(k0 / BK) * (S * BM * BK) + swz32(r, k0 % BK);
@@ -310,18 +440,28 @@ __global__ void split_rows_kernel(const OzOperand X, int rows, int rows_pad, int
   }
 }
 
-// Column maxima of Y (k x n) as IEEE bit patterns (monotone for |y|): grid (n/256, k/256).
+// Column maxima of Y (k x n) as IEEE bit patterns (monotone for |y|): grid (n/256, k/64).
+template <int NT>
 __global__ void colmax_kernel(const OzOperand Y, int K, int N, unsigned long long* __restrict__ cmax) {
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= N) return;
-  const int k0 = blockIdx.y * 256, k1 = min(K, k0 + 256);
-  double mx = 0.0;
+  const int k0 = blockIdx.y * 64, k1 = min(K, k0 + 64);
+  double mx = 0.0, m2 = 0.0;
   bool bad = false;
-  for (int k = k0; k < k1; ++k) {
-    const double y = fabs(term_sum(Y, k, col));
+  int k = k0;
+#pragma unroll 4
+  for (; k + 1 < k1; k += 2) {
+    const double y1 = fabs(term_sum<NT>(Y, k, col)), y2 = fabs(term_sum<NT>(Y, k + 1, col));
+    bad |= !(y1 <= 1.7976931348623157e308) | !(y2 <= 1.7976931348623157e308);
+    mx = fmax(mx, y1);
+    m2 = fmax(m2, y2);
+  }
+  if (k < k1) {
+    const double y = fabs(term_sum<NT>(Y, k, col));
     bad |= !(y <= 1.7976931348623157e308);
     mx = fmax(mx, y);
   }
+  mx = fmax(mx, m2);
   const unsigned long long bits = bad ? 0x7ff0000000000000ull : (unsigned long long)__double_as_longlong(mx);
   atomicMax(&cmax[col], bits);
 }
@@ -335,7 +475,7 @@ __global__ void colexp_kernel(const unsigned long long* __restrict__ cmax, int N
 // Y (k x n, row-major) -> S digit planes of Y^T in the product kernel's tile images
 // ([tile_n][kb][S][64 x 32 B], swizzled; K-major for the B operand), 32 x 32 tiles through shared
 // memory. Block (32, 8); the grid covers the padded tile edges (zeros).
-template <int S>
+template <int S, int NT>
 __global__ void split_cols_kernel(const OzOperand Y, int K, int N, int nkb, const int32_t* __restrict__ fy,
                                   uint8_t* __restrict__ planes) {
   __shared__ uint32_t sm[S][32][9];  // [plane][col][k/4] (+1 pad)
@@ -349,7 +489,7 @@ __global__ void split_cols_kernel(const OzOperand Y, int K, int N, int nkb, cons
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int k = k0 + 4 * ty + i;
-    x[i] = (col < N && k < K && scale != 0.0) ? term_sum(Y, k, col) : 0.0;
+    x[i] = (col < N && k < K && scale != 0.0) ? term_sum<NT>(Y, k, col) : 0.0;
   }
   uint32_t w[S];
   digits4<S, true>(x, scale, w, nullptr);
@@ -376,7 +516,7 @@ static int64_t kpad(int64_t k) { return (k + KPAD - 1) / KPAD * KPAD; }
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t planes_x, planes_y, ex, fy, cmax, rs, total;
+  size_t planes_x, planes_y, ex, fy, cmax, rs, rmax, total;
 };
 static Layout layout(int64_t m, int64_t n, int64_t k, int S) {
   Layout L;
@@ -388,7 +528,8 @@ static Layout layout(int64_t m, int64_t n, int64_t k, int S) {
   L.fy = align256(L.ex + 4 * (size_t)m);
   L.cmax = align256(L.fy + 4 * (size_t)n);
   L.rs = align256(L.cmax + 8 * (size_t)n);
-  L.total = align256(L.rs + 4 * (size_t)S * m);
+  L.rmax = align256(L.rs + 4 * (size_t)S * m);
+  L.total = align256(L.rmax + 8 * (size_t)m);
   return L;
 }
 
@@ -418,14 +559,36 @@ static int run(const OzOperand& X, const OzOperand& Y, double* C, int64_t ldc, i
   auto* cmax = reinterpret_cast<unsigned long long*>(ws + L.cmax);
   int32_t* rs = reinterpret_cast<int32_t*>(ws + L.rs);
 
-  split_rows_kernel<S><<<(unsigned)((tiles_m * BM * 32 + 255) / 256), 256, 0, st>>>(X, (int)m, (int)(tiles_m * BM),
-                                                                                 (int)k, (int)nkb, ex, rs, px);
+  auto* rmax = reinterpret_cast<unsigned long long*>(ws + L.rmax);
+  cudaMemsetAsync(rmax, 0, 8 * (size_t)m, st);
+  auto x_side = [&](auto nt) {
+    constexpr int NT = decltype(nt)::value;
+    rowmax_kernel<NT><<<dim3((unsigned)((m * 32 + 255) / 256), (unsigned)((k + 1023) / 1024)), 256, 0, st>>>(
+        X, (int)m, (int)k, rmax);
+    split_rows_kernel<S, NT><<<(unsigned)((tiles_m * BM * 32 + 255) / 256), 256, 0, st>>>(
+        X, (int)m, (int)(tiles_m * BM), (int)k, (int)nkb, rmax, ex, rs, px);
+  };
+  auto y_side = [&](auto nt) {
+    constexpr int NT = decltype(nt)::value;
+    colmax_kernel<NT><<<dim3((unsigned)((n + 255) / 256), (unsigned)((k + 63) / 64)), 256, 0, st>>>(Y, (int)k,
+                                                                                                  (int)n, cmax);
+    colexp_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(cmax, (int)n, fy);
+    split_cols_kernel<S, NT><<<dim3((unsigned)(tiles_n * BN / 32), (unsigned)nkb), dim3(32, 8), 0, st>>>(
+        Y, (int)k, (int)n, (int)nkb, fy, py);
+  };
+  switch (X.n) {
+    case 1: x_side(std::integral_constant<int, 1>{}); break;
+    case 2: x_side(std::integral_constant<int, 2>{}); break;
+    case 3: x_side(std::integral_constant<int, 3>{}); break;
+    default: x_side(std::integral_constant<int, 4>{}); break;
+  }
   cudaMemsetAsync(cmax, 0, 8 * (size_t)n, st);
-  colmax_kernel<<<dim3((unsigned)((n + 255) / 256), (unsigned)((k + 255) / 256)), 256, 0, st>>>(Y, (int)k, (int)n,
-                                                                                                cmax);
-  colexp_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(cmax, (int)n, fy);
-  split_cols_kernel<S><<<dim3((unsigned)(tiles_n * BN / 32), (unsigned)nkb), dim3(32, 8), 0, st>>>(
-      Y, (int)k, (int)n, (int)nkb, fy, py);
+  switch (Y.n) {
+    case 1: y_side(std::integral_constant<int, 1>{}); break;
+    case 2: y_side(std::integral_constant<int, 2>{}); break;
+    case 3: y_side(std::integral_constant<int, 3>{}); break;
+    default: y_side(std::integral_constant<int, 4>{}); break;
+  }
 
   Args a;
   a.px = px;
@@ -448,7 +611,38 @@ static int run(const OzOperand& X, const OzOperand& Y, double* C, int64_t ldc, i
   std::call_once(attr_once, [&] {
     cudaFuncSetAttribute(ozaki_product_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   });
+  static const bool trace = getenv("MK_OZ_TRACE") && getenv("MK_OZ_TRACE")[0] == '1';
+  a.trace = nullptr;
+  if (trace) cudaMalloc(&a.trace, 10 * sizeof(unsigned long long) * tiles);
   ozaki_product_kernel<S><<<tiles, NTHREADS, smem, st>>>(a);
+  if (trace) {  // debug: per-phase medians over the tiles, stderr
+    std::vector<unsigned long long> h(10 * (size_t)tiles);
+    cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    cudaFree(a.trace);
+    const char* names[6] = {"alloc", "fill", "mainloop", "mma_drain", "epilogue", "teardown"};
+    unsigned long long t0 = ~0ull, t1 = 0;
+    for (int t = 0; t < tiles; ++t) { t0 = std::min(t0, h[10 * t]); t1 = std::max(t1, h[10 * t + 6]); }
+    fprintf(stderr, "ozaki trace S=%d M=%lld N=%lld K=%lld tiles=%d span=%.1f us:", S, (long long)m, (long long)n,
+            (long long)k, tiles, (t1 - t0) / 1e3);
+    for (int ph = 0; ph < 6; ++ph) {
+      std::vector<long long> d(tiles);
+      for (int t = 0; t < tiles; ++t) d[t] = ph < 6 ? (long long)h[10 * t + ph + 1] - (long long)h[10 * t + ph] : (long long)h[10 * t + ph + 1] - (long long)h[10 * t + ph];
+      std::sort(d.begin(), d.end());
+      fprintf(stderr, " %s %.2f", names[ph], d[tiles / 2] / 1e3);
+    }
+    {
+      const char* sub[3] = {"c0_tmem_ld", "c0_compute", "c0_store"};
+      const int from[3] = {4, 7, 8};
+      for (int ph = 0; ph < 3; ++ph) {
+        std::vector<long long> d(tiles);
+        for (int t = 0; t < tiles; ++t) d[t] = (long long)h[10 * t + from[ph] + (ph == 0 ? 3 : 1)] - (long long)h[10 * t + from[ph]];
+        std::sort(d.begin(), d.end());
+        fprintf(stderr, " %s %.2f", sub[ph], d[tiles / 2] / 1e3);
+      }
+    }
+    fprintf(stderr, " (us, medians)\n");
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("ozaki_product_kernel launch: ") + cudaGetErrorString(e);
