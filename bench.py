@@ -53,6 +53,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only for 1-GPU plumbing checks")
     p.add_argument("--alt", default="8192,2048", help="extra cutoffs to report (comma list, '' for none)")
+    p.add_argument("--ozaki-slices", type=int, default=8,
+                   help="also time the same workload with INT8 tensor-core (Ozaki) leaves, 0 = skip")
     return p.parse_args()
 
 
@@ -234,6 +236,85 @@ def run_reference(args):
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- Ozaki leg
+def ozaki_leg(args, pk, lib, _lib, torch, A, B, C, dc, host_a, host_b, policy, stream, local):
+    """The same workload with every leaf product on the INT8 tensor cores (Ozaki scheme I,
+    set_leaf("ozaki", S)): value / e2e like the headline, the leaf launches' int8 roofline, and
+    the max difference from the DMMA (FP64 tensor-core) result of the same inputs."""
+    n, S = args.n, args.ozaki_slices
+    call = {"winograd-block": pk.winograd_block_mul, "strassen": pk.strassen_mul,
+            "winograd-knuth": pk.winograd_knuth_mul}[args.algo]
+    pk.set_leaf("dmma")
+    call(A, B, C, policy)
+    ref = dc.clone()
+    try:
+        pk.set_leaf("ozaki", S)
+        with ClockSampler(local) as clk:
+            for _ in range(max(args.warmup, 3)):
+                call(A, B, C, policy)
+            torch.cuda.synchronize()
+            clk.mark()
+            _lib.check(lib.mk_timing_begin(), "mk_timing_begin")
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps - 1)]
+            e0.record(stream)
+            for i in range(args.steps):
+                call(A, B, C, policy)
+                if i < args.steps - 1:
+                    marks[i].record(stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+        kms, kcnt, kfl = ctypes.c_double(), ctypes.c_int(), ctypes.c_double()
+        _lib.check(lib.mk_timing_end(ctypes.byref(kms), ctypes.byref(kcnt), ctypes.byref(kfl)), "mk_timing_end")
+        ms = e0.elapsed_time(e1) / args.steps
+        bounds = [e0] + marks + [e1]
+        step_ms = [bounds[i].elapsed_time(bounds[i + 1]) for i in range(args.steps)]
+        diff = float((dc - ref).abs().max())
+        scale = float(torch.linalg.vector_norm(ref, ord=float("inf")))
+        # e2e through the public API with pinned host buffers
+        host_c = torch.empty((n, n), dtype=torch.float64).pin_memory()
+        hA, hB, hC = pk.Matrix(host_a.numpy()), pk.Matrix(host_b.numpy()), pk.Matrix(host_c.numpy())
+        call(hA, hB, hC, policy)
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            call(hA, hB, hC, policy)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ems = f0.elapsed_time(f1) / args.steps
+    finally:
+        pk.set_leaf("dmma")
+    pairs = S * (S + 1) // 2
+    peak = None
+    src = "nominal 4500 TOPS dense INT8 (B200 datasheet)"
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        if mp.get("bf16_tflops"):
+            peak = 2.0 * float(mp["bf16_tflops"])
+            src = "2 x MEASURED_PEAKS.json bf16_tflops (burst; the tensor pipe's 8-bit rate is twice its 16-bit rate)"
+    except Exception:
+        pass
+    if peak is None:
+        peak = 4500.0
+    achieved = pairs * kfl.value / (kms.value * 1e-3) / 1e12 if kms.value > 0 else None
+    return {
+        "slices": S, "digit_bits": 7 + 8 * (S - 1), "int8_products_per_leaf": pairs,
+        "value": round(2.0 * n ** 3 / (ms * 1e-3) / 1e12, 4), "unit": UNIT, "ms_per_step": round(ms, 3),
+        "step_ms": {"median": round(statistics.median(step_ms), 3), "best": round(min(step_ms), 3),
+                    "worst": round(max(step_ms), 3)},
+        "e2e": {"value": round(2.0 * n ** 3 / (ems * 1e-3) / 1e12, 4), "unit": UNIT, "ms_per_step": round(ems, 2),
+                "h2d_bytes_per_step": 2 * n * n * 8, "d2h_bytes_per_step": n * n * 8},
+        "max_abs_diff_vs_dmma_result": diff, "result_max_abs": scale,
+        "roofline": {"bound": "tensor", "achieved": round(achieved, 1) if achieved else None, "peak": round(peak, 1),
+                     "unit": "TOPS (int8)", "frac": round(achieved / peak, 4) if achieved else None,
+                     "kernel": "mk::oz::ozaki_product_kernel + digit splitting (per leaf, CUDA events)",
+                     "peak_source": src},
+        "clocks": clk.summary(),
+        "dtype": "f64 operands/results; int8 x int8 -> int32 tensor-core products (Ozaki scheme I)",
+    }
 
 
 # ----------------------------------------------------------------------------- GPU arm
@@ -479,6 +560,9 @@ def main():
                      "workspace_bytes": int(lib.mk_workspace_bytes(_lib.ALGO_IDS["in-place"], n, levels))})
         del a2, b2
         line["memory_lean"] = lean
+    if world == 1 and args.ozaki_slices:
+        line["ozaki_leaf"] = ozaki_leg(args, pk, lib, _lib, torch, A, B, C, dc, host_a, host_b, policy, stream,
+                                       local)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, levels)
     print(json.dumps(line), flush=True)

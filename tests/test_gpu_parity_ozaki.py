@@ -1,0 +1,110 @@
+"""The whole GPU parity suite again with INT8 tensor-core leaves (Ozaki scheme I, 8 slices).
+
+Every test of test_gpu_parity.py is re-collected here and runs with
+``set_leaf("ozaki", 8)``: integer data must stay bit-exact, real data must meet the same stated
+bound and the same secondary gates (no larger than the reference CPU's own error on cfg3/cfg4).
+Below them, direct tests of the C-ABI entry point ``mk_ozaki_dgemm``.
+"""
+import ctypes
+
+import numpy as np
+import pytest
+
+import paper_2309_00628_b200 as pk
+from conftest import has_gpu
+from paper_2309_00628_b200 import _lib
+from test_gpu_parity import *  # noqa: F401,F403  (re-collect every parity test under Ozaki leaves)
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")]
+
+
+@pytest.fixture(autouse=True)
+def ozaki_leaves():
+    pk.set_leaf("ozaki", 8)
+    assert pk.get_leaf() == ("ozaki", 8)
+    yield
+    pk.set_leaf("dmma")
+
+
+def _dgemm(a, b, slices, ws_bytes=None):
+    import torch
+
+    m, k = a.shape
+    n = b.shape[1]
+    lib = _lib.load()
+    c = torch.full((m, n), 7.0, dtype=torch.float64, device="cuda")
+    need = lib.mk_ozaki_workspace_bytes(m, n, k, slices)
+    ws = torch.empty(max(need, 256) + 256, dtype=torch.uint8, device="cuda")
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    rc = lib.mk_ozaki_dgemm(a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), c.data_ptr(), c.stride(0), m, n, k,
+                            slices, ws.data_ptr(), need if ws_bytes is None else ws_bytes, st)
+    torch.cuda.synchronize()
+    return rc, c
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (128, 64, 32), (300, 200, 260), (129, 65, 33), (64, 64, 1),
+                                   (257, 130, 9000)])
+@pytest.mark.parametrize("slices", [4, 8])
+def test_ozaki_dgemm_integer_exact(shape, slices):
+    """Integer data in the reference fixtures' range is exact at any slice count (the digits hold
+    it), including ragged tiles and K above the int32 chunk limit (9000 > 4402: two K chunks)."""
+    import torch
+
+    m, n, k = shape
+    r = np.random.default_rng(20240901 + m + n + k)
+    a = torch.from_numpy(r.integers(-8, 9, (m, k)).astype(np.float64)).cuda()
+    b = torch.from_numpy(r.integers(-8, 9, (k, n)).astype(np.float64)).cuda()
+    rc, c = _dgemm(a, b, slices)
+    assert rc == 0, _lib.load().mk_last_error()
+    assert torch.equal(c, a @ b)
+
+
+def test_ozaki_dgemm_accuracy_at_least_dmma():
+    """8 slices (63 digit bits) against an extended-precision product: no larger error than the
+    FP64 tensor-core (DMMA) product of the same operands."""
+    import torch
+
+    r = np.random.default_rng(20240901)
+    an, bn = r.standard_normal((384, 512)), r.standard_normal((512, 320))
+    exact = np.matmul(an.astype(np.longdouble), bn.astype(np.longdouble))
+    a, b = torch.from_numpy(an).cuda(), torch.from_numpy(bn).cuda()
+    rc, c = _dgemm(a, b, 8)
+    assert rc == 0
+    c_dmma = torch.empty_like(c)
+    pk.set_leaf("dmma")
+    pk.naive_mul(pk.Matrix(a), pk.Matrix(b), pk.Matrix(c_dmma))
+    err_oz = float(np.abs(c.cpu().numpy().astype(np.longdouble) - exact).max())
+    err_dmma = float(np.abs(c_dmma.cpu().numpy().astype(np.longdouble) - exact).max())
+    assert err_oz <= err_dmma, (err_oz, err_dmma)
+
+
+def test_ozaki_dgemm_nonfinite_rows_and_columns_are_nan():
+    import torch
+
+    r = np.random.default_rng(1)
+    a = torch.from_numpy(r.uniform(-1, 1, (130, 70))).cuda()
+    b = torch.from_numpy(r.uniform(-1, 1, (70, 90))).cuda()
+    a[5, 3] = float("inf")
+    b[7, 11] = float("nan")
+    rc, c = _dgemm(a, b, 8)
+    assert rc == 0
+    ref = a @ b
+    bad = torch.zeros_like(c, dtype=torch.bool)
+    bad[5, :] = True
+    bad[:, 11] = True
+    assert torch.isnan(c[bad]).all()
+    assert torch.allclose(c[~bad], ref[~bad], rtol=0, atol=1e-13)
+
+
+def test_ozaki_dgemm_errors():
+    import torch
+
+    a = torch.zeros((64, 64), dtype=torch.float64, device="cuda")
+    rc, _ = _dgemm(a, a, 3)
+    assert rc == 5  # MK_ERR_ARG
+    rc, _ = _dgemm(a, a, 8, ws_bytes=16)
+    assert rc == 4  # MK_ERR_WORKSPACE
+    with pytest.raises(ValueError):
+        pk.set_leaf("ozaki", 9)
+    with pytest.raises(ValueError):
+        pk.set_leaf("int8")
