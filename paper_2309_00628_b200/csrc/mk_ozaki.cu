@@ -40,6 +40,7 @@ struct Args {
   int32_t M, N, K, tiles_n;
   int32_t nd, pad_;
   unsigned long long* trace;  // debug (MK_OZ_TRACE=1): 7 %globaltimer stamps per tile
+  int32_t probe;              // debug (MK_OZ_PROBE): 1 = 9 MMAs of N=256 per stage (wrong results), 2 = no MMAs
   OzDest d[kOzMaxDests];  // destinations: C[d.row + i][d.col + j] (+)= d.sign * P_ij
 };
 
@@ -180,6 +181,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // accumulators (anti-diagonals s+t) are consecutive 64-column TMEM blocks, so one MMA
         // with N = 64 * #planes (<= 256) covers up to 4 pairs: S(S+1)/2 pairs in
         // sum_s ceil((S-s)/4) MMAs, each reading its X plane once.
+        if (a.probe == 1) {
+          for (int i = 0; i < (S * (S + 1) / 2 + 3) / 4; ++i)
+            mma_i8(tmem + (uint32_t)((i & 1) * 4 * BN), smem_desc_sw32(sa + (i % S) * A_TILE), smem_desc_sw32(sb),
+                   idesc_i8(4 * BN, false, false), 1u);
+        } else if (a.probe != 2)
 #pragma unroll
         for (int s = 0; s < S; ++s) {
           const uint64_t da = smem_desc_sw32(sa + s * A_TILE);
@@ -330,32 +336,32 @@ __device__ __forceinline__ int row_exponent(double mx) {
   return e;
 }
 
-// x * scale = y in (-1, 1) is written as 2^-7 * sum_s d_s 2^(-8s): d_0 = floor(128 y) in
-// [-128, 127] (signed plane), then d_s = floor(256 r) in [0, 255] of the remainder r in [0, 1)
-// (unsigned planes, 8 bits each): 7 + 8 (S - 1) bits. Every step is exact in FP64.
-// OFFSET: plane 0 stored as d_0 + 128 in [0, 255] (the Y side: every Y plane unsigned, so one MMA
-// can span several planes); the product kernel subtracts 128 * rowsum(X plane) per diagonal.
-// dsum (may be null): per-plane sums of the 4 digits (signed plane 0), for those row sums.
+// x * 2^-e = y in (-1, 1) is written as 2^-7 * sum_s d_s 2^(-8s): d_0 = floor(128 y) in
+// [-128, 127] (signed plane), then d_s in [0, 255] the floor digits of the remainder (unsigned
+// planes): 7 + 8 (S - 1) bits. These are exactly the bytes of the two's-complement integer
+// floor(y * 2^63) (|y * 2^63| < 2^63; the power-of-two scaling is exact; truncating the low
+// bytes is the floor at S digits), so one floor conversion per element yields all S digits.
+// scale = 2^(63 - e). OFFSET: plane 0 stored as d_0 + 128 (top bit flipped) for the Y side.
+// dsum (may be null): per-plane sums of the 4 digits (signed plane 0), for the row sums.
 template <int S, bool OFFSET>
 __device__ __forceinline__ void digits4(const double x[4], double scale, uint32_t out[S], int* dsum) {
-  double y[4];
+  unsigned long long v[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) y[i] = x[i] * scale;  // |y| < 1, exact (power-of-two scaling)
+  for (int i = 0; i < 4; ++i) v[i] = (unsigned long long)__double2ll_rd(x[i] * scale);
 #pragma unroll
   for (int s = 0; s < S; ++s) {
+    const int sh = 8 * (7 - s);
     uint32_t w = 0;
-    int sum = 0;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const double z = y[i] * (s == 0 ? 128.0 : 256.0);  // exact
-      const double dg = floor(z);
-      y[i] = z - dg;  // exact remainder in [0, 1)
-      const int di = (int)dg;
-      sum += di;
-      w |= ((uint32_t)(s == 0 ? (uint8_t)(OFFSET ? di + 128 : di) : (uint8_t)di)) << (8 * i);
+    for (int i = 0; i < 4; ++i) w |= (uint32_t)((v[i] >> sh) & 0xff) << (8 * i);
+    if (dsum) {
+      if (s == 0)
+        dsum[0] += (int)(int8_t)(w & 0xff) + (int)(int8_t)((w >> 8) & 0xff) + (int)(int8_t)((w >> 16) & 0xff) +
+                   (int)(int8_t)(w >> 24);
+      else
+        dsum[s] += (int)(w & 0xff) + (int)((w >> 8) & 0xff) + (int)((w >> 16) & 0xff) + (int)(w >> 24);
     }
-    out[s] = w;
-    if (dsum) dsum[s] += sum;
+    out[s] = (OFFSET && s == 0) ? (w ^ 0x80808080u) : w;
   }
 }
 
@@ -412,7 +418,7 @@ __global__ void split_rows_kernel(const OzOperand X, int rows, int rows_pad, int
   const bool live = warp < rows;
   const int e = live ? row_exponent(__longlong_as_double((long long)rmax[warp])) : 0;
   if (lane == 0 && live) ex[warp] = e;
-  const double scale = (e == EXP_NONFINITE) ? 0.0 : ldexp(1.0, -e);
+  const double scale = (e == EXP_NONFINITE) ? 0.0 : ldexp(1.0, 63 - e);
   const bool load = live && e != EXP_NONFINITE;
   const int tmi = warp / BM, r = warp % BM;
   uint8_t* base = planes + (int64_t)tmi * nkb * (S * BM * BK);
@@ -483,7 +489,7 @@ __global__ void split_cols_kernel(const OzOperand Y, int K, int N, int nkb, cons
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int col = n0 + tx;
   const int f = col < N ? fy[col] : 0;
-  const double scale = (col < N && f != EXP_NONFINITE) ? ldexp(1.0, -f) : 0.0;
+  const double scale = (col < N && f != EXP_NONFINITE) ? ldexp(1.0, 63 - f) : 0.0;
   // thread (tx, ty) converts k = k0 + 4*ty .. +3 of column col
   double x[4];
 #pragma unroll
@@ -613,6 +619,8 @@ static int run(const OzOperand& X, const OzOperand& Y, double* C, int64_t ldc, i
   });
   static const bool trace = getenv("MK_OZ_TRACE") && getenv("MK_OZ_TRACE")[0] == '1';
   a.trace = nullptr;
+  static const int probe = getenv("MK_OZ_PROBE") ? atoi(getenv("MK_OZ_PROBE")) : 0;
+  a.probe = probe;
   if (trace) cudaMalloc(&a.trace, 10 * sizeof(unsigned long long) * tiles);
   ozaki_product_kernel<S><<<tiles, NTHREADS, smem, st>>>(a);
   if (trace) {  // debug: per-phase medians over the tiles, stderr
@@ -727,6 +735,18 @@ int ozaki_product_multi(const OzOperand& X, const OzOperand& Y, double* C, int64
     return MK_ERR_ARG;
   }
   const size_t wsb = ozaki_workspace_bytes(m, n, k, slices);
+  {  // keep freed leaf workspaces in the stream-ordered pool (default threshold 0 unmaps them)
+    static thread_local int pool_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && dev != pool_dev) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      pool_dev = dev;
+    }
+  }
   void* ws = nullptr;
   cudaError_t e = cudaMallocAsync(&ws, wsb, st);
   if (e != cudaSuccess) {
