@@ -136,7 +136,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tm = blockIdx.x / a.tiles_n, tn = blockIdx.x % a.tiles_n;
+  // grouped rasterisation: 16 tile rows at a time, column-major inside the group, so the digit
+  // planes a wave of CTAs reads (16 X panels + a few Y panels) stay in L2
+  int tm, tn;
+  {
+    const int tiles_m = (a.M + BM - 1) / BM, g = 16;
+    const int per_group = g * a.tiles_n, grp = blockIdx.x / per_group, first = grp * g;
+    const int rows = min(g, tiles_m - first), local = blockIdx.x - grp * per_group;
+    tm = first + local % rows;
+    tn = local / rows;
+  }
   const int nkb = (a.K + BK - 1) / BK;
   unsigned long long* tr = a.trace ? a.trace + 10 * (size_t)blockIdx.x : nullptr;
   if (tr && threadIdx.x == 0) tr[0] = gtimer();
