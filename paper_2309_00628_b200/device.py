@@ -303,18 +303,51 @@ def check_disjoint(a: MatrixView, b: MatrixView, c: MatrixView) -> None:
         raise AliasError("output view must not alias an input view")
 
 
-def workspace(nbytes: int):
-    return torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device="cuda")
-
-
 _plan_lock = threading.Lock()
+# Engine workspaces are kept per (device, stream) and reused by later calls on that stream (work on
+# one stream is ordered, so reuse is safe even while earlier calls still run): a 15.5 GB
+# breadth-first workspace is neither re-requested from the allocator nor re-checked against free
+# device memory on every call (either occasionally stalled the host for tens of ms).
+_ws_cache: dict = {}
+_ws_lock = threading.Lock()
+
+
+def _ws_key():
+    return (torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream)
+
+
+def workspace(nbytes: int):
+    nbytes = max(int(nbytes), 16)
+    key = _ws_key()
+    with _ws_lock:
+        t = _ws_cache.get(key)
+        if t is not None and t.numel() >= nbytes:
+            return t
+        _ws_cache.pop(key, None)  # a smaller one goes back to torch's stream-ordered cache first
+    t = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    with _ws_lock:
+        _ws_cache[key] = t
+    return t
+
+
+def release_workspaces() -> None:
+    """Drop the cached engine workspaces (their memory returns to torch's caching allocator)."""
+    with _ws_lock:
+        _ws_cache.clear()
+
+
+
 _WS_MARGIN = 256 << 20
 _WS_QUERY_MIN = 1 << 30  # workspaces below 1 GiB are allocated without asking the driver first
 
 
 def _fits(nbytes: int) -> bool:
-    """Whether a workspace of nbytes can be allocated now (free device memory plus what torch's
-    caching allocator holds unused)."""
+    """Whether a workspace of nbytes can be allocated now (this stream's cached workspace, else free
+    device memory plus what torch's caching allocator holds unused)."""
+    with _ws_lock:
+        t = _ws_cache.get(_ws_key())
+    if t is not None and t.numel() >= nbytes:
+        return True
     free, _ = torch.cuda.mem_get_info()
     slack = torch.cuda.memory_reserved() - torch.cuda.memory_allocated()
     return nbytes + _WS_MARGIN <= free + slack
