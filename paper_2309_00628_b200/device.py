@@ -304,8 +304,8 @@ def check_disjoint(a: MatrixView, b: MatrixView, c: MatrixView) -> None:
 
 
 _plan_lock = threading.Lock()
-# Engine workspaces are kept per (device, stream) and reused by later calls on that stream (work on
-# one stream is ordered, so reuse is safe even while earlier calls still run): a 15.5 GB
+# Engine workspaces are kept per (device, stream, thread) and reused by later calls of that thread on
+# that stream (work on one stream is ordered, so reuse is safe even while earlier calls still run): a 15.5 GB
 # breadth-first workspace is neither re-requested from the allocator nor re-checked against free
 # device memory on every call (either occasionally stalled the host for tens of ms).
 _ws_cache: dict = {}
@@ -313,7 +313,8 @@ _ws_lock = threading.Lock()
 
 
 def _ws_key():
-    return (torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream)
+    # per calling thread too: two threads enqueueing on one stream interleave their launches
+    return (torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream, threading.get_ident())
 
 
 def workspace(nbytes: int):
