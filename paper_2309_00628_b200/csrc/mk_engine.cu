@@ -1647,8 +1647,9 @@ int mk_strassen(int algo, double* A, int64_t lda, double* B, int64_t ldb, double
 // and downloads (one unit each, once a C quadrant's last contributor finished; the D2H
 // direction is independent of H2D), and keep the permutation that finishes first.
 // Winograd: P1 P2 P5 P6 P3 P7 P4 -- only A11, B11 before the first product, only C21 after the last.
-static std::vector<int> overlap_order(const Coeffs& co, std::vector<int>* uploads) {
-  const double kProd = 3.0;  // one top-level product ~ 3 quadrant transfers (n=16384, L=2, PCIe 5)
+static std::vector<int> overlap_order(const Coeffs& co, std::vector<int>* uploads, double kProd) {
+  // kProd: one top-level product in quadrant-transfer units (n=16384, L=2, PCIe 5): ~3 with DMMA
+  // leaves, ~1.5 with INT8 (Ozaki) leaves
   std::vector<int> perm(co.nprod), best;
   for (int i = 0; i < co.nprod; ++i) perm[i] = i;
   double best_t = 1e30;
@@ -1667,10 +1668,13 @@ static std::vector<int> overlap_order(const Coeffs& co, std::vector<int>* upload
     for (size_t i = 0; i < up.size(); ++i) ready[up[i]] = (double)(i + 1);
     double tc = 0, done[4] = {0};
     for (int p : perm) {
-      double start = tc;
+      double last = 0;
       for (int q = 0; q < 8; ++q)
-        if ((q < 4 ? co.a[p][q] : co.b[p][q - 4]) && ready[q] > start) start = ready[q];
-      tc = start + kProd;
+        if ((q < 4 ? co.a[p][q] : co.b[p][q - 4]) && ready[q] > last) last = ready[q];
+      // DMMA leaves (kProd >= 2): a product starts once all its quadrants have landed. Faster
+      // (INT8) leaves: the sub-block pipeline lets a product's children run while its last
+      // quadrant is still arriving -- it ends no earlier than half a product after that.
+      tc = kProd >= 2.0 ? std::max(tc, last) + kProd : std::max(tc + kProd, last + 0.5 * kProd);
       for (int q = 0; q < 4; ++q)
         if (co.c[q][p]) done[q] = tc;
     }
@@ -1691,8 +1695,7 @@ static std::vector<int> overlap_order(const Coeffs& co, std::vector<int>* upload
 // operand sub-blocks go up one unit each in the children's order of first use and gate the
 // children (kChild units each: a 4096^3 leaf vs a 128 MiB upload at n = 16384); keep the
 // permutation whose last child finishes first (ties: table order).
-static std::vector<int> head_child_order(const Coeffs& co, int p0) {
-  const double kChild = 1.7;
+static std::vector<int> head_child_order(const Coeffs& co, int p0, double kChild) {
   std::vector<int> perm(co.nprod), best;
   for (int i = 0; i < co.nprod; ++i) perm[i] = i;
   double best_t = 1e30;
@@ -1733,7 +1736,7 @@ int mk_overlap_order(int algo, int* order_out, int* uploads_out) {
   g_last_error.clear();
   if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_WINOGRAD_KNUTH_8CALL) return fail(MK_ERR_ARG, "fused algorithms only");
   std::vector<int> up;
-  const std::vector<int> ord = overlap_order(coeffs_for(algo), &up);
+  const std::vector<int> ord = overlap_order(coeffs_for(algo), &up, leaf_slices() ? 1.35 : 3.0);
   for (size_t i = 0; i < ord.size(); ++i) order_out[i] = ord[i];
   for (size_t i = 0; i < up.size(); ++i) uploads_out[i] = up[i];
   return (int)ord.size();
@@ -1744,25 +1747,29 @@ int mk_overlap_order(int algo, int* order_out, int* uploads_out) {
 static std::map<int, std::pair<std::vector<int>, std::vector<int>>> g_order_cache;
 static std::map<int, std::vector<int>> g_head_cache;
 static std::mutex g_order_mu;
-static std::vector<int> head_child_order(const Coeffs& co, int p0);
-static std::vector<int> overlap_order(const Coeffs& co, std::vector<int>* uploads);
+static std::vector<int> head_child_order(const Coeffs& co, int p0, double kChild);
+static std::vector<int> overlap_order(const Coeffs& co, std::vector<int>* uploads, double kProd);
 // overlap_order is a search over all product permutations (~1.6 ms): computed once per algorithm
+// and leaf arithmetic (the INT8 leaf halves the compute time per product relative to transfers)
 static std::vector<int> cached_order(int algo, std::vector<int>* uploads) {
   std::lock_guard<std::mutex> lk(g_order_mu);
-  auto it = g_order_cache.find(algo);
+  const int key = algo * 16 + leaf_slices();
+  auto it = g_order_cache.find(key);
   if (it == g_order_cache.end()) {
     std::vector<int> up;
-    std::vector<int> ord = overlap_order(coeffs_for(algo), &up);
-    it = g_order_cache.emplace(algo, std::make_pair(ord, up)).first;
+    std::vector<int> ord = overlap_order(coeffs_for(algo), &up, leaf_slices() ? 1.35 : 3.0);
+    it = g_order_cache.emplace(key, std::make_pair(ord, up)).first;
   }
   if (uploads) *uploads = it->second.second;
   return it->second.first;
 }
 static std::vector<int> cached_head_children(int algo, int p0) {
   std::lock_guard<std::mutex> lk(g_order_mu);
-  auto it = g_head_cache.find(algo);
+  const int key = (algo * 16 + leaf_slices()) * 8 + p0;
+  auto it = g_head_cache.find(key);
   if (it != g_head_cache.end()) return it->second;
-  return g_head_cache[algo] = head_child_order(coeffs_for(algo), p0);
+  // kChild: one 4096^3 leaf in 128 MiB sub-block upload units: ~1.7 DMMA, ~0.85 INT8 (Ozaki)
+  return g_head_cache[key] = head_child_order(coeffs_for(algo), p0, leaf_slices() ? 0.85 : 1.7);
 }
 
 // Synchronous host <-> device block copies for the staging of operands and results: pageable

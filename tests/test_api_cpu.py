@@ -206,3 +206,46 @@ def test_set_plan_validates_and_round_trips():
     assert lib.mk_get_option(_lib.MK_OPT_PLAN, ctypes.byref(v)) == 0 and v.value == 0
     assert lib.mk_workspace_bytes(_lib.ALGO_IDS["winograd-block"], 4096, 3) > lean
     assert lib.mk_get_option(99, ctypes.byref(v)) == _lib.MK_ERR_ARG
+
+
+def test_set_leaf_validates_and_round_trips():
+    """set_leaf (B200 addition): the INT8 tensor-core (Ozaki) leaf takes 4..8 slices; bad kinds and
+    slice counts raise ValueError; the option reaches the engine (and its overlapped host path
+    picks a product order for the faster leaves); the DMMA leaf is the default. Host-only."""
+    import ctypes
+
+    from paper_2309_00628_b200 import _lib
+
+    lib = _lib.load()
+    assert pk.get_leaf() == ("dmma", 0)
+    with pytest.raises(ValueError):
+        pk.set_leaf("int8")
+    with pytest.raises(ValueError):
+        pk.set_leaf("ozaki", 3)
+    assert lib.mk_set_option(_lib.MK_OPT_LEAF_SLICES, 9) == _lib.MK_ERR_ARG
+    order, up = (ctypes.c_int * 8)(), (ctypes.c_int * 8)()
+    assert lib.mk_overlap_order(_lib.ALGO_IDS["winograd-block"], order, up) == 7
+    dmma_order = list(order)[:7]
+    try:
+        pk.set_leaf("ozaki", 6)
+        assert pk.get_leaf() == ("ozaki", 6)
+        lib.mk_overlap_order(_lib.ALGO_IDS["winograd-block"], order, up)
+        assert sorted(list(order)[:7]) == list(range(7)) and list(order)[:7] != dmma_order
+        assert list(order)[0] == 0  # P1 = A11 B11 first: the fewest quadrants before any product
+    finally:
+        pk.set_leaf("dmma")
+    assert pk.get_leaf() == ("dmma", 0)
+
+
+def test_ozaki_workspace_and_chunking_bounds():
+    """mk_ozaki_workspace_bytes: digit planes of both operands padded to whole tiles; K longer than
+    the exact int32 accumulation allows is processed in chunks, so the workspace stops growing."""
+    from paper_2309_00628_b200 import _lib
+
+    lib = _lib.load()
+    assert lib.mk_ozaki_workspace_bytes(1024, 1024, 1024, 3) == 0
+    w8 = lib.mk_ozaki_workspace_bytes(4096, 4096, 4096, 8)
+    assert w8 >= 8 * (4096 + 4096) * 4096
+    assert lib.mk_ozaki_workspace_bytes(4096, 4096, 4096, 4) < w8
+    # K = 4096 fits one chunk at 8 slices; 3 x 4096 runs as three chunks of 4096 (same workspace)
+    assert lib.mk_ozaki_workspace_bytes(4096, 4096, 3 * 4096, 8) == w8
