@@ -191,6 +191,22 @@ int mk_strassen_partial(int algo, const double* A, int64_t lda, const double* B,
                         int64_t ldc, int64_t n, int levels, int first, int count, int panels, void* ws,
                         size_t ws_bytes, void* stream);
 
+/* Enable NVLink peer access from the current device to peer_device (idempotent). */
+int mk_enable_peer_access(int peer_device);
+
+/* Fused multi-GPU reduce-scatter form of mk_strassen_partial: the
+ * leaf epilogue adds this rank's contributions straight into the C row slab of the rank that owns
+ * each row -- slabs[r] is rank r's (slab_rows x n, leading dimension ldc) buffer, its own one local
+ * and the others peer (IPC-mapped, NVLink) addresses -- with REDG.ADD.F64, so the partial-C buffer
+ * and the separate reduce collective disappear. Every slab must be zeroed before any rank starts
+ * (barrier), and read after every rank has finished (device sync + barrier). nslabs * slab_rows
+ * == n; levels <= 2 (every leaf contribution then lands in the epilogue); the leaves run on the
+ * DMMA kernel. FP64 summation order at a row follows arrival order (integer data stays exact). */
+int mk_strassen_partial_slabs(int algo, const double* A, int64_t lda, const double* B, int64_t ldb,
+                              double* const* slabs, int nslabs, int64_t slab_rows, int64_t ldc, int64_t n,
+                              int levels, int first, int count, int panels, void* ws, size_t ws_bytes,
+                              void* stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -468,6 +468,10 @@ struct Engine {
   int64_t panels = 1;
   int launches = 0;
   bool fuse_preadds = false;  // K2 in-kernel combiner for the last level's operand sums
+  // fused multi-GPU reduce-scatter (mk_strassen_partial_slabs): C rows routed to owner slabs
+  int nslab = 0;
+  int64_t slab_rows = 0;
+  double* slab[MK_MAX_SLABS] = {nullptr};
 
   int add_base(double* p, int64_t ld, int64_t rows, int64_t cols, int64_t cell_r, int64_t cell_c) {
     Base b;
@@ -637,7 +641,7 @@ struct Engine {
     }
     ++launches;
     if (dry || no_launch) return MK_OK;
-    if (leaf_slices() > 0) {  // INT8 tensor-core leaf; multi-term operands summed as they are split
+    if (leaf_slices() > 0 && nslab == 0) {  // INT8 tensor-core leaf; multi-term operands summed as they are split
       std::vector<OzDest> od(p.nd);
       for (int i = 0; i < p.nd; ++i) od[i] = OzDest{p.d[i].row, p.d[i].col, p.d[i].sign, p.d[i].accumulate, 0};
       return ozaki_leaf(oz_operand(X), oz_operand(Y), bases[bd].ptr, bases[bd].ld, M, N, K, od.data(), p.nd);
@@ -646,7 +650,7 @@ struct Engine {
     MK_TRY(cached_map(bx, 0, &tmA));
     MK_TRY(cached_map(by, 1, &tmB));
     const int slab = consumer_layout() == 16 ? 32 : 64;  // rows per consumer warp
-    bool async_ok = async_epilogue_enabled() && (M % slab == 0) && (N % 16 == 0) &&
+    bool async_ok = async_epilogue_enabled() && nslab == 0 && (M % slab == 0) && (N % 16 == 0) &&
                     (reinterpret_cast<uintptr_t>(bases[bd].ptr) % 16 == 0) && (bases[bd].ld % 2 == 0);
     for (int i = 0; i < p.nd; ++i) async_ok = async_ok && ((D[i].row | D[i].col) % 2 == 0);
     if (async_ok) MK_TRY(cached_map(bd, slab == 64 ? 2 : 3, &tmC));
@@ -662,6 +666,14 @@ struct Engine {
     g.group_m = 16;
     g.vec_ok = vec_ok ? 1 : 0;
     g.async_epi = async_ok ? 1 : 0;
+    if (nslab && bd == BASE_C) {  // output rows routed to their owners' slabs (REDG.ADD epilogue)
+      g.nslab = nslab;
+      g.slab_rows = slab_rows;
+      for (int i = 0; i < nslab; ++i) {
+        g.slab[i] = this->slab[i];
+        if (reinterpret_cast<uintptr_t>(this->slab[i]) % 32 != 0 || bases[bd].ld % 4 != 0) g.vec_ok = 0;
+      }
+    }
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     if (g_timing.on) {
       MK_CUDA_TRY(cudaEventCreate(&t0));
@@ -2033,6 +2045,57 @@ int mk_strassen_partial(int algo, const double* A, int64_t lda, const double* B,
   e.leaf_first = first;
   e.leaf_count = count;
   e.set_state(BASE_C, 0, 0, n, n, 1);  // partial C is zero-initialised by the caller: accumulate
+  return run_square(e);
+}
+
+int mk_enable_peer_access(int peer_device) {
+  g_last_error.clear();
+  int dev = 0;
+  MK_CUDA_TRY(cudaGetDevice(&dev));
+  if (peer_device == dev) return MK_OK;
+  int ok = 0;
+  MK_CUDA_TRY(cudaDeviceCanAccessPeer(&ok, dev, peer_device));
+  if (!ok) return fail(MK_ERR_CUDA, "no peer access between these devices");
+  const cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return MK_OK;
+  }
+  MK_CUDA_TRY(e);
+  return MK_OK;
+}
+
+int mk_strassen_partial_slabs(int algo, const double* A, int64_t lda, const double* B, int64_t ldb,
+                              double* const* slabs, int nslabs, int64_t slab_rows, int64_t ldc, int64_t n, int levels,
+                              int first, int count, int panels, void* ws, size_t ws_bytes, void* stream) {
+  g_last_error.clear();
+  if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_WINOGRAD_KNUTH_8CALL)
+    return fail(MK_ERR_ARG, "partial products support the fused algorithms only");
+  if (!slabs || nslabs < 1 || nslabs > MK_MAX_SLABS) return fail(MK_ERR_ARG, "1..8 output slabs");
+  if (slab_rows < 1 || slab_rows * nslabs != n || ldc < n)
+    return fail(MK_ERR_DIMENSION, "the slabs must tile the n x n output (nslabs * slab_rows == n, ldc >= n)");
+  if (levels < 0 || levels > 2)
+    return fail(MK_ERR_ARG, "row-slab output needs every leaf contribution in the epilogue (levels <= 2)");
+  if (panels < 1 || ((n >> levels) % panels) != 0 || (((n >> levels) / panels) % 2) != 0)
+    return fail(MK_ERR_ARG, "panels must divide the leaf order into even row panels");
+  if (first < 0 || count < 0) return fail(MK_ERR_ARG, "negative shard range");
+  for (int i = 0; i < nslabs; ++i) {
+    if (!slabs[i]) return fail(MK_ERR_ARG, "null slab");
+    if (overlaps(slabs[i], ldc, slab_rows, n, A, lda, n, n) || overlaps(slabs[i], ldc, slab_rows, n, B, ldb, n, n))
+      return fail(MK_ERR_ALIAS, "an output slab must not alias an input");
+  }
+  Engine e;
+  MK_TRY(setup_square(e, algo, const_cast<double*>(A), lda, const_cast<double*>(B), ldb, slabs[0], ldc, n, levels));
+  e.panels = panels;
+  e.st = static_cast<cudaStream_t>(stream);
+  e.ws = static_cast<char*>(ws);
+  e.ws_bytes = ws ? ws_bytes : 0;
+  e.leaf_first = first;
+  e.leaf_count = count;
+  e.nslab = nslabs;
+  e.slab_rows = slab_rows;
+  for (int i = 0; i < nslabs; ++i) e.slab[i] = slabs[i];
+  e.set_state(BASE_C, 0, 0, n, n, 1);  // every rank's contributions accumulate into zeroed slabs
   return run_square(e);
 }
 

@@ -32,6 +32,14 @@
 
 namespace mk {
 
+// Row-slab routing of the fused multi-GPU reduce-scatter (MkGemmArgs::nslab > 0): C row R goes to
+// its owner's slab (a local buffer or a peer's, IPC-mapped over NVLink).
+__device__ __forceinline__ double* slab_row(const MkGemmArgs& a, int64_t R, int64_t ldc) {
+  const int64_t o = R / a.slab_rows;
+  return a.slab[o] + (R - o * a.slab_rows) * ldc;
+}
+
+
 constexpr int kOpStageBytes = 2 * MK_TILE_BYTES;  // summed A tile + summed B tile
 constexpr int kMaxStages = 8;
 
@@ -472,7 +480,7 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const __grid
     for (int i = 0; i < MT; ++i) {
       const int row = m0 + warp_m * (8 * MT) + 8 * i + prow;
       if (row >= args.M) continue;
-      double* crow = Cd + (int64_t)row * ldc;
+      double* crow = args.nslab ? slab_row(args, dst.row + row, ldc) + dst.col : Cd + (int64_t)row * ldc;
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int col = n0 + warp_n * 32 + 16 * j + 4 * q;
@@ -821,7 +829,7 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
         for (int i = 0; i < MT; ++i) {
           const int row = m0 + warp_m * (8 * MT) + 8 * i + prow;
           if (row >= args.M) continue;
-          double* crow = Cd + (int64_t)row * ldc;
+          double* crow = args.nslab ? slab_row(args, dst.row + row, ldc) + dst.col : Cd + (int64_t)row * ldc;
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
             const int col = n0 + warp_n * 32 + 16 * j + 4 * q;

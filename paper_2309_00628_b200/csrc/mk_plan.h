@@ -19,6 +19,7 @@
 #define MK_SMEM_BUDGET (224 * 1024)
 #define MK_MIN_LEAF 32    // smallest leaf order the level policy recurses to
 #define MK_MAX_LEVELS 5   // deepest recursion the level policy plans (7^5 leaves)
+#define MK_MAX_SLABS 8    // output row slabs (ranks) of the fused multi-GPU reduce-scatter
 
 struct MkTerm {
   int32_t row, col;  // offset of the term block inside the operand base matrix
@@ -56,4 +57,10 @@ struct MkGemmArgs {
   int32_t tiles_per_prod;             // batched launch: CTAs per product
   int32_t nprod;                      // batched launch: products in the batch (persistent kernel)
   const MkBatchEntry* batch;          // batched launch: per-product maps/descriptors (nullptr: single)
+  // Row-slab output (fused multi-GPU reduce-scatter, mk_strassen_partial_slabs): nslab > 0 routes
+  // C row R (relative to C's base) to slab[R / slab_rows] + (R % slab_rows) * ldc -- each slab
+  // owned by one rank, peers' slabs mapped over NVLink -- with the synchronous REDG.ADD epilogue.
+  int32_t nslab, pad_slab;
+  int64_t slab_rows;
+  double* slab[MK_MAX_SLABS];
 };

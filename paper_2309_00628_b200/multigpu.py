@@ -14,6 +14,13 @@ BASELINE.json's multi-GPU config states) and nothing else crosses GPUs.
 
 Load balance: with whole leaves 49 over 8 GPUs would cap efficiency at 49/56; in row-panel
 units (49 x 8 = 392) the split is exact.
+
+Fused alternative (``fused_sharded_multiply``): C is split into W row slabs, slab r owned by
+rank r; every rank maps all slabs (its own local, the others through CUDA IPC handles exchanged
+with the process group -- NVLink peer memory on a multi-GPU node) and its leaf epilogue adds each
+contribution straight into the owning rank's slab (``mk_strassen_partial_slabs``, REDG.ADD.F64):
+the compute and the reduce-scatter are one kernel, there is no partial-C buffer and no reduce
+collective. Rank 0 then pulls the other slabs over peer memory if it needs the whole C.
 """
 from __future__ import annotations
 
@@ -154,3 +161,110 @@ def sharded_multiply(algo: str, a, b, levels: int, group=None, out=None, ws=None
     if count:
         partial_product(algo, a, b, out, levels, first, count, ws=ws)
     return assemble(out, 0, group)
+
+
+# ------------------------------------------------------------------------------------------
+# fused reduce-scatter: leaf epilogues write into the owning rank's C row slab (peer memory)
+# ------------------------------------------------------------------------------------------
+def slab_rows(n: int, world: int) -> int:
+    """Rows of C each rank owns in the fused path (C = W row slabs of n / W rows)."""
+    if world < 1 or n % world:
+        raise ValueError(f"the order {n} must split into {world} equal row slabs")
+    return n // world
+
+
+def slab_owner(row: int, n: int, world: int) -> tuple[int, int]:
+    """(owning rank, row inside its slab) of C row ``row`` -- the routing the epilogue applies."""
+    sr = slab_rows(n, world)
+    return row // sr, row % sr
+
+
+def enable_peer_access(peer_device: int) -> None:
+    """Let the current device address ``peer_device``'s memory (NVLink P2P); no-op for itself."""
+    lib = _lib.load()
+    _lib.check(lib.mk_enable_peer_access(int(peer_device)), "mk_enable_peer_access")
+
+
+class SlabExchange:
+    """Every rank's C row slab mapped into this process: its own as a local tensor, the peers'
+    through CUDA IPC handles gathered over the process group (torch's CUDA tensor reductions).
+    Keep the object alive on every rank until all ranks are done with the slabs."""
+
+    def __init__(self, n: int, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.group = group
+        self.n = n
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.slab = torch.zeros((slab_rows(n, self.world), n), dtype=torch.float64, device=dev)
+        if self.world == 1:
+            self.slabs = [self.slab]
+            return
+        rebuild, args = reduce_tensor(self.slab)
+        gathered = [None] * self.world
+        dist.all_gather_object(gathered, args, group=group)
+        self.slabs = []
+        for r in range(self.world):
+            if r == self.rank:
+                self.slabs.append(self.slab)
+                continue
+            peer = rebuild(*gathered[r])
+            if peer.device != dev:
+                enable_peer_access(peer.device.index)
+            self.slabs.append(peer)
+
+
+def partial_product_slabs(algo: str, a, b, slabs, levels: int, first: int, count: int, stream=None, ws=None,
+                          panels: int = PANELS) -> int:
+    """Add shard units [first, first+count) of A B into the row slabs ``slabs`` (W tensors of
+    n / W x n with one common row stride; local or peer-mapped), each row into its owner's slab."""
+    import torch
+
+    lib = _lib.load()
+    n = a.shape[0]
+    aid = _lib.ALGO_IDS[algo]
+    need = int(lib.mk_partial_workspace_bytes(aid, n, levels))
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(max(need, 16), dtype=torch.uint8, device=a.device)
+    ld = slabs[0].stride(0)
+    if any(s.stride(0) != ld or s.shape != slabs[0].shape for s in slabs):
+        raise ValueError("slabs must share shape and row stride")
+    ptrs = (ctypes.c_void_p * len(slabs))(*[s.data_ptr() for s in slabs])
+    st = ctypes.c_void_p((stream or torch.cuda.current_stream()).cuda_stream)
+    rc = lib.mk_strassen_partial_slabs(aid, ctypes.c_void_p(a.data_ptr()), a.stride(0), ctypes.c_void_p(b.data_ptr()),
+                                       b.stride(0), ptrs, len(slabs), slabs[0].shape[0], ld, n, levels, first, count,
+                                       panels, ctypes.c_void_p(ws.data_ptr()), need, st)
+    _lib.check(rc, "mk_strassen_partial_slabs")
+    return need
+
+
+def fused_sharded_multiply(algo: str, a, b, levels: int, exchange: SlabExchange, out=None, ws=None):
+    """C = A B with the fused reduce-scatter: this rank's leaves are added straight into the owning
+    ranks' row slabs (one kernel does the product and the exchange); on return every rank's
+    ``exchange.slab`` holds its rows of C, and ``out`` (rank 0 only, optional) the whole C, pulled
+    from the peers' slabs. Host barriers only -- no kernel waits on another rank."""
+    import torch
+    import torch.distributed as dist
+
+    world, rank, group = exchange.world, exchange.rank, exchange.group
+    total = leaf_count(algo, levels) * PANELS
+    first, count = shard_range(total, world, rank)
+    exchange.slab.zero_()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier(group)  # every slab is zero before any rank adds into it
+    if count:
+        partial_product_slabs(algo, a, b, exchange.slabs, levels, first, count, ws=ws)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier(group)  # every contribution has landed
+    if out is not None and rank == 0:
+        sr = exchange.slab.shape[0]
+        for r, s in enumerate(exchange.slabs):
+            out[r * sr:(r + 1) * sr].copy_(s)
+        torch.cuda.synchronize()
+    return exchange.slab

@@ -1,0 +1,116 @@
+"""Fused multi-GPU reduce-scatter (mk_strassen_partial_slabs) on the B200.
+
+* one process: the W ranks' shards run in turn, each routing its leaf contributions into the W
+  row slabs (local buffers) -- the slabs together must be the product (bit-exact on integers);
+* two processes on the same GPU (gloo for the host barriers): each maps the other's slab through
+  a CUDA IPC handle and its leaf epilogue adds straight into it -- the cross-process peer-memory
+  path of a multi-GPU node, minus NVLink. The processes only meet at host barriers; no kernel
+  waits on another process's kernel.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import has_gpu
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")]
+
+
+@pytest.mark.parametrize("algo", ["strassen", "winograd-block", "winograd-knuth"])
+@pytest.mark.parametrize("levels", [1, 2])
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_slab_partials_assemble_the_product(algo, levels, world):
+    import torch
+
+    from paper_2309_00628_b200 import multigpu as mg
+
+    n = 1024
+    r = np.random.default_rng(world * 10 + levels)
+    a = torch.from_numpy(r.integers(-8, 9, (n, n)).astype(np.float64)).cuda()
+    b = torch.from_numpy(r.integers(-8, 9, (n, n)).astype(np.float64)).cuda()
+    sr = mg.slab_rows(n, world)
+    panels = 8
+    slabs = [torch.zeros((sr, n), dtype=torch.float64, device="cuda") for _ in range(world)]
+    total = mg.leaf_count(algo, levels) * panels
+    for rank in range(world):
+        first, count = mg.shard_range(total, world, rank)
+        if count:
+            mg.partial_product_slabs(algo, a, b, slabs, levels, first, count, panels=panels)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(slabs), a @ b)
+
+
+def test_slab_path_rejects_bad_layouts():
+    import torch
+
+    from paper_2309_00628_b200 import _lib
+    from paper_2309_00628_b200 import multigpu as mg
+
+    n = 256
+    a = torch.zeros((n, n), dtype=torch.float64, device="cuda")
+    slabs = [torch.zeros((n // 2, n), dtype=torch.float64, device="cuda") for _ in range(2)]
+    with pytest.raises(Exception):
+        mg.partial_product_slabs("winograd-block", a, a, slabs, 3, 0, 1)  # levels > 2: post-adds outside the epilogue
+    with pytest.raises(Exception):
+        mg.partial_product_slabs("winograd-block", a, a, slabs[:1], 1, 0, 1)  # slabs do not tile C
+    assert _lib.load().mk_enable_peer_access(torch.cuda.current_device()) == 0
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _ipc_worker(rank, world, port, levels, exact, result_path):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2309_00628_b200 import multigpu as mg
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = 2048
+        r = np.random.default_rng(20240901)
+        if exact:
+            an = r.integers(-8, 9, (n, n)).astype(np.float64)
+            bn = r.integers(-8, 9, (n, n)).astype(np.float64)
+        else:
+            an, bn = r.uniform(-1, 1, (n, n)), r.uniform(-1, 1, (n, n))
+        a, b = torch.from_numpy(an).cuda(), torch.from_numpy(bn).cuda()
+        ex = mg.SlabExchange(n)
+        assert ex.slabs[rank].data_ptr() == ex.slab.data_ptr()
+        out = torch.empty((n, n), dtype=torch.float64, device="cuda") if rank == 0 else None
+        for _ in range(2):  # the slabs are re-zeroed and reused
+            mg.fused_sharded_multiply("winograd-block", a, b, levels, ex, out=out)
+        if rank == 0:
+            ref = a @ b
+            ok = bool(torch.equal(out, ref)) if exact else float((out - ref).abs().max()) < 1e-11
+            with open(result_path, "w") as f:
+                f.write("ok" if ok else f"mismatch {float((out - ref).abs().max())}")
+        dist.barrier()  # peers keep their slabs alive until rank 0 has read them
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("levels,exact", [(1, True), (2, True), (2, False)])
+def test_two_process_ipc_fused_reduce_scatter(levels, exact, tmp_path):
+    import torch.multiprocessing as mp
+
+    result = str(tmp_path / "result.txt")
+    ctx = mp.get_context("spawn")
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, levels, exact, result)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    assert open(result).read() == "ok"
