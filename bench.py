@@ -52,6 +52,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only for 1-GPU plumbing checks")
+    p.add_argument("--fused-reduce", action="store_true",
+                   help="N > 1: leaf epilogues add into the owning rank's C row slab over peer memory "
+                        "(mk_strassen_partial_slabs) instead of partial C + NCCL reduce")
     p.add_argument("--alt", default="8192,2048", help="extra cutoffs to report (comma list, '' for none)")
     p.add_argument("--ozaki-slices", type=int, default=8,
                    help="also time the same workload with INT8 tensor-core (Ozaki) leaves, 0 = skip")
@@ -59,12 +62,17 @@ def parse():
 
 
 def config(args, levels):
-    return {
+    c = {
         "workload": f"BASELINE cfg4: n={args.n} standard-normal FP64, {args.algo}, naive_cutoff({args.cutoff}) "
                     f"-> {levels} levels ({7 ** levels} DMMA leaf GEMMs)",
         "n": args.n, "cutoff": args.cutoff, "levels": levels, "algo": args.algo,
         "l2": "inputs 2 GiB each > 126 MB L2 (no flush needed)",
     }
+    if args.gpus > 1:
+        c["parallelism"] = (f"leaf row panels over {args.gpus} ranks; " +
+                            ("fused reduce-scatter into owner row slabs over peer memory, slabs pulled to rank 0"
+                             if args.fused_reduce else "partial C per rank + NCCL reduce to rank 0"))
+    return c
 
 
 def levels_for(n, cutoff):
@@ -360,14 +368,19 @@ def main():
     dc = torch.empty((n, n), dtype=torch.float64, device=dev)
     A, B, C = pk.Matrix(da), pk.Matrix(db), pk.Matrix(dc)
     ws = None
+    ex = None
     if world > 1:
         need = int(lib.mk_partial_workspace_bytes(_lib.ALGO_IDS[args.algo], n, levels))
         ws = torch.empty(max(need, 16), dtype=torch.uint8, device=dev)
+        if args.fused_reduce:
+            ex = multigpu.SlabExchange(n)
 
     def step():
         if world == 1:
             {"winograd-block": pk.winograd_block_mul, "strassen": pk.strassen_mul,
              "winograd-knuth": pk.winograd_knuth_mul}[args.algo](A, B, C, policy)
+        elif ex is not None:
+            multigpu.fused_sharded_multiply(args.algo, da, db, levels, ex, out=dc if rank == 0 else None, ws=ws)
         else:
             multigpu.sharded_multiply(args.algo, da, db, levels, out=dc, ws=ws)
 
@@ -430,7 +443,11 @@ def main():
                 pk.winograd_block_mul(hA, hB, hC, policy)
             else:  # each rank uploads only the operand quadrants its shard reads
                 moved[0] = multigpu.upload_operands(args.algo, levels, host_a, host_b, da, db)
-                multigpu.sharded_multiply(args.algo, da, db, levels, out=dc, ws=ws)
+                if ex is not None:
+                    multigpu.fused_sharded_multiply(args.algo, da, db, levels, ex, out=dc if rank == 0 else None,
+                                                    ws=ws)
+                else:
+                    multigpu.sharded_multiply(args.algo, da, db, levels, out=dc, ws=ws)
                 if rank == 0:
                     host_c.copy_(dc, non_blocking=True)
                 torch.cuda.current_stream().synchronize()
