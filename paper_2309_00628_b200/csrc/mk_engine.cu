@@ -574,6 +574,32 @@ struct Engine {
 
   // ---- one leaf product launch ----
   // Leaf product on the INT8 tensor cores (mk_ozaki.cu), timed like the DMMA launches.
+  // Many leaf products on the INT8 tensor cores, splitting overlapped with the product kernels.
+  int ozaki_batch(const std::vector<OzItem>& items) {
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    if (g_timing.on) {
+      MK_CUDA_TRY(cudaEventCreate(&t0));
+      MK_CUDA_TRY(cudaEventCreate(&t1));
+      MK_CUDA_TRY(cudaEventRecord(t0, st));
+    }
+    std::string err;
+    const int rc = ozaki_product_batch(items.data(), (int)items.size(), leaf_slices(), st, &err);
+    if (rc != MK_OK) return fail(rc, err);
+    g_launch_count += 8 * (long long)items.size();
+    if (g_timing.on) {
+      MK_CUDA_TRY(cudaEventRecord(t1, st));
+      g_timing.ev.emplace_back(t0, t1);
+      double fl = 0;
+      for (const OzItem& it : items) fl += 2.0 * (double)it.m * (double)it.n * (double)it.k;
+      g_timing.flops.push_back(fl);
+    }
+    if (debug_sync()) {
+      cudaError_t e2 = cudaStreamSynchronize(st);
+      if (e2 != cudaSuccess) return fail(MK_ERR_CUDA, std::string("Ozaki batch: ") + cudaGetErrorString(e2));
+    }
+    return MK_OK;
+  }
+
   OzOperand oz_operand(const Lin& T) const {
     OzOperand o{};
     o.n = (int)T.size();
@@ -1262,6 +1288,7 @@ struct Engine {
       for (int p = 0; p < np; ++p) groups.push_back({p});
     }
     std::vector<MkBatchEntry> ents;
+    std::vector<OzItem> oz_items;
     for (const auto& gr : groups) {
       struct Dests {
         MkDest dt[4];
@@ -1314,17 +1341,25 @@ struct Engine {
           }
         }
       }
-      if (leaf_slices() > 0) {  // INT8 tensor-core leaves: one Ozaki product per entry
+      if (leaf_slices() > 0) {  // INT8 tensor-core leaves: queued, run as one pipelined batch below
         launches += (int)ents.size();
         if (dry || no_launch) continue;
         for (size_t gi = 0; gi < gr.size(); ++gi) {
           for (size_t i = 0; i < par.size(); ++i) {
             const BNode& lf = lv[L][i * np + gr[gi]];
             const MkBatchEntry& e = ents[gi * par.size() + i];
-            OzDest od[MK_MAX_DESTS];
+            OzItem it{};
+            it.X = oz_operand(Lin{lf.x});
+            it.Y = oz_operand(Lin{lf.y});
+            it.C = e.C;
+            it.ldc = e.ldc;
+            it.m = lm;
+            it.n = ln;
+            it.k = lk;
+            it.nd = e.prod.nd;
             for (int k = 0; k < e.prod.nd; ++k)
-              od[k] = OzDest{e.prod.d[k].row, e.prod.d[k].col, e.prod.d[k].sign, e.prod.d[k].accumulate, 0};
-            MK_TRY(ozaki_leaf(oz_operand(Lin{lf.x}), oz_operand(Lin{lf.y}), e.C, e.ldc, lm, ln, lk, od, e.prod.nd));
+              it.d[k] = OzDest{e.prod.d[k].row, e.prod.d[k].col, e.prod.d[k].sign, e.prod.d[k].accumulate, 0};
+            oz_items.push_back(it);
           }
         }
         continue;
@@ -1361,6 +1396,7 @@ struct Engine {
         if (e2 != cudaSuccess) return fail(MK_ERR_CUDA, std::string("batched leaf launch: ") + cudaGetErrorString(e2));
       }
     }
+    if (!oz_items.empty()) MK_TRY(ozaki_batch(oz_items));
     // ---- post-additions: child outputs -> parent quadrants, deepest first ----
     for (int d = L - 1; d >= 1; --d) {
       std::vector<BNode>& ch = lv[d];

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <map>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -560,10 +561,10 @@ static size_t smem_bytes() {
   return STAGES * S * (BM + BN) * BK + 1024 /*align*/ + 256 /*barriers*/;
 }
 
-// One K chunk: split both operands, then the product kernel into every destination.
+// One K chunk, phase 1: split both operands into the digit planes / exponents / row sums of ws.
 template <int S>
-static int run(const OzOperand& X, const OzOperand& Y, double* C, int64_t ldc, int64_t m, int64_t n, int64_t k,
-               const OzDest* d, int nd, uint8_t* ws, cudaStream_t st, std::string* err) {
+static void split_phase(const OzOperand& X, const OzOperand& Y, int64_t m, int64_t n, int64_t k, uint8_t* ws,
+                        cudaStream_t st) {
   const Layout L = layout(m, n, k, S);
   const int64_t kp = kpad(k), nkb = kp / BK;
   const int64_t tiles_m = (m + BM - 1) / BM, tiles_n = (n + BN - 1) / BN;
@@ -578,14 +579,16 @@ static int run(const OzOperand& X, const OzOperand& Y, double* C, int64_t ldc, i
   cudaMemsetAsync(rmax, 0, 8 * (size_t)m, st);
   auto x_side = [&](auto nt) {
     constexpr int NT = decltype(nt)::value;
-    rowmax_kernel<NT><<<dim3((unsigned)((m * 32 + 255) / 256), (unsigned)((k + 1023) / 1024)), 256, 0, st>>>(
+    // 128-thread blocks: they fit in the registers a resident product CTA leaves free, so the
+    // splitting of the next leaf can run beside the current product kernel (ozaki_product_batch)
+    rowmax_kernel<NT><<<dim3((unsigned)((m * 32 + 127) / 128), (unsigned)((k + 1023) / 1024)), 128, 0, st>>>(
         X, (int)m, (int)k, rmax);
-    split_rows_kernel<S, NT><<<(unsigned)((tiles_m * BM * 32 + 255) / 256), 256, 0, st>>>(
+    split_rows_kernel<S, NT><<<(unsigned)((tiles_m * BM * 32 + 127) / 128), 128, 0, st>>>(
         X, (int)m, (int)(tiles_m * BM), (int)k, (int)nkb, rmax, ex, rs, px);
   };
   auto y_side = [&](auto nt) {
     constexpr int NT = decltype(nt)::value;
-    colmax_kernel<NT><<<dim3((unsigned)((n + 255) / 256), (unsigned)((k + 63) / 64)), 256, 0, st>>>(Y, (int)k,
+    colmax_kernel<NT><<<dim3((unsigned)((n + 127) / 128), (unsigned)((k + 63) / 64)), 128, 0, st>>>(Y, (int)k,
                                                                                                   (int)n, cmax);
     colexp_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(cmax, (int)n, fy);
     split_cols_kernel<S, NT><<<dim3((unsigned)(tiles_n * BN / 32), (unsigned)nkb), dim3(32, 8), 0, st>>>(
@@ -604,7 +607,18 @@ static int run(const OzOperand& X, const OzOperand& Y, double* C, int64_t ldc, i
     case 3: y_side(std::integral_constant<int, 3>{}); break;
     default: y_side(std::integral_constant<int, 4>{}); break;
   }
+}
 
+// One K chunk, phase 2: the product kernel from ws's digit planes into every destination.
+template <int S>
+static int product_phase(double* C, int64_t ldc, int64_t m, int64_t n, int64_t k, const OzDest* d, int nd,
+                         uint8_t* ws, cudaStream_t st, std::string* err) {
+  const Layout L = layout(m, n, k, S);
+  uint8_t* px = ws + L.planes_x;
+  uint8_t* py = ws + L.planes_y;
+  int32_t* ex = reinterpret_cast<int32_t*>(ws + L.ex);
+  int32_t* fy = reinterpret_cast<int32_t*>(ws + L.fy);
+  int32_t* rs = reinterpret_cast<int32_t*>(ws + L.rs);
   Args a;
   a.px = px;
   a.py = py;
@@ -666,6 +680,34 @@ static int run(const OzOperand& X, const OzOperand& Y, double* C, int64_t ldc, i
     return MK_ERR_CUDA;
   }
   return MK_OK;
+}
+
+template <int S>
+static int run(const OzOperand& X, const OzOperand& Y, double* C, int64_t ldc, int64_t m, int64_t n, int64_t k,
+               const OzDest* d, int nd, uint8_t* ws, cudaStream_t st, std::string* err) {
+  split_phase<S>(X, Y, m, n, k, ws, st);
+  return product_phase<S>(C, ldc, m, n, k, d, nd, ws, st, err);
+}
+
+static void split_any(int S, const OzOperand& X, const OzOperand& Y, int64_t m, int64_t n, int64_t k, uint8_t* ws,
+                      cudaStream_t st) {
+  switch (S) {
+    case 4: split_phase<4>(X, Y, m, n, k, ws, st); break;
+    case 5: split_phase<5>(X, Y, m, n, k, ws, st); break;
+    case 6: split_phase<6>(X, Y, m, n, k, ws, st); break;
+    case 7: split_phase<7>(X, Y, m, n, k, ws, st); break;
+    default: split_phase<8>(X, Y, m, n, k, ws, st); break;
+  }
+}
+static int product_any(int S, double* C, int64_t ldc, int64_t m, int64_t n, int64_t k, const OzDest* d, int nd,
+                       uint8_t* ws, cudaStream_t st, std::string* err) {
+  switch (S) {
+    case 4: return product_phase<4>(C, ldc, m, n, k, d, nd, ws, st, err);
+    case 5: return product_phase<5>(C, ldc, m, n, k, d, nd, ws, st, err);
+    case 6: return product_phase<6>(C, ldc, m, n, k, d, nd, ws, st, err);
+    case 7: return product_phase<7>(C, ldc, m, n, k, d, nd, ws, st, err);
+    default: return product_phase<8>(C, ldc, m, n, k, d, nd, ws, st, err);
+  }
 }
 
 // Whole product: K in chunks of chunk_k (later chunks accumulate into every destination).
@@ -736,6 +778,116 @@ int ozaki_product(const double* X, int64_t ldx, const double* Y, int64_t ldy, do
   return oz::product_chunks(ox, oy, C, ldc, m, n, k, slices, &dst, 1, static_cast<uint8_t*>(ws), st, err);
 }
 
+static void keep_pool_memory() {  // freed leaf workspaces stay in the stream-ordered pool
+  static thread_local int pool_dev = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess && dev != pool_dev) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool_dev = dev;
+  }
+}
+
+int ozaki_product_batch(const OzItem* items, int count, int slices, cudaStream_t st, std::string* err) {
+  if (count <= 0) return MK_OK;
+  struct Sub {
+    const OzItem* it;
+    int64_t k0, kk;
+    bool first;
+  };
+  std::vector<Sub> subs;
+  size_t wsb = 0;
+  for (int i = 0; i < count; ++i) {
+    const OzItem& it = items[i];
+    if (int rc = check_args(it.m, it.n, slices, it.nd, err)) return rc;
+    if (it.X.n < 1 || it.X.n > kOzMaxTerms || it.Y.n < 1 || it.Y.n > kOzMaxTerms) {
+      *err = "internal: operand term count out of range";
+      return MK_ERR_ARG;
+    }
+    const int64_t kc = oz::chunk_k(it.k, slices);
+    for (int64_t k0 = 0; k0 < it.k; k0 += kc) subs.push_back(Sub{&it, k0, std::min(kc, it.k - k0), k0 == 0});
+    wsb = std::max(wsb, ozaki_workspace_bytes(it.m, it.n, it.k, slices));
+  }
+  keep_pool_memory();
+  const int nbuf = subs.size() > 1 ? 2 : 1;
+  uint8_t* ws[2] = {nullptr, nullptr};
+  for (int b = 0; b < nbuf; ++b) {
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ws[b]), wsb, st);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      for (int j = 0; j < b; ++j) cudaFreeAsync(ws[j], st);
+      *err = std::string("Ozaki leaf workspace: ") + cudaGetErrorString(e);
+      return e == cudaErrorMemoryAllocation ? MK_ERR_WORKSPACE : MK_ERR_CUDA;
+    }
+  }
+  // Splitting (HBM bound) of item i+1 runs on a side stream while the product kernel of item i
+  // (tensor bound) runs on st: two workspaces, events in both directions.
+  static thread_local std::map<int, cudaStream_t> side_streams;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaStream_t side = nullptr;
+  if (nbuf == 2) {
+    auto itx = side_streams.find(dev);
+    if (itx == side_streams.end()) {
+      cudaStream_t s2;
+      if (cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        s2 = nullptr;
+      }
+      itx = side_streams.emplace(dev, s2).first;
+    }
+    side = itx->second;
+  }
+  cudaEvent_t start = nullptr, split_ev[2] = {nullptr, nullptr}, prod_ev[2] = {nullptr, nullptr};
+  auto mkev = [](cudaEvent_t* e) { return cudaEventCreateWithFlags(e, cudaEventDisableTiming); };
+  if (side) {
+    if (mkev(&start) || mkev(&split_ev[0]) || mkev(&split_ev[1]) || mkev(&prod_ev[0]) || mkev(&prod_ev[1])) {
+      cudaGetLastError();
+      side = nullptr;
+    } else {
+      cudaEventRecord(start, st);
+      cudaStreamWaitEvent(side, start, 0);  // operands produced earlier on st
+    }
+  }
+  int rc = MK_OK;
+  for (size_t i = 0; i < subs.size() && rc == MK_OK; ++i) {
+    const Sub& sb = subs[i];
+    const OzItem& it = *sb.it;
+    const int b = (int)(i % nbuf);
+    OzOperand Xc = it.X, Yc = it.Y;
+    for (int t = 0; t < Xc.n; ++t) Xc.p[t] = it.X.p[t] + sb.k0;
+    for (int t = 0; t < Yc.n; ++t) Yc.p[t] = it.Y.p[t] + sb.k0 * it.Y.ld;
+    OzDest dd[kOzMaxDests];
+    for (int t = 0; t < it.nd; ++t) {
+      dd[t] = it.d[t];
+      if (!sb.first) dd[t].accumulate = 1;
+    }
+    if (side) {
+      if (i >= 2) cudaStreamWaitEvent(side, prod_ev[b], 0);  // product i-2 is done with ws[b]
+      oz::split_any(slices, Xc, Yc, it.m, it.n, sb.kk, ws[b], side);
+      cudaEventRecord(split_ev[b], side);
+      cudaStreamWaitEvent(st, split_ev[b], 0);
+      rc = oz::product_any(slices, it.C, it.ldc, it.m, it.n, sb.kk, dd, it.nd, ws[b], st, err);
+      cudaEventRecord(prod_ev[b], st);
+    } else {
+      oz::split_any(slices, Xc, Yc, it.m, it.n, sb.kk, ws[b], st);
+      rc = oz::product_any(slices, it.C, it.ldc, it.m, it.n, sb.kk, dd, it.nd, ws[b], st, err);
+    }
+  }
+  for (int b = 0; b < nbuf; ++b) cudaFreeAsync(ws[b], st);  // after every product (and so every split)
+  for (cudaEvent_t e : {start, split_ev[0], split_ev[1], prod_ev[0], prod_ev[1]})
+    if (e) cudaEventDestroy(e);
+  cudaError_t e = cudaGetLastError();
+  if (rc == MK_OK && e != cudaSuccess) {
+    *err = std::string("Ozaki batch: ") + cudaGetErrorString(e);
+    rc = MK_ERR_CUDA;
+  }
+  return rc;
+}
+
 int ozaki_product_multi(const OzOperand& X, const OzOperand& Y, double* C, int64_t ldc, int64_t m, int64_t n,
                         int64_t k, int slices, const OzDest* d, int nd, cudaStream_t st, std::string* err) {
   if (int rc = check_args(m, n, slices, nd, err)) return rc;
@@ -744,18 +896,7 @@ int ozaki_product_multi(const OzOperand& X, const OzOperand& Y, double* C, int64
     return MK_ERR_ARG;
   }
   const size_t wsb = ozaki_workspace_bytes(m, n, k, slices);
-  {  // keep freed leaf workspaces in the stream-ordered pool (default threshold 0 unmaps them)
-    static thread_local int pool_dev = -1;
-    int dev = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess && dev != pool_dev) {
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = ~0ull;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-      }
-      pool_dev = dev;
-    }
-  }
+  keep_pool_memory();
   void* ws = nullptr;
   cudaError_t e = cudaMallocAsync(&ws, wsb, st);
   if (e != cudaSuccess) {

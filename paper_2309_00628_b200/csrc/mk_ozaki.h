@@ -58,6 +58,17 @@ struct OzOperand {
 int ozaki_product_multi(const OzOperand& X, const OzOperand& Y, double* C, int64_t ldc, int64_t m, int64_t n,
                         int64_t k, int slices, const OzDest* d, int nd, cudaStream_t st, std::string* err);
 
+// Several leaf products in stream order on `st`; the digit splitting of the next K chunk / item
+// runs on a side stream while the current product kernel runs (two pooled workspaces).
+struct OzItem {
+  OzOperand X, Y;
+  double* C;
+  int64_t ldc, m, n, k;
+  int nd;
+  OzDest d[kOzMaxDests];
+};
+int ozaki_product_batch(const OzItem* items, int count, int slices, cudaStream_t st, std::string* err);
+
 // C (+)= sign * X * Y on `st` with a caller-owned workspace (ozaki_workspace_bytes).
 // accumulate = 0 overwrites C. Returns 0 or an MK_ERR_* code with *err set. A non-finite operand
 // entry cannot be written as digits: every result entry in its row (X) or column (Y) is NaN.
