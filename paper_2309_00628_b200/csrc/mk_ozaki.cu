@@ -353,11 +353,13 @@ __device__ __forceinline__ int row_exponent(double mx) {
 // bytes is the floor at S digits), so one floor conversion per element yields all S digits.
 // scale = 2^(63 - e). OFFSET: plane 0 stored as d_0 + 128 (top bit flipped) for the Y side.
 // dsum (may be null): per-plane sums of the 4 digits (signed plane 0), for the row sums.
+// scale = s1 * s2 (two factors: 2^(63 - e) overflows a double for row maxima below 2^-960;
+// each product stays exact).
 template <int S, bool OFFSET>
-__device__ __forceinline__ void digits4(const double x[4], double scale, uint32_t out[S], int* dsum) {
+__device__ __forceinline__ void digits4(const double x[4], double s1, double s2, uint32_t out[S], int* dsum) {
   unsigned long long v[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) v[i] = (unsigned long long)__double2ll_rd(x[i] * scale);
+  for (int i = 0; i < 4; ++i) v[i] = (unsigned long long)__double2ll_rd((x[i] * s1) * s2);
 #pragma unroll
   for (int s = 0; s < S; ++s) {
     const int sh = 8 * (7 - s);
@@ -428,7 +430,8 @@ __global__ void split_rows_kernel(const OzOperand X, int rows, int rows_pad, int
   const bool live = warp < rows;
   const int e = live ? row_exponent(__longlong_as_double((long long)rmax[warp])) : 0;
   if (lane == 0 && live) ex[warp] = e;
-  const double scale = (e == EXP_NONFINITE) ? 0.0 : ldexp(1.0, 63 - e);
+  const int sh = 63 - e, sh1 = sh < 1000 ? sh : 1000;
+  const double scale = (e == EXP_NONFINITE) ? 0.0 : ldexp(1.0, sh1), scale2 = ldexp(1.0, sh - sh1);
   const bool load = live && e != EXP_NONFINITE;
   const int tmi = warp / BM, r = warp % BM;
   uint8_t* base = planes + (int64_t)tmi * nkb * (S * BM * BK);
@@ -442,7 +445,7 @@ __global__ void split_rows_kernel(const OzOperand X, int rows, int rows_pad, int
 #pragma unroll
     for (int i = 0; i < 4; ++i) x[i] = (load && k0 + i < K) ? term_sum<NT>(X, warp, k0 + i) : 0.0;
     uint32_t w[S];
-    digits4<S, false>(x, scale, w, dsum);
+    digits4<S, false>(x, scale, scale2, w, dsum);
     uint8_t* t = base + (int64_t)(k0 / BK) * (S * BM * BK) + swz32(r, k0 % BK);
 #pragma unroll
     for (int s = 0; s < S; ++s) *reinterpret_cast<uint32_t*>(t + s * (BM * BK)) = w[s];
@@ -499,7 +502,8 @@ __global__ void split_cols_kernel(const OzOperand Y, int K, int N, int nkb, cons
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int col = n0 + tx;
   const int f = col < N ? fy[col] : 0;
-  const double scale = (col < N && f != EXP_NONFINITE) ? ldexp(1.0, 63 - f) : 0.0;
+  const int sh = 63 - f, sh1 = sh < 1000 ? sh : 1000;
+  const double scale = (col < N && f != EXP_NONFINITE) ? ldexp(1.0, sh1) : 0.0, scale2 = ldexp(1.0, sh - sh1);
   // thread (tx, ty) converts k = k0 + 4*ty .. +3 of column col
   double x[4];
 #pragma unroll
@@ -508,7 +512,7 @@ __global__ void split_cols_kernel(const OzOperand Y, int K, int N, int nkb, cons
     x[i] = (col < N && k < K && scale != 0.0) ? term_sum<NT>(Y, k, col) : 0.0;
   }
   uint32_t w[S];
-  digits4<S, true>(x, scale, w, nullptr);
+  digits4<S, true>(x, scale, scale2, w, nullptr);
   if (col >= N) {  // padded columns: zero digits (not the +128 offset)
 #pragma unroll
     for (int s = 0; s < S; ++s) w[s] = 0;

@@ -108,3 +108,29 @@ def test_ozaki_dgemm_errors():
         pk.set_leaf("ozaki", 9)
     with pytest.raises(ValueError):
         pk.set_leaf("int8")
+
+
+def test_ozaki_dgemm_extreme_exponents():
+    """Rows / columns whose maxima span the double range (down to subnormal scale, up to 1e300):
+    every product stays within 8 ulps of its own magnitude scale (no overflow of the digit scale,
+    no underflow of the recombination), like the FP64 product of the same data."""
+    import torch
+
+    r = np.random.default_rng(7)
+    m, k, n = 130, 96, 70
+    a = r.uniform(-1, 1, (m, k))
+    b = r.uniform(-1, 1, (k, n))
+    row_scale = np.array([1e-300, 1e-200, 1e-100, 1.0, 1e100, 1e150] * 22)[:m]
+    col_scale = np.array([1e-150, 1e-20, 1.0, 1e20, 1e140] * 14)[:n]
+    a *= row_scale[:, None]
+    b *= col_scale[None, :]
+    a[3, :] = 0.0  # a zero row
+    at, bt = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    rc, c = _dgemm(at, bt, 8)
+    assert rc == 0
+    ref = np.matmul(a.astype(np.longdouble), b.astype(np.longdouble))
+    bound = (np.abs(a).max(1)[:, None].astype(np.longdouble) * np.abs(b).max(0)[None, :].astype(np.longdouble)
+             * k * 2.0 ** -50 + k * np.longdouble(2.0) ** -1074)  # + FP64 subnormal rounding
+    err = np.abs(c.cpu().numpy().astype(np.longdouble) - ref)
+    assert np.all(err <= bound), float((err / np.maximum(bound, 1e-300)).max())
+    assert np.all(c[3].cpu().numpy() == 0.0)
