@@ -293,6 +293,21 @@ def ozaki_leg(args, pk, lib, _lib, torch, A, B, C, dc, host_a, host_b, policy, s
         f1.record(stream)
         torch.cuda.synchronize()
         ems = f0.elapsed_time(f1) / args.steps
+        alts = []
+        for cut in [int(x) for x in args.alt.split(",") if x]:  # same extra cutoffs as the DMMA leg
+            pol = pk.BasePolicy.naive_cutoff(cut)
+            for _ in range(2):
+                call(A, B, C, pol)
+            torch.cuda.synchronize()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            for _ in range(3):
+                call(A, B, C, pol)
+            g1.record(stream)
+            torch.cuda.synchronize()
+            ams = g0.elapsed_time(g1) / 3
+            alts.append({"cutoff": cut, "levels": levels_for(n, cut), "ms_per_step": round(ams, 3),
+                         "value": round(2.0 * n ** 3 / (ams * 1e-3) / 1e12, 4)})
     finally:
         pk.set_leaf("dmma")
     pairs = S * (S + 1) // 2
@@ -321,6 +336,7 @@ def ozaki_leg(args, pk, lib, _lib, torch, A, B, C, dc, host_a, host_b, policy, s
                      "kernel": "mk::oz::ozaki_product_kernel + digit splitting (per leaf, CUDA events)",
                      "peak_source": src},
         "clocks": clk.summary(),
+        "alt_cutoffs": alts,
         "dtype": "f64 operands/results; int8 x int8 -> int32 tensor-core products (Ozaki scheme I)",
     }
 
