@@ -41,7 +41,6 @@ struct Args {
   int32_t M, N, K, tiles_n;
   int32_t nd, pad_;
   unsigned long long* trace;  // debug (MK_OZ_TRACE=1): 7 %globaltimer stamps per tile
-  int32_t probe;              // debug (MK_OZ_PROBE): 1 = 9 MMAs of N=256 per stage (wrong results), 2 = no MMAs
   OzDest d[kOzMaxDests];  // destinations: C[d.row + i][d.col + j] (+)= d.sign * P_ij
 };
 
@@ -191,11 +190,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // accumulators (anti-diagonals s+t) are consecutive 64-column TMEM blocks, so one MMA
         // with N = 64 * #planes (<= 256) covers up to 4 pairs: S(S+1)/2 pairs in
         // sum_s ceil((S-s)/4) MMAs, each reading its X plane once.
-        if (a.probe == 1) {
-          for (int i = 0; i < (S * (S + 1) / 2 + 3) / 4; ++i)
-            mma_i8(tmem + (uint32_t)((i & 1) * 4 * BN), smem_desc_sw32(sa + (i % S) * A_TILE), smem_desc_sw32(sb),
-                   idesc_i8(4 * BN, false, false), 1u);
-        } else if (a.probe != 2)
 #pragma unroll
         for (int s = 0; s < S; ++s) {
           const uint64_t da = smem_desc_sw32(sa + s * A_TILE);
@@ -640,14 +634,14 @@ static int product_phase(double* C, int64_t ldc, int64_t m, int64_t n, int64_t k
   for (int i = 0; i < nd; ++i) a.d[i] = d[i];
   const int tiles = (int)((m + BM - 1) / BM) * a.tiles_n;
   const size_t smem = smem_bytes<S>();
-  static std::once_flag attr_once;
-  std::call_once(attr_once, [&] {
-    cudaFuncSetAttribute(ozaki_product_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  });
+  // per launch (the attribute is per device; the call is cheap next to a leaf product)
+  cudaError_t ae = cudaFuncSetAttribute(ozaki_product_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (ae != cudaSuccess) {
+    *err = std::string("ozaki_product_kernel smem attribute: ") + cudaGetErrorString(ae);
+    return MK_ERR_CUDA;
+  }
   static const bool trace = getenv("MK_OZ_TRACE") && getenv("MK_OZ_TRACE")[0] == '1';
   a.trace = nullptr;
-  static const int probe = getenv("MK_OZ_PROBE") ? atoi(getenv("MK_OZ_PROBE")) : 0;
-  a.probe = probe;
   if (trace) cudaMalloc(&a.trace, 10 * sizeof(unsigned long long) * tiles);
   ozaki_product_kernel<S><<<tiles, NTHREADS, smem, st>>>(a);
   if (trace) {  // debug: per-phase medians over the tiles, stderr
