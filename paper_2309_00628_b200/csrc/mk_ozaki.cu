@@ -329,6 +329,200 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 }
 
 // ---------------------------------------------------------------------------------------------
+// Persistent variant: one CTA per SM walks tiles t = blockIdx.x, += gridDim.x. The TMA warp
+// streams k-stages across tile boundaries (the next tile's first stages land during the
+// epilogue); the epilogue warps drain TMEM into FP64 registers, release it (tmem_empty) so the
+// next tile's MMAs start, and only then write C -- the stores overlap the next main loop.
+// ---------------------------------------------------------------------------------------------
+constexpr int PT_THREADS = 320;  // warp 0 TMA, warp 1 MMA issuer + TMEM owner, warps 2-9 epilogue
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr)
+               : "memory");
+}
+
+__device__ __forceinline__ void map_tile(const Args& a, int t, int& tm, int& tn) {
+  const int tiles_m = (a.M + BM - 1) / BM, g = 16;
+  const int per_group = g * a.tiles_n, grp = t / per_group, first = grp * g;
+  const int rows = min(g, tiles_m - first), local = t - grp * per_group;
+  tm = first + local % rows;
+  tn = local / rows;
+}
+
+template <int S>
+__global__ void __launch_bounds__(PT_THREADS, 1) ozaki_persistent_kernel(const __grid_constant__ Args a, int tiles) {
+  constexpr int A_TILE = BM * BK;
+  constexpr int B_TILE = BN * BK;
+  constexpr int STAGE_BYTES = S * (A_TILE + B_TILE);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint64_t* tmem_empty = tmem_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nkb = (a.K + BK - 1) / BK;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(tmem_full, 1);
+    mbar_init(tmem_empty, 8);  // one arrival per epilogue warp
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        int tm, tn;
+        map_tile(a, t, tm, tn);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int st = it % STAGES;
+          if (it >= STAGES) mbar_wait(&empty[st], ((it / STAGES) - 1) & 1);
+          uint8_t* sa = smem + st * STAGE_BYTES;
+          mbar_arrive_expect_tx(&full[st], STAGE_BYTES);
+          bulk_load(sa, a.px + ((int64_t)tm * nkb + kb) * (S * A_TILE), S * A_TILE, &full[st]);
+          bulk_load(sa + S * A_TILE, a.py + ((int64_t)tn * nkb + kb) * (S * B_TILE), S * B_TILE, &full[st]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int it = 0, ti = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++ti) {
+        if (ti > 0) {  // the epilogue has drained the previous tile's accumulators
+          mbar_wait(tmem_empty, (ti - 1) & 1);
+          tmem_fence_after();
+        }
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int st = it % STAGES;
+          mbar_wait(&full[st], (it / STAGES) & 1);
+          tmem_fence_after();
+          const uint8_t* sa = smem + st * STAGE_BYTES;
+          const uint8_t* sb = sa + S * A_TILE;
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+            const uint64_t da = smem_desc_sw32(sa + s * A_TILE);
+            const uint32_t acc = (kb > 0 || s > 0) ? 1u : 0u;
+#pragma unroll
+            for (int t0 = 0; t0 < S - s; t0 += 4) {
+              const int cnt = (S - s - t0) < 4 ? (S - s - t0) : 4;
+              mma_i8(tmem + (uint32_t)((s + t0) * BN), da, smem_desc_sw32(sb + t0 * B_TILE),
+                     idesc_i8(cnt * BN, s == 0, false), acc);
+            }
+          }
+          mma_commit(&empty[st]);
+        }
+        mma_commit(tmem_full);
+      }
+    }
+  } else {
+    // epilogue warps 2..9: lane quarter q = warp % 4 (TMEM lanes 32q..), column half = (warp-2)/4
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    int ti = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++ti) {
+      int tm, tn;
+      map_tile(a, t, tm, tn);
+      const int row = tm * BM + q * 32 + lane;
+      const bool row_ok = row < a.M;
+      const int e = row_ok ? a.ex[row] : 0;
+      long long chi = 0, clo = 0;
+#pragma unroll
+      for (int d = 0; d < S; ++d) {
+        const long long c = row_ok ? 128ll * a.rs[(int64_t)d * a.M + row] : 0ll;
+        if (d < 4) chi += c << (8 * (3 - d));
+        else clo += c << (8 * (7 - d));
+      }
+      const bool e_fast = e > -900 && e < 900;
+      const double escale = e_fast ? __longlong_as_double((long long)(e - 7 - 24 + 1023) << 52) : 0.0;
+      const int col0 = tn * BN + half * (BN / 2);
+      const int fl = col0 + lane < a.N ? a.fy[col0 + lane] : 0;
+      mbar_wait_sleep(tmem_full, ti & 1);
+      tmem_fence_after();
+      const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+      double p[BN / 2];
+#pragma unroll
+      for (int c8 = 0; c8 < BN / 2; c8 += 8) {
+        long long hi[8], lo[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) hi[j] = lo[j] = 0;
+#pragma unroll
+        for (int d0 = 0; d0 < S; d0 += 2) {
+          uint32_t r[2][8];
+          tmem_ld8(tl + (uint32_t)(d0 * BN + half * (BN / 2) + c8), r[0]);
+          if (d0 + 1 < S) tmem_ld8(tl + (uint32_t)((d0 + 1) * BN + half * (BN / 2) + c8), r[1]);
+          tmem_wait_ld();
+#pragma unroll
+          for (int dd = 0; dd < 2; ++dd) {
+            const int d = d0 + dd;
+            if (d >= S) break;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const long long x = (long long)(int32_t)r[dd][j];
+              if (d < 4) hi[j] += x << (8 * (3 - d));
+              else lo[j] += x << (8 * (7 - d));
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const double v = fma((double)(lo[j] - clo), 2.3283064365386963e-10, (double)(hi[j] - chi));
+          const int f = __shfl_sync(0xffffffffu, fl, c8 + j);
+          const bool fast = e_fast && f > -900 && f < 900;
+          double pj = (v * escale) * __longlong_as_double((long long)((fast ? f : 0) - 7 + 1023) << 52);
+          if (!fast)
+            pj = (e == EXP_NONFINITE || f == EXP_NONFINITE) ? __longlong_as_double(0x7ff8000000000000ll)
+                                                            : ldexp(v, e + f - 38);
+          p[c8 + j] = pj;
+        }
+      }
+      tmem_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tmem_empty);  // accumulators free: the next tile's MMAs may start
+      // write back (overlaps the next tile's main loop): this thread's row, 32 columns
+      if (row_ok) {
+        double* crow = a.C + (int64_t)row * a.ldc;
+        for (int d = 0; d < a.nd; ++d) {
+          const OzDest dd = a.d[d];
+          double* dst = crow + dd.row * a.ldc + dd.col + col0;
+          const bool vec = col0 + BN / 2 <= a.N && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
+          if (vec) {
+#pragma unroll
+            for (int j = 0; j < BN / 2; j += 2) {
+              double2* p2 = reinterpret_cast<double2*>(dst + j);
+              double2 o = make_double2(dd.sign * p[j], dd.sign * p[j + 1]);
+              if (dd.accumulate) {
+                const double2 c = *p2;
+                o = make_double2(fma(dd.sign, p[j], c.x), fma(dd.sign, p[j + 1], c.y));
+              }
+              *p2 = o;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 2; ++j)
+              if (col0 + j < a.N) dst[j] = dd.accumulate ? fma(dd.sign, p[j], dst[j]) : dd.sign * p[j];
+          }
+        }
+      }
+    }
+  }
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+// ---------------------------------------------------------------------------------------------
 // Digit splitting (HBM bound): X rows -> exponents + S int8 planes [S][rows][kp].
 // One warp per row; lane handles 4 consecutive k per iteration (one 32-bit store per plane).
 // ---------------------------------------------------------------------------------------------
@@ -642,6 +836,26 @@ static int product_phase(double* C, int64_t ldc, int64_t m, int64_t n, int64_t k
   }
   static const bool trace = getenv("MK_OZ_TRACE") && getenv("MK_OZ_TRACE")[0] == '1';
   a.trace = nullptr;
+  static const bool persistent = !(getenv("MK_OZ_PERSISTENT") && getenv("MK_OZ_PERSISTENT")[0] == '0');
+  if (persistent && !trace) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t psmem = smem + 8;
+    cudaError_t pe = cudaFuncSetAttribute(ozaki_persistent_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)psmem);
+    if (pe != cudaSuccess) {
+      *err = std::string("ozaki_persistent_kernel smem attribute: ") + cudaGetErrorString(pe);
+      return MK_ERR_CUDA;
+    }
+    ozaki_persistent_kernel<S><<<std::min(tiles, sms), PT_THREADS, psmem, st>>>(a, tiles);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      *err = std::string("ozaki_persistent_kernel launch: ") + cudaGetErrorString(e);
+      return MK_ERR_CUDA;
+    }
+    return MK_OK;
+  }
   if (trace) cudaMalloc(&a.trace, 10 * sizeof(unsigned long long) * tiles);
   ozaki_product_kernel<S><<<tiles, NTHREADS, smem, st>>>(a);
   if (trace) {  // debug: per-phase medians over the tiles, stderr
