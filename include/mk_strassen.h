@@ -201,7 +201,8 @@ int mk_enable_peer_access(int peer_device);
  * and the separate reduce collective disappear. Every slab must be zeroed before any rank starts
  * (barrier), and read after every rank has finished (device sync + barrier). nslabs * slab_rows
  * == n; levels <= 2 (every leaf contribution then lands in the epilogue); the leaves run on the
- * DMMA kernel. FP64 summation order at a row follows arrival order (integer data stays exact). */
+ * DMMA kernel or, with MK_OPT_LEAF_SLICES set, the INT8 (Ozaki) kernel, whose write-back then uses
+ * atomic adds. FP64 summation order at a row follows arrival order (integer data stays exact). */
 int mk_strassen_partial_slabs(int algo, const double* A, int64_t lda, const double* B, int64_t ldb,
                               double* const* slabs, int nslabs, int64_t slab_rows, int64_t ldc, int64_t n,
                               int levels, int first, int count, int panels, void* ws, size_t ws_bytes,

@@ -619,7 +619,13 @@ struct Engine {
       MK_CUDA_TRY(cudaEventRecord(t0, st));
     }
     std::string err;
-    const int rc = ozaki_product_multi(x, y, c, ldc, M, N, K, leaf_slices(), od, nd, st, &err);
+    OzSlabs sl{};
+    if (nslab) {
+      sl.n = nslab;
+      sl.rows = slab_rows;
+      for (int i = 0; i < nslab; ++i) sl.p[i] = slab[i];
+    }
+    const int rc = ozaki_product_multi(x, y, c, ldc, M, N, K, leaf_slices(), od, nd, st, &err, nslab ? &sl : nullptr);
     if (rc != MK_OK) return fail(rc, err);
     g_launch_count += 5;
     if (g_timing.on) {
@@ -667,7 +673,7 @@ struct Engine {
     }
     ++launches;
     if (dry || no_launch) return MK_OK;
-    if (leaf_slices() > 0 && nslab == 0) {  // INT8 tensor-core leaf; multi-term operands summed as they are split
+    if (leaf_slices() > 0) {  // INT8 tensor-core leaf; multi-term operands summed as they are split
       std::vector<OzDest> od(p.nd);
       for (int i = 0; i < p.nd; ++i) od[i] = OzDest{p.d[i].row, p.d[i].col, p.d[i].sign, p.d[i].accumulate, 0};
       return ozaki_leaf(oz_operand(X), oz_operand(Y), bases[bd].ptr, bases[bd].ld, M, N, K, od.data(), p.nd);

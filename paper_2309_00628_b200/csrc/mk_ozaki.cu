@@ -44,6 +44,7 @@ struct Args {
   int32_t M, N, K, tiles_n;
   int32_t nd, pad_;
   unsigned long long* trace;  // debug (MK_OZ_TRACE=1): 7 %globaltimer stamps per tile
+  OzSlabs slabs;              // slabs.n > 0: C rows routed to owner slabs, atomic adds (persistent kernel)
   OzDest d[kOzMaxDests];  // destinations: C[d.row + i][d.col + j] (+)= d.sign * P_ij
 };
 
@@ -494,7 +495,16 @@ __global__ void __launch_bounds__(PT_THREADS, 1) ozaki_persistent_kernel(const _
       __syncwarp();
       if (lane == 0) mbar_arrive(tmem_empty);  // accumulators free: the next tile's MMAs may start
       // write back (overlaps the next tile's main loop): this thread's row, 32 columns
-      if (row_ok) {
+      if (row_ok && a.slabs.n > 0) {  // fused reduce-scatter: owner slab rows, atomic adds (RED.ADD.F64)
+        for (int d = 0; d < a.nd; ++d) {
+          const OzDest dd = a.d[d];
+          const int64_t R = dd.row + row, o = R / a.slabs.rows;
+          double* dst = a.slabs.p[o] + (R - o * a.slabs.rows) * a.ldc + dd.col + col0;
+#pragma unroll
+          for (int j = 0; j < BN / 2; ++j)
+            if (col0 + j < a.N) atomicAdd(dst + j, dd.sign * p[j]);
+        }
+      } else if (row_ok) {
         double* crow = a.C + (int64_t)row * a.ldc;
         for (int d = 0; d < a.nd; ++d) {
           const OzDest dd = a.d[d];
@@ -807,7 +817,7 @@ static void split_phase(const OzOperand& X, const OzOperand& Y, int64_t m, int64
 // One K chunk, phase 2: the product kernel from ws's digit planes into every destination.
 template <int S>
 static int product_phase(double* C, int64_t ldc, int64_t m, int64_t n, int64_t k, const OzDest* d, int nd,
-                         uint8_t* ws, cudaStream_t st, std::string* err) {
+                         uint8_t* ws, cudaStream_t st, std::string* err, const OzSlabs* slabs = nullptr) {
   const Layout L = layout(m, n, k, S);
   uint8_t* px = ws + L.planes_x;
   uint8_t* py = ws + L.planes_y;
@@ -829,6 +839,7 @@ static int product_phase(double* C, int64_t ldc, int64_t m, int64_t n, int64_t k
   a.nd = nd;
   a.pad_ = 0;
   for (int i = 0; i < nd; ++i) a.d[i] = d[i];
+  a.slabs = slabs ? *slabs : OzSlabs{0, 1, {nullptr}};
   const int tiles = (int)((m + BM - 1) / BM) * a.tiles_n;
   const size_t smem = smem_bytes<S>();
   // per launch (the attribute is per device; the call is cheap next to a leaf product)
@@ -840,7 +851,7 @@ static int product_phase(double* C, int64_t ldc, int64_t m, int64_t n, int64_t k
   static const bool trace = getenv("MK_OZ_TRACE") && getenv("MK_OZ_TRACE")[0] == '1';
   a.trace = nullptr;
   static const bool persistent = !(getenv("MK_OZ_PERSISTENT") && getenv("MK_OZ_PERSISTENT")[0] == '0');
-  if (persistent && !trace) {
+  if ((persistent && !trace) || a.slabs.n > 0) {  // slab routing lives in the persistent kernel
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -899,9 +910,10 @@ static int product_phase(double* C, int64_t ldc, int64_t m, int64_t n, int64_t k
 
 template <int S>
 static int run(const OzOperand& X, const OzOperand& Y, double* C, int64_t ldc, int64_t m, int64_t n, int64_t k,
-               const OzDest* d, int nd, uint8_t* ws, cudaStream_t st, std::string* err) {
+               const OzDest* d, int nd, uint8_t* ws, cudaStream_t st, std::string* err,
+               const OzSlabs* slabs = nullptr) {
   split_phase<S>(X, Y, m, n, k, ws, st);
-  return product_phase<S>(C, ldc, m, n, k, d, nd, ws, st, err);
+  return product_phase<S>(C, ldc, m, n, k, d, nd, ws, st, err, slabs);
 }
 
 static void split_any(int S, const OzOperand& X, const OzOperand& Y, int64_t m, int64_t n, int64_t k, uint8_t* ws,
@@ -927,7 +939,8 @@ static int product_any(int S, double* C, int64_t ldc, int64_t m, int64_t n, int6
 
 // Whole product: K in chunks of chunk_k (later chunks accumulate into every destination).
 static int product_chunks(const OzOperand& X, const OzOperand& Y, double* C, int64_t ldc, int64_t m, int64_t n,
-                          int64_t k, int S, const OzDest* d, int nd, uint8_t* ws, cudaStream_t st, std::string* err) {
+                          int64_t k, int S, const OzDest* d, int nd, uint8_t* ws, cudaStream_t st, std::string* err,
+                          const OzSlabs* slabs = nullptr) {
   const int64_t kc = chunk_k(k, S);
   OzDest dd[kOzMaxDests];
   for (int i = 0; i < nd; ++i) dd[i] = d[i];
@@ -938,11 +951,11 @@ static int product_chunks(const OzOperand& X, const OzOperand& Y, double* C, int
     for (int i = 0; i < Y.n; ++i) Yc.p[i] = Y.p[i] + k0 * Y.ld;
     int rc;
     switch (S) {
-      case 4: rc = run<4>(Xc, Yc, C, ldc, m, n, kk, dd, nd, ws, st, err); break;
-      case 5: rc = run<5>(Xc, Yc, C, ldc, m, n, kk, dd, nd, ws, st, err); break;
-      case 6: rc = run<6>(Xc, Yc, C, ldc, m, n, kk, dd, nd, ws, st, err); break;
-      case 7: rc = run<7>(Xc, Yc, C, ldc, m, n, kk, dd, nd, ws, st, err); break;
-      default: rc = run<8>(Xc, Yc, C, ldc, m, n, kk, dd, nd, ws, st, err); break;
+      case 4: rc = run<4>(Xc, Yc, C, ldc, m, n, kk, dd, nd, ws, st, err, slabs); break;
+      case 5: rc = run<5>(Xc, Yc, C, ldc, m, n, kk, dd, nd, ws, st, err, slabs); break;
+      case 6: rc = run<6>(Xc, Yc, C, ldc, m, n, kk, dd, nd, ws, st, err, slabs); break;
+      case 7: rc = run<7>(Xc, Yc, C, ldc, m, n, kk, dd, nd, ws, st, err, slabs); break;
+      default: rc = run<8>(Xc, Yc, C, ldc, m, n, kk, dd, nd, ws, st, err, slabs); break;
     }
     if (rc != MK_OK) return rc;
     for (int i = 0; i < nd; ++i) dd[i].accumulate = 1;
@@ -1104,7 +1117,8 @@ int ozaki_product_batch(const OzItem* items, int count, int slices, cudaStream_t
 }
 
 int ozaki_product_multi(const OzOperand& X, const OzOperand& Y, double* C, int64_t ldc, int64_t m, int64_t n,
-                        int64_t k, int slices, const OzDest* d, int nd, cudaStream_t st, std::string* err) {
+                        int64_t k, int slices, const OzDest* d, int nd, cudaStream_t st, std::string* err,
+                        const OzSlabs* slabs) {
   if (int rc = check_args(m, n, slices, nd, err)) return rc;
   if (X.n < 1 || X.n > kOzMaxTerms || Y.n < 1 || Y.n > kOzMaxTerms) {
     *err = "internal: operand term count out of range";
@@ -1119,7 +1133,7 @@ int ozaki_product_multi(const OzOperand& X, const OzOperand& Y, double* C, int64
     *err = std::string("Ozaki leaf workspace: ") + cudaGetErrorString(e);
     return e == cudaErrorMemoryAllocation ? MK_ERR_WORKSPACE : MK_ERR_CUDA;
   }
-  int rc = oz::product_chunks(X, Y, C, ldc, m, n, k, slices, d, nd, static_cast<uint8_t*>(ws), st, err);
+  int rc = oz::product_chunks(X, Y, C, ldc, m, n, k, slices, d, nd, static_cast<uint8_t*>(ws), st, err, slabs);
   e = cudaFreeAsync(ws, st);
   if (rc == MK_OK && e != cudaSuccess) {
     *err = std::string("Ozaki leaf workspace free: ") + cudaGetErrorString(e);

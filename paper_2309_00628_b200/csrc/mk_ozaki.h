@@ -53,10 +53,20 @@ struct OzOperand {
   int64_t ld;
 };
 
+// Row-slab output (fused multi-GPU reduce-scatter): C row R (relative to C's base) lives at
+// p[R / rows] + (R % rows) * ldc; every contribution is an atomic add (other ranks add too).
+constexpr int kOzMaxSlabs = 8;
+struct OzSlabs {
+  int n;
+  int64_t rows;
+  double* p[kOzMaxSlabs];
+};
+
 // P = X * Y written to every destination of `d` (stream-ordered workspace from the CUDA pool;
-// K beyond ozaki_max_k is processed in chunks).
+// K beyond ozaki_max_k is processed in chunks). slabs: optional row-slab routing of C.
 int ozaki_product_multi(const OzOperand& X, const OzOperand& Y, double* C, int64_t ldc, int64_t m, int64_t n,
-                        int64_t k, int slices, const OzDest* d, int nd, cudaStream_t st, std::string* err);
+                        int64_t k, int slices, const OzDest* d, int nd, cudaStream_t st, std::string* err,
+                        const OzSlabs* slabs = nullptr);
 
 // Several leaf products in stream order on `st`; the digit splitting of the next K chunk / item
 // runs on a side stream while the current product kernel runs (two pooled workspaces).

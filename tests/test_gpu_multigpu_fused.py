@@ -18,10 +18,21 @@ from conftest import has_gpu
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")]
 
 
+@pytest.fixture(params=["dmma", "ozaki"])
+def leaf(request):
+    import paper_2309_00628_b200 as pk
+
+    pk.set_leaf(request.param, 8) if request.param == "ozaki" else pk.set_leaf("dmma")
+    yield request.param
+    pk.set_leaf("dmma")
+
+
 @pytest.mark.parametrize("algo", ["strassen", "winograd-block", "winograd-knuth"])
 @pytest.mark.parametrize("levels", [1, 2])
 @pytest.mark.parametrize("world", [2, 4, 8])
-def test_slab_partials_assemble_the_product(algo, levels, world):
+def test_slab_partials_assemble_the_product(algo, levels, world, leaf):
+    """Both leaf kernels route rows to owner slabs (DMMA: REDG.ADD epilogue; INT8 Ozaki: atomic
+    adds from the persistent kernel's write-back)."""
     import torch
 
     from paper_2309_00628_b200 import multigpu as mg
@@ -66,11 +77,15 @@ def _free_port():
     return p
 
 
-def _ipc_worker(rank, world, port, levels, exact, result_path):
+def _ipc_worker(rank, world, port, levels, exact, result_path, leaf="dmma"):
     import torch
     import torch.distributed as dist
 
+    import paper_2309_00628_b200 as pk
     from paper_2309_00628_b200 import multigpu as mg
+
+    if leaf == "ozaki":
+        pk.set_leaf("ozaki", 8)
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -100,14 +115,15 @@ def _ipc_worker(rank, world, port, levels, exact, result_path):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("levels,exact", [(1, True), (2, True), (2, False)])
-def test_two_process_ipc_fused_reduce_scatter(levels, exact, tmp_path):
+@pytest.mark.parametrize("levels,exact,leaf", [(1, True, "dmma"), (2, True, "dmma"), (2, False, "dmma"),
+                                               (2, True, "ozaki"), (2, False, "ozaki")])
+def test_two_process_ipc_fused_reduce_scatter(levels, exact, leaf, tmp_path):
     import torch.multiprocessing as mp
 
     result = str(tmp_path / "result.txt")
     ctx = mp.get_context("spawn")
     port = _free_port()
-    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, levels, exact, result)) for r in range(2)]
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, levels, exact, result, leaf)) for r in range(2)]
     for p in procs:
         p.start()
     for p in procs:
