@@ -28,6 +28,7 @@
 #include <mutex>
 #include <string>
 #include <vector>
+#include <cmath>
 
 #include "../../include/mk_strassen.h"
 #include "mk_blockops.h"
@@ -324,6 +325,22 @@ static int leaf_slices() {
     g_leaf_slices = (v >= kOzMinSlices && v <= kOzMaxSlices) ? v : 0;
   }
   return g_leaf_slices;
+}
+// MK_OPT_LEAF_MIN_LOG2: INT8 leaves only for products with m*n*k >= 2^v (default 31, about 1290^3;
+// env MK_LEAF_MIN_LOG2): smaller leaves are launch- and wave-bound on the per-leaf INT8 kernels
+// (n = 8192 at 1024^3 leaves: 32.4 ms INT8 vs 24.2 ms DMMA; cfg5 at ~1500 x 1750 x 1250 leaves:
+// 57 vs 77 ms; 4096^3: 1.9x faster) and stay DMMA.
+static std::atomic<int> g_leaf_min_log2{-1};
+static int leaf_min_log2() {
+  if (g_leaf_min_log2 < 0) {
+    const char* e = getenv("MK_LEAF_MIN_LOG2");
+    const int v = e ? atoi(e) : 31;
+    g_leaf_min_log2 = (v >= 0 && v <= 62) ? v : 31;
+  }
+  return g_leaf_min_log2;
+}
+static bool ozaki_leaf_for(int64_t m, int64_t n, int64_t k) {
+  return leaf_slices() > 0 && (double)m * (double)n * (double)k >= std::ldexp(1.0, leaf_min_log2());
 }
 
 static bool debug_sync() {
@@ -673,7 +690,7 @@ struct Engine {
     }
     ++launches;
     if (dry || no_launch) return MK_OK;
-    if (leaf_slices() > 0) {  // INT8 tensor-core leaf; multi-term operands summed as they are split
+    if (ozaki_leaf_for(M, N, K)) {  // INT8 tensor-core leaf; multi-term operands summed as they are split
       std::vector<OzDest> od(p.nd);
       for (int i = 0; i < p.nd; ++i) od[i] = OzDest{p.d[i].row, p.d[i].col, p.d[i].sign, p.d[i].accumulate, 0};
       return ozaki_leaf(oz_operand(X), oz_operand(Y), bases[bd].ptr, bases[bd].ld, M, N, K, od.data(), p.nd);
@@ -1347,7 +1364,7 @@ struct Engine {
           }
         }
       }
-      if (leaf_slices() > 0) {  // INT8 tensor-core leaves: queued, run as one pipelined batch below
+      if (ozaki_leaf_for(lm, ln, lk)) {  // INT8 tensor-core leaves: queued, run as one pipelined batch below
         launches += (int)ents.size();
         if (dry || no_launch) continue;
         for (size_t gi = 0; gi < gr.size(); ++gi) {
@@ -1575,6 +1592,11 @@ int mk_set_option(int key, int value) {
     g_leaf_slices = value;
     return MK_OK;
   }
+  if (key == MK_OPT_LEAF_MIN_LOG2) {
+    if (value < 0 || value > 62) return fail(MK_ERR_ARG, "MK_OPT_LEAF_MIN_LOG2 takes 0..62");
+    g_leaf_min_log2 = value;
+    return MK_OK;
+  }
   return fail(MK_ERR_ARG, "unknown option key");
 }
 
@@ -1589,6 +1611,8 @@ int mk_get_option(int key, int* value) {
     *value = literal_bfs_tail() ? 1 : 0;
   } else if (key == MK_OPT_LEAF_SLICES) {
     *value = leaf_slices();
+  } else if (key == MK_OPT_LEAF_MIN_LOG2) {
+    *value = leaf_min_log2();
   } else {
     return fail(MK_ERR_ARG, "unknown option key");
   }

@@ -73,7 +73,7 @@ def set_plan(plan: str = "breadth-first", two_temp_tail: bool = True) -> None:
     _lib.check(lib.mk_set_option(_lib.MK_OPT_LITERAL_TAIL, 1 if two_temp_tail else 0), "mk_set_option")
 
 
-def set_leaf(kind: str = "dmma", slices: int = 8) -> None:
+def set_leaf(kind: str = "dmma", slices: int = 8, min_work: int = 2 ** 31) -> None:
     """Process-wide leaf arithmetic (B200 addition; the reference's leaf is np.matmul, kernels.py:261).
 
     ``"dmma"`` (default): every leaf product on the FP64 tensor cores (mma.sync f64 -> DMMA).
@@ -82,14 +82,20 @@ def set_leaf(kind: str = "dmma", slices: int = 8) -> None:
     the digit-pair products are exact int32 sums in tensor memory and are recombined in FP64.
     With 8 slices the leaf error is at or below the DMMA leaf's (56 digit bits vs 53); integer
     data is exact either way. Fewer slices trade accuracy for speed. Modeled OpCounter values
-    never change.
+    never change. ``min_work``: only leaf products with m*n*k >= min_work (rounded up to a power
+    of two; default 2^31, about 1290^3) use the INT8 kernels -- smaller leaves are launch- and
+    wave-bound there and stay on DMMA (0: every leaf).
     """
     if kind not in ("dmma", "ozaki"):
         raise ValueError(f"leaf must be 'dmma' or 'ozaki', got {kind!r}")
     if kind == "ozaki" and not (4 <= int(slices) <= 8):
         raise ValueError(f"slices must be in [4, 8], got {slices!r}")
+    if min_work < 0:
+        raise ValueError("min_work must be >= 0")
     lib = _lib.load(required=True)
     _lib.check(lib.mk_set_option(_lib.MK_OPT_LEAF_SLICES, int(slices) if kind == "ozaki" else 0), "mk_set_option")
+    log2 = 0 if min_work <= 1 else min(62, int(min_work - 1).bit_length())
+    _lib.check(lib.mk_set_option(_lib.MK_OPT_LEAF_MIN_LOG2, log2), "mk_set_option")
 
 
 def get_leaf() -> tuple:

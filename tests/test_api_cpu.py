@@ -232,6 +232,13 @@ def test_set_leaf_validates_and_round_trips():
         lib.mk_overlap_order(_lib.ALGO_IDS["winograd-block"], order, up)
         assert sorted(list(order)[:7]) == list(range(7)) and list(order)[:7] != dmma_order
         assert list(order)[0] == 0  # P1 = A11 B11 first: the fewest quadrants before any product
+        v = ctypes.c_int(-1)
+        assert lib.mk_get_option(_lib.MK_OPT_LEAF_MIN_LOG2, ctypes.byref(v)) == 0 and v.value == 31
+        pk.set_leaf("ozaki", 8, min_work=4096 ** 3)
+        assert lib.mk_get_option(_lib.MK_OPT_LEAF_MIN_LOG2, ctypes.byref(v)) == 0 and v.value == 36
+        pk.set_leaf("ozaki", 8, min_work=0)
+        assert lib.mk_get_option(_lib.MK_OPT_LEAF_MIN_LOG2, ctypes.byref(v)) == 0 and v.value == 0
+        assert lib.mk_set_option(_lib.MK_OPT_LEAF_MIN_LOG2, 63) == _lib.MK_ERR_ARG
     finally:
         pk.set_leaf("dmma")
     assert pk.get_leaf() == ("dmma", 0)

@@ -22,7 +22,7 @@ pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not has_gpu(), reason="needs a
 def leaf(request):
     import paper_2309_00628_b200 as pk
 
-    pk.set_leaf(request.param, 8) if request.param == "ozaki" else pk.set_leaf("dmma")
+    pk.set_leaf(request.param, 8, min_work=0) if request.param == "ozaki" else pk.set_leaf("dmma")
     yield request.param
     pk.set_leaf("dmma")
 
@@ -85,7 +85,7 @@ def _ipc_worker(rank, world, port, levels, exact, result_path, leaf="dmma"):
     from paper_2309_00628_b200 import multigpu as mg
 
     if leaf == "ozaki":
-        pk.set_leaf("ozaki", 8)
+        pk.set_leaf("ozaki", 8, min_work=0)
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)

@@ -20,7 +20,7 @@ pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not has_gpu(), reason="needs a
 
 @pytest.fixture(autouse=True)
 def ozaki_leaves():
-    pk.set_leaf("ozaki", 8)
+    pk.set_leaf("ozaki", 8, min_work=0)  # every leaf, however small, on the INT8 kernels
     assert pk.get_leaf() == ("ozaki", 8)
     yield
     pk.set_leaf("dmma")
