@@ -68,7 +68,7 @@ int mk_version(void);
  *   INT8 tensor cores (tcgen05 kind::i8, Ozaki scheme I) with that many 7-bit digit slices per
  *   operand (see mk_ozaki_dgemm; 8 is as accurate as the DMMA leaf, fewer trade accuracy for speed).
  *   Applies to every leaf product of the engine with m*n*k >= 2^MK_OPT_LEAF_MIN_LOG2.
- * MK_OPT_LEAF_MIN_LOG2: the INT8 leaf's size threshold, log2 of m*n*k (default 31, about 1290^3):
+ * MK_OPT_LEAF_MIN_LOG2: the INT8 leaf's size threshold, log2 of m*n*k (default 29, about 812^3):
  *   smaller leaves stay on DMMA (the per-leaf INT8 kernels are launch- and wave-bound there). */
 enum mk_option { MK_OPT_FUSE_PREADDS = 1, MK_OPT_PLAN = 2, MK_OPT_LITERAL_TAIL = 3, MK_OPT_LEAF_SLICES = 4,
                  MK_OPT_LEAF_MIN_LOG2 = 5 };

@@ -326,16 +326,17 @@ static int leaf_slices() {
   }
   return g_leaf_slices;
 }
-// MK_OPT_LEAF_MIN_LOG2: INT8 leaves only for products with m*n*k >= 2^v (default 31, about 1290^3;
-// env MK_LEAF_MIN_LOG2): smaller leaves are launch- and wave-bound on the per-leaf INT8 kernels
-// (n = 8192 at 1024^3 leaves: 32.4 ms INT8 vs 24.2 ms DMMA; cfg5 at ~1500 x 1750 x 1250 leaves:
-// 57 vs 77 ms; 4096^3: 1.9x faster) and stay DMMA.
+// MK_OPT_LEAF_MIN_LOG2: INT8 leaves only for products with m*n*k >= 2^v (default 29, about 812^3;
+// env MK_LEAF_MIN_LOG2). Breadth-first levels run their INT8 leaves as batches (one split launch
+// per kernel, one product launch per colour group); measured (tools/leaf_compare.py): 256^3
+// leaves 6.2 ms INT8 vs 4.3 DMMA, 512^3 24.3 vs 24.2 (break-even), 1024^3 15.9 vs 24.2,
+// 2048^3 99.7 vs 177.5 -- smaller leaves stay on DMMA.
 static std::atomic<int> g_leaf_min_log2{-1};
 static int leaf_min_log2() {
   if (g_leaf_min_log2 < 0) {
     const char* e = getenv("MK_LEAF_MIN_LOG2");
-    const int v = e ? atoi(e) : 31;
-    g_leaf_min_log2 = (v >= 0 && v <= 62) ? v : 31;
+    const int v = e ? atoi(e) : 29;
+    g_leaf_min_log2 = (v >= 0 && v <= 62) ? v : 29;
   }
   return g_leaf_min_log2;
 }
@@ -1312,6 +1313,7 @@ struct Engine {
     }
     std::vector<MkBatchEntry> ents;
     std::vector<OzItem> oz_items;
+    int64_t oz_groups = 0;
     for (const auto& gr : groups) {
       struct Dests {
         MkDest dt[4];
@@ -1380,11 +1382,13 @@ struct Engine {
             it.n = ln;
             it.k = lk;
             it.nd = e.prod.nd;
+            it.group = (int)oz_groups;
             for (int k = 0; k < e.prod.nd; ++k)
               it.d[k] = OzDest{e.prod.d[k].row, e.prod.d[k].col, e.prod.d[k].sign, e.prod.d[k].accumulate, 0};
             oz_items.push_back(it);
           }
         }
+        ++oz_groups;
         continue;
       }
       const int nprod_launch = (int)ents.size();

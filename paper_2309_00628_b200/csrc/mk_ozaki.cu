@@ -355,8 +355,23 @@ __device__ __forceinline__ void map_tile(const Args& a, int t, int& tm, int& tn)
   tn = local / rows;
 }
 
-template <int S>
-__global__ void __launch_bounds__(PT_THREADS, 1) ozaki_persistent_kernel(const __grid_constant__ Args a, int tiles) {
+// Item lookup for the batched form: the tiles of item i are [tile_start[i], tile_start[i+1]).
+__device__ __forceinline__ int find_item(const int* __restrict__ tile_start, int nitems, int t) {
+  int lo = 0, hi = nitems - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(tile_start + mid) <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// BATCH: the tiles of several products (one colour group of leaves: disjoint destinations) in
+// one launch, each product's Args in global memory; otherwise one product, Args by value.
+template <int S, bool BATCH>
+__global__ void __launch_bounds__(PT_THREADS, 1)
+    ozaki_persistent_kernel(const __grid_constant__ Args a0, const Args* __restrict__ items,
+                            const int* __restrict__ tile_start, int nitems, int tiles) {
   constexpr int A_TILE = BM * BK;
   constexpr int B_TILE = BN * BK;
   constexpr int STAGE_BYTES = S * (A_TILE + B_TILE);
@@ -368,8 +383,18 @@ __global__ void __launch_bounds__(PT_THREADS, 1) ozaki_persistent_kernel(const _
   uint64_t* tmem_empty = tmem_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
 
+  // (item args, tile index inside the item) of global tile t
+  auto item_of = [&](int t, int& lt) -> const Args& {
+    if (!BATCH) {
+      lt = t;
+      return a0;
+    }
+    const int i = find_item(tile_start, nitems, t);
+    lt = t - __ldg(tile_start + i);
+    return items[i];
+  };
+
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nkb = (a.K + BK - 1) / BK;
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
@@ -389,8 +414,11 @@ __global__ void __launch_bounds__(PT_THREADS, 1) ozaki_persistent_kernel(const _
     if (lane == 0) {
       int it = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        int lt;
+        const Args& a = item_of(t, lt);
         int tm, tn;
-        map_tile(a, t, tm, tn);
+        map_tile(a, lt, tm, tn);
+        const int nkb = (a.K + BK - 1) / BK;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int st = it % STAGES;
           if (it >= STAGES) mbar_wait(&empty[st], ((it / STAGES) - 1) & 1);
@@ -405,6 +433,9 @@ __global__ void __launch_bounds__(PT_THREADS, 1) ozaki_persistent_kernel(const _
     if (lane == 0) {
       int it = 0, ti = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++ti) {
+        int lt;
+        const Args& a = item_of(t, lt);
+        const int nkb = (a.K + BK - 1) / BK;
         if (ti > 0) {  // the epilogue has drained the previous tile's accumulators
           mbar_wait(tmem_empty, (ti - 1) & 1);
           tmem_fence_after();
@@ -436,8 +467,10 @@ __global__ void __launch_bounds__(PT_THREADS, 1) ozaki_persistent_kernel(const _
     const int q = warp & 3, half = (warp - 2) >> 2;
     int ti = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++ti) {
+      int lt;
+      const Args& a = item_of(t, lt);
       int tm, tn;
-      map_tile(a, t, tm, tn);
+      map_tile(a, lt, tm, tn);
       const int row = tm * BM + q * 32 + lane;
       const bool row_ok = row < a.M;
       const int e = row_ok ? a.ex[row] : 0;
@@ -594,7 +627,7 @@ __device__ __forceinline__ double term_sum(const OzOperand& o, int64_t r, int64_
 // Row maxima of X as IEEE bit patterns (monotone for |x|; inf / nan -> +inf): one warp per
 // (row, 1024-wide k chunk), 8 independent loads in flight per lane, one atomicMax per warp.
 template <int NT>
-__global__ void rowmax_kernel(const OzOperand X, int rows, int K, unsigned long long* __restrict__ rmax) {
+__device__ __forceinline__ void rowmax_body(const OzOperand& X, int rows, int K, unsigned long long* __restrict__ rmax) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= rows) return;
   const int k0 = blockIdx.y * 1024, k1 = min(K, k0 + 1024);
@@ -623,7 +656,7 @@ __global__ void rowmax_kernel(const OzOperand X, int rows, int K, unsigned long 
 // ([tile_m][kb][S][128 x 32 B], swizzled): one warp per row (rows up to the padded tile edge
 // write zeros), each lane 4 consecutive k per step, 4 steps in flight.
 template <int S, int NT>
-__global__ void split_rows_kernel(const OzOperand X, int rows, int rows_pad, int K, int nkb,
+__device__ __forceinline__ void split_rows_body(const OzOperand& X, int rows, int rows_pad, int K, int nkb,
                                   const unsigned long long* __restrict__ rmax, int32_t* __restrict__ ex,
                                   int32_t* __restrict__ rs, uint8_t* __restrict__ planes) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -662,7 +695,7 @@ __global__ void split_rows_kernel(const OzOperand X, int rows, int rows_pad, int
 
 // Column maxima of Y (k x n) as IEEE bit patterns (monotone for |y|): grid (n/256, k/64).
 template <int NT>
-__global__ void colmax_kernel(const OzOperand Y, int K, int N, unsigned long long* __restrict__ cmax) {
+__device__ __forceinline__ void colmax_body(const OzOperand& Y, int K, int N, unsigned long long* __restrict__ cmax) {
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= N) return;
   const int k0 = blockIdx.y * 64, k1 = min(K, k0 + 64);
@@ -686,7 +719,7 @@ __global__ void colmax_kernel(const OzOperand Y, int K, int N, unsigned long lon
   atomicMax(&cmax[col], bits);
 }
 
-__global__ void colexp_kernel(const unsigned long long* __restrict__ cmax, int N, int32_t* __restrict__ fy) {
+__device__ __forceinline__ void colexp_body(const unsigned long long* __restrict__ cmax, int N, int32_t* __restrict__ fy) {
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= N) return;
   fy[col] = row_exponent(__longlong_as_double((long long)cmax[col]));
@@ -696,7 +729,7 @@ __global__ void colexp_kernel(const unsigned long long* __restrict__ cmax, int N
 // ([tile_n][kb][S][64 x 32 B], swizzled; K-major for the B operand), 32 x 32 tiles through shared
 // memory. Block (32, 8); the grid covers the padded tile edges (zeros).
 template <int S, int NT>
-__global__ void split_cols_kernel(const OzOperand Y, int K, int N, int nkb, const int32_t* __restrict__ fy,
+__device__ __forceinline__ void split_cols_body(const OzOperand& Y, int K, int N, int nkb, const int32_t* __restrict__ fy,
                                   uint8_t* __restrict__ planes) {
   __shared__ uint32_t sm[S][32][9];  // [plane][col][k/4] (+1 pad)
   const int n0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
@@ -728,6 +761,71 @@ __global__ void split_cols_kernel(const OzOperand Y, int K, int N, int nkb, cons
   uint8_t* dst = planes + ((int64_t)(n / BN) * nkb + k0 / BK) * (S * BN * BK) + swz32(n % BN, 4 * wi);
 #pragma unroll
   for (int s = 0; s < S; ++s) *reinterpret_cast<uint32_t*>(dst + s * (BN * BK)) = sm[s][r][wi];
+}
+
+// Kernels: one product's operands (grid-constant parameters), or a batch of equally shaped
+// products (one job per blockIdx.z) -- the leaves of a breadth-first level split with one launch
+// per kernel instead of one per leaf.
+struct SplitJob {
+  OzOperand X, Y;
+  unsigned long long *rmax, *cmax;
+  int32_t *ex, *fy, *rs;
+  uint8_t *px, *py;
+};
+
+template <int NT>
+__global__ void rowmax_kernel(const OzOperand X, int rows, int K, unsigned long long* __restrict__ rmax) {
+  rowmax_body<NT>(X, rows, K, rmax);
+}
+template <int S, int NT>
+__global__ void split_rows_kernel(const OzOperand X, int rows, int rows_pad, int K, int nkb,
+                                  const unsigned long long* __restrict__ rmax, int32_t* __restrict__ ex,
+                                  int32_t* __restrict__ rs, uint8_t* __restrict__ planes) {
+  split_rows_body<S, NT>(X, rows, rows_pad, K, nkb, rmax, ex, rs, planes);
+}
+template <int NT>
+__global__ void colmax_kernel(const OzOperand Y, int K, int N, unsigned long long* __restrict__ cmax) {
+  colmax_body<NT>(Y, K, N, cmax);
+}
+__global__ void colexp_kernel(const unsigned long long* __restrict__ cmax, int N, int32_t* __restrict__ fy) {
+  colexp_body(cmax, N, fy);
+}
+template <int S, int NT>
+__global__ void split_cols_kernel(const OzOperand Y, int K, int N, int nkb, const int32_t* __restrict__ fy,
+                                  uint8_t* __restrict__ planes) {
+  split_cols_body<S, NT>(Y, K, N, nkb, fy, planes);
+}
+
+__global__ void zero_max_batch(const SplitJob* __restrict__ jobs, int rows, int cols) {
+  const SplitJob& j = jobs[blockIdx.y];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows || i < cols; i += gridDim.x * blockDim.x) {
+    if (i < rows) j.rmax[i] = 0;
+    if (i < cols) j.cmax[i] = 0;
+  }
+}
+template <int NT>
+__global__ void rowmax_batch(const SplitJob* __restrict__ jobs, int rows, int K) {
+  const SplitJob& j = jobs[blockIdx.z];
+  rowmax_body<NT>(j.X, rows, K, j.rmax);
+}
+template <int S, int NT>
+__global__ void split_rows_batch(const SplitJob* __restrict__ jobs, int rows, int rows_pad, int K, int nkb) {
+  const SplitJob& j = jobs[blockIdx.z];
+  split_rows_body<S, NT>(j.X, rows, rows_pad, K, nkb, j.rmax, j.ex, j.rs, j.px);
+}
+template <int NT>
+__global__ void colmax_batch(const SplitJob* __restrict__ jobs, int K, int N) {
+  const SplitJob& j = jobs[blockIdx.z];
+  colmax_body<NT>(j.Y, K, N, j.cmax);
+}
+__global__ void colexp_batch(const SplitJob* __restrict__ jobs, int N) {
+  const SplitJob& j = jobs[blockIdx.z];
+  colexp_body(j.cmax, N, j.fy);
+}
+template <int S, int NT>
+__global__ void split_cols_batch(const SplitJob* __restrict__ jobs, int K, int N, int nkb) {
+  const SplitJob& j = jobs[blockIdx.z];
+  split_cols_body<S, NT>(j.Y, K, N, nkb, j.fy, j.py);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -814,22 +912,16 @@ static void split_phase(const OzOperand& X, const OzOperand& Y, int64_t m, int64
   }
 }
 
-// One K chunk, phase 2: the product kernel from ws's digit planes into every destination.
-template <int S>
-static int product_phase(double* C, int64_t ldc, int64_t m, int64_t n, int64_t k, const OzDest* d, int nd,
-                         uint8_t* ws, cudaStream_t st, std::string* err, const OzSlabs* slabs = nullptr) {
+// Kernel arguments of one product whose digit planes / exponents / row sums live in ws.
+static Args make_args(int S, double* C, int64_t ldc, int64_t m, int64_t n, int64_t k, const OzDest* d, int nd,
+                      uint8_t* ws, const OzSlabs* slabs) {
   const Layout L = layout(m, n, k, S);
-  uint8_t* px = ws + L.planes_x;
-  uint8_t* py = ws + L.planes_y;
-  int32_t* ex = reinterpret_cast<int32_t*>(ws + L.ex);
-  int32_t* fy = reinterpret_cast<int32_t*>(ws + L.fy);
-  int32_t* rs = reinterpret_cast<int32_t*>(ws + L.rs);
-  Args a;
-  a.px = px;
-  a.py = py;
-  a.ex = ex;
-  a.fy = fy;
-  a.rs = rs;
+  Args a{};
+  a.px = ws + L.planes_x;
+  a.py = ws + L.planes_y;
+  a.ex = reinterpret_cast<int32_t*>(ws + L.ex);
+  a.fy = reinterpret_cast<int32_t*>(ws + L.fy);
+  a.rs = reinterpret_cast<int32_t*>(ws + L.rs);
   a.C = C;
   a.ldc = ldc;
   a.M = (int)m;
@@ -840,6 +932,39 @@ static int product_phase(double* C, int64_t ldc, int64_t m, int64_t n, int64_t k
   a.pad_ = 0;
   for (int i = 0; i < nd; ++i) a.d[i] = d[i];
   a.slabs = slabs ? *slabs : OzSlabs{0, 1, {nullptr}};
+  a.trace = nullptr;
+  return a;
+}
+
+// Several products (disjoint destinations: one colour group of leaves) in one persistent launch;
+// args_dev / tile_start_dev already on the device.
+template <int S>
+static int product_batch_launch(const Args* args_dev, const int* tile_start_dev, int nitems, int tiles,
+                                cudaStream_t st, std::string* err) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t psmem = smem_bytes<S>() + 8;
+  cudaError_t e = cudaFuncSetAttribute(ozaki_persistent_kernel<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)psmem);
+  if (e == cudaSuccess) {
+    Args dummy{};
+    ozaki_persistent_kernel<S, true><<<std::min(tiles, sms), PT_THREADS, psmem, st>>>(dummy, args_dev, tile_start_dev,
+                                                                                       nitems, tiles);
+    e = cudaGetLastError();
+  }
+  if (e != cudaSuccess) {
+    *err = std::string("ozaki_persistent_kernel (batch) launch: ") + cudaGetErrorString(e);
+    return MK_ERR_CUDA;
+  }
+  return MK_OK;
+}
+
+// One K chunk, phase 2: the product kernel from ws's digit planes into every destination.
+template <int S>
+static int product_phase(double* C, int64_t ldc, int64_t m, int64_t n, int64_t k, const OzDest* d, int nd,
+                         uint8_t* ws, cudaStream_t st, std::string* err, const OzSlabs* slabs = nullptr) {
+  Args a = make_args(S, C, ldc, m, n, k, d, nd, ws, slabs);
   const int tiles = (int)((m + BM - 1) / BM) * a.tiles_n;
   const size_t smem = smem_bytes<S>();
   // per launch (the attribute is per device; the call is cheap next to a leaf product)
@@ -856,13 +981,13 @@ static int product_phase(double* C, int64_t ldc, int64_t m, int64_t n, int64_t k
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const size_t psmem = smem + 8;
-    cudaError_t pe = cudaFuncSetAttribute(ozaki_persistent_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)psmem);
+    cudaError_t pe = cudaFuncSetAttribute(ozaki_persistent_kernel<S, false>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
     if (pe != cudaSuccess) {
       *err = std::string("ozaki_persistent_kernel smem attribute: ") + cudaGetErrorString(pe);
       return MK_ERR_CUDA;
     }
-    ozaki_persistent_kernel<S><<<std::min(tiles, sms), PT_THREADS, psmem, st>>>(a, tiles);
+    ozaki_persistent_kernel<S, false><<<std::min(tiles, sms), PT_THREADS, psmem, st>>>(a, nullptr, nullptr, 1, tiles);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
       *err = std::string("ozaki_persistent_kernel launch: ") + cudaGetErrorString(e);
@@ -924,6 +1049,59 @@ static void split_any(int S, const OzOperand& X, const OzOperand& Y, int64_t m, 
     case 6: split_phase<6>(X, Y, m, n, k, ws, st); break;
     case 7: split_phase<7>(X, Y, m, n, k, ws, st); break;
     default: split_phase<8>(X, Y, m, n, k, ws, st); break;
+  }
+}
+// Digit splitting of `nitems` equally shaped single-term products in one launch per kernel.
+template <int S>
+static void split_batch_phase(const SplitJob* jobs, int64_t m, int64_t n, int64_t k, int nitems, cudaStream_t st) {
+  const int64_t kp = kpad(k), nkb = kp / BK;
+  const int64_t tiles_m = (m + BM - 1) / BM, tiles_n = (n + BN - 1) / BN;
+  const unsigned z = (unsigned)nitems;
+  zero_max_batch<<<dim3((unsigned)((std::max(m, n) + 255) / 256), z), 256, 0, st>>>(jobs, (int)m, (int)n);
+  rowmax_batch<1><<<dim3((unsigned)((m * 32 + 127) / 128), (unsigned)((k + 1023) / 1024), z), 128, 0, st>>>(
+      jobs, (int)m, (int)k);
+  split_rows_batch<S, 1><<<dim3((unsigned)((tiles_m * BM * 32 + 127) / 128), 1, z), 128, 0, st>>>(
+      jobs, (int)m, (int)(tiles_m * BM), (int)k, (int)nkb);
+  colmax_batch<1><<<dim3((unsigned)((n + 127) / 128), (unsigned)((k + 63) / 64), z), 128, 0, st>>>(jobs, (int)k,
+                                                                                                    (int)n);
+  colexp_batch<<<dim3((unsigned)((n + 255) / 256), 1, z), 256, 0, st>>>(jobs, (int)n);
+  split_cols_batch<S, 1><<<dim3((unsigned)(tiles_n * BN / 32), (unsigned)nkb, z), dim3(32, 8), 0, st>>>(
+      jobs, (int)k, (int)n, (int)nkb);
+}
+static void split_batch_any(int S, const SplitJob* jobs, int64_t m, int64_t n, int64_t k, int nitems,
+                            cudaStream_t st) {
+  switch (S) {
+    case 4: split_batch_phase<4>(jobs, m, n, k, nitems, st); break;
+    case 5: split_batch_phase<5>(jobs, m, n, k, nitems, st); break;
+    case 6: split_batch_phase<6>(jobs, m, n, k, nitems, st); break;
+    case 7: split_batch_phase<7>(jobs, m, n, k, nitems, st); break;
+    default: split_batch_phase<8>(jobs, m, n, k, nitems, st); break;
+  }
+}
+static SplitJob split_job(int S, const OzOperand& X, const OzOperand& Y, int64_t m, int64_t n, int64_t k,
+                          uint8_t* ws) {
+  const Layout L = layout(m, n, k, S);
+  SplitJob j;
+  j.X = X;
+  j.Y = Y;
+  j.rmax = reinterpret_cast<unsigned long long*>(ws + L.rmax);
+  j.cmax = reinterpret_cast<unsigned long long*>(ws + L.cmax);
+  j.ex = reinterpret_cast<int32_t*>(ws + L.ex);
+  j.fy = reinterpret_cast<int32_t*>(ws + L.fy);
+  j.rs = reinterpret_cast<int32_t*>(ws + L.rs);
+  j.px = ws + L.planes_x;
+  j.py = ws + L.planes_y;
+  return j;
+}
+
+static int batch_launch_any(int S, const Args* args_dev, const int* tile_start_dev, int nitems, int tiles,
+                            cudaStream_t st, std::string* err) {
+  switch (S) {
+    case 4: return product_batch_launch<4>(args_dev, tile_start_dev, nitems, tiles, st, err);
+    case 5: return product_batch_launch<5>(args_dev, tile_start_dev, nitems, tiles, st, err);
+    case 6: return product_batch_launch<6>(args_dev, tile_start_dev, nitems, tiles, st, err);
+    case 7: return product_batch_launch<7>(args_dev, tile_start_dev, nitems, tiles, st, err);
+    default: return product_batch_launch<8>(args_dev, tile_start_dev, nitems, tiles, st, err);
   }
 }
 static int product_any(int S, double* C, int64_t ldc, int64_t m, int64_t n, int64_t k, const OzDest* d, int nd,
@@ -1006,6 +1184,21 @@ int ozaki_product(const double* X, int64_t ldx, const double* Y, int64_t ldy, do
   return oz::product_chunks(ox, oy, C, ldc, m, n, k, slices, &dst, 1, static_cast<uint8_t*>(ws), st, err);
 }
 
+// Per thread and device: the side stream the digit splitting runs on beside the product kernels.
+static cudaStream_t side_stream(int dev) {
+  static thread_local std::map<int, cudaStream_t> side_streams;
+  auto itx = side_streams.find(dev);
+  if (itx == side_streams.end()) {
+    cudaStream_t s2;
+    if (cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaGetLastError();
+      s2 = nullptr;
+    }
+    itx = side_streams.emplace(dev, s2).first;
+  }
+  return itx->second;
+}
+
 static void keep_pool_memory() {  // freed leaf workspaces stay in the stream-ordered pool
   static thread_local int pool_dev = -1;
   int dev = 0;
@@ -1019,6 +1212,116 @@ static void keep_pool_memory() {  // freed leaf workspaces stay in the stream-or
   }
 }
 
+// Grouped form of ozaki_product_batch (every item one K chunk): the items of a launch group (equal
+// OzItem::group, disjoint destinations) are split into one workspace and multiplied by ONE
+// persistent launch over all their tiles -- small leaves fill the GPU together; the next group's
+// splitting runs on the side stream meanwhile (two group workspaces).
+static int batch_grouped(const OzItem* items, int count, int slices, cudaStream_t st, cudaStream_t side,
+                         std::string* err) {
+  constexpr size_t kMaxGroupBytes = size_t(4) << 30;
+  struct Grp {
+    int b, e;
+    size_t bytes;
+  };
+  std::vector<Grp> groups;
+  for (int i = 0; i < count; ++i) {
+    const size_t wb = oz::align256(ozaki_workspace_bytes(items[i].m, items[i].n, items[i].k, slices));
+    if (groups.empty() || items[i].group != items[groups.back().b].group || groups.back().bytes + wb > kMaxGroupBytes)
+      groups.push_back(Grp{i, i, 0});
+    groups.back().e = i + 1;
+    groups.back().bytes += wb;
+  }
+  size_t maxb = 0;
+  for (const Grp& g : groups) maxb = std::max(maxb, g.bytes);
+  const int nbuf = (groups.size() > 1 && side) ? 2 : 1;
+  uint8_t* ws[2] = {nullptr, nullptr};
+  for (int b = 0; b < nbuf; ++b) {
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ws[b]), maxb, st);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      for (int j = 0; j < b; ++j) cudaFreeAsync(ws[j], st);
+      *err = std::string("Ozaki batch workspace: ") + cudaGetErrorString(e);
+      return e == cudaErrorMemoryAllocation ? MK_ERR_WORKSPACE : MK_ERR_CUDA;
+    }
+  }
+  cudaEvent_t start = nullptr, split_ev[2] = {nullptr, nullptr}, prod_ev[2] = {nullptr, nullptr};
+  auto mkev = [](cudaEvent_t* e) { return cudaEventCreateWithFlags(e, cudaEventDisableTiming); };
+  if (nbuf == 2) {
+    if (mkev(&start) || mkev(&split_ev[0]) || mkev(&split_ev[1]) || mkev(&prod_ev[0]) || mkev(&prod_ev[1])) {
+      cudaGetLastError();
+      side = nullptr;
+    } else {
+      cudaEventRecord(start, st);
+      cudaStreamWaitEvent(side, start, 0);
+    }
+  }
+  const bool use_side = nbuf == 2 && side;
+  int rc = MK_OK;
+  for (size_t gi = 0; gi < groups.size() && rc == MK_OK; ++gi) {
+    const Grp& g = groups[gi];
+    const int b = (int)(gi % nbuf);
+    cudaStream_t ss = use_side ? side : st;
+    if (use_side && gi >= 2) cudaStreamWaitEvent(side, prod_ev[b], 0);
+    std::vector<oz::Args> args(g.e - g.b);
+    std::vector<int> tstart(g.e - g.b + 1, 0);
+    std::vector<oz::SplitJob> jobs;
+    bool uniform = true;  // equal shapes, single-term operands: one split launch per kernel
+    for (int i = g.b; i < g.e; ++i)
+      uniform = uniform && items[i].m == items[g.b].m && items[i].n == items[g.b].n && items[i].k == items[g.b].k &&
+                items[i].X.n == 1 && items[i].Y.n == 1;
+    size_t off = 0;
+    for (int i = g.b; i < g.e; ++i) {
+      const OzItem& it = items[i];
+      uint8_t* w = ws[b] + off;
+      off += oz::align256(ozaki_workspace_bytes(it.m, it.n, it.k, slices));
+      if (uniform)
+        jobs.push_back(oz::split_job(slices, it.X, it.Y, it.m, it.n, it.k, w));
+      else
+        oz::split_any(slices, it.X, it.Y, it.m, it.n, it.k, w, ss);
+      args[i - g.b] = oz::make_args(slices, it.C, it.ldc, it.m, it.n, it.k, it.d, it.nd, w, nullptr);
+      const int tiles_i = (int)((it.m + oz::BM - 1) / oz::BM) * args[i - g.b].tiles_n;
+      tstart[i - g.b + 1] = tstart[i - g.b] + tiles_i;
+    }
+    if (uniform) {
+      void* jd = nullptr;
+      cudaError_t je = cudaMallocAsync(&jd, sizeof(oz::SplitJob) * jobs.size(), ss);
+      if (je == cudaSuccess)
+        je = cudaMemcpyAsync(jd, jobs.data(), sizeof(oz::SplitJob) * jobs.size(), cudaMemcpyHostToDevice, ss);
+      if (je != cudaSuccess) {
+        *err = std::string("Ozaki split jobs: ") + cudaGetErrorString(je);
+        rc = MK_ERR_CUDA;
+        break;
+      }
+      oz::split_batch_any(slices, static_cast<const oz::SplitJob*>(jd), items[g.b].m, items[g.b].n, items[g.b].k,
+                          (int)jobs.size(), ss);
+      cudaFreeAsync(jd, ss);
+    }
+    if (use_side) {
+      cudaEventRecord(split_ev[b], side);
+      cudaStreamWaitEvent(st, split_ev[b], 0);
+    }
+    const int n_it = g.e - g.b, tiles = tstart[n_it];
+    void* dev = nullptr;
+    const size_t abytes = sizeof(oz::Args) * n_it, tbytes = sizeof(int) * (n_it + 1);
+    cudaError_t e = cudaMallocAsync(&dev, abytes + tbytes + 256, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dev, args.data(), abytes, cudaMemcpyHostToDevice, st);
+    int* tdev = reinterpret_cast<int*>(static_cast<char*>(dev) + ((abytes + 255) / 256) * 256);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(tdev, tstart.data(), tbytes, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) {
+      *err = std::string("Ozaki batch arguments: ") + cudaGetErrorString(e);
+      rc = MK_ERR_CUDA;
+      break;
+    }
+    rc = oz::batch_launch_any(slices, static_cast<const oz::Args*>(dev), tdev, n_it, tiles, st, err);
+    cudaFreeAsync(dev, st);
+    if (use_side) cudaEventRecord(prod_ev[b], st);
+  }
+  for (int b = 0; b < nbuf; ++b) cudaFreeAsync(ws[b], st);
+  for (cudaEvent_t ev : {start, split_ev[0], split_ev[1], prod_ev[0], prod_ev[1]})
+    if (ev) cudaEventDestroy(ev);
+  return rc;
+}
+
 int ozaki_product_batch(const OzItem* items, int count, int slices, cudaStream_t st, std::string* err) {
   if (count <= 0) return MK_OK;
   struct Sub {
@@ -1028,6 +1331,7 @@ int ozaki_product_batch(const OzItem* items, int count, int slices, cudaStream_t
   };
   std::vector<Sub> subs;
   size_t wsb = 0;
+  bool one_chunk = true;
   for (int i = 0; i < count; ++i) {
     const OzItem& it = items[i];
     if (int rc = check_args(it.m, it.n, slices, it.nd, err)) return rc;
@@ -1035,6 +1339,17 @@ int ozaki_product_batch(const OzItem* items, int count, int slices, cudaStream_t
       *err = "internal: operand term count out of range";
       return MK_ERR_ARG;
     }
+    one_chunk = one_chunk && it.k <= oz::chunk_k(it.k, slices);
+  }
+  static const bool grouped_on = !(getenv("MK_OZ_GROUPED") && getenv("MK_OZ_GROUPED")[0] == '0');
+  if (grouped_on && one_chunk && count > 1) {
+    keep_pool_memory();
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return batch_grouped(items, count, slices, st, side_stream(dev), err);
+  }
+  for (int i = 0; i < count; ++i) {
+    const OzItem& it = items[i];
     const int64_t kc = oz::chunk_k(it.k, slices);
     for (int64_t k0 = 0; k0 < it.k; k0 += kc) subs.push_back(Sub{&it, k0, std::min(kc, it.k - k0), k0 == 0});
     wsb = std::max(wsb, ozaki_workspace_bytes(it.m, it.n, it.k, slices));
@@ -1053,22 +1368,9 @@ int ozaki_product_batch(const OzItem* items, int count, int slices, cudaStream_t
   }
   // Splitting (HBM bound) of item i+1 runs on a side stream while the product kernel of item i
   // (tensor bound) runs on st: two workspaces, events in both directions.
-  static thread_local std::map<int, cudaStream_t> side_streams;
   int dev = 0;
   cudaGetDevice(&dev);
-  cudaStream_t side = nullptr;
-  if (nbuf == 2) {
-    auto itx = side_streams.find(dev);
-    if (itx == side_streams.end()) {
-      cudaStream_t s2;
-      if (cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) != cudaSuccess) {
-        cudaGetLastError();
-        s2 = nullptr;
-      }
-      itx = side_streams.emplace(dev, s2).first;
-    }
-    side = itx->second;
-  }
+  cudaStream_t side = nbuf == 2 ? side_stream(dev) : nullptr;
   cudaEvent_t start = nullptr, split_ev[2] = {nullptr, nullptr}, prod_ev[2] = {nullptr, nullptr};
   auto mkev = [](cudaEvent_t* e) { return cudaEventCreateWithFlags(e, cudaEventDisableTiming); };
   if (side) {

@@ -75,6 +75,7 @@ struct OzItem {
   double* C;
   int64_t ldc, m, n, k;
   int nd;
+  int group;  // items of one group have disjoint destinations and may share one launch
   OzDest d[kOzMaxDests];
 };
 int ozaki_product_batch(const OzItem* items, int count, int slices, cudaStream_t st, std::string* err);

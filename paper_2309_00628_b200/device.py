@@ -73,7 +73,7 @@ def set_plan(plan: str = "breadth-first", two_temp_tail: bool = True) -> None:
     _lib.check(lib.mk_set_option(_lib.MK_OPT_LITERAL_TAIL, 1 if two_temp_tail else 0), "mk_set_option")
 
 
-def set_leaf(kind: str = "dmma", slices: int = 8, min_work: int = 2 ** 31) -> None:
+def set_leaf(kind: str = "dmma", slices: int = 8, min_work: int = 2 ** 29) -> None:
     """Process-wide leaf arithmetic (B200 addition; the reference's leaf is np.matmul, kernels.py:261).
 
     ``"dmma"`` (default): every leaf product on the FP64 tensor cores (mma.sync f64 -> DMMA).
@@ -83,7 +83,7 @@ def set_leaf(kind: str = "dmma", slices: int = 8, min_work: int = 2 ** 31) -> No
     With 8 slices the leaf error is at or below the DMMA leaf's (56 digit bits vs 53); integer
     data is exact either way. Fewer slices trade accuracy for speed. Modeled OpCounter values
     never change. ``min_work``: only leaf products with m*n*k >= min_work (rounded up to a power
-    of two; default 2^31, about 1290^3) use the INT8 kernels -- smaller leaves are launch- and
+    of two; default 2^29, about 812^3) use the INT8 kernels -- smaller leaves are launch- and
     wave-bound there and stay on DMMA (0: every leaf).
     """
     if kind not in ("dmma", "ozaki"):

@@ -233,7 +233,7 @@ def test_set_leaf_validates_and_round_trips():
         assert sorted(list(order)[:7]) == list(range(7)) and list(order)[:7] != dmma_order
         assert list(order)[0] == 0  # P1 = A11 B11 first: the fewest quadrants before any product
         v = ctypes.c_int(-1)
-        assert lib.mk_get_option(_lib.MK_OPT_LEAF_MIN_LOG2, ctypes.byref(v)) == 0 and v.value == 31
+        assert lib.mk_get_option(_lib.MK_OPT_LEAF_MIN_LOG2, ctypes.byref(v)) == 0 and v.value == 29
         pk.set_leaf("ozaki", 8, min_work=4096 ** 3)
         assert lib.mk_get_option(_lib.MK_OPT_LEAF_MIN_LOG2, ctypes.byref(v)) == 0 and v.value == 36
         pk.set_leaf("ozaki", 8, min_work=0)
