@@ -1341,8 +1341,13 @@ int ozaki_product_batch(const OzItem* items, int count, int slices, cudaStream_t
     }
     one_chunk = one_chunk && it.k <= oz::chunk_k(it.k, slices);
   }
-  static const bool grouped_on = !(getenv("MK_OZ_GROUPED") && getenv("MK_OZ_GROUPED")[0] == '0');
-  if (grouped_on && one_chunk && count > 1) {
+  // Grouped launches pay off for small and medium leaves (fewer, fuller launches); for big leaves
+  // (>= 2^34 work, e.g. the bench's 4096^3) the per-item pipeline overlaps splitting better.
+  static const int grouped_mode = getenv("MK_OZ_GROUPED") ? atoi(getenv("MK_OZ_GROUPED")) : -1;  // -1 auto
+  bool small = true;
+  for (int i = 0; i < count; ++i) small = small && (double)items[i].m * items[i].n * items[i].k < 17179869184.0;
+  const bool grouped = grouped_mode == 1 || (grouped_mode < 0 && small);
+  if (grouped && one_chunk && count > 1) {
     keep_pool_memory();
     int dev = 0;
     cudaGetDevice(&dev);
