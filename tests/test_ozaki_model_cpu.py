@@ -1,0 +1,97 @@
+"""CPU model of the INT8 (Ozaki scheme I) leaf arithmetic of mk_ozaki.cu, checked with exact
+integer / rational arithmetic: digit splitting, the +128 offset of Y's leading plane and its
+row-sum correction, the anti-diagonal int32 bound (ozaki_max_k), and the exact int64 hi/lo
+recombination. Test infrastructure only -- the product path is the CUDA kernel.
+"""
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+S = 8
+
+
+def row_exponent(mx: float) -> int:
+    if mx == 0.0:
+        return 0
+    return int(np.frexp(mx)[1])  # mx = f 2^e, f in [0.5, 1): every |x| < 2^e
+
+
+def digits(x: float, e: int, s: int = S):
+    """mk_ozaki.cu digits4: the bytes of floor(x * 2^(63 - e)) -- d_0 signed, d_1.. unsigned."""
+    v = int(np.floor(np.ldexp(x, 63 - e)))  # exact: a power-of-two scaling of a double
+    assert -(1 << 63) <= v < (1 << 63)
+    u = v & ((1 << 64) - 1)
+    out = []
+    for t in range(s):
+        byte = (u >> (8 * (7 - t))) & 0xFF
+        out.append(byte - 256 if (t == 0 and byte >= 128) else byte)
+    return out
+
+
+def value(d, e):
+    """x ~= 2^(e-7) * sum_s d_s 2^(-8 s)  (exact Fraction)."""
+    return Fraction(2) ** (e - 7) * sum(Fraction(dv) * Fraction(2) ** (-8 * t) for t, dv in enumerate(d))
+
+
+@pytest.mark.parametrize("x", [0.0, 1.0, -1.0, 0.75, -0.3, 1e-300, -7.123456789012345, 2.0 ** -1074, 123456789.5])
+def test_digits_reconstruct_the_truncated_value(x):
+    e = row_exponent(abs(x)) if x != 0 else 0
+    d = digits(x, e)
+    assert -128 <= d[0] <= 127 and all(0 <= t <= 255 for t in d[1:])
+    rec = value(d, e)
+    # floor truncation at 2^(e-63): 0 <= x - rec < 2^(e-63)
+    err = Fraction(x) - rec
+    assert 0 <= err < Fraction(2) ** (e - 63)
+
+
+def test_integers_are_exact():
+    r = np.random.default_rng(3)
+    for x in r.integers(-(1 << 40), 1 << 40, 200):
+        e = row_exponent(abs(float(x)))
+        assert value(digits(float(x), e), e) == x
+
+
+def test_product_offset_correction_and_recombination():
+    """P = 2^(e+f-14) sum_{s+t<=S-1} 2^(-8(s+t)) (a_s . b_t): with Y's plane 0 stored as b_0 + 128
+    the accumulator of diagonal d holds (a_d . (b_0 + 128)) + ... and 128 * rowsum(a_d) is taken
+    back out; the int64 hi/lo recombination reproduces the exact diagonal sum."""
+    r = np.random.default_rng(11)
+    k = 37
+    x = r.standard_normal(k)
+    y = r.standard_normal(k)
+    e = row_exponent(np.abs(x).max())
+    f = row_exponent(np.abs(y).max())
+    a = np.array([digits(v, e) for v in x], dtype=np.int64).T  # [S][k]
+    b = np.array([digits(v, f) for v in y], dtype=np.int64).T
+    b_off = b.copy()
+    b_off[0] += 128  # unsigned storage of the signed plane
+    acc = np.zeros(S, dtype=np.int64)
+    for s in range(S):
+        for t in range(S - s):
+            acc[s + t] += int(a[s] @ b_off[t])
+    rowsum = a.sum(axis=1)
+    acc_corr = acc - 128 * rowsum  # diagonal d gets (a_d . b_0) + 128 rowsum(a_d) from the offset
+    want = np.zeros(S, dtype=np.int64)
+    for s in range(S):
+        for t in range(S - s):
+            want[s + t] += int(a[s] @ b[t])
+    assert np.array_equal(acc_corr, want)
+    # exact int64 hi/lo recombination (epilogue): v = sum_d acc_d 2^(-8d) = 2^-24 (hi + 2^-32 lo)
+    hi = sum(int(want[d]) << (8 * (3 - d)) for d in range(4))
+    lo = sum(int(want[d]) << (8 * (7 - d)) for d in range(4, S))
+    v = Fraction(hi) + Fraction(lo, 1 << 32)
+    assert v * Fraction(1, 1 << 24) == sum(Fraction(int(want[d])) * Fraction(2) ** (-8 * d) for d in range(S))
+    p = v * Fraction(2) ** (e + f - 38)
+    exact = sum(Fraction(float(xi)) * Fraction(float(yi)) for xi, yi in zip(x, y))
+    # dropped pairs (s + t >= S) and floor truncation: far below FP64 rounding of the result
+    assert abs(float(p - exact)) <= k * 2.0 ** (e + f - 58)
+
+
+def test_int32_accumulator_bound_matches_ozaki_max_k():
+    """Worst anti-diagonal per k: one signed x unsigned pair (|.| <= 128 * 255) and S-1 unsigned
+    pairs with the offset plane (<= 255^2); K of them must fit int32 (mk_ozaki.cu ozaki_max_k)."""
+    worst = 128 * 255 + (S - 1) * 255 * 255
+    kmax = (2 ** 31 - 1) // worst
+    assert kmax == 4402
+    assert kmax * worst < 2 ** 31 and (kmax + 1) * worst >= 2 ** 31
