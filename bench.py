@@ -325,6 +325,9 @@ def ozaki_leg(args, pk, lib, _lib, torch, A, B, C, dc, host_a, host_b, policy, s
     achieved = pairs * kfl.value / (kms.value * 1e-3) / 1e12 if kms.value > 0 else None
     return {
         "slices": S, "digit_bits": 7 + 8 * (S - 1), "int8_products_per_leaf": pairs,
+        "extra_workspace_bytes": 2 * int(lib.mk_ozaki_workspace_bytes(n >> levels_for(n, args.cutoff),
+                                                                       n >> levels_for(n, args.cutoff),
+                                                                       n >> levels_for(n, args.cutoff), S)),
         "value": round(2.0 * n ** 3 / (ms * 1e-3) / 1e12, 4), "unit": UNIT, "ms_per_step": round(ms, 3),
         "step_ms": {"median": round(statistics.median(step_ms), 3), "best": round(min(step_ms), 3),
                     "worst": round(max(step_ms), 3)},
