@@ -308,8 +308,28 @@ def ozaki_leg(args, pk, lib, _lib, torch, A, B, C, dc, host_a, host_b, policy, s
             ams = g0.elapsed_time(g1) / 3
             alts.append({"cutoff": cut, "levels": levels_for(n, cut), "ms_per_step": round(ams, 3),
                          "value": round(2.0 * n ** 3 / (ams * 1e-3) / 1e12, 4)})
+        lean = []  # the paper's memory-reduced schedules (literal to the leaves) with INT8 leaves
+        if args.alt:
+            pk.set_plan("breadth-first", two_temp_tail=False)
+            for name, fn, mk_in in (("two-temp", pk.two_temp_winograd, False), ("in-place", pk.in_place_winograd, True)):
+                a2, b2 = (dc.new_empty(dc.shape).copy_(A.arr), dc.new_empty(dc.shape).copy_(B.arr)) if mk_in else (None, None)
+                X, Y = (pk.Matrix(a2), pk.Matrix(b2)) if mk_in else (A, B)
+                fn(X, Y, C, policy)
+                torch.cuda.synchronize()
+                g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                g0.record(stream)
+                fn(X, Y, C, policy)
+                g1.record(stream)
+                torch.cuda.synchronize()
+                lms = g0.elapsed_time(g1)
+                lean.append({"variant": name, "ms_per_step": round(lms, 3),
+                             "value": round(2.0 * n ** 3 / (lms * 1e-3) / 1e12, 4),
+                             "workspace_bytes": int(lib.mk_workspace_bytes(_lib.ALGO_IDS[name], n,
+                                                                           levels_for(n, args.cutoff)))})
+                del a2, b2
     finally:
         pk.set_leaf("dmma")
+        pk.set_plan()
     pairs = S * (S + 1) // 2
     peak = None
     src = "nominal 4500 TOPS dense INT8 (B200 datasheet)"
@@ -340,6 +360,7 @@ def ozaki_leg(args, pk, lib, _lib, torch, A, B, C, dc, host_a, host_b, policy, s
                      "peak_source": src},
         "clocks": clk.summary(),
         "alt_cutoffs": alts,
+        "memory_lean": lean,
         "dtype": "f64 operands/results; int8 x int8 -> int32 tensor-core products (Ozaki scheme I)",
     }
 
