@@ -84,7 +84,9 @@ def set_leaf(kind: str = "dmma", slices: int = 8, min_work: int = 2 ** 29) -> No
     data is exact either way. Fewer slices trade accuracy for speed. Modeled OpCounter values
     never change. ``min_work``: only leaf products with m*n*k >= min_work (rounded up to a power
     of two; default 2^29, about 812^3) use the INT8 kernels -- smaller leaves are launch- and
-    wave-bound there and stay on DMMA (0: every leaf).
+    wave-bound there and stay on DMMA (0: every leaf). Non-finite operand entries cannot be written
+    as digits: an inf or NaN in a leaf operand's row (column) makes that whole row (column) of the
+    leaf product NaN, where the FP64 product would give inf for some entries.
     """
     if kind not in ("dmma", "ozaki"):
         raise ValueError(f"leaf must be 'dmma' or 'ozaki', got {kind!r}")
