@@ -643,7 +643,22 @@ struct Engine {
       sl.rows = slab_rows;
       for (int i = 0; i < nslab; ++i) sl.p[i] = slab[i];
     }
-    const int rc = ozaki_product_multi(x, y, c, ldc, M, N, K, leaf_slices(), od, nd, st, &err, nslab ? &sl : nullptr);
+    int rc;
+    if (!nslab && K > ozaki_max_k(leaf_slices())) {  // several K chunks: pipelined split / product
+      OzItem it{};
+      it.X = x;
+      it.Y = y;
+      it.C = c;
+      it.ldc = ldc;
+      it.m = M;
+      it.n = N;
+      it.k = K;
+      it.nd = nd;
+      for (int i = 0; i < nd; ++i) it.d[i] = od[i];
+      rc = ozaki_product_batch(&it, 1, leaf_slices(), st, &err);
+    } else {
+      rc = ozaki_product_multi(x, y, c, ldc, M, N, K, leaf_slices(), od, nd, st, &err, nslab ? &sl : nullptr);
+    }
     if (rc != MK_OK) return fail(rc, err);
     g_launch_count += 5;
     if (g_timing.on) {
