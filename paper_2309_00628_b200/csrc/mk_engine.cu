@@ -1829,11 +1829,17 @@ static std::vector<int> head_child_order(const Coeffs& co, int p0, double kChild
   return best;
 }
 
+// INT8 leaves: one top-level product in quadrant-transfer units (env MK_HOST_KPROD for studies)
+static double int8_kprod() {
+  const char* e = getenv("MK_HOST_KPROD");
+  return e ? atof(e) : 1.35;
+}
+
 int mk_overlap_order(int algo, int* order_out, int* uploads_out) {
   g_last_error.clear();
   if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_WINOGRAD_KNUTH_8CALL) return fail(MK_ERR_ARG, "fused algorithms only");
   std::vector<int> up;
-  const std::vector<int> ord = overlap_order(coeffs_for(algo), &up, leaf_slices() ? 1.35 : 3.0);
+  const std::vector<int> ord = overlap_order(coeffs_for(algo), &up, leaf_slices() ? int8_kprod() : 3.0);
   for (size_t i = 0; i < ord.size(); ++i) order_out[i] = ord[i];
   for (size_t i = 0; i < up.size(); ++i) uploads_out[i] = up[i];
   return (int)ord.size();
@@ -1845,6 +1851,7 @@ static std::map<int, std::pair<std::vector<int>, std::vector<int>>> g_order_cach
 static std::map<int, std::vector<int>> g_head_cache;
 static std::mutex g_order_mu;
 static std::vector<int> head_child_order(const Coeffs& co, int p0, double kChild);
+
 static std::vector<int> overlap_order(const Coeffs& co, std::vector<int>* uploads, double kProd);
 // overlap_order is a search over all product permutations (~1.6 ms): computed once per algorithm
 // and leaf arithmetic (the INT8 leaf halves the compute time per product relative to transfers)
@@ -1854,7 +1861,7 @@ static std::vector<int> cached_order(int algo, std::vector<int>* uploads) {
   auto it = g_order_cache.find(key);
   if (it == g_order_cache.end()) {
     std::vector<int> up;
-    std::vector<int> ord = overlap_order(coeffs_for(algo), &up, leaf_slices() ? 1.35 : 3.0);
+    std::vector<int> ord = overlap_order(coeffs_for(algo), &up, leaf_slices() ? int8_kprod() : 3.0);
     it = g_order_cache.emplace(key, std::make_pair(ord, up)).first;
   }
   if (uploads) *uploads = it->second.second;
