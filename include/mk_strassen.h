@@ -65,8 +65,8 @@ int mk_version(void);
  *   Table-2 levels (default), 0 = the literal schedule down to the leaves (2 (n/2)^2-style
  *   scratch only, the paper's memory bound).
  * MK_OPT_LEAF_SLICES: 0 = leaf products on the FP64 tensor cores (DMMA, default); 4..8 = on the
- *   INT8 tensor cores (tcgen05 kind::i8, Ozaki scheme I) with that many 7-bit digit slices per
- *   operand (see mk_ozaki_dgemm; 8 is as accurate as the DMMA leaf, fewer trade accuracy for speed).
+ *   INT8 tensor cores (tcgen05 kind::i8, Ozaki scheme I) with that many digit slices per operand
+ *   (see mk_ozaki_dgemm; 8 is more accurate than the DMMA leaf, fewer trade accuracy for speed).
  *   Applies to every leaf product of the engine with m*n*k >= 2^MK_OPT_LEAF_MIN_LOG2.
  * MK_OPT_LEAF_MIN_LOG2: the INT8 leaf's size threshold, log2 of m*n*k (default 29, about 812^3):
  *   smaller leaves stay on DMMA (the per-leaf INT8 kernels are launch- and wave-bound there). */
@@ -96,14 +96,17 @@ int mk_dgemm(const double* A, int64_t lda, const double* B, int64_t ldb, double*
              int64_t m, int64_t n, int64_t k, void* stream);
 
 /* C[m x n] = A[m x k] * B[k x n] with FP64 operands multiplied on the INT8 tensor cores
- * (Ozaki scheme I: each row of A / column of B split into `slices` signed 7-bit digits under a
- * power-of-two scale, the slices*(slices+1)/2 digit-pair products accumulated exactly in int32
- * by tcgen05.mma kind::i8, recombined in FP64). Same operand/alias rules as mk_dgemm; an
- * opt-in alternative to the DMMA leaf (mk_set_option(MK_OPT_LEAF_SLICES, s)). slices in [4, 8];
- * k <= 2^31 / (slices * 127^2). ws: mk_ozaki_workspace_bytes(m, n, k, slices) bytes of device
- * memory, 256-byte aligned. Integer-valued data with <= 7*slices significant bits relative to
- * each row / column maximum is reproduced exactly; otherwise the per-term error is
- * <= (slices + 2) * 2^(-7 slices) * 2^(e_i + f_j) (e_i, f_j: row / column max exponents).
+ * (Ozaki scheme I: each row of A / column of B scaled by a power of two and split into `slices`
+ * digit planes -- a signed 7-bit leading digit and unsigned 8-bit digits, 7 + 8 (slices - 1) bits,
+ * the floor digits of the value; the slices*(slices+1)/2 digit-pair products accumulated exactly in
+ * int32 TMEM accumulators by tcgen05.mma kind::i8 (pairs on one anti-diagonal share one), the
+ * diagonal sums recombined exactly in int64 and rounded once to FP64). Same operand/alias rules
+ * as mk_dgemm; the opt-in alternative to the DMMA leaf (mk_set_option(MK_OPT_LEAF_SLICES, s)).
+ * slices in [4, 8]; any k (k > 4402 at 8 slices runs in K chunks that accumulate). ws:
+ * mk_ozaki_workspace_bytes(m, n, k, slices) bytes of device memory, 256-byte aligned.
+ * Integer-valued data that fits the digits (|x| < 2^56 at 8 slices) is reproduced exactly; at 8
+ * slices real data is more accurate than the FP64 tensor-core product (K5).
+ * A non-finite entry makes its whole row (of A) / column (of B) of C NaN.
  * Replaces the same call sites as mk_dgemm (kernels.py:258-266). */
 size_t mk_ozaki_workspace_bytes(int64_t m, int64_t n, int64_t k, int slices);
 int mk_ozaki_dgemm(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
