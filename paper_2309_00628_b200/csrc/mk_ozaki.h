@@ -10,10 +10,12 @@
 //   P_ij = 2^(e_i + f_j - 14) * sum_{s+t <= S-1} 2^(-8(s+t)) * (a_s . b_t)_ij
 //
 // where every a_s . b_t is an exact 8-bit x 8-bit -> int32 tensor-core product (tcgen05.mma
-// kind::i8, accumulators in TMEM), pairs on the same anti-diagonal d = s + t share one
-// accumulator (still exact for K <= ozaki_max_k(S): 4715 at S = 8; longer K runs in chunks), and
-// the S diagonal sums are combined in FP64 in the epilogue (Horner in 2^-8, one rounding per
-// step). Floor truncation and the dropped pairs (s + t >= S) bound the error per product term by
+// kind::i8, accumulators in TMEM; Y's signed plane is stored with a +128 offset so every Y plane
+// is unsigned, and 128 * rowsum(a_d) is subtracted per diagonal), pairs on the same
+// anti-diagonal d = s + t share one accumulator (still exact for K <= ozaki_max_k(S): 4402 at
+// S = 8; longer K runs in chunks), and the S diagonal sums are recombined exactly in int64
+// (hi / lo) and rounded once to FP64 in the epilogue. Floor truncation and the dropped pairs
+// (s + t >= S) bound the error per product term by
 // about (S + 2) * 2^(2 - 8S) * 2^(e_i + f_j) -- far below FP64 rounding at S = 8 (63 digit bits);
 // integer-valued data is reproduced exactly while it fits the digits (|x| < 2^56 at S = 8).
 #pragma once
