@@ -197,6 +197,16 @@ int mk_strassen_partial(int algo, const double* A, int64_t lda, const double* B,
                         int64_t ldc, int64_t n, int levels, int first, int count, int panels, void* ws,
                         size_t ws_bytes, void* stream);
 
+/* Sharded form of mk_multiply_rect (BASELINE cfg5 on N GPUs): this rank's leaf row-panel units
+ * [first, first+count) of the padded rectangular product (panels per leaf; mk_product_count(algo,
+ * levels) * panels units in all), written to C (m x n) as a partial -- C is overwritten with this
+ * rank's contribution; the ranks' partials sum to A*B (e.g. one NCCL reduce). Replaces
+ * hybrid.multiply (hybrid.py:105-146) with its products sharded. */
+size_t mk_rect_partial_workspace_bytes(int algo, int64_t m, int64_t n, int64_t k, int levels, int panels);
+int mk_multiply_rect_partial(int algo, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                             int64_t ldc, int64_t m, int64_t n, int64_t k, int levels, int first, int count,
+                             int panels, void* ws, size_t ws_bytes, void* stream);
+
 /* Enable NVLink peer access from the current device to peer_device (idempotent). */
 int mk_enable_peer_access(int peer_device);
 

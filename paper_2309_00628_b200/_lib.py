@@ -67,6 +67,9 @@ SIGNATURES = {
     "mk_strassen_host": (_INT, [_INT, _VP, _I64, _VP, _I64, _VP, _I64, _I64, _INT, _VP, _VP, _VP, _I64, _VP, _SZ,
                                 _VP, _VP]),
     "mk_enable_peer_access": (_INT, [_INT]),
+    "mk_rect_partial_workspace_bytes": (_SZ, [_INT, _I64, _I64, _I64, _INT, _INT]),
+    "mk_multiply_rect_partial": (_INT, [_INT, _VP, _I64, _VP, _I64, _VP, _I64, _I64, _I64, _I64, _INT, _INT, _INT,
+                                        _INT, _VP, _SZ, _VP]),
     "mk_strassen_partial_slabs": (_INT, [_INT, _VP, _I64, _VP, _I64, ctypes.POINTER(_VP), _INT, _I64, _I64, _I64,
                                          _INT, _INT, _INT, _INT, _VP, _SZ, _VP]),
     "mk_overlap_order": (_INT, [_INT, ctypes.POINTER(_INT), ctypes.POINTER(_INT)]),

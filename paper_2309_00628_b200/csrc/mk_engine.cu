@@ -542,6 +542,13 @@ struct Engine {
     ws_used += bytes;
     ws_peak = std::max(ws_peak, ws_used);
     *base_out = add_base(p, ld, rows, cols, leaf_m, leaf_n);
+    if (leaf_count >= 0) {
+      // shard mode: some leaves of a materialised product are skipped (other ranks) and leaves
+      // may be split into row panels, so no contribution can rely on being the block's first
+      // writer -- slots start zeroed and every contribution accumulates
+      if (!dry && !no_launch) MK_CUDA_TRY(cudaMemsetAsync(p, 0, bytes, st));
+      set_state(*base_out, 0, 0, rows, cols, 1);
+    }
     return MK_OK;
   }
 
@@ -2191,13 +2198,19 @@ int mk_strassen_partial_slabs(int algo, const double* A, int64_t lda, const doub
   return run_square(e);
 }
 
+// Rectangular driver. Shard mode (first >= 0): only leaf row-panel units [first, first+count)
+// (panels per leaf) are computed, accumulated into a zeroed padded C, whose valid region is then
+// copied to C (the caller's zeroed partial; the ranks' partials are summed afterwards).
 static int run_rect(int algo, const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                     int64_t m, int64_t n, int64_t k, int levels, void* ws, size_t ws_bytes, cudaStream_t st,
-                    bool dry, size_t* need_out) {
+                    bool dry, size_t* need_out, int64_t first = -1, int64_t count = 0, int panels = 1) {
   // every level halves each extent and the leaves need even extents (16-byte TMA origins) and
-  // a leaf N divisible by 4 (32-byte epilogue rows): pad m, k to 2^(L+1) and n to 2^(L+2)
+  // a leaf N divisible by 4 (32-byte epilogue rows): pad m, k to 2^(L+1) and n to 2^(L+2);
+  // shard mode also needs even row panels: m to 2 * panels * 2^L
+  const bool shard = first >= 0;
   const int64_t qm = (int64_t)2 << levels, qn = (int64_t)4 << levels;
-  const int64_t mp = (m + qm - 1) / qm * qm, np_ = (n + qn - 1) / qn * qn, kp = (k + qm - 1) / qm * qm;
+  const int64_t qmm = shard ? std::max<int64_t>(qm, ((int64_t)2 * panels) << levels) : qm;
+  const int64_t mp = (m + qmm - 1) / qmm * qmm, np_ = (n + qn - 1) / qn * qn, kp = (k + qm - 1) / qm * qm;
   size_t off = 0;
   auto carve = [&](size_t elems) {
     double* p = dry ? reinterpret_cast<double*>(0x1000 + off) : reinterpret_cast<double*>(static_cast<char*>(ws) + off);
@@ -2208,7 +2221,7 @@ static int run_rect(int algo, const double* A, int64_t lda, const double* B, int
   // needs TMA-compatible operands (16-byte aligned, even leading dimensions). Sizing assumes
   // the in-place case whenever the extents conform.
   auto tma_ok = [](const void* p, int64_t ld) { return reinterpret_cast<uintptr_t>(p) % 16 == 0 && ld % 2 == 0; };
-  const bool conform = mp == m && np_ == n && kp == k;
+  const bool conform = mp == m && np_ == n && kp == k && !shard;  // shards always accumulate in a padded C
   const bool direct = conform && (dry || (tma_ok(A, lda) && tma_ok(B, ldb) && tma_ok(C, ldc)));
   if (conform && !direct) return fail(MK_ERR_ARG, "operands need 16-byte alignment and even leading dimensions");
   double* Ap = direct ? const_cast<double*>(A) : carve((size_t)mp * kp);
@@ -2226,6 +2239,7 @@ static int run_rect(int algo, const double* A, int64_t lda, const double* B, int
     s[0] = B;
     l[0] = ldb;
     MK_CUDA_TRY(launch_combine(Bp, np_, s, l, sg, 1, k, n, st));
+    if (shard) MK_CUDA_TRY(cudaMemsetAsync(Cp, 0, (size_t)mp * np_ * 8, st));
   }
   Engine e;
   e.dry = dry;
@@ -2242,7 +2256,13 @@ static int run_rect(int algo, const double* A, int64_t lda, const double* B, int
   e.add_base(Cp, ldcp, mp, np_, e.leaf_m, e.leaf_n);
   e.ws = dry ? nullptr : static_cast<char*>(ws) + off;
   e.ws_bytes = dry ? 0 : ws_bytes - off;
-  if (plan_kind() == 2 && levels >= 2 && !e.fuse_preadds && algo >= MK_ALGO_STRASSEN &&
+  if (shard) {
+    e.leaf_first = first;
+    e.leaf_count = count;
+    e.panels = panels;
+    e.set_state(BASE_C, 0, 0, mp, np_, 1);  // accumulate into the zeroed padded C
+  }
+  if (!shard && plan_kind() == 2 && levels >= 2 && !e.fuse_preadds && algo >= MK_ALGO_STRASSEN &&
       algo <= MK_ALGO_WINOGRAD_KNUTH_8CALL) {  // hybrid (see run_square)
     const Lin A0{Blk{BASE_A, 0, 0, 1.0}}, B0{Blk{BASE_B, 0, 0, 1.0}}, C0{Blk{BASE_C, 0, 0, 1.0}};
     for (int p = 0; p < e.co->nprod; ++p) MK_TRY(e.top_product_bfs(p, A0, B0, C0, mp / 2, np_ / 2, kp / 2));
@@ -2284,6 +2304,34 @@ int mk_multiply_rect(int algo, const double* A, int64_t lda, const double* B, in
   if (!ws || ws_bytes < need) return fail(MK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
   return run_rect(algo, A, lda, B, ldb, C, ldc, m, n, k, levels, ws, ws_bytes, static_cast<cudaStream_t>(stream),
                   false, nullptr);
+}
+
+size_t mk_rect_partial_workspace_bytes(int algo, int64_t m, int64_t n, int64_t k, int levels, int panels) {
+  if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_WINOGRAD_KNUTH_8CALL || m < 1 || n < 1 || k < 1 || levels < 0 ||
+      panels < 1)
+    return 0;
+  size_t need = 0;
+  if (run_rect(algo, nullptr, 0, nullptr, 0, nullptr, 0, m, n, k, levels, nullptr, 0, nullptr, true, &need, 0,
+               1 << 30, panels) != MK_OK)
+    return 0;
+  return need;
+}
+
+int mk_multiply_rect_partial(int algo, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                             int64_t ldc, int64_t m, int64_t n, int64_t k, int levels, int first, int count,
+                             int panels, void* ws, size_t ws_bytes, void* stream) {
+  g_last_error.clear();
+  if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_WINOGRAD_KNUTH_8CALL)
+    return fail(MK_ERR_ARG, "rectangular driver supports the fused algorithms");
+  if (m < 1 || n < 1 || k < 1) return fail(MK_ERR_DIMENSION, "extents must be positive");
+  if (levels < 0 || levels > 20 || panels < 1 || first < 0 || count < 0) return fail(MK_ERR_ARG, "invalid arguments");
+  if (lda < k || ldb < n || ldc < n) return fail(MK_ERR_DIMENSION, "leading dimension smaller than the extent");
+  if (overlaps(C, ldc, m, n, A, lda, m, k) || overlaps(C, ldc, m, n, B, ldb, k, n))
+    return fail(MK_ERR_ALIAS, "output view must not alias an input view");
+  const size_t need = mk_rect_partial_workspace_bytes(algo, m, n, k, levels, panels);
+  if (!ws || ws_bytes < need) return fail(MK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
+  return run_rect(algo, A, lda, B, ldb, C, ldc, m, n, k, levels, ws, ws_bytes, static_cast<cudaStream_t>(stream),
+                  false, nullptr, first, count, panels);
 }
 
 int mk_block_combine(double* dst, int64_t ldd, const double* const* src, const int64_t* lds, const double* sign,

@@ -268,3 +268,41 @@ def fused_sharded_multiply(algo: str, a, b, levels: int, exchange: SlabExchange,
             out[r * sr:(r + 1) * sr].copy_(s)
         torch.cuda.synchronize()
     return exchange.slab
+
+
+# ------------------------------------------------------------------------------------------
+# rectangular products (BASELINE cfg5 on N GPUs): the padded rectangular recursion, sharded the
+# same way (leaf row panels), partials summed by one reduce
+# ------------------------------------------------------------------------------------------
+def rect_partial_product(algo: str, a, b, out, levels: int, first: int, count: int, ws=None,
+                         panels: int = PANELS) -> int:
+    """out (m x n) := shard units [first, first+count) of A B (CUDA FP64, any m, k, n)."""
+    import torch
+
+    lib = _lib.load()
+    m, k = a.shape
+    n = b.shape[1]
+    aid = _lib.ALGO_IDS[algo]
+    need = int(lib.mk_rect_partial_workspace_bytes(aid, m, n, k, levels, panels))
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(max(need, 16), dtype=torch.uint8, device=a.device)
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    rc = lib.mk_multiply_rect_partial(aid, ctypes.c_void_p(a.data_ptr()), a.stride(0), ctypes.c_void_p(b.data_ptr()),
+                                      b.stride(0), ctypes.c_void_p(out.data_ptr()), out.stride(0), m, n, k, levels,
+                                      first, count, panels, ctypes.c_void_p(ws.data_ptr()), need, st)
+    _lib.check(rc, "mk_multiply_rect_partial")
+    return need
+
+
+def sharded_multiply_rect(algo: str, a, b, levels: int, group=None, out=None, ws=None):
+    """C = A B (rectangular) with this rank's share of the leaves plus the reduce; C on rank 0."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    first, count = shard_range(leaf_count(algo, levels) * PANELS, world, rank)
+    if out is None:
+        out = torch.empty((a.shape[0], b.shape[1]), dtype=torch.float64, device=a.device)
+    rect_partial_product(algo, a, b, out, levels, first, count, ws=ws)
+    return assemble(out, 0, group)

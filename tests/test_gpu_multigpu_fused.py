@@ -130,3 +130,50 @@ def test_two_process_ipc_fused_reduce_scatter(levels, exact, leaf, tmp_path):
         p.join(timeout=300)
         assert p.exitcode == 0
     assert open(result).read() == "ok"
+
+
+@pytest.mark.parametrize("shape,levels,world", [((300, 500, 200), 2, 3), ((12000 // 8, 14000 // 8, 10000 // 8), 3, 8),
+                                                ((129, 77, 65), 1, 2)])
+def test_rect_partials_sum_to_the_product(shape, levels, world):
+    """BASELINE cfg5 on N GPUs: the ranks' rectangular partials (leaf row panels of the padded
+    recursion) sum to the product -- bit-exact on integer data (ranks run in turn on one GPU)."""
+    import torch
+
+    from paper_2309_00628_b200 import multigpu as mg
+
+    m, k, n = shape
+    r = np.random.default_rng(m + k + n)
+    a = torch.from_numpy(r.integers(-8, 9, (m, k)).astype(np.float64)).cuda()
+    b = torch.from_numpy(r.integers(-8, 9, (k, n)).astype(np.float64)).cuda()
+    total = torch.zeros((m, n), dtype=torch.float64, device="cuda")
+    part = torch.empty_like(total)
+    units = mg.leaf_count("winograd-block", levels) * mg.PANELS
+    for rank in range(world):
+        first, count = mg.shard_range(units, world, rank)
+        mg.rect_partial_product("winograd-block", a, b, part, levels, first, count)
+        total += part
+    torch.cuda.synchronize()
+    assert torch.equal(total, a @ b)
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_square_partials_three_levels(world):
+    """Square shards at 3 levels (leaf fan-out 64 > 16: products materialised in slots, some of
+    their leaves on other ranks): the partials still sum to the product exactly."""
+    import torch
+
+    from paper_2309_00628_b200 import multigpu as mg
+
+    n = 1024
+    r = np.random.default_rng(world)
+    a = torch.from_numpy(r.integers(-8, 9, (n, n)).astype(np.float64)).cuda()
+    b = torch.from_numpy(r.integers(-8, 9, (n, n)).astype(np.float64)).cuda()
+    total = torch.zeros((n, n), dtype=torch.float64, device="cuda")
+    units = mg.leaf_count("winograd-block", 3) * mg.PANELS
+    for rank in range(world):
+        first, count = mg.shard_range(units, world, rank)
+        part = torch.zeros_like(total)
+        mg.partial_product("winograd-block", a, b, part, 3, first, count)
+        total += part
+    torch.cuda.synchronize()
+    assert torch.equal(total, a @ b)
