@@ -74,6 +74,11 @@ enum mk_option { MK_OPT_FUSE_PREADDS = 1, MK_OPT_PLAN = 2, MK_OPT_LITERAL_TAIL =
                  MK_OPT_LEAF_MIN_LOG2 = 5 };
 int mk_set_option(int key, int value);
 int mk_get_option(int key, int* value);
+/* Calling-thread override of MK_OPT_PLAN / MK_OPT_LITERAL_TAIL (value -1 removes it). Applies to
+ * every later sizing (mk_*_workspace_bytes) and launch made from this thread, so a workspace sized
+ * under an override always fits the launch that follows, whatever other threads set meanwhile.
+ * mk_get_option reports the effective value for the calling thread. */
+int mk_set_thread_option(int key, int value);
 
 /* Instrumentation (bench.py). mk_launch_count: kernels this thread has launched so far.
  * mk_timing_begin / mk_timing_end: bracket engine calls; every leaf-product (DMMA) launch in

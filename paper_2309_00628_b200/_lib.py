@@ -45,6 +45,7 @@ SIGNATURES = {
     "mk_fp64_peak": (_INT, [_DP, _VP]),
     "mk_set_option": (_INT, [_INT, _INT]),
     "mk_get_option": (_INT, [_INT, ctypes.POINTER(ctypes.c_int)]),
+    "mk_set_thread_option": (_INT, [_INT, _INT]),
     "mk_last_error": (ctypes.c_char_p, []),
     "mk_dgemm": (_INT, [_VP, _I64, _VP, _I64, _VP, _I64, _I64, _I64, _I64, _VP]),
     "mk_ozaki_workspace_bytes": (_SZ, [_I64, _I64, _I64, _INT]),

@@ -297,7 +297,12 @@ static bool async_epilogue_enabled() {
 
 // MK_OPT_LITERAL_TAIL / MK_OPT_PLAN (mk_set_option); -1 = take the environment default
 static std::atomic<int> g_literal_tail{-1}, g_plan_dfs{-1};  // process-wide options
+// per-thread overrides (mk_set_thread_option; -1 = none): a caller that sizes a workspace and then
+// launches with non-default plan options does both under its own thread's settings, so another
+// thread changing the process-wide options in between cannot make the launch outgrow the workspace
+static thread_local int t_literal_tail = -1, t_plan = -1;
 static bool literal_bfs_tail() {
+  if (t_literal_tail >= 0) return t_literal_tail == 1;
   if (g_literal_tail < 0) {
     const char* e = getenv("MK_LITERAL_TAIL");
     g_literal_tail = (e && e[0] == '0') ? 0 : 1;
@@ -307,6 +312,7 @@ static bool literal_bfs_tail() {
 // MK_OPT_PLAN: 0 breadth-first, 1 depth-first, 2 top-level depth-first with a breadth-first plan
 // under each top-level product (env MK_PLAN=dfs / hybrid)
 static int plan_kind() {
+  if (t_plan >= 0) return t_plan;
   if (g_plan_dfs < 0) {
     const char* env = getenv("MK_PLAN");
     g_plan_dfs = (env && std::string(env) == "dfs") ? 1 : (env && std::string(env) == "hybrid") ? 2 : 0;
@@ -527,7 +533,9 @@ struct Engine {
       for (int64_t c = col / cc; c < (col + cols + cc - 1) / cc; ++c) written[base][(size_t)(r * ncc + c)] = v;
   }
 
-  int alloc_slot(int64_t rows, int64_t cols, int* base_out) {
+  // product = the slot receives leaf / post-add contributions (zeroed in shard mode); operand-sum
+  // slots are fully overwritten by combine() before anything reads them
+  int alloc_slot(int64_t rows, int64_t cols, int* base_out, bool product = false) {
     int64_t ld = (cols + 3) / 4 * 4;  // 32B rows for the vector epilogue / TMA
     size_t bytes = (size_t)rows * ld * 8;
     bytes = (bytes + 1023) / 1024 * 1024;
@@ -542,10 +550,10 @@ struct Engine {
     ws_used += bytes;
     ws_peak = std::max(ws_peak, ws_used);
     *base_out = add_base(p, ld, rows, cols, leaf_m, leaf_n);
-    if (leaf_count >= 0) {
+    if (leaf_count >= 0 && product) {
       // shard mode: some leaves of a materialised product are skipped (other ranks) and leaves
       // may be split into row panels, so no contribution can rely on being the block's first
-      // writer -- slots start zeroed and every contribution accumulates
+      // writer -- product slots start zeroed and every contribution accumulates
       if (!dry && !no_launch) MK_CUDA_TRY(cudaMemsetAsync(p, 0, bytes, st));
       set_state(*base_out, 0, 0, rows, cols, 1);
     }
@@ -856,7 +864,7 @@ struct Engine {
     for (int i = 1; i < remaining; ++i) worst *= 4;
     if (worst > MK_MAX_DESTS) {
       int pb;
-      MK_TRY(alloc_slot(hm, hn, &pb));
+      MK_TRY(alloc_slot(hm, hn, &pb, true));
       MK_TRY(fused(remaining - 1, Xp, Yp, Lin{Blk{pb, 0, 0, 1.0}}, hm, hn, hk, level + 1));
       // post-add the materialised product into its destinations
       for (const Blk& d : Dp) {
@@ -1012,7 +1020,7 @@ struct Engine {
       Yb = Blk{sb, 0, 0, 1.0};
     }
     int pb;
-    MK_TRY(alloc_slot(hm, hn, &pb));
+    MK_TRY(alloc_slot(hm, hn, &pb, true));
     MK_TRY(bfs(L - 1, hm, hn, hk, Xb, Yb, Blk{pb, 0, 0, 1.0}));
     for (const Blk& d : Dp) {
       const int s = state(d.base, d.row, d.col, hm, hn);
@@ -1106,8 +1114,8 @@ struct Engine {
     const int nb_mark = nbases;
     if (use_xy) {
       int bx, by;
-      MK_TRY(alloc_slot(h, h, &bx));
-      MK_TRY(alloc_slot(h, h, &by));
+      MK_TRY(alloc_slot(h, h, &bx, true));
+      MK_TRY(alloc_slot(h, h, &by, true));
       loc["X"] = Blk{bx, 0, 0, 1.0};
       loc["Y"] = Blk{by, 0, 0, 1.0};
     }
@@ -1319,7 +1327,7 @@ struct Engine {
       par[0].o = D;
     } else {  // parents' outputs row-stacked in one arena
       int ob;
-      MK_TRY(alloc_slot((int64_t)par.size() * 2 * lm, 2 * ln, &ob));
+      MK_TRY(alloc_slot((int64_t)par.size() * 2 * lm, 2 * ln, &ob, true));
       for (size_t i = 0; i < par.size(); ++i) par[i].o = Blk{ob, (int64_t)i * 2 * lm, 0, 1.0};
     }
     const int slab = consumer_layout() == 16 ? 32 : 64;
@@ -1453,7 +1461,7 @@ struct Engine {
       const int64_t cm = M >> d, cn = N >> d;
       std::vector<MkXformJob> jobs;
       int pb_arena = -1;
-      if (d - 1 != 0) MK_TRY(alloc_slot((int64_t)pa.size() * 2 * cm, 2 * cn, &pb_arena));
+      if (d - 1 != 0) MK_TRY(alloc_slot((int64_t)pa.size() * 2 * cm, 2 * cn, &pb_arena, true));
       for (size_t j = 0; j < pa.size(); ++j) {
         if (d - 1 == 0) {
           pa[j].o = D;
@@ -1624,6 +1632,21 @@ int mk_set_option(int key, int value) {
     return MK_OK;
   }
   return fail(MK_ERR_ARG, "unknown option key");
+}
+
+int mk_set_thread_option(int key, int value) {
+  g_last_error.clear();
+  if (key == MK_OPT_PLAN) {
+    if (value < -1 || value > 2)
+      return fail(MK_ERR_ARG, "MK_OPT_PLAN takes -1 (process-wide), 0, 1 or 2 as a thread option");
+    t_plan = value;
+    return MK_OK;
+  }
+  if (key == MK_OPT_LITERAL_TAIL) {
+    t_literal_tail = value < 0 ? -1 : (value ? 1 : 0);
+    return MK_OK;
+  }
+  return fail(MK_ERR_ARG, "only MK_OPT_PLAN and MK_OPT_LITERAL_TAIL have thread overrides");
 }
 
 int mk_get_option(int key, int* value) {

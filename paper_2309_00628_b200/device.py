@@ -80,8 +80,9 @@ def set_leaf(kind: str = "dmma", slices: int = 8, min_work: int = 2 ** 29) -> No
     ``"ozaki"``: on the INT8 tensor cores (tcgen05.mma kind::i8, Ozaki scheme I): each operand
     row / column is split into ``slices`` (4..8) signed 7-bit digits under a power-of-two scale,
     the digit-pair products are exact int32 sums in tensor memory and are recombined in FP64.
-    With 8 slices the leaf error is at or below the DMMA leaf's (56 digit bits vs 53); integer
-    data is exact either way. Fewer slices trade accuracy for speed. Modeled OpCounter values
+    With 8 slices the leaf error is at or below the DMMA leaf's (63 digit bits vs 53) and integer
+    data is exact whenever the FP64 guard passes; with fewer slices integer operands must also fit
+    the digits (ozaki_exactness_guard: ExactnessError otherwise, never a silently truncated result). Fewer slices trade accuracy for speed. Modeled OpCounter values
     never change. ``min_work``: only leaf products with m*n*k >= min_work (rounded up to a power
     of two; default 2^29, about 812^3) use the INT8 kernels -- smaller leaves are launch- and
     wave-bound there and stay on DMMA (0: every leaf). Non-finite operand entries cannot be written
@@ -261,6 +262,35 @@ def exactness_guard(a: MatrixView, b: MatrixView, inner: int, levels: int) -> No
         raise _lib.ExactnessError(
             f"integer operands too large for an exact FP64 engine run: max|a|*max|b|*n*64^L = {bound:.3e} >= 2^53"
         )
+    kind, slices = get_leaf()
+    if kind == "ozaki":
+        ozaki_exactness_guard(ma, mb, levels, slices)
+
+
+def ozaki_exactness_guard(ma: float, mb: float, levels: int, slices: int) -> None:
+    """INT8 (Ozaki) leaves with S slices write a leaf operand row (column) scaled by 2^-e
+    (|x| < 2^e) as a signed leading digit of weight 2^(e-7) and S-1 unsigned 8-bit digits
+    below it, and drop the digit pairs s + t >= S. For integer data digit s is nonzero only if
+    s <= ceil((e - 7) / 8) (lower digits cover weights below 2^0), so the product is exact iff
+    ceil((e - 7)/8) + ceil((f - 7)/8) <= S - 1 (which also keeps every bit inside the S digits).
+    Leaf operand sums grow by <= 4x per level and side: e and f are bounded from max|a| 4^L and
+    max|b| 4^L. At S = 8 the FP64 bound above already implies the condition."""
+
+    def exp2_above(x: float) -> int:  # smallest e with x < 2^e
+        e = 0
+        while x >= 2.0 ** e:
+            e += 1
+        return e
+
+    def top_digit(e: int) -> int:
+        return max(0, -(-(e - 7) // 8))
+
+    e, f = exp2_above(ma * 4.0 ** levels), exp2_above(mb * 4.0 ** levels)
+    if top_digit(e) + top_digit(f) > slices - 1:
+        raise _lib.ExactnessError(
+            f"integer operands too large for exact INT8 (Ozaki) leaves with {slices} slices: leaf operand "
+            f"scales 2^{e}, 2^{f} put nonzero digits at {top_digit(e)} + {top_digit(f)} > {slices - 1} "
+            f"(dropped digit pairs); use set_leaf('ozaki', 8) or set_leaf('dmma')")
 
 
 class Output:
@@ -311,7 +341,6 @@ def check_disjoint(a: MatrixView, b: MatrixView, c: MatrixView) -> None:
         raise AliasError("output view must not alias an input view")
 
 
-_plan_lock = threading.Lock()
 # Engine workspaces are kept per (device, stream, thread) and reused by later calls of that thread on
 # that stream (work on one stream is ordered, so reuse is safe even while earlier calls still run): a 15.5 GB
 # breadth-first workspace is neither re-requested from the allocator nor re-checked against free
@@ -367,31 +396,28 @@ def _memory_aware_plan(size_of, levels: int = 3):
     """Yield the workspace size for this call. When the configured plan's workspace does not fit
     in device memory, the call runs with leaner options instead -- the hybrid plan first for
     deep recursions (breadth-first speed at ~1/7 of the memory), else the depth-first plan and the
-    literal two-temp schedule (same results on integer data) -- and the options are restored."""
+    literal two-temp schedule (same results on integer data). The leaner options are set as
+    calling-thread overrides (mk_set_thread_option) for both the sizing and the launch inside the
+    ``with`` block, then removed: other threads' options are never touched, and another thread's
+    set_plan() cannot change this call's plan between its sizing and its launch."""
     need = int(size_of())
     if need < _WS_QUERY_MIN or _fits(need):  # small workspaces: skip the (~0.7 ms) memory query
         yield need
         return
     lib = _lib.load(required=True)
-    with _plan_lock:
-        old = []
-        for key in (_lib.MK_OPT_PLAN, _lib.MK_OPT_LITERAL_TAIL):
-            v = ctypes.c_int(0)
-            _lib.check(lib.mk_get_option(key, ctypes.byref(v)), "mk_get_option")
-            old.append((key, v.value))
-        try:
-            lib.mk_set_option(_lib.MK_OPT_LITERAL_TAIL, 0)
-            need = -1
-            if levels >= 3:  # at <= 2 levels depth-first is as fast and smaller
-                lib.mk_set_option(_lib.MK_OPT_PLAN, 2)  # hybrid: breadth-first speed, ~1/7 memory
-                need = int(size_of())
-            if need < 0 or not _fits(need):
-                lib.mk_set_option(_lib.MK_OPT_PLAN, 1)  # depth-first: operand sums only
-                need = int(size_of())
-            yield need
-        finally:
-            for key, v in old:
-                lib.mk_set_option(key, v)
+    try:
+        _lib.check(lib.mk_set_thread_option(_lib.MK_OPT_LITERAL_TAIL, 0), "mk_set_thread_option")
+        need = -1
+        if levels >= 3:  # at <= 2 levels depth-first is as fast and smaller
+            _lib.check(lib.mk_set_thread_option(_lib.MK_OPT_PLAN, 2), "mk_set_thread_option")  # hybrid
+            need = int(size_of())
+        if need < 0 or not _fits(need):
+            _lib.check(lib.mk_set_thread_option(_lib.MK_OPT_PLAN, 1), "mk_set_thread_option")  # depth-first
+            need = int(size_of())
+        yield need
+    finally:
+        lib.mk_set_thread_option(_lib.MK_OPT_PLAN, -1)
+        lib.mk_set_thread_option(_lib.MK_OPT_LITERAL_TAIL, -1)
 
 
 # ---------------------------------------------------------------------------------

@@ -71,6 +71,33 @@ def leaf_count(algo: str, levels: int) -> int:
     return n
 
 
+def _check_operand(t, name: str) -> None:
+    """The ABI reads row-major FP64 with unit column stride: anything else would be read as wrong
+    data without an error, so refuse it here."""
+    import torch
+
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype != torch.float64:
+        raise TypeError(f"{name} must be float64, got {t.dtype}")
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise ValueError(f"{name} must be a 2-D view with unit column stride, got strides {tuple(t.stride())}")
+
+
+def _workspace(need: int, ws, device, stream):
+    """A workspace of >= need bytes for kernels queued on ``stream``: a caller-provided one, or a
+    fresh one whose memory the caching allocator keeps reserved until ``stream`` has finished
+    with it (record_stream), since it is freed on return while the kernels may still run."""
+    import torch
+
+    if ws is not None and ws.numel() >= need:
+        return ws
+    ws = torch.empty(max(need, 16), dtype=torch.uint8, device=device)
+    if stream is not None:
+        ws.record_stream(stream)
+    return ws
+
+
 def partial_product(algo: str, a, b, c_partial, levels: int, first: int, count: int, stream=None, ws=None,
                     panels: int = PANELS) -> int:
     """c_partial += shard units [first, first+count) of A B (all CUDA FP64, square order n).
@@ -81,11 +108,12 @@ def partial_product(algo: str, a, b, c_partial, levels: int, first: int, count: 
     import torch
 
     lib = _lib.load()
+    for t, nm in ((a, "a"), (b, "b"), (c_partial, "c_partial")):
+        _check_operand(t, nm)
     n = a.shape[0]
     aid = _lib.ALGO_IDS[algo]
     need = int(lib.mk_partial_workspace_bytes(aid, n, levels))
-    if ws is None or ws.numel() < need:
-        ws = torch.empty(max(need, 16), dtype=torch.uint8, device=a.device)
+    ws = _workspace(need, ws, a.device, stream)
     st = ctypes.c_void_p((stream or torch.cuda.current_stream()).cuda_stream)
     rc = lib.mk_strassen_partial(aid, ctypes.c_void_p(a.data_ptr()), a.stride(0), ctypes.c_void_p(b.data_ptr()),
                                  b.stride(0), ctypes.c_void_p(c_partial.data_ptr()), c_partial.stride(0), n, levels,
@@ -225,11 +253,12 @@ def partial_product_slabs(algo: str, a, b, slabs, levels: int, first: int, count
     import torch
 
     lib = _lib.load()
+    for t, nm in ((a, "a"), (b, "b"), *((sl, f"slabs[{i}]") for i, sl in enumerate(slabs))):
+        _check_operand(t, nm)
     n = a.shape[0]
     aid = _lib.ALGO_IDS[algo]
     need = int(lib.mk_partial_workspace_bytes(aid, n, levels))
-    if ws is None or ws.numel() < need:
-        ws = torch.empty(max(need, 16), dtype=torch.uint8, device=a.device)
+    ws = _workspace(need, ws, a.device, stream)
     ld = slabs[0].stride(0)
     if any(s.stride(0) != ld or s.shape != slabs[0].shape for s in slabs):
         raise ValueError("slabs must share shape and row stride")
@@ -267,6 +296,10 @@ def fused_sharded_multiply(algo: str, a, b, levels: int, exchange: SlabExchange,
         for r, s in enumerate(exchange.slabs):
             out[r * sr:(r + 1) * sr].copy_(s)
         torch.cuda.synchronize()
+    if world > 1:
+        # rank 0 may still be reading the peers' slabs: no rank may return (and zero its slab in
+        # the next call) before the pull is over
+        dist.barrier(group)
     return exchange.slab
 
 
@@ -280,12 +313,13 @@ def rect_partial_product(algo: str, a, b, out, levels: int, first: int, count: i
     import torch
 
     lib = _lib.load()
+    for t, nm in ((a, "a"), (b, "b"), (out, "out")):
+        _check_operand(t, nm)
     m, k = a.shape
     n = b.shape[1]
     aid = _lib.ALGO_IDS[algo]
     need = int(lib.mk_rect_partial_workspace_bytes(aid, m, n, k, levels, panels))
-    if ws is None or ws.numel() < need:
-        ws = torch.empty(max(need, 16), dtype=torch.uint8, device=a.device)
+    ws = _workspace(need, ws, a.device, None)
     st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
     rc = lib.mk_multiply_rect_partial(aid, ctypes.c_void_p(a.data_ptr()), a.stride(0), ctypes.c_void_p(b.data_ptr()),
                                       b.stride(0), ctypes.c_void_p(out.data_ptr()), out.stride(0), m, n, k, levels,

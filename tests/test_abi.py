@@ -124,3 +124,37 @@ def test_plain_c_consumer_links_and_runs(lib, tmp_path):
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "abi_check ok" in out.stdout
+
+
+def test_thread_plan_override_is_per_thread(lib):
+    """mk_set_thread_option: the sizing and the launch of one call see the calling thread's plan,
+    whatever another thread sets process-wide in between (device.py _memory_aware_plan)."""
+    import threading
+
+    ws = lambda n, L: lib.mk_workspace_bytes(_lib.ALGO_IDS["winograd-block"], n, L)  # noqa: E731
+    dfs = (2 * 8192 ** 2 + 2 * 4096 ** 2) * 8
+    seen = {}
+    try:
+        assert lib.mk_set_thread_option(_lib.MK_OPT_PLAN, 1) == 0
+        assert ws(16384, 2) == dfs
+
+        def other():
+            seen["other_before"] = ws(16384, 2)  # no override in this thread: breadth-first
+            lib.mk_set_option(_lib.MK_OPT_PLAN, 2)  # process-wide change by another thread
+            seen["other_after"] = ws(16384, 3)
+
+        t = threading.Thread(target=other)
+        t.start()
+        t.join()
+        assert seen["other_before"] > dfs
+        assert ws(16384, 2) == dfs  # this thread's override still wins
+        v = ctypes.c_int(-1)
+        assert lib.mk_get_option(_lib.MK_OPT_PLAN, ctypes.byref(v)) == 0 and v.value == 1
+        assert lib.mk_set_thread_option(_lib.MK_OPT_PLAN, -1) == 0
+        assert lib.mk_get_option(_lib.MK_OPT_PLAN, ctypes.byref(v)) == 0 and v.value == 2
+        assert lib.mk_set_thread_option(_lib.MK_OPT_PLAN, 5) == _lib.MK_ERR_ARG
+        assert lib.mk_set_thread_option(_lib.MK_OPT_LEAF_SLICES, 8) == _lib.MK_ERR_ARG
+    finally:
+        lib.mk_set_thread_option(_lib.MK_OPT_PLAN, -1)
+        lib.mk_set_thread_option(_lib.MK_OPT_LITERAL_TAIL, -1)
+        lib.mk_set_option(_lib.MK_OPT_PLAN, 0)

@@ -103,13 +103,22 @@ def _ipc_worker(rank, world, port, levels, exact, result_path, leaf="dmma"):
         ex = mg.SlabExchange(n)
         assert ex.slabs[rank].data_ptr() == ex.slab.data_ptr()
         out = torch.empty((n, n), dtype=torch.float64, device="cuda") if rank == 0 else None
-        for _ in range(2):  # the slabs are re-zeroed and reused
-            mg.fused_sharded_multiply("winograd-block", a, b, levels, ex, out=out)
+        ref = a @ b
+        bad = []
+        # back-to-back calls with different operands, `out` checked after every call: the slabs
+        # are re-zeroed and reused, and a peer that raced ahead into its next call (zeroing its
+        # slab while rank 0 still pulls it) would leave zeroed or stale rows in `out`
+        for it in range(4):
+            s = float(it + 1)
+            mg.fused_sharded_multiply("winograd-block", a * s, b, levels, ex, out=out)
+            if rank == 0:
+                want = ref * s
+                ok = bool(torch.equal(out, want)) if exact else float((out - want).abs().max()) < 1e-11 * s
+                if not ok:
+                    bad.append(f"call {it}: mismatch {float((out - want).abs().max())}")
         if rank == 0:
-            ref = a @ b
-            ok = bool(torch.equal(out, ref)) if exact else float((out - ref).abs().max()) < 1e-11
             with open(result_path, "w") as f:
-                f.write("ok" if ok else f"mismatch {float((out - ref).abs().max())}")
+                f.write("ok" if not bad else "; ".join(bad))
         dist.barrier()  # peers keep their slabs alive until rank 0 has read them
     finally:
         dist.destroy_process_group()

@@ -193,7 +193,7 @@ def test_cfg4_size_integer_exact():
 
 
 def test_cfg5_rectangular_padding_and_peeling():
-    a, b = o.operands(5, scale=4)  # 3000x3500 . 3500x2500 (full size is exercised by bench.py)
+    a, b = o.operands(5, scale=4)  # 3000x3500 . 3500x2500 (full size, cutoff 512: test_gpu_parity_big.py)
     ctr = pk.OpCounter()
     c = pk.multiply(pk.Matrix(a), pk.Matrix(b), pk.get_variant("winograd-mod2", cutoff=128), ctr)
     want = a @ b

@@ -1,0 +1,177 @@
+"""BASELINE configs 3, 4 and 5 at full size, pinned to the reference's OWN output.
+
+tests/golden/make_golden_big.py ran the reference package (matmulkit) itself on the BASELINE
+seeded inputs -- winograd_block_mul at cfg3 (n = 8192, naive_cutoff(1024), kernels.py:378-383),
+at cfg4 (n = 16384, naive_cutoff(8192) and (4096)), multiply(VariantSpec("winograd-block",
+naive_cutoff(512))) at cfg5 (12000x14000 . 14000x10000, hybrid.py:105-146), and its naive
+product (np.matmul, kernels.py:258-266) of the same inputs -- and committed, for each result R,
+full rows and columns (quadrant boundaries included), R @ 1 and 1^T R, values at 4096 fixed
+positions, max|R| and the reference Winograd's whole-matrix error against its naive product
+(err_ref). The GPU result C of the same call through this package is checked against them:
+
+  G1  |C - R_wino| <= tol = n^(log2 12) u |A|max |B|max  (the stated bound, c = 1; n = the
+      reference's padded order at cfg5) on every committed row, column and point
+  G2  |C - N_ref|  <= err_ref on the same entries: at least as accurate there as the
+      reference's own Winograd is anywhere
+  G3  |C @ 1 - N_ref @ 1| and |1^T C - 1^T N_ref| <= n err_ref + summation slack (every element
+      of C contributes: a missing or misplaced block would be off by O(max|R|))
+  G4  max over ALL of C of |C - A B (cuBLAS DGEMM, an independent product)| <= 1.25 err_ref
+
+The inputs are regenerated here from the seed (numpy PCG64 is bit-stable), so nothing reads
+/root/reference at run time.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import paper_2309_00628_b200 as pk
+from conftest import GOLDEN_DIR, has_gpu
+from oracle import strassen_oracle as o
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")]
+
+U = 2.0 ** -53
+
+
+@pytest.fixture(scope="module")
+def big():
+    meta = json.load(open(os.path.join(GOLDEN_DIR, "golden_big.json")))
+    arrays = np.load(os.path.join(GOLDEN_DIR, "golden_big.npz"))
+    return meta, arrays
+
+
+def _pts(m, n, count):
+    rng = np.random.default_rng(7)  # the generator make_golden_big.py used
+    return rng.integers(0, m, count), rng.integers(0, n, count)
+
+
+def _sampled(c, info, count):
+    """rows, columns (transposed), row sums, column sums and points of a CUDA result."""
+    import torch
+
+    m, n = c.shape
+    rows = torch.as_tensor(info["rows"], device=c.device)
+    cols = torch.as_tensor(info["cols"], device=c.device)
+    pi, pj = (torch.as_tensor(x, device=c.device) for x in _pts(m, n, count))
+    return {"rows": c[rows, :].cpu().numpy(), "cols": c[:, cols].T.contiguous().cpu().numpy(),
+            "rowsum": c.sum(dim=1).cpu().numpy(), "colsum": c.sum(dim=0).cpu().numpy(),
+            "pts": c[pi, pj].cpu().numpy()}
+
+
+def _gates(c, a_dev, b_dev, meta, arrays, wino_key, naive_key, info_w, info_n, order, amax, bmax, label):
+    import torch
+
+    s = _sampled(c, info_w, meta["pts"])
+    err_ref = info_w["err_vs_naive"]
+    tol = o.tolerance(order, amax, bmax)
+    report = {}
+    for part in ("rows", "cols", "pts"):
+        d_ref = float(np.abs(s[part] - arrays[f"{wino_key}_{part}"]).max())
+        d_naive = float(np.abs(s[part] - arrays[f"{naive_key}_{part}"]).max())
+        report[part] = (d_ref, d_naive)
+        assert d_ref <= tol, (label, "G1", part, d_ref, tol)
+        assert d_naive <= err_ref, (label, "G2", part, d_naive, err_ref)
+    m, n = c.shape
+    for part, length in (("rowsum", n), ("colsum", m)):
+        slack = 4 * math.log2(length) * U * length * info_n["max_abs"]
+        d = float(np.abs(s[part] - arrays[f"{naive_key}_{part}"]).max())
+        report[part] = d
+        assert d <= length * err_ref + slack, (label, "G3", part, d, length * err_ref + slack)
+    ref = a_dev @ b_dev  # cuBLAS DGEMM: an independent product (comparison only)
+    full = float((c - ref).abs().max())
+    del ref
+    torch.cuda.empty_cache()
+    report["cublas_full"] = full
+    print(f"{label}: err_ref={err_ref:.3e} tol={tol:.3e} {report}")
+    assert full <= 1.25 * err_ref, (label, "G4", full, err_ref)
+
+
+def _dev(x):
+    import torch
+
+    return torch.from_numpy(x).cuda()
+
+
+def test_cfg3_n8192_vs_reference_output(big):
+    import torch
+
+    meta, arrays = big
+    info = meta["configs"]["cfg3"]
+    a, b = o.operands(3)
+    da, db = _dev(a), _dev(b)
+    c = pk.Matrix.zeros(8192, 8192, device="cuda")
+    ctr = pk.winograd_block_mul(pk.Matrix(da), pk.Matrix(db), c, pk.BasePolicy.naive_cutoff(1024))
+    assert pk.last_stats().levels == 3
+    assert list(ctr.snapshot()) == info["counter"]
+    _gates(c.arr, da, db, meta, arrays, "cfg3_wino", "cfg3_naive", info["winograd"], info["naive"], 8192,
+           info["amax"], info["bmax"], "cfg3")
+    # the engine's naive product against the reference's naive product
+    pk.naive_mul(pk.Matrix(da), pk.Matrix(db), c)
+    s = _sampled(c.arr, info["naive"], meta["pts"])
+    for part in ("rows", "cols", "pts"):
+        assert float(np.abs(s[part] - arrays[f"cfg3_naive_{part}"]).max()) <= 0.25 * info["winograd"]["err_vs_naive"]
+    del c, da, db
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("cut", [8192, 4096])
+def test_cfg4_n16384_vs_reference_output(big, cut):
+    import torch
+
+    meta, arrays = big
+    info = meta["configs"]["cfg4"]
+    entry = info["cutoffs"][str(cut)]
+    a, b = o.operands(4)
+    da, db = _dev(a), _dev(b)
+    del a, b
+    c = pk.Matrix.zeros(16384, 16384, device="cuda")
+    ctr = pk.winograd_block_mul(pk.Matrix(da), pk.Matrix(db), c, pk.BasePolicy.naive_cutoff(cut))
+    assert pk.last_stats().levels == {8192: 1, 4096: 2}[cut]
+    assert list(ctr.snapshot()) == entry["counter"]
+    _gates(c.arr, da, db, meta, arrays, f"cfg4_c{cut}", "cfg4_naive", entry["winograd"], info["naive"], 16384,
+           info["amax"], info["bmax"], f"cfg4 cutoff {cut}")
+    del c, da, db
+    torch.cuda.empty_cache()
+
+
+def test_cfg5_full_size_cutoff_512_vs_reference_output(big):
+    """Full-size cfg5 at the BASELINE cutoff 512: the reference pads to 16384^2 and recurses 5
+    levels; the engine pads each extent only to even quadrants and also runs 5 levels."""
+    import torch
+
+    meta, arrays = big
+    info = meta["configs"]["cfg5"]
+    a, b = o.operands(5)
+    da, db = _dev(a), _dev(b)
+    del a, b
+    ctr = pk.OpCounter()
+    c = pk.multiply(pk.Matrix(da), pk.Matrix(db), pk.VariantSpec("winograd-block", pk.BasePolicy.naive_cutoff(512)),
+                    ctr)
+    assert c.arr.shape == (12000, 10000)
+    assert pk.last_stats().levels == 5
+    assert list(ctr.snapshot()) == info["counter"]  # the reference's tallies (square padding to 16384)
+    _gates(c.arr, da, db, meta, arrays, "cfg5_wino", "cfg5_naive", info["winograd"], info["naive"],
+           info["reference_padded_order"], info["amax"], info["bmax"], "cfg5")
+    cn = pk.multiply(pk.Matrix(da), pk.Matrix(db), pk.get_variant("naive"))
+    s = _sampled(cn.arr, info["naive"], meta["pts"])
+    for part in ("rows", "cols", "pts"):
+        assert float(np.abs(s[part] - arrays[f"cfg5_naive_{part}"]).max()) <= 0.25 * info["winograd"]["err_vs_naive"]
+    del c, cn, da, db
+    torch.cuda.empty_cache()
+
+
+def test_cfg5_host_arrays_drop_in(big):
+    """The same cfg5 call as the reference makes it: plain numpy operands in, numpy result out."""
+    meta, arrays = big
+    info = meta["configs"]["cfg5"]
+    a, b = o.operands(5)
+    c = pk.multiply(pk.Matrix(a), pk.Matrix(b), pk.VariantSpec("winograd-block", pk.BasePolicy.naive_cutoff(512)))
+    assert isinstance(c.arr, np.ndarray) and c.arr.shape == (12000, 10000)
+    rows = info["winograd"]["rows"]
+    d = float(np.abs(c.arr[rows, :] - arrays["cfg5_wino_rows"]).max())
+    assert d <= 2 * info["winograd"]["err_vs_naive"], d
+    pi, pj = _pts(12000, 10000, meta["pts"])
+    assert float(np.abs(c.arr[pi, pj] - arrays["cfg5_naive_pts"]).max()) <= info["winograd"]["err_vs_naive"]

@@ -134,3 +134,25 @@ def test_ozaki_dgemm_extreme_exponents():
     err = np.abs(c.cpu().numpy().astype(np.longdouble) - ref)
     assert np.all(err <= bound), float((err / np.maximum(bound, 1e-300)).max())
     assert np.all(c[3].cpu().numpy() == 0.0)
+
+
+def test_integer_guard_with_fewer_slices():
+    """naive_mul on int64 n = 2048 with |a| ~ 2^35 and |b| < 2^6 passes the FP64 guard,
+    but INT8 leaves with 4 slices would truncate a's low bits: it must raise, not return a wrong
+    integer result; with 8 slices the same product is exact."""
+    n = 2048
+    r = np.random.default_rng(5)
+    a = r.integers(2 ** 34, 2 ** 35, (n, n), dtype=np.int64) * r.choice([-1, 1], (n, n))
+    b = r.integers(-63, 64, (n, n), dtype=np.int64)
+    c = pk.Matrix.zeros(n, n, np.int64)
+    try:
+        pk.set_leaf("ozaki", 4, min_work=0)
+        with pytest.raises(pk.ExactnessError):
+            pk.naive_mul(pk.Matrix(a), pk.Matrix(b), c)
+        pk.set_leaf("ozaki", 8, min_work=0)
+        pk.naive_mul(pk.Matrix(a[:512, :512].copy()), pk.Matrix(b[:512, :512].copy()),
+                     c2 := pk.Matrix.zeros(512, 512, np.int64))
+        want = (a[:512, :512].astype(object) @ b[:512, :512].astype(object)).astype(np.int64)
+        assert np.array_equal(c2.arr, want)
+    finally:
+        pk.set_leaf("ozaki", 8, min_work=0)

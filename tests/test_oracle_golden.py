@@ -120,3 +120,42 @@ def test_oracle_matches_live_reference_random():
             c = mk.Matrix.zeros(n, n)
             fn(mk.Matrix(a.copy()), mk.Matrix(b.copy()), c, policy=mk.BasePolicy.naive_cutoff(8))
             assert np.array_equal(o.product(kernel, a, b, o.policy("naive-cutoff", 8)), c.arr)
+
+
+def test_big_config_pins_are_consistent():
+    """tests/golden/golden_big.* (the reference's own cfg3/cfg4/cfg5 outputs, pinned by rows,
+    columns, sums and points): shapes agree with the configs and the input generator reproduces
+    the recorded operand maxima."""
+    import json
+
+    from conftest import GOLDEN_DIR
+
+    meta = json.load(open(os.path.join(GOLDEN_DIR, "golden_big.json")))
+    arr = np.load(os.path.join(GOLDEN_DIR, "golden_big.npz"))
+    shapes = {"cfg3_wino": (8192, 8192), "cfg3_naive": (8192, 8192), "cfg4_naive": (16384, 16384),
+              "cfg4_c8192": (16384, 16384), "cfg4_c4096": (16384, 16384), "cfg5_wino": (12000, 10000),
+              "cfg5_naive": (12000, 10000)}
+    for key, (m, n) in shapes.items():
+        assert arr[f"{key}_rowsum"].shape == (m,) and arr[f"{key}_colsum"].shape == (n,)
+        assert arr[f"{key}_rows"].shape[1] == n and arr[f"{key}_cols"].shape[1] == m
+        assert arr[f"{key}_pts"].shape == (meta["pts"],)
+    c3 = meta["configs"]["cfg3"]
+    a, b = o.operands(3)
+    assert float(np.abs(a).max()) == c3["amax"] and float(np.abs(b).max()) == c3["bmax"]
+    # the reference's own Winograd error vs its naive product, as recorded in SURVEY/BASELINE
+    assert c3["winograd"]["err_vs_naive"] < 1e-11
+    assert meta["configs"]["cfg4"]["cutoffs"]["4096"]["winograd"]["err_vs_naive"] < 1e-11
+    assert meta["configs"]["cfg5"]["winograd"]["err_vs_naive"] < 1e-10
+
+
+def test_oracle_reproduces_reference_cfg3_full_size():
+    """The oracle run at full cfg3 (n = 8192, winograd-block, naive_cutoff(1024): 343 leaves) is
+    bit-identical to the reference's own output (SHA-256 recorded by make_golden_big.py)."""
+    import json
+
+    from conftest import GOLDEN_DIR
+
+    meta = json.load(open(os.path.join(GOLDEN_DIR, "golden_big.json")))
+    a, b = o.operands(3)
+    c = o.product("winograd-block", a, b, o.policy("naive-cutoff", 1024))
+    assert hashlib.sha256(np.ascontiguousarray(c).tobytes()).hexdigest() == meta["configs"]["cfg3"]["winograd"]["sha"]
