@@ -61,17 +61,21 @@ int mk_version(void);
  *   fastest, largest workspace), 1 = depth-first (workspace-minimal: operand sums only, P_i
  *   accumulated straight into C by the epilogue), 2 = hybrid (top level depth-first, each
  *   top-level product breadth-first below it: about 1/7 of the breadth-first workspace).
- * MK_OPT_LITERAL_TAIL (two-temp): 1 = run the last two levels breadth-first under the literal
- *   Table-2 levels (default), 0 = the literal schedule down to the leaves (2 (n/2)^2-style
- *   scratch only, the paper's memory bound).
+ * MK_OPT_LITERAL_TAIL (two-temp): 0 = the literal Table-2 schedule down to the leaves (default:
+ *   two (n/2^(l+1))^2 scratch blocks per level, the paper's memory bound), 1 = the last two levels
+ *   breadth-first under the literal levels (faster at >= 3 levels, more scratch).
  * MK_OPT_LEAF_SLICES: 0 = leaf products on the FP64 tensor cores (DMMA, default); 4..8 = on the
  *   INT8 tensor cores (tcgen05 kind::i8, Ozaki scheme I) with that many digit slices per operand
  *   (see mk_ozaki_dgemm; 8 is more accurate than the DMMA leaf, fewer trade accuracy for speed).
  *   Applies to every leaf product of the engine with m*n*k >= 2^MK_OPT_LEAF_MIN_LOG2.
  * MK_OPT_LEAF_MIN_LOG2: the INT8 leaf's size threshold, log2 of m*n*k (default 29, about 812^3):
- *   smaller leaves stay on DMMA (the per-leaf INT8 kernels are launch- and wave-bound there). */
+ *   smaller leaves stay on DMMA (the per-leaf INT8 kernels are launch- and wave-bound there).
+ * MK_OPT_BFS_GROUP (breadth-first plan, L >= 2): top-level products per pass. 0 = auto (4: two
+ *   passes over the 7 products, each keeping only its own operand sums and outputs -- about half
+ *   the single-pass workspace); 7 or 8 = one pass (largest workspace); 1 = one top-level subtree
+ *   at a time (smallest). Results differ only in the order C's partial sums are added. */
 enum mk_option { MK_OPT_FUSE_PREADDS = 1, MK_OPT_PLAN = 2, MK_OPT_LITERAL_TAIL = 3, MK_OPT_LEAF_SLICES = 4,
-                 MK_OPT_LEAF_MIN_LOG2 = 5 };
+                 MK_OPT_LEAF_MIN_LOG2 = 5, MK_OPT_BFS_GROUP = 6 };
 int mk_set_option(int key, int value);
 int mk_get_option(int key, int* value);
 /* Calling-thread override of MK_OPT_PLAN / MK_OPT_LITERAL_TAIL (value -1 removes it). Applies to

@@ -34,6 +34,7 @@ MK_OPT_PLAN = 2  # 0 breadth-first (default), 1 depth-first (workspace-minimal),
 MK_OPT_LITERAL_TAIL = 3  # two-temp: 1 breadth-first last two levels (default), 0 literal to the leaves
 MK_OPT_LEAF_SLICES = 4  # 0 DMMA leaves (default), 4..8 INT8 tensor-core (Ozaki) leaves with that many slices
 MK_OPT_LEAF_MIN_LOG2 = 5  # INT8 leaves only for products with m*n*k >= 2^v (default 29)
+MK_OPT_BFS_GROUP = 6  # top-level products per breadth-first pass (0 = auto)
 
 # every exported symbol with (restype, argtypes)
 _I64, _VP, _INT, _SZ, _DP = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t, ctypes.POINTER(ctypes.c_double)

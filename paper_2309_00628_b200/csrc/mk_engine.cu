@@ -303,9 +303,9 @@ static std::atomic<int> g_literal_tail{-1}, g_plan_dfs{-1};  // process-wide opt
 static thread_local int t_literal_tail = -1, t_plan = -1;
 static bool literal_bfs_tail() {
   if (t_literal_tail >= 0) return t_literal_tail == 1;
-  if (g_literal_tail < 0) {
+  if (g_literal_tail < 0) {  // default 0: two_temp_winograd keeps the paper's two-temporary bound
     const char* e = getenv("MK_LITERAL_TAIL");
-    g_literal_tail = (e && e[0] == '0') ? 0 : 1;
+    g_literal_tail = (e && e[0] == '1') ? 1 : 0;
   }
   return g_literal_tail == 1;
 }
@@ -320,6 +320,17 @@ static int plan_kind() {
   return g_plan_dfs;
 }
 static bool plan_dfs() { return plan_kind() == 1; }
+// MK_OPT_BFS_GROUP: top-level products per breadth-first pass (env MK_BFS_GROUP). 0 = auto
+// (bfs_group_for), 7 or more = one pass over all of them (the round-1 plan, largest workspace).
+static std::atomic<int> g_bfs_group{-1};
+static int bfs_group_option() {
+  if (g_bfs_group < 0) {
+    const char* e = getenv("MK_BFS_GROUP");
+    const int v = e ? atoi(e) : 0;
+    g_bfs_group = v < 0 ? 0 : v;
+  }
+  return g_bfs_group;
+}
 
 // MK_OPT_LEAF_SLICES: 0 = leaf products on the FP64 tensor cores (DMMA, default); 4..8 = on the
 // INT8 tensor cores with that many Ozaki digit slices (env MK_LEAF_SLICES)
@@ -1252,12 +1263,22 @@ struct Engine {
   struct BNode {
     Blk x, y;                     // operands: single signed blocks (views or materialised sums)
     Blk o{-1, 0, 0, 1.0};         // output block (inner nodes; the root's is the caller's D)
+    bool on = true;               // part of this pass (grouped plan: a subset of the top-level products)
   };
 
   // Breadth-first product of the root operands X (M x K), Y (K x N) into block D (store
   // semantics: D is fully overwritten) with `L` levels.
-  int bfs(int L, int64_t M, int64_t N, int64_t K, Blk X, Blk Y, Blk D) {
+  //
+  // Grouped pass (grp != nullptr, L >= 2): only the top-level products listed in grp and their
+  // subtrees run, and their contributions are added into D's quadrants: root_touched[q] says
+  // whether quadrant q already holds an earlier pass's partial sum (accumulate) or not (store);
+  // it is updated. The workspace of one pass is freed before the next, so the peak scales with
+  // the largest group (run_square's grouped plan).
+  int bfs(int L, int64_t M, int64_t N, int64_t K, Blk X, Blk Y, Blk D, const std::vector<int>* grp = nullptr,
+          bool* root_touched = nullptr) {
     const int np = co->nprod;
+    if (grp && L < 2) return fail(MK_ERR_ARG, "internal: a grouped breadth-first pass needs >= 2 levels");
+    auto in_grp = [&](int p) { return !grp || std::find(grp->begin(), grp->end(), p) != grp->end(); };
     std::vector<std::vector<BNode>> lv(1);
     lv[0].push_back(BNode{X, Y, Blk{-1, 0, 0, 1.0}});
     // ---- operand sums, depth by depth ----
@@ -1272,18 +1293,23 @@ struct Engine {
       // which the kernel's row masking and K-tail zeroing already ignore.
       int arena[2] = {-1, -1};
       int64_t arena_next[2] = {0, 0};
+      for (size_t i = 0; i < cur.size(); ++i)
+        for (int p = 0; p < np; ++p) next[i * np + p].on = cur[i].on && (d > 0 || in_grp(p));
+      int64_t active = 0;
+      for (const BNode& b : cur) active += b.on ? 1 : 0;
       for (int side = 0; side < 2; ++side) {
         int64_t count = 0;
         for (int p = 0; p < np; ++p) {
           const int* cf = side == 0 ? co->a[p] : co->b[p];
           int terms = 0;
           for (int q = 0; q < 4; ++q) terms += cf[q] != 0;
-          if (terms > 1) count += (int64_t)cur.size();
+          if (terms > 1) count += d == 0 ? (in_grp(p) ? 1 : 0) : active;
         }
         const int64_t hr = side == 0 ? hm : hk, hc = side == 0 ? hk : hn;
         if (count) MK_TRY(alloc_slot(count * hr, hc, &arena[side]));
       }
       for (size_t i = 0; i < cur.size(); ++i) {
+        if (!cur[i].on) continue;
         for (int side = 0; side < 2; ++side) {
           const Blk& src = side == 0 ? cur[i].x : cur[i].y;
           const int64_t hr = side == 0 ? hm : hk, hc = side == 0 ? hk : hn;
@@ -1294,6 +1320,7 @@ struct Engine {
             job.lds[q] = bases[src.base].ld;
           }
           for (int p = 0; p < np; ++p) {
+            if (!next[i * np + p].on) continue;
             const int* cf = side == 0 ? co->a[p] : co->b[p];
             int terms = 0, q1 = -1;
             for (int q = 0; q < 4; ++q)
@@ -1323,12 +1350,15 @@ struct Engine {
     // ---- leaves: one batched launch per sibling index ----
     std::vector<BNode>& par = lv[L - 1];
     const int64_t lm = M >> L, ln = N >> L, lk = K >> L;
+    std::vector<size_t> act;  // the parents taking part in this pass
+    for (size_t i = 0; i < par.size(); ++i)
+      if (par[i].on) act.push_back(i);
     if (L == 1) {
       par[0].o = D;
     } else {  // parents' outputs row-stacked in one arena
       int ob;
-      MK_TRY(alloc_slot((int64_t)par.size() * 2 * lm, 2 * ln, &ob, true));
-      for (size_t i = 0; i < par.size(); ++i) par[i].o = Blk{ob, (int64_t)i * 2 * lm, 0, 1.0};
+      MK_TRY(alloc_slot((int64_t)act.size() * 2 * lm, 2 * ln, &ob, true));
+      for (size_t j = 0; j < act.size(); ++j) par[act[j]].o = Blk{ob, (int64_t)j * 2 * lm, 0, 1.0};
     }
     const int slab = consumer_layout() == 16 ? 32 : 64;
     bool touched[4] = {false, false, false, false};
@@ -1368,14 +1398,15 @@ struct Engine {
       }
       bool async_ok = async_epilogue_enabled() && lm % slab == 0 && ln % 16 == 0;
       bool vec_ok = ln % 4 == 0;
-      ents.assign(par.size() * gr.size(), MkBatchEntry{});
+      ents.assign(act.size() * gr.size(), MkBatchEntry{});
       for (size_t gi = 0; gi < gr.size(); ++gi) {
         const int p = gr[gi];
-        for (size_t i = 0; i < par.size(); ++i) {
+        for (size_t ai = 0; ai < act.size(); ++ai) {
+          const size_t i = act[ai];
           const BNode& lf = lv[L][i * np + p];
           if (((lf.x.row | lf.x.col | lf.y.row | lf.y.col) & 1) != 0)
             return fail(MK_ERR_ARG, "leaf order must be >= 2 (odd TMA term offset)");
-          MkBatchEntry& e = ents[gi * par.size() + i];
+          MkBatchEntry& e = ents[gi * act.size() + ai];
           std::memset(&e, 0, sizeof e);
           e.prod.na = e.prod.nb = 1;
           e.prod.nd = dd[gi].nd;
@@ -1400,9 +1431,9 @@ struct Engine {
         launches += (int)ents.size();
         if (dry || no_launch) continue;
         for (size_t gi = 0; gi < gr.size(); ++gi) {
-          for (size_t i = 0; i < par.size(); ++i) {
-            const BNode& lf = lv[L][i * np + gr[gi]];
-            const MkBatchEntry& e = ents[gi * par.size() + i];
+          for (size_t ai = 0; ai < act.size(); ++ai) {
+            const BNode& lf = lv[L][act[ai] * np + gr[gi]];
+            const MkBatchEntry& e = ents[gi * act.size() + ai];
             OzItem it{};
             it.X = oz_operand(Lin{lf.x});
             it.Y = oz_operand(Lin{lf.y});
@@ -1460,13 +1491,48 @@ struct Engine {
       std::vector<BNode>& pa = lv[d - 1];
       const int64_t cm = M >> d, cn = N >> d;
       std::vector<MkXformJob> jobs;
+      if (d - 1 == 0 && grp) {  // grouped pass: this group's products into (or onto) D's quadrants
+        MkXformJob job{};
+        std::vector<int> ps;
+        for (int p = 0; p < np; ++p)
+          if (ch[p].on) ps.push_back(p);
+        job.nsrc = (int)ps.size();
+        for (size_t si = 0; si < ps.size(); ++si) {
+          job.src[si] = ptr_of(ch[ps[si]].o);
+          job.lds[si] = bases[ch[ps[si]].o.base].ld;
+        }
+        for (int q = 0; q < 4; ++q) {
+          bool any = false;
+          for (int p : ps) any = any || co->c[q][p] != 0;
+          if (!any) continue;
+          const int j = job.ndst++;
+          job.dst[j] = ptr_of(Blk{D.base, D.row + (q >> 1) * cm, D.col + (q & 1) * cn, 1.0});
+          job.ldd[j] = bases[D.base].ld;
+          for (size_t si = 0; si < ps.size(); ++si) job.coef[j][si] = (int8_t)co->c[q][ps[si]];
+          if (root_touched[q]) {  // accumulate onto the earlier passes' partial sum
+            if (job.nsrc >= MK_XFORM_MAX) return fail(MK_ERR_ARG, "internal: grouped pass has too many sources");
+            const int si = job.nsrc++;
+            job.src[si] = job.dst[j];
+            job.lds[si] = job.ldd[j];
+            job.coef[j][si] = 1;
+          }
+          root_touched[q] = true;
+        }
+        jobs.push_back(job);
+        MK_TRY(xform_batch(jobs, cm, cn));
+        continue;
+      }
+      std::vector<size_t> pact;
+      for (size_t j = 0; j < pa.size(); ++j)
+        if (pa[j].on) pact.push_back(j);
       int pb_arena = -1;
-      if (d - 1 != 0) MK_TRY(alloc_slot((int64_t)pa.size() * 2 * cm, 2 * cn, &pb_arena, true));
-      for (size_t j = 0; j < pa.size(); ++j) {
+      if (d - 1 != 0) MK_TRY(alloc_slot((int64_t)pact.size() * 2 * cm, 2 * cn, &pb_arena, true));
+      for (size_t jj = 0; jj < pact.size(); ++jj) {
+        const size_t j = pact[jj];
         if (d - 1 == 0) {
           pa[j].o = D;
         } else {
-          pa[j].o = Blk{pb_arena, (int64_t)j * 2 * cm, 0, 1.0};
+          pa[j].o = Blk{pb_arena, (int64_t)jj * 2 * cm, 0, 1.0};
         }
         MkXformJob job{};
         job.nsrc = np;
@@ -1530,6 +1596,39 @@ static bool use_bfs(const Engine& e, int64_t lm, int64_t ln) {
   return plan_kind() == 0;
 }
 
+// Top-level products per breadth-first pass. Auto: 4 at >= 2 levels (two passes for the
+// 7-product tables: each pass keeps only its own products' operand sums and outputs, so the peak
+// workspace is about half of a single pass -- n = 16384, L = 2: 7.5 GiB instead of 14.5 -- while
+// every leaf launch still spans several thousand tiles); the passes add into C.
+static int bfs_group_for(const Engine& e) {
+  const int opt = bfs_group_option();
+  if (opt > 0) return opt;
+  return e.L >= 2 ? 4 : e.co->nprod;
+}
+
+static int run_bfs_grouped(Engine& e, int64_t M, int64_t N, int64_t K) {
+  const Blk A{BASE_A, 0, 0, 1.0}, B{BASE_B, 0, 0, 1.0}, C{BASE_C, 0, 0, 1.0};
+  const int np = e.co->nprod;
+  const int g = bfs_group_for(e);
+  if (g >= np || e.L < 2) return e.bfs(e.L, M, N, K, A, B, C);
+  bool touched[4] = {false, false, false, false};
+  for (int p0 = 0; p0 < np; p0 += g) {
+    std::vector<int> grp;
+    for (int p = p0; p < std::min(np, p0 + g); ++p) grp.push_back(p);
+    const size_t mark = e.ws_used;
+    const int nb_mark = e.nbases;
+    MK_TRY(e.bfs(e.L, M, N, K, A, B, C, &grp, touched));
+    e.ws_used = mark;  // the next pass reuses this pass's workspace (stream-ordered)
+    while (e.nbases > nb_mark) {
+      --e.nbases;
+      e.written.pop_back();
+      e.cell_rows.pop_back();
+      e.cell_cols.pop_back();
+    }
+  }
+  return MK_OK;
+}
+
 static int run_square(Engine& e) {
   const int64_t n = e.n;
   if (plan_kind() == 2 && !e.fuse_preadds && e.leaf_count < 0 && e.L >= 2 && e.algo >= MK_ALGO_STRASSEN &&
@@ -1541,7 +1640,7 @@ static int run_square(Engine& e) {
     return MK_OK;
   }
   if (use_bfs(e, e.leaf_m, e.leaf_n))
-    return e.bfs(e.L, n, n, n, Blk{BASE_A, 0, 0, 1.0}, Blk{BASE_B, 0, 0, 1.0}, Blk{BASE_C, 0, 0, 1.0});
+    return run_bfs_grouped(e, n, n, n);
   if (e.algo == MK_ALGO_TWO_TEMP)
     return e.literal(kTwoTemp, true, e.L, Blk{BASE_A, 0, 0, 1.0}, Blk{BASE_B, 0, 0, 1.0}, Blk{BASE_C, 0, 0, 1.0}, n);
   if (e.algo == MK_ALGO_IN_PLACE)
@@ -1631,6 +1730,11 @@ int mk_set_option(int key, int value) {
     g_leaf_min_log2 = value;
     return MK_OK;
   }
+  if (key == MK_OPT_BFS_GROUP) {
+    if (value < 0 || value > 8) return fail(MK_ERR_ARG, "MK_OPT_BFS_GROUP takes 0 (auto) .. 8");
+    g_bfs_group = value;
+    return MK_OK;
+  }
   return fail(MK_ERR_ARG, "unknown option key");
 }
 
@@ -1662,6 +1766,8 @@ int mk_get_option(int key, int* value) {
     *value = leaf_slices();
   } else if (key == MK_OPT_LEAF_MIN_LOG2) {
     *value = leaf_min_log2();
+  } else if (key == MK_OPT_BFS_GROUP) {
+    *value = bfs_group_option();
   } else {
     return fail(MK_ERR_ARG, "unknown option key");
   }
@@ -2290,7 +2396,7 @@ static int run_rect(int algo, const double* A, int64_t lda, const double* B, int
     const Lin A0{Blk{BASE_A, 0, 0, 1.0}}, B0{Blk{BASE_B, 0, 0, 1.0}}, C0{Blk{BASE_C, 0, 0, 1.0}};
     for (int p = 0; p < e.co->nprod; ++p) MK_TRY(e.top_product_bfs(p, A0, B0, C0, mp / 2, np_ / 2, kp / 2));
   } else if (use_bfs(e, e.leaf_m, e.leaf_n))
-    MK_TRY(e.bfs(levels, mp, np_, kp, Blk{BASE_A, 0, 0, 1.0}, Blk{BASE_B, 0, 0, 1.0}, Blk{BASE_C, 0, 0, 1.0}));
+    MK_TRY(run_bfs_grouped(e, mp, np_, kp));
   else
     MK_TRY(e.fused(levels, Lin{Blk{BASE_A, 0, 0, 1.0}}, Lin{Blk{BASE_B, 0, 0, 1.0}}, Lin{Blk{BASE_C, 0, 0, 1.0}},
                    mp, np_, kp, 0));

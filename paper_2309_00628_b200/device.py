@@ -54,23 +54,28 @@ def require_engine():
     return _lib.load(required=True)
 
 
-def set_plan(plan: str = "breadth-first", two_temp_tail: bool = True) -> None:
+def set_plan(plan: str = "breadth-first", two_temp_tail: bool = False, group: int = 0) -> None:
     """Process-wide engine plan (B200 addition; the reference has no counterpart).
 
-    ``plan``: "breadth-first" (default for >= 2 levels: batched leaf launches, fastest, largest
-    workspace), "hybrid" (top level depth-first, each top-level product breadth-first below it:
-    about 1/7 of the breadth-first workspace) or "depth-first" (workspace-minimal: operand sums
-    only, each P_i accumulated straight into C by the leaf epilogue). ``two_temp_tail``: two_temp_winograd runs its last two
-    levels breadth-first (default) or the literal Table-2 schedule down to the leaves (the paper's
-    2 x (n/2)^2-per-level scratch bound). Results are unchanged on integer data; float results
-    differ only in summation order. Modeled OpCounter values never change.
+    ``plan``: "breadth-first" (default for >= 2 levels: batched leaf launches, fastest),
+    "hybrid" (top level depth-first, each top-level product breadth-first below it) or
+    "depth-first" (workspace-minimal: operand sums only, each P_i accumulated straight into C by
+    the leaf epilogue). ``group`` (breadth-first): top-level products per pass -- 0 = auto (4:
+    two passes, about half the single-pass workspace), 7 = one pass (largest workspace), 1 = one
+    top-level subtree at a time. ``two_temp_tail``: two_temp_winograd runs the literal Table-2
+    schedule down to the leaves (default: the paper's two-temporary bound) or, if True, its last two
+    levels breadth-first (faster at >= 3 levels, more scratch). Results are unchanged on integer
+    data; float results differ only in summation order. Modeled OpCounter values never change.
     """
     kinds = {"breadth-first": 0, "depth-first": 1, "hybrid": 2}
     if plan not in kinds:
         raise ValueError(f"plan must be one of {sorted(kinds)}, got {plan!r}")
+    if not 0 <= int(group) <= 8:
+        raise ValueError(f"group must be in [0, 8], got {group!r}")
     lib = _lib.load(required=True)
     _lib.check(lib.mk_set_option(_lib.MK_OPT_PLAN, kinds[plan]), "mk_set_option")
     _lib.check(lib.mk_set_option(_lib.MK_OPT_LITERAL_TAIL, 1 if two_temp_tail else 0), "mk_set_option")
+    _lib.check(lib.mk_set_option(_lib.MK_OPT_BFS_GROUP, int(group)), "mk_set_option")
 
 
 def set_leaf(kind: str = "dmma", slices: int = 8, min_work: int = 2 ** 29) -> None:
