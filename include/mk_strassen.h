@@ -216,6 +216,23 @@ int mk_multiply_rect_partial(int algo, const double* A, int64_t lda, const doubl
                              int64_t ldc, int64_t m, int64_t n, int64_t k, int levels, int first, int count,
                              int panels, void* ws, size_t ws_bytes, void* stream);
 
+/* Multi-GPU product in ONE process (the single-process counterpart of the torch.distributed
+ * path; SURVEY.md 8(b) "mk_multi_gpu_winograd"): C = A B, algo as mk_strassen (fused kinds),
+ * square order n = 2^j, `levels` >= 1. A, B and C are device memory of devices[0]. The 7^L leaf
+ * products, split into 8 row panels each, are dealt out to the ngpu devices in contiguous
+ * level-major ranges (balanced to one panel); rank r >= 1 receives by peer copies (NVLink) only
+ * the top-level operand quadrants its panels read, accumulates its partial C locally, and
+ * device 0 adds the partials into C in rank order, reading them over peer memory. ws[r] /
+ * ws_bytes[r]: workspace on devices[r] of mk_multi_gpu_workspace_bytes(algo, n, levels, r, ngpu)
+ * bytes; streams[r]: a stream of devices[r]. Work is enqueued asynchronously (ordered by events);
+ * synchronise streams[0] before reading C. A device may appear more than once (ranks sharing a
+ * GPU: the same code path on one device). Peer access between devices[0] and the others is
+ * enabled on the way. */
+size_t mk_multi_gpu_workspace_bytes(int algo, int64_t n, int levels, int rank, int ngpu);
+int mk_multi_gpu_winograd(int algo, int ngpu, const int* devices, const double* A, int64_t lda, const double* B,
+                          int64_t ldb, double* C, int64_t ldc, int64_t n, int levels, void* const* ws,
+                          const size_t* ws_bytes, void* const* streams);
+
 /* Enable NVLink peer access from the current device to peer_device (idempotent). */
 int mk_enable_peer_access(int peer_device);
 

@@ -31,7 +31,7 @@ ALGO_IDS = {
 }
 MK_OPT_FUSE_PREADDS = 1
 MK_OPT_PLAN = 2  # 0 breadth-first (default), 1 depth-first (workspace-minimal), 2 hybrid
-MK_OPT_LITERAL_TAIL = 3  # two-temp: 1 breadth-first last two levels (default), 0 literal to the leaves
+MK_OPT_LITERAL_TAIL = 3  # two-temp: 0 literal to the leaves (default), 1 breadth-first last two levels
 MK_OPT_LEAF_SLICES = 4  # 0 DMMA leaves (default), 4..8 INT8 tensor-core (Ozaki) leaves with that many slices
 MK_OPT_LEAF_MIN_LOG2 = 5  # INT8 leaves only for products with m*n*k >= 2^v (default 29)
 MK_OPT_BFS_GROUP = 6  # top-level products per breadth-first pass (0 = auto)
@@ -77,6 +77,9 @@ SIGNATURES = {
     "mk_overlap_order": (_INT, [_INT, ctypes.POINTER(_INT), ctypes.POINTER(_INT)]),
     "mk_strassen_partial": (_INT, [_INT, _VP, _I64, _VP, _I64, _VP, _I64, _I64, _INT, _INT, _INT, _INT, _VP, _SZ,
                                    _VP]),
+    "mk_multi_gpu_workspace_bytes": (_SZ, [_INT, _I64, _INT, _INT, _INT]),
+    "mk_multi_gpu_winograd": (_INT, [_INT, _INT, ctypes.POINTER(_INT), _VP, _I64, _VP, _I64, _VP, _I64, _I64, _INT,
+                                     ctypes.POINTER(_VP), ctypes.POINTER(_SZ), ctypes.POINTER(_VP)]),
 }
 
 

@@ -45,6 +45,10 @@ cudaError_t measure_dmma_peak(double* tflops_out, cudaStream_t st);
 cudaError_t launch_fused_product(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
                                  const MkGemmArgs& args, const MkProduct& prod, cudaStream_t stream);
 int consumer_layout();
+// Tile width (64 or 128) the persistent kernel will use for a launch, and the row height of the
+// TMA epilogue's C boxes that launch needs (32 for narrow tiles and the 16-warp layout, else 64).
+int persistent_tile_n(int64_t tiles_m, int64_t N, int nprod);
+int epilogue_box_rows(int64_t M, int64_t N, int nprod, bool single_terms);
 
 // Launch `nprod` single-term products of identical M x N x K (entries already in device memory).
 cudaError_t launch_product_batch(const MkBatchEntry* entries_dev, int nprod, const MkGemmArgs& args,

@@ -417,19 +417,23 @@ struct TableRing {
   int device = -1;
   std::map<cudaStream_t, cudaEvent_t> last;
 };
-static TableRing& table_ring() {
-  static TableRing r;
-  return r;
+static TableRing& table_ring(int dev) {  // one ring per device (multi-device callers switch devices)
+  static std::mutex mu;
+  static std::map<int, TableRing*> rings;
+  std::lock_guard<std::mutex> lk(mu);
+  TableRing*& r = rings[dev];
+  if (!r) r = new TableRing();
+  return *r;
 }
 // Copy a plan table to the device through the ring; false if the ring is unavailable (the caller
 // then copies from pageable memory). Staging, copy and event happen under one lock.
 static bool table_ring_copy(void* dev_dst, const void* host, size_t bytes, cudaStream_t st, cudaError_t* err) {
   constexpr size_t kCap = 64u << 20;
-  TableRing& r = table_ring();
-  std::lock_guard<std::mutex> lk(r.mu);
   int dev = 0;
   cudaGetDevice(&dev);
-  if (r.device != dev) {  // one ring per process, re-made on a device switch
+  TableRing& r = table_ring(dev);
+  std::lock_guard<std::mutex> lk(r.mu);
+  if (r.device != dev) {
     for (auto& kv : r.last) cudaEventDestroy(kv.second);
     r.last.clear();
     if (r.buf) cudaFreeHost(r.buf);
@@ -740,7 +744,7 @@ struct Engine {
     CUtensorMap tmA, tmB, tmC;
     MK_TRY(cached_map(bx, 0, &tmA));
     MK_TRY(cached_map(by, 1, &tmB));
-    const int slab = consumer_layout() == 16 ? 32 : 64;  // rows per consumer warp
+    const int slab = epilogue_box_rows(M, N, 1, p.na == 1 && p.nb == 1);  // rows per consumer warp's epilogue box
     bool async_ok = async_epilogue_enabled() && nslab == 0 && (M % slab == 0) && (N % 16 == 0) &&
                     (reinterpret_cast<uintptr_t>(bases[bd].ptr) % 16 == 0) && (bases[bd].ld % 2 == 0);
     for (int i = 0; i < p.nd; ++i) async_ok = async_ok && ((D[i].row | D[i].col) % 2 == 0);
@@ -1360,7 +1364,6 @@ struct Engine {
       MK_TRY(alloc_slot((int64_t)act.size() * 2 * lm, 2 * ln, &ob, true));
       for (size_t j = 0; j < act.size(); ++j) par[act[j]].o = Blk{ob, (int64_t)j * 2 * lm, 0, 1.0};
     }
-    const int slab = consumer_layout() == 16 ? 32 : 64;
     bool touched[4] = {false, false, false, false};
     // Siblings conflict only through a shared output quadrant: colour them greedily (in table
     // order) so that each launch holds products with disjoint quadrants -- e.g. Winograd
@@ -1396,6 +1399,7 @@ struct Engine {
         MK_TRY(product(Lin{lf.x}, Lin{lf.y}, Dl, lm, ln, lk));
         continue;
       }
+      const int slab = epilogue_box_rows(lm, ln, (int)(act.size() * gr.size()), true);
       bool async_ok = async_epilogue_enabled() && lm % slab == 0 && ln % 16 == 0;
       bool vec_ok = ln % 4 == 0;
       ents.assign(act.size() * gr.size(), MkBatchEntry{});
@@ -2276,6 +2280,152 @@ int mk_strassen_partial(int algo, const double* A, int64_t lda, const double* B,
   return run_square(e);
 }
 
+// ---- multi-GPU product in one process (SURVEY.md 8(b) mk_multi_gpu_winograd) ----------------
+// The shard units of mk_strassen_partial (leaf row panels, contiguous level-major ranges) spread
+// over `ngpu` devices of this process. A, B and C live on devices[0]. Rank r >= 1 gets over
+// NVLink (peer copies) only the top-level operand quadrants its units read, accumulates its
+// partial C in its own workspace, and device 0 adds every partial into C in rank order (peer
+// loads over NVLink; deterministic). Everything is enqueued on the callers' streams, ordered by
+// events; the call returns once enqueued.
+static constexpr int kMultiPanels = 8;
+
+static void multi_units(int algo, int levels, int ngpu, int rank, int* first, int* count) {
+  const int total = mk_product_count(algo, levels) * kMultiPanels;
+  const int base = total / ngpu, extra = total % ngpu;
+  *first = rank * base + std::min(rank, extra);
+  *count = base + (rank < extra ? 1 : 0);
+}
+
+static void multi_quadrants(int algo, int levels, int first, int count, bool qa[4], bool qb[4]) {
+  const Coeffs& co = coeffs_for(algo);
+  int per_parent = kMultiPanels;
+  for (int i = 1; i < levels; ++i) per_parent *= co.nprod;
+  for (int q = 0; q < 4; ++q) qa[q] = qb[q] = false;
+  if (count <= 0) return;
+  for (int p = first / per_parent; p <= (first + count - 1) / per_parent; ++p)
+    for (int q = 0; q < 4; ++q) {
+      qa[q] = qa[q] || co.a[p][q] != 0;
+      qb[q] = qb[q] || co.b[p][q] != 0;
+    }
+}
+
+size_t mk_multi_gpu_workspace_bytes(int algo, int64_t n, int levels, int rank, int ngpu) {
+  if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_WINOGRAD_KNUTH_8CALL || levels < 1 || ngpu < 1 || rank < 0 ||
+      rank >= ngpu || !is_pow2(n) || ((n >> levels) % kMultiPanels) != 0 || (((n >> levels) / kMultiPanels) % 2))
+    return 0;
+  const size_t part = mk_partial_workspace_bytes(algo, n, levels);
+  if (rank == 0) return part;
+  const size_t block = ((size_t)n * n * 8 + 1023) / 1024 * 1024;
+  return 3 * block + part;  // A copy, B copy, partial C, partial-product workspace
+}
+
+int mk_multi_gpu_winograd(int algo, int ngpu, const int* devices, const double* A, int64_t lda, const double* B,
+                          int64_t ldb, double* C, int64_t ldc, int64_t n, int levels, void* const* ws,
+                          const size_t* ws_bytes, void* const* streams) {
+  g_last_error.clear();
+  if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_WINOGRAD_KNUTH_8CALL)
+    return fail(MK_ERR_ARG, "multi-GPU products support the fused algorithms only");
+  if (ngpu < 1 || ngpu > 64 || !devices || !ws || !ws_bytes || !streams) return fail(MK_ERR_ARG, "bad device list");
+  if (!is_pow2(n) || levels < 1 || (n >> levels) < 2 * kMultiPanels || ((n >> levels) % kMultiPanels) != 0)
+    return fail(MK_ERR_DIMENSION, "order must be a power of two with leaf rows divisible into 8 even panels");
+  if (lda < n || ldb < n || ldc < n) return fail(MK_ERR_DIMENSION, "leading dimension smaller than the order");
+  if (overlaps(C, ldc, n, n, A, lda, n, n) || overlaps(C, ldc, n, n, B, ldb, n, n))
+    return fail(MK_ERR_ALIAS, "output view must not alias an input view");
+  for (int r = 0; r < ngpu; ++r)
+    if (ws_bytes[r] < mk_multi_gpu_workspace_bytes(algo, n, levels, r, ngpu) || (!ws[r] && ws_bytes[r]))
+      return fail(MK_ERR_WORKSPACE, "workspace of rank " + std::to_string(r) + " too small");
+  int dev0 = 0;
+  MK_CUDA_TRY(cudaGetDevice(&dev0));
+  struct Restore {
+    int d;
+    ~Restore() { cudaSetDevice(d); }
+  } restore{dev0};
+  const size_t block = ((size_t)n * n * 8 + 1023) / 1024 * 1024;
+  const int64_t h = n / 2;
+  std::vector<cudaEvent_t> evs;
+  auto event = [&](cudaEvent_t* e) -> int {
+    MK_CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    evs.push_back(*e);
+    return MK_OK;
+  };
+  struct Cleanup {
+    std::vector<cudaEvent_t>* v;
+    ~Cleanup() {
+      for (cudaEvent_t e : *v) cudaEventDestroy(e);  // destroying a recorded event is deferred safely
+    }
+  } cleanup{&evs};
+  cudaStream_t s0 = static_cast<cudaStream_t>(streams[0]);
+  MK_CUDA_TRY(cudaSetDevice(devices[0]));
+  cudaEvent_t in_ready;
+  MK_TRY(event(&in_ready));
+  MK_CUDA_TRY(cudaEventRecord(in_ready, s0));
+  std::vector<const double*> partials(ngpu, nullptr);
+  partials[0] = C;
+  std::vector<cudaEvent_t> done(ngpu, nullptr);
+  for (int r = 0; r < ngpu; ++r) {
+    MK_CUDA_TRY(cudaSetDevice(devices[r]));
+    if (r > 0 && devices[r] != devices[0]) MK_TRY(mk_enable_peer_access(devices[0]));
+    cudaStream_t sr = static_cast<cudaStream_t>(streams[r]);
+    int first = 0, count = 0;
+    multi_units(algo, levels, ngpu, r, &first, &count);
+    const double *Ar = A, *Br = B;
+    double* Cr = C;
+    int64_t la = lda, lb = ldb, lc = ldc;
+    char* wsr = static_cast<char*>(ws[r]);
+    size_t wsb = ws_bytes[r];
+    if (r > 0) {
+      double* a_copy = reinterpret_cast<double*>(wsr);
+      double* b_copy = reinterpret_cast<double*>(wsr + block);
+      Cr = reinterpret_cast<double*>(wsr + 2 * block);
+      wsr += 3 * block;
+      wsb -= 3 * block;
+      MK_CUDA_TRY(cudaStreamWaitEvent(sr, in_ready, 0));
+      bool qa[4], qb[4];
+      multi_quadrants(algo, levels, first, count, qa, qb);
+      for (int q = 0; q < 4; ++q) {  // peer copies of the quadrants this rank's units read
+        const int64_t r0 = (q >> 1) * h, c0 = (q & 1) * h;
+        if (qa[q])
+          MK_CUDA_TRY(cudaMemcpy2DAsync(a_copy + r0 * n + c0, n * 8, A + r0 * lda + c0, lda * 8, h * 8, h,
+                                        cudaMemcpyDefault, sr));
+        if (qb[q])
+          MK_CUDA_TRY(cudaMemcpy2DAsync(b_copy + r0 * n + c0, n * 8, B + r0 * ldb + c0, ldb * 8, h * 8, h,
+                                        cudaMemcpyDefault, sr));
+      }
+      Ar = a_copy;
+      Br = b_copy;
+      la = lb = lc = n;
+      partials[r] = Cr;
+    }
+    MK_CUDA_TRY(cudaMemset2DAsync(Cr, lc * 8, 0, n * 8, n, sr));
+    if (count)
+      MK_TRY(mk_strassen_partial(algo, Ar, la, Br, lb, Cr, lc, n, levels, first, count, kMultiPanels, wsr, wsb, sr));
+    if (r > 0) {
+      MK_TRY(event(&done[r]));
+      MK_CUDA_TRY(cudaEventRecord(done[r], sr));
+    }
+  }
+  // device 0: C += partial_1 + ... + partial_{g-1}, in rank order, reading peer memory
+  MK_CUDA_TRY(cudaSetDevice(devices[0]));
+  for (int r = 1; r < ngpu; ++r) MK_CUDA_TRY(cudaStreamWaitEvent(s0, done[r], 0));
+  for (int r0 = 1; r0 < ngpu; r0 += MK_COMBINE_MAX - 1) {
+    const double* sp[MK_COMBINE_MAX];
+    int64_t lds[MK_COMBINE_MAX];
+    double sg[MK_COMBINE_MAX];
+    int ns = 0;
+    sp[ns] = C;
+    lds[ns] = ldc;
+    sg[ns++] = 1.0;
+    for (int r = r0; r < ngpu && ns < MK_COMBINE_MAX; ++r) {
+      sp[ns] = partials[r];
+      lds[ns] = n;
+      sg[ns++] = 1.0;
+    }
+    MK_CUDA_TRY(launch_combine(C, ldc, sp, lds, sg, ns, n, n, s0));
+    ++g_launch_count;
+  }
+  return MK_OK;
+}
+
 int mk_enable_peer_access(int peer_device) {
   g_last_error.clear();
   int dev = 0;
@@ -2333,13 +2483,17 @@ int mk_strassen_partial_slabs(int algo, const double* A, int64_t lda, const doub
 static int run_rect(int algo, const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                     int64_t m, int64_t n, int64_t k, int levels, void* ws, size_t ws_bytes, cudaStream_t st,
                     bool dry, size_t* need_out, int64_t first = -1, int64_t count = 0, int panels = 1) {
-  // every level halves each extent and the leaves need even extents (16-byte TMA origins) and
-  // a leaf N divisible by 4 (32-byte epilogue rows): pad m, k to 2^(L+1) and n to 2^(L+2);
-  // shard mode also needs even row panels: m to 2 * panels * 2^L
+  // every level halves each extent; the leaves need even K (16-byte TMA origins), and the TMA
+  // epilogue needs leaf rows in whole 64-row boxes and leaf columns in whole 16-column boxes:
+  // pad k to 2^(L+1), m to 64 * 2^L and n to 16 * 2^L (at L >= 1; the leaf GEMM's 128 x 64/128
+  // tiles compute those rows and columns anyway, so only the block additions see the extra
+  // padding, e.g. cfg5 at L = 5: 12288 x 14016 x 10240); shard mode also needs even row panels:
+  // m to 2 * panels * 2^L
   const bool shard = first >= 0;
-  const int64_t qm = (int64_t)2 << levels, qn = (int64_t)4 << levels;
+  const int64_t qk = (int64_t)2 << levels;
+  const int64_t qm = levels >= 1 ? (int64_t)64 << levels : 2, qn = levels >= 1 ? (int64_t)16 << levels : 4;
   const int64_t qmm = shard ? std::max<int64_t>(qm, ((int64_t)2 * panels) << levels) : qm;
-  const int64_t mp = (m + qmm - 1) / qmm * qmm, np_ = (n + qn - 1) / qn * qn, kp = (k + qm - 1) / qm * qm;
+  const int64_t mp = (m + qmm - 1) / qmm * qmm, np_ = (n + qn - 1) / qn * qn, kp = (k + qk - 1) / qk * qk;
   size_t off = 0;
   auto carve = [&](size_t elems) {
     double* p = dry ? reinterpret_cast<double*>(0x1000 + off) : reinterpret_cast<double*>(static_cast<char*>(ws) + off);

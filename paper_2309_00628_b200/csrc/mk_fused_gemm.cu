@@ -23,8 +23,11 @@
 // (g>>1) + 4*(g&1).  A lane reads one 16B chunk of a B row holding columns 2g, 2g+1, which
 // feeds two n-fragments per LDS.128; the k order (2q+8t+e) matches A's.
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <atomic>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <type_traits>
 #include "mk_device.cuh"
 #include "mk_plan.h"
@@ -541,7 +544,27 @@ struct PLayout {
   static constexpr int kConsumerRegs = kThreads == 384 ? 224 : 112;
 };
 
-template <int MT, int BN>
+// Work units of one persistent CTA: its data-parallel tiles (t = b, b + G, ... < sk_tile0, whole
+// K), then its share [lo(b), lo(b + 1)) of the stream-K iterations (tile-major, k-minor) of the
+// tiles from sk_tile0 on, as segments (tile, [kb, ke)). Producer and consumers walk the same
+// sequence. The launcher guarantees (total - sk_tile0) * KT * G < 2^31.
+__device__ __forceinline__ int sk_total(const MkGemmArgs& a) { return a.tiles_per_prod * (a.batch ? a.nprod : 1); }
+__device__ __forceinline__ int sk_kt(const MkGemmArgs& a) { return (a.K + MK_BK - 1) / MK_BK; }
+__device__ __forceinline__ int sk_tile0(const MkGemmArgs& a) { return min(a.sk_tile0, sk_total(a)); }
+__device__ __forceinline__ int sk_lo(const MkGemmArgs& a, int c) {
+  return (sk_total(a) - sk_tile0(a)) * sk_kt(a) * c / (int)gridDim.x;
+}
+__device__ __forceinline__ bool sk_unit(const MkGemmArgs& a, int it, int& t, int& kb, int& ke) {
+  const int hi = sk_lo(a, (int)blockIdx.x + 1);
+  if (it >= hi) return false;
+  const int KT = sk_kt(a);
+  const int tr = it / KT;
+  t = sk_tile0(a) + tr;
+  kb = it - tr * KT;
+  ke = min(KT, kb + (hi - it));
+  return true;
+}
+template <int MT, int BN, bool SK>
 __global__ void __launch_bounds__(PLayout<MT, BN>::kThreads, 1)
 persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const __grid_constant__ CUtensorMap tmB_param,
                           const __grid_constant__ CUtensorMap tmC_param, const MkGemmArgs args,
@@ -590,7 +613,7 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
     int s = 0;            // ring slot of the next stage (carried across tiles)
     uint32_t eph = 0;     // parity of the empty-barrier phase to wait for (first lap: no wait)
     bool first_lap = true;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    auto unit = [&](const int t, const int kb, const int ke) {
       int pi, m0, n0;
       tile_of(t, pi, m0, n0);
       const MkBatchEntry* ent = args.batch ? args.batch + pi : nullptr;
@@ -599,7 +622,7 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
       const CUtensorMap* tmB = ent ? &ent->tmB : &tmB_param;
       const int ar = m0 + prod.a[0].row, ac = prod.a[0].col;
       const int br = prod.b[0].row, bc = n0 + prod.b[0].col;
-      for (int k = 0; k < KT; ++k) {
+      for (int k = kb; k < ke; ++k) {
         if (!first_lap) mbar_wait(&empty_bar[s], eph);
         uint8_t* opA = smem_gen + (size_t)s * PL::kStageBytes;
         uint8_t* opB = opA + MK_TILE_BYTES;
@@ -616,6 +639,16 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
             eph ^= 1u;
         }
       }
+    };
+    if constexpr (!SK) {  // data-parallel tiles [0, min(total, sk_tile0))
+      const int lim = min(total, args.sk_tile0);
+      for (int t = blockIdx.x; t < lim; t += gridDim.x) unit(t, 0, KT);
+    } else {  // stream-K segments of tiles [sk_tile0, total)
+      const int tile0 = sk_tile0(args);
+      int t, kb, ke;
+      for (bool live = sk_unit(args, sk_lo(args, blockIdx.x), t, kb, ke); live;
+           live = sk_unit(args, (t - tile0) * KT + ke, t, kb, ke))
+        unit(t, kb, ke);
     }
     return;
   }
@@ -728,17 +761,16 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
   int rs = 0;         // ring slot of the next stage (carried across tiles)
   uint32_t fph = 0;   // parity of the full-barrier phase to wait for
 
-  for (int t = blockIdx.x; t < total; t += gridDim.x) {
-    int pi, m0, n0;
-    tile_of(t, pi, m0, n0);
-    const MkBatchEntry* ent = args.batch ? args.batch + pi : nullptr;
-    const MkProduct& prod = ent ? ent->prod : prod_param;
+  // One unit: tile t, k-stages [kb, ke). Instantiated twice below -- data-parallel tiles (kb = 0,
+  // ke = KT: the original loop, no extra live registers next to the 128-register accumulator)
+  // and stream-K segments.
+  auto unit = [&](const int t, const int kb, const int ke) {
 #pragma unroll
     for (int i = 0; i < MT; ++i)
 #pragma unroll
       for (int f = 0; f < 4; ++f) acc[i][f][0] = acc[i][f][1] = 0.0;
     master_live = false;
-    for (int kt = 0; kt < KT; ++kt) {
+    for (int kt = kb; kt < ke; ++kt) {
       mbar_wait(&full_bar[rs], fph);
       const uint8_t* sA = smem_gen + (size_t)rs * PL::kStageBytes;
       const uint8_t* sB = sA + MK_TILE_BYTES;
@@ -752,8 +784,12 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
         rs = 0;
         fph ^= 1u;
       }
-      if (chunk && (kt + 1) % chunk == 0 && kt + 1 < KT) fold_to_tmem();
+      if (chunk && (kt + 1 - kb) % chunk == 0 && kt + 1 < ke) fold_to_tmem();
     }
+    int pi, m0, n0;
+    tile_of(t, pi, m0, n0);
+    const MkBatchEntry* ent = args.batch ? args.batch + pi : nullptr;
+    const MkProduct& prod = ent ? ent->prod : prod_param;
     if (chunk && master_live) {
 #pragma unroll
       for (int pc = 0; pc < kPieces; ++pc) {
@@ -767,6 +803,72 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
           a = __hiloint2double((int)w[2 * u + 1], (int)w[2 * u]) + a;
         }
       }
+    }
+
+    // ---- stream-K: a tile split over several CTAs is finished by whichever segment arrives last
+    // (per warp: each warp's 64 x 32 piece is independent). Every segment publishes its partial
+    // sum in its own slot (2 per CTA: its head segment and its other one) and counts up the
+    // tile's flag; the last arriver adds all slots in k order -- deterministic, and nobody waits.
+    if (SK && (kb > 0 || ke < KT)) {
+      // slot layout [e/2][lane] of double2: every access is one 512-byte warp transaction
+      constexpr int kPairs = MT * 4;  // accumulator double pairs per thread
+      const size_t slot_pairs = (size_t)PL::kConsumerWarps * kPairs * 32;
+      double2* const base2 = reinterpret_cast<double2*>(args.sk_partial);
+      auto slot_of = [&](int cta, bool head) {
+        return base2 + (size_t)(2 * cta + (head ? 1 : 0)) * slot_pairs + (size_t)cw * kPairs * 32 + lane;
+      };
+      {
+        double2* mine = slot_of(blockIdx.x, kb == 0);
+#pragma unroll
+        for (int e2 = 0; e2 < kPairs; ++e2) {
+          const int e = 2 * e2;
+          __stcg(mine + e2 * 32, make_double2(acc[e >> 3][(e >> 1) & 3][e & 1], acc[e >> 3][(e >> 1) & 3][(e & 1) + 1]));
+        }
+      }
+      // CTAs holding the tile's segments: b0 (head) .. b1
+      const int G = gridDim.x, tile0 = sk_tile0(args);
+      const int tile_begin = (t - tile0) * KT, tile_end = tile_begin + KT;
+      int b0 = (int)((long long)tile_begin * G / ((long long)(total - tile0) * KT));
+      while (b0 > 0 && sk_lo(args, b0) > tile_begin) --b0;
+      while (b0 + 1 < G && sk_lo(args, b0 + 1) <= tile_begin) ++b0;
+      int b1 = b0, nseg = 1;  // CTAs with a non-empty share of the tile: b0 and the non-empty ones up to b1
+      while (b1 + 1 < G && sk_lo(args, b1 + 1) < tile_end) {
+        ++b1;
+        if (sk_lo(args, b1) < sk_lo(args, b1 + 1)) ++nseg;
+      }
+      int32_t* flag = args.sk_flags + (size_t)(t - tile0) * PL::kConsumerWarps + cw;
+      __syncwarp();  // the warp's partial stores precede lane 0's release below
+      int old = 0;
+      if (lane == 0)
+        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(flag) : "memory");
+      old = __shfl_sync(0xffffffffu, old, 0);
+      if (old != nseg - 1) return;  // another segment finishes this piece
+      // last arriver: sum the segments in k order (head first) -- deterministic. A head that
+      // arrives last (the usual case: heads close their CTA's range) keeps its own sum in registers.
+      auto add_slot = [&](const double2* sl) {
+#pragma unroll
+        for (int e2 = 0; e2 < kPairs; ++e2) {
+          const double2 v = __ldcg(sl + e2 * 32);
+          const int e = 2 * e2;
+          acc[e >> 3][(e >> 1) & 3][e & 1] += v.x;
+          acc[e >> 3][(e >> 1) & 3][(e & 1) + 1] += v.y;
+          if ((e2 & 15) == 15) asm volatile("" ::: "memory");  // <= 16 loads in flight (registers)
+        }
+      };
+      if (kb != 0) {  // reload the head's sum
+        const double2* hs = slot_of(b0, true);
+#pragma unroll
+        for (int e2 = 0; e2 < kPairs; ++e2) {
+          const double2 v = __ldcg(hs + e2 * 32);
+          const int e = 2 * e2;
+          acc[e >> 3][(e >> 1) & 3][e & 1] = v.x;
+          acc[e >> 3][(e >> 1) & 3][(e & 1) + 1] = v.y;
+          if ((e2 & 15) == 15) asm volatile("" ::: "memory");
+        }
+      }
+      for (int c = b0 + 1; c <= b1; ++c)
+        if (sk_lo(args, c) < sk_lo(args, c + 1)) add_slot(slot_of(c, false));
+      if (lane == 0) *flag = 0;  // ready for the next launch on this stream
     }
 
     // ---- epilogue: every destination of the product, signs grouped into two passes ----
@@ -857,6 +959,16 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
         }
       }
     }
+  };
+  if constexpr (!SK) {
+    const int lim = min(total, args.sk_tile0);
+    for (int t = blockIdx.x; t < lim; t += gridDim.x) unit(t, 0, KT);
+  } else {
+    const int tile0 = sk_tile0(args);
+    int t, kb, ke;
+    for (bool live = sk_unit(args, sk_lo(args, blockIdx.x), t, kb, ke); live;
+         live = sk_unit(args, (t - tile0) * KT + ke, t, kb, ke))
+      unit(t, kb, ke);
   }
   if (lane == 0) bulk_wait_read_all();  // the boxes must stay valid until the TMA unit has read them
   __syncwarp();
@@ -921,26 +1033,84 @@ static int sm_count() {
   }
   return cache[dev];
 }
+// Stream-K tail of the persistent kernel (default on; env MK_STREAMK=0 disables): launches
+// whose tiles leave the last wave partial split the k-iterations of the tail over every SM.
+static std::atomic<int> g_streamk{-1};
+bool streamk_enabled() {
+  if (g_streamk < 0) {
+    const char* e = getenv("MK_STREAMK");
+    g_streamk = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_streamk == 1;
+}
+
+// Per (device, stream) stream-K scratch: two partial-tile slots per CTA and one flag per
+// (stream-K tile, consumer warp). Flags start at zero and every owner resets the ones it used,
+// so launches on one stream reuse them; launches on different streams never share them.
+struct SkScratch {
+  double* partial = nullptr;
+  int32_t* flags = nullptr;
+  size_t partial_bytes = 0, flag_count = 0;
+};
+static cudaError_t sk_scratch(cudaStream_t stream, int ctas, int warps, int acc_per_thread, int sk_tiles,
+                              SkScratch** out) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, SkScratch> cache;
+  int dev = 0;
+  cudaError_t err = cudaGetDevice(&dev);
+  if (err != cudaSuccess) return err;
+  std::lock_guard<std::mutex> lock(mu);
+  SkScratch& sc = cache[{dev, stream}];
+  const size_t pbytes = (size_t)2 * ctas * warps * acc_per_thread * 32 * sizeof(double);
+  const size_t nflags = (size_t)sk_tiles * warps;
+  if (sc.partial_bytes < pbytes) {
+    if (sc.partial) cudaFree(sc.partial);
+    sc.partial = nullptr;
+    sc.partial_bytes = 0;
+    err = cudaMalloc(&sc.partial, pbytes);
+    if (err != cudaSuccess) return err;
+    sc.partial_bytes = pbytes;
+  }
+  if (sc.flag_count < nflags) {
+    if (sc.flags) cudaFree(sc.flags);
+    sc.flags = nullptr;
+    sc.flag_count = 0;
+    const size_t want = nflags < 4096 ? 4096 : nflags;
+    err = cudaMalloc(&sc.flags, want * sizeof(int32_t));
+    if (err != cudaSuccess) return err;
+    err = cudaMemsetAsync(sc.flags, 0, want * sizeof(int32_t), stream);
+    if (err != cudaSuccess) return err;
+    sc.flag_count = want;
+  }
+  *out = &sc;
+  return cudaSuccess;
+}
+
 // Tile width of the persistent kernel: 64 when it cuts the column padding of the leaf by more
-// than 10% (only with the synchronous epilogue: the TMA epilogue's C maps are built for the
-// default box shape), else 128. Env MK_NARROW=0 disables narrow tiles.
-// Also narrow when 128-column tiles would leave most SMs idle (a launch of fewer than 60% of the
-// SM count in tiles, e.g. one 1024^2 leaf of a literal schedule: 64 tiles -> 128); such launches
-// switch to the synchronous epilogue.
+// than 10% (e.g. cfg5's 320-column leaves: 5 tiles instead of 3 x 128 with 17% padding), else
+// 128. Env MK_NARROW=0 disables narrow tiles. Also narrow when 128-column tiles would leave most
+// SMs idle (fewer than 60% of the SM count in tiles, e.g. one 1024^2 leaf of a literal schedule). Narrow tiles run 8 warps
+// of 32 x 32, so their TMA epilogue boxes are 32 rows (the planner builds the C maps to match:
+// epilogue_box_rows).
 static int sm_count();
-static int persistent_bn(const MkGemmArgs& a, int nprod) {
+int persistent_tile_n(int64_t tiles_m, int64_t N, int nprod) {
   static std::atomic<int> narrow{-1};
   if (narrow < 0) {
     const char* e = getenv("MK_NARROW");
     narrow = (e && e[0] == '0') ? 0 : 1;
   }
   if (!narrow) return 128;
-  const int64_t tiles128 = (int64_t)a.tiles_m * ((a.N + 127) / 128) * nprod;
+  const int64_t tiles128 = tiles_m * ((N + 127) / 128) * nprod;
   if (tiles128 * 10 < (int64_t)sm_count() * 6) return 64;
-  if (a.async_epi) return 128;
-  const int64_t w128 = (a.N + 127) / 128 * 128, w64 = (a.N + 63) / 64 * 64;
+  const int64_t w128 = (N + 127) / 128 * 128, w64 = (N + 63) / 64 * 64;
   return (w64 * 10 < w128 * 9) ? 64 : 128;
 }
+int epilogue_box_rows(int64_t M, int64_t N, int nprod, bool single_terms) {
+  // multi-term operands run the one-CTA-per-tile combiner kernel (128-column tiles)
+  if (single_terms && persistent_enabled() && persistent_tile_n((M + MK_BM - 1) / MK_BM, N, nprod) == 64) return 32;
+  return consumer_layout() == 16 ? 32 : 64;
+}
+static int persistent_bn(const MkGemmArgs& a, int nprod) { return persistent_tile_n(a.tiles_m, a.N, nprod); }
 
 // One CTA per SM over the launch's tiles; the ring keeps S = (budget - boxes) / stage stages.
 template <int MT, int BN>
@@ -958,21 +1128,49 @@ static cudaError_t launch_persistent_t(const CUtensorMap& tmA, const CUtensorMap
   args.raw_sets = 0;
   args.chunk_stages = accumulate_chunk_stages();
   const size_t smem = (size_t)args.stages * PL::kStageBytes + PL::kBoxBytes + 1024;
-  auto fn = persistent_product_kernel<MT, BN>;
-  cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (err != cudaSuccess) return err;
+  cudaError_t err = cudaSuccess;
   const int total = tiles * nprod;
-  const int grid = total < sm_count() ? total : sm_count();
-  fn<<<grid, PL::kThreads, smem, stream>>>(tmA, tmB, tmC, args, prod);
+  int grid = total < sm_count() ? total : sm_count();
+  args.sk_tile0 = total;
+  args.sk_partial = nullptr;
+  args.sk_flags = nullptr;
+  const int G = sm_count();
+  const int KT = (args.K + MK_BK - 1) / MK_BK;
+  const int rem = total % G;
+  auto dp = persistent_product_kernel<MT, BN, false>;
+  err = cudaFuncSetAttribute(dp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
+  if (streamk_enabled() && total > G && rem != 0 && KT >= 8 && (int64_t)(rem + G) * KT * G < ((int64_t)1 << 31)) {
+    // Data-parallel waves, then stream-K over the partial last wave plus one full wave (every
+    // CTA's share is one to two tiles of k-iterations), as two launches: the stream-K kernel's
+    // extra state would cost the data-parallel main loop registers. Launches of less than one
+    // wave stay data-parallel (narrow tiles fill the SMs there; measured faster at 1024^2).
+    const int tile0 = (total / G - 1) * G;
+    SkScratch* sc = nullptr;
+    err = sk_scratch(stream, G, PL::kConsumerWarps, MT * 8, total - tile0, &sc);
+    if (err != cudaSuccess) return err;
+    args.sk_tile0 = tile0;
+    args.sk_partial = sc->partial;
+    args.sk_flags = sc->flags;
+    if (tile0 > 0) {
+      dp<<<G, PL::kThreads, smem, stream>>>(tmA, tmB, tmC, args, prod);
+      err = cudaGetLastError();
+      if (err != cudaSuccess) return err;
+    }
+    auto sk = persistent_product_kernel<MT, BN, true>;
+    err = cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+    sk<<<G, PL::kThreads, smem, stream>>>(tmA, tmB, tmC, args, prod);
+    return cudaGetLastError();
+  }
+  dp<<<grid, PL::kThreads, smem, stream>>>(tmA, tmB, tmC, args, prod);
   return cudaGetLastError();
 }
 
 static cudaError_t launch_persistent(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
                                      MkGemmArgs args, const MkProduct& prod, int nprod, cudaStream_t stream) {
-  if (persistent_bn(args, nprod) == 64) {
-    args.async_epi = 0;  // the TMA epilogue's C maps are built for the 128-column layouts' boxes
+  if (persistent_bn(args, nprod) == 64)  // async epilogue: tmC has 32-row boxes (epilogue_box_rows)
     return launch_persistent_t<4, 64>(tmA, tmB, tmC, args, prod, nprod, stream);
-  }
   if (consumer_layout() == 16) return launch_persistent_t<4, 128>(tmA, tmB, tmC, args, prod, nprod, stream);
   return launch_persistent_t<8, 128>(tmA, tmB, tmC, args, prod, nprod, stream);
 }

@@ -63,4 +63,12 @@ struct MkGemmArgs {
   int32_t nslab, pad_slab;
   int64_t slab_rows;
   double* slab[MK_MAX_SLABS];
+  // Stream-K tail (persistent kernel): tiles [0, sk_tile0) run whole, one CTA each (data-parallel
+  // waves); the k-iterations of tiles [sk_tile0, total) are split evenly over the grid. A tile's
+  // head segment (k from 0) owns it: the CTAs holding its later k-segments write their partial
+  // accumulators to sk_partial (one slot per CTA) and count up sk_flags[tile][warp]; the owner
+  // adds them in k order (deterministic) and runs the epilogue. sk_tile0 >= total: no stream-K.
+  int32_t sk_tile0, pad_sk;
+  double* sk_partial;
+  int32_t* sk_flags;
 };

@@ -340,3 +340,47 @@ def sharded_multiply_rect(algo: str, a, b, levels: int, group=None, out=None, ws
         out = torch.empty((a.shape[0], b.shape[1]), dtype=torch.float64, device=a.device)
     rect_partial_product(algo, a, b, out, levels, first, count, ws=ws)
     return assemble(out, 0, group)
+
+
+# ------------------------------------------------------------------------------------------
+# one process driving several GPUs (the C ABI's mk_multi_gpu_winograd): no process group
+# ------------------------------------------------------------------------------------------
+def single_process_multiply(algo: str, a, b, levels: int, devices=None, out=None):
+    """C = A B over the GPUs ``devices`` (default: every visible GPU) from ONE process: A, B and C
+    live on devices[0]; every other device receives over NVLink only the operand quadrants its
+    leaf row panels read, computes its partial C, and device 0 adds the partials in rank order
+    (mk_multi_gpu_winograd). A device may be listed more than once (ranks sharing one GPU)."""
+    import torch
+
+    lib = _lib.load()
+    for t, nm in ((a, "a"), (b, "b")):
+        _check_operand(t, nm)
+    n = a.shape[0]
+    if devices is None:
+        devices = list(range(torch.cuda.device_count()))
+    devices = [int(d) for d in devices]
+    if a.device.index != devices[0] or b.device.index != devices[0]:
+        raise ValueError("a and b must live on devices[0]")
+    if out is None:
+        out = torch.empty((n, n), dtype=torch.float64, device=a.device)
+    _check_operand(out, "out")
+    aid = _lib.ALGO_IDS[algo]
+    g = len(devices)
+    wss, streams = [], []
+    for r, d in enumerate(devices):
+        need = int(lib.mk_multi_gpu_workspace_bytes(aid, n, levels, r, g))
+        if need == 0 and r > 0:
+            raise ValueError(f"unsupported multi-GPU shape: n={n}, levels={levels}")
+        wss.append(torch.empty(max(need, 16), dtype=torch.uint8, device=torch.device("cuda", d)))
+        streams.append(torch.cuda.current_stream(d) if r == 0 else torch.cuda.Stream(device=d))
+    dev_arr = (ctypes.c_int * g)(*devices)
+    ws_arr = (ctypes.c_void_p * g)(*[w.data_ptr() for w in wss])
+    sz_arr = (ctypes.c_size_t * g)(*[w.numel() for w in wss])
+    st_arr = (ctypes.c_void_p * g)(*[s.cuda_stream for s in streams])
+    rc = lib.mk_multi_gpu_winograd(aid, g, dev_arr, ctypes.c_void_p(a.data_ptr()), a.stride(0),
+                                   ctypes.c_void_p(b.data_ptr()), b.stride(0), ctypes.c_void_p(out.data_ptr()),
+                                   out.stride(0), n, levels, ws_arr, sz_arr, st_arr)
+    _lib.check(rc, "mk_multi_gpu_winograd")
+    for w, s in zip(wss[1:], streams[1:]):
+        w.record_stream(s)  # freed on return while the peers' kernels may still run
+    return out

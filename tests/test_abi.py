@@ -76,10 +76,9 @@ def test_workspace_sizes(lib):
     assert ws("in-place", 1024, 1) == 0 and ws("in-place", 1024, 3) == 0
     assert ws("winograd-block", 1024, 1) == 2 * 512 * 512 * 8
     assert ws("two-temp", 1024, 1) == 2 * 512 * 512 * 8
-    # deeper: two-temp keeps its two (n/2)^2 slots at the literal top level; its last two levels
-    # run breadth-first (more scratch), still below the all-breadth-first plan
-    assert 2 * 8 * 512 ** 2 < ws("two-temp", 1024, 3) <= ws("winograd-block", 1024, 3)
-    assert ws("two-temp", 1024, 2) == ws("winograd-block", 1024, 2)
+    # deeper: two-temp keeps the paper's two (n/2^(l+1))^2 slots per literal level (default)
+    assert ws("two-temp", 1024, 3) == 2 * 8 * (512 ** 2 + 256 ** 2 + 128 ** 2)
+    assert ws("two-temp", 1024, 2) == 2 * 8 * (512 ** 2 + 256 ** 2) < ws("winograd-block", 1024, 2)
     assert ws("winograd-block", 16384, 1) == 2 * 8192 * 8192 * 8
     assert ws("winograd-block", 16, 5) == 0  # invalid (leaf order < 2)
     assert lib.mk_rect_workspace_bytes(_lib.ALGO_IDS["winograd-block"], 12000, 10000, 14000, 5) > 0
@@ -93,14 +92,21 @@ def test_plan_options_change_workspace_not_counts(lib):
         assert lib.mk_set_option(_lib.MK_OPT_PLAN, 2) == 0  # hybrid: one top-level subtree at a time
         hybrid = ws("winograd-block", 16384, 3)
         assert lib.mk_set_option(_lib.MK_OPT_PLAN, 0) == 0
-        assert ws("winograd-block", 16384, 2) > 7 * 16384 ** 2 * 8  # breadth-first: every depth
+        # breadth-first, default passes of 4 top-level products: at most the reference's own
+        # modeled block-Winograd peak (4.97 n^2 elements, 9.9 GiB at n = 16384)
+        assert ws("winograd-block", 16384, 2) <= 4.97 * 16384 ** 2 * 8
+        assert lib.mk_set_option(_lib.MK_OPT_BFS_GROUP, 7) == 0  # one pass: every depth at once
+        assert ws("winograd-block", 16384, 2) > 7 * 16384 ** 2 * 8
         assert hybrid * 4 < ws("winograd-block", 16384, 3)
-        assert lib.mk_set_option(_lib.MK_OPT_LITERAL_TAIL, 0) == 0  # two-temp literal to the leaves
-        assert ws("two-temp", 16384, 2) == (2 * 8192 ** 2 + 2 * 4096 ** 2) * 8
+        assert lib.mk_set_option(_lib.MK_OPT_BFS_GROUP, 9) == _lib.MK_ERR_ARG
+        assert ws("two-temp", 16384, 2) == (2 * 8192 ** 2 + 2 * 4096 ** 2) * 8  # literal to the leaves
+        assert lib.mk_set_option(_lib.MK_OPT_LITERAL_TAIL, 1) == 0  # breadth-first tail: more scratch
+        assert ws("two-temp", 16384, 2) > (2 * 8192 ** 2 + 2 * 4096 ** 2) * 8
         assert lib.mk_set_option(_lib.MK_OPT_PLAN, 7) == _lib.MK_ERR_ARG
     finally:
         lib.mk_set_option(_lib.MK_OPT_PLAN, 0)
-        lib.mk_set_option(_lib.MK_OPT_LITERAL_TAIL, 1)
+        lib.mk_set_option(_lib.MK_OPT_LITERAL_TAIL, 0)
+        lib.mk_set_option(_lib.MK_OPT_BFS_GROUP, 0)
 
 
 def test_product_counts(lib):

@@ -186,3 +186,27 @@ def test_square_partials_three_levels(world):
         total += part
     torch.cuda.synchronize()
     assert torch.equal(total, a @ b)
+
+
+@pytest.mark.parametrize("ranks,levels,algo", [(2, 1, "winograd-block"), (3, 2, "winograd-block"), (4, 2, "strassen"),
+                                               (8, 2, "winograd-knuth")])
+def test_single_process_multi_gpu_abi(ranks, levels, algo):
+    """mk_multi_gpu_winograd (one process, several devices): here every rank is device 0, which
+    runs the same code path -- quadrant peer copies into each rank's workspace, the rank's leaf row
+    panels into its partial C, device 0 summing the partials in rank order -- on one GPU. Integer
+    data is exact; reals match the single-GPU product to rounding."""
+    import torch
+
+    from paper_2309_00628_b200 import multigpu as mg
+
+    n = 2048
+    r = np.random.default_rng(ranks + 10 * levels)
+    a = torch.from_numpy(r.integers(-8, 9, (n, n)).astype(np.float64)).cuda()
+    b = torch.from_numpy(r.integers(-8, 9, (n, n)).astype(np.float64)).cuda()
+    c = mg.single_process_multiply(algo, a, b, levels, devices=[0] * ranks)
+    torch.cuda.synchronize()
+    assert torch.equal(c, a @ b)
+    ar, br = torch.rand_like(a), torch.rand_like(b)
+    cr = mg.single_process_multiply(algo, ar, br, levels, devices=[0] * ranks)
+    torch.cuda.synchronize()
+    assert float((cr - ar @ br).abs().max()) < 1e-10
