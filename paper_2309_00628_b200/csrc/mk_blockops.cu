@@ -180,6 +180,212 @@ cudaError_t launch_xform_batch(const MkXformJob* jobs_dev, int njobs, int64_t ro
   return cudaGetLastError();
 }
 
+// ---- two-level operand transform (breadth-first plan, K2'') ---------------------------------
+// One job = one recursion node's operand block X (4 x 4 sub-blocks of rows x cols: sub-block
+// (q1, q2) is sub-quadrant q2 of quadrant q1) -> all its grandchildren's operands
+//     G(p, p2) = sum_q2 c[p2][q2] * ( sum_q1 c[p][q1] * X(q1, q2) )
+// in one pass: the children's sums T(p, .) stay in registers, so two depths of the recursion
+// cost one read of X and one write of the grandchildren instead of writing and re-reading the
+// children. The coefficient tables are compile-time constants (every zero term is skipped at
+// compile time, so the kernel stays memory-bound; the round-1 runtime-table version was
+// instruction-bound); sums run in quadrant order from zero, exactly as two one-level passes
+// would compute them (bit-identical results). Tables: reference kernels.py:66-160.
+template <int TAB, int SIDE>
+struct X2Tab;
+// quadrant order 11, 12, 21, 22; [product][quadrant]
+template <> struct X2Tab<0, 0> {  // Strassen, A side
+  static constexpr int np = 7;
+  __host__ __device__ static constexpr int cf(int p, int q) {
+    constexpr int8_t c[8][4] = {{1, 0, 0, 1}, {0, 0, 1, 1}, {1, 0, 0, 0}, {0, 0, 0, 1},
+                                     {1, 1, 0, 0}, {-1, 0, 1, 0}, {0, 1, 0, -1}, {0, 0, 0, 0}};
+    return c[p][q];
+  }
+};
+template <> struct X2Tab<0, 1> {  // Strassen, B side
+  static constexpr int np = 7;
+  __host__ __device__ static constexpr int cf(int p, int q) {
+    constexpr int8_t c[8][4] = {{1, 0, 0, 1}, {1, 0, 0, 0}, {0, 1, 0, -1}, {-1, 0, 1, 0},
+                                     {0, 0, 0, 1}, {1, 1, 0, 0}, {0, 0, 1, 1}, {0, 0, 0, 0}};
+    return c[p][q];
+  }
+};
+template <> struct X2Tab<1, 0> {  // Winograd block, A side
+  static constexpr int np = 7;
+  __host__ __device__ static constexpr int cf(int p, int q) {
+    constexpr int8_t c[8][4] = {{1, 0, 0, 0}, {0, 1, 0, 0}, {1, 1, -1, -1}, {0, 0, 0, 1},
+                                     {0, 0, 1, 1}, {-1, 0, 1, 1}, {1, 0, -1, 0}, {0, 0, 0, 0}};
+    return c[p][q];
+  }
+};
+template <> struct X2Tab<1, 1> {  // Winograd block, B side
+  static constexpr int np = 7;
+  __host__ __device__ static constexpr int cf(int p, int q) {
+    constexpr int8_t c[8][4] = {{1, 0, 0, 0}, {0, 0, 1, 0}, {0, 0, 0, 1}, {1, -1, -1, 1},
+                                     {-1, 1, 0, 0}, {1, -1, 0, 1}, {0, -1, 0, 1}, {0, 0, 0, 0}};
+    return c[p][q];
+  }
+};
+template <> struct X2Tab<2, 0> {  // Winograd Knuth, A side
+  static constexpr int np = 7;
+  __host__ __device__ static constexpr int cf(int p, int q) {
+    constexpr int8_t c[8][4] = {{1, 0, 0, 0}, {0, 1, 0, 0}, {-1, 0, 1, 0}, {0, 0, 1, 1},
+                                     {-1, 0, 1, 1}, {1, 1, -1, -1}, {0, 0, 0, 1}, {0, 0, 0, 0}};
+    return c[p][q];
+  }
+};
+template <> struct X2Tab<2, 1> {  // Winograd Knuth, B side
+  static constexpr int np = 7;
+  __host__ __device__ static constexpr int cf(int p, int q) {
+    constexpr int8_t c[8][4] = {{1, 0, 0, 0}, {0, 0, 1, 0}, {0, 1, 0, -1}, {-1, 1, 0, 0},
+                                     {1, -1, 0, 1}, {0, 0, 0, 1}, {-1, 1, 1, -1}, {0, 0, 0, 0}};
+    return c[p][q];
+  }
+};
+template <> struct X2Tab<3, 0> {  // Winograd Knuth, 8 calls (first product recomputed), A side
+  static constexpr int np = 8;
+  __host__ __device__ static constexpr int cf(int p, int q) {
+    constexpr int8_t c[8][4] = {{1, 0, 0, 0}, {0, 1, 0, 0}, {-1, 0, 1, 0}, {0, 0, 1, 1},
+                                     {-1, 0, 1, 1}, {1, 1, -1, -1}, {0, 0, 0, 1}, {1, 0, 0, 0}};
+    return c[p][q];
+  }
+};
+template <> struct X2Tab<3, 1> {  // Winograd Knuth, 8 calls, B side
+  static constexpr int np = 8;
+  __host__ __device__ static constexpr int cf(int p, int q) {
+    constexpr int8_t c[8][4] = {{1, 0, 0, 0}, {0, 0, 1, 0}, {0, 1, 0, -1}, {-1, 1, 0, 0},
+                                     {1, -1, 0, 1}, {0, 0, 0, 1}, {-1, 1, 1, -1}, {1, 0, 0, 0}};
+    return c[p][q];
+  }
+};
+
+int xform2_table_coef(int tab, int side, int p, int q) {
+  switch (tab * 2 + side) {
+    case 0: return X2Tab<0, 0>::cf(p, q);
+    case 1: return X2Tab<0, 1>::cf(p, q);
+    case 2: return X2Tab<1, 0>::cf(p, q);
+    case 3: return X2Tab<1, 1>::cf(p, q);
+    case 4: return X2Tab<2, 0>::cf(p, q);
+    case 5: return X2Tab<2, 1>::cf(p, q);
+    case 6: return X2Tab<3, 0>::cf(p, q);
+    default: return X2Tab<3, 1>::cf(p, q);
+  }
+}
+
+template <int TAB, int SIDE, int W>
+__global__ void __launch_bounds__(256) xform2_kernel(const MkXform2Job* __restrict__ jobs, int64_t rows,
+                                                     int64_t cols) {
+  using T = X2Tab<TAB, SIDE>;
+  constexpr int NP = T::np;
+  __shared__ double* dst_sh[MK_XFORM2_MAX];
+  const MkXform2Job& jb = jobs[blockIdx.y];
+  if (threadIdx.x < NP * NP) dst_sh[threadIdx.x] = jb.dst[threadIdx.x];
+  __syncthreads();
+  const int64_t cv = cols / W;
+  const uint32_t total = (uint32_t)(rows * cv), ucv = (uint32_t)cv;
+  const double* src = jb.src;
+  const int64_t lds = jb.lds, ldd = jb.ldd;
+  for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    const uint32_t r = idx / ucv;
+    const int64_t c = (int64_t)(idx - r * ucv) * W;
+    Vec<W> x[4][4];
+#pragma unroll
+    for (int q1 = 0; q1 < 4; ++q1)
+#pragma unroll
+      for (int q2 = 0; q2 < 4; ++q2) {
+        const int64_t rr = ((q1 >> 1) * 2 + (q2 >> 1)) * rows + r;
+        const int64_t cc = ((q1 & 1) * 2 + (q2 & 1)) * cols + c;
+        x[q1][q2] = ld_vec<W>(src + rr * lds + cc);
+      }
+    const int64_t off = (int64_t)r * ldd + c;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      bool any = false;
+#pragma unroll
+      for (int p2 = 0; p2 < NP; ++p2) any = any || dst_sh[p * NP + p2] != nullptr;
+      if (!any) continue;  // job-uniform: this child is not in the pass, or all its grandchildren are views
+      Vec<W> t[4];
+#pragma unroll
+      for (int q2 = 0; q2 < 4; ++q2) {
+#pragma unroll
+        for (int u = 0; u < W; ++u) t[q2].v[u] = 0.0;
+#pragma unroll
+        for (int q1 = 0; q1 < 4; ++q1) {
+          if constexpr (true) {
+            const int cf = T::cf(p, q1);
+            if (cf > 0) {
+#pragma unroll
+              for (int u = 0; u < W; ++u) t[q2].v[u] += x[q1][q2].v[u];
+            } else if (cf < 0) {
+#pragma unroll
+              for (int u = 0; u < W; ++u) t[q2].v[u] -= x[q1][q2].v[u];
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int p2 = 0; p2 < NP; ++p2) {
+        double* d = dst_sh[p * NP + p2];
+        if (!d) continue;
+        Vec<W> o;
+#pragma unroll
+        for (int u = 0; u < W; ++u) o.v[u] = 0.0;
+#pragma unroll
+        for (int q2 = 0; q2 < 4; ++q2) {
+          const int cf = T::cf(p2, q2);
+          if (cf > 0) {
+#pragma unroll
+            for (int u = 0; u < W; ++u) o.v[u] += t[q2].v[u];
+          } else if (cf < 0) {
+#pragma unroll
+            for (int u = 0; u < W; ++u) o.v[u] -= t[q2].v[u];
+          }
+        }
+        st_vec<W>(d + off, o);
+      }
+    }
+  }
+}
+
+template <int TAB, int SIDE>
+static void launch_xform2_t(dim3 grid, const MkXform2Job* jobs, int64_t rows, int64_t cols, int width,
+                            cudaStream_t stream) {
+  if (width == 4)
+    xform2_kernel<TAB, SIDE, 4><<<grid, 256, 0, stream>>>(jobs, rows, cols);
+  else if (width == 2)
+    xform2_kernel<TAB, SIDE, 2><<<grid, 256, 0, stream>>>(jobs, rows, cols);
+  else
+    xform2_kernel<TAB, SIDE, 1><<<grid, 256, 0, stream>>>(jobs, rows, cols);
+}
+
+cudaError_t launch_xform2_batch(const MkXform2Job* jobs_dev, int njobs, int table, int side, int64_t rows,
+                                int64_t cols, int width, cudaStream_t stream) {
+  if (njobs <= 0 || rows <= 0 || cols <= 0) return cudaSuccess;
+  if (table < 0 || table > 3 || side < 0 || side > 1) return cudaErrorInvalidValue;
+  if (width != 4 && width != 2) width = 1;
+  const int64_t work = rows * (cols / width);
+  if (work >= (int64_t)1 << 32) return cudaErrorInvalidValue;
+  int64_t bx = (work + 255) / 256;
+  const int64_t cap = (148 * 16 + njobs - 1) / njobs;
+  if (bx > cap) bx = cap;
+  if (bx < 1) bx = 1;
+  for (int j0 = 0; j0 < njobs; j0 += 65535) {
+    const int nj = njobs - j0 < 65535 ? njobs - j0 : 65535;
+    dim3 grid((unsigned)bx, (unsigned)nj);
+    const MkXform2Job* jb = jobs_dev + j0;
+    switch (table * 2 + side) {
+      case 0: launch_xform2_t<0, 0>(grid, jb, rows, cols, width, stream); break;
+      case 1: launch_xform2_t<0, 1>(grid, jb, rows, cols, width, stream); break;
+      case 2: launch_xform2_t<1, 0>(grid, jb, rows, cols, width, stream); break;
+      case 3: launch_xform2_t<1, 1>(grid, jb, rows, cols, width, stream); break;
+      case 4: launch_xform2_t<2, 0>(grid, jb, rows, cols, width, stream); break;
+      case 5: launch_xform2_t<2, 1>(grid, jb, rows, cols, width, stream); break;
+      case 6: launch_xform2_t<3, 0>(grid, jb, rows, cols, width, stream); break;
+      default: launch_xform2_t<3, 1>(grid, jb, rows, cols, width, stream); break;
+    }
+  }
+  return cudaGetLastError();
+}
+
 __global__ void i64_to_f64_kernel(const int64_t* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
                                   int64_t cols) {
   const int64_t total = rows * cols;

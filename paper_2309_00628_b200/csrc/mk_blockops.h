@@ -19,6 +19,18 @@ struct MkXformJob {
   int8_t coef[MK_XFORM_MAX][MK_XFORM_MAX];  // [dst][src] in {-1, 0, 1}
 };
 
+// One job of the two-level operand transform: a node's operand block (4 x 4 sub-blocks of
+// rows x cols, base src, leading dimension lds) -> its grandchildren's operands, grandchild
+// (p, p2) into dst[p * np + p2] (leading dimension ldd); nullptr = not written (a view of src,
+// or not part of this pass).
+#define MK_XFORM2_MAX 64
+struct MkXform2Job {
+  const double* src;
+  int64_t lds;
+  double* dst[MK_XFORM2_MAX];
+  int64_t ldd;
+};
+
 // One product of a batched leaf launch (device table, 64-byte aligned entries).
 struct alignas(64) MkBatchEntry {
   CUtensorMap tmA, tmB, tmC;
@@ -42,6 +54,10 @@ cudaError_t launch_absmax_i64(const int64_t* src, int64_t lds, int64_t rows, int
 cudaError_t launch_xform_batch(const MkXformJob* jobs_dev, int njobs, int64_t rows, int64_t cols, int width,
                                cudaStream_t stream);
 cudaError_t measure_dmma_peak(double* tflops_out, cudaStream_t st);
+// table: 0 Strassen, 1 Winograd block, 2 Winograd Knuth, 3 Knuth 8-call; side: 0 A, 1 B.
+cudaError_t launch_xform2_batch(const MkXform2Job* jobs_dev, int njobs, int table, int side, int64_t rows,
+                                int64_t cols, int width, cudaStream_t stream);
+int xform2_table_coef(int table, int side, int p, int q);
 cudaError_t launch_fused_product(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
                                  const MkGemmArgs& args, const MkProduct& prod, cudaStream_t stream);
 int consumer_layout();

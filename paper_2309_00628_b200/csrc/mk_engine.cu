@@ -320,6 +320,15 @@ static int plan_kind() {
   return g_plan_dfs;
 }
 static bool plan_dfs() { return plan_kind() == 1; }
+// Breadth-first operand sums two depths per pass (xform2_kernel; env MK_XFORM2=0 disables).
+static bool xform2_pairs() {
+  static std::atomic<int> v{-1};
+  if (v < 0) {
+    const char* e = getenv("MK_XFORM2");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
 // MK_OPT_BFS_GROUP: top-level products per breadth-first pass (env MK_BFS_GROUP). 0 = auto
 // (bfs_group_for), 7 or more = one pass over all of them (the round-1 plan, largest workspace).
 static std::atomic<int> g_bfs_group{-1};
@@ -1270,6 +1279,119 @@ struct Engine {
     bool on = true;               // part of this pass (grouped plan: a subset of the top-level products)
   };
 
+  // Two depths of operand sums in one pass (xform2_kernel): every active node of depth d writes
+  // its grandchildren's operands (depth d + 2) directly; the children's (depth d + 1) sums are
+  // never materialised (their nodes get no operand blocks -- only leaves and the next pass read
+  // operands). Grandchild (p, p2) is a view of the node's block when both p and p2 take a single
+  // quadrant. Sets *done = false (nothing planned) when a node's operand carries a negative sign
+  // or the table has no compiled form, so the caller runs the one-depth path instead.
+  int bfs_xform2(int d, int64_t M, int64_t N, int64_t K, const std::vector<int>* grp, std::vector<std::vector<BNode>>& lv,
+                 bool* done) {
+    *done = false;
+    const int np = co->nprod;
+    const int table = algo == MK_ALGO_STRASSEN ? 0 : algo == MK_ALGO_WINOGRAD_BLOCK ? 1
+                    : algo == MK_ALGO_WINOGRAD_KNUTH ? 2 : algo == MK_ALGO_WINOGRAD_KNUTH_8CALL ? 3 : -1;
+    if (table < 0 || np * np > MK_XFORM2_MAX) return MK_OK;
+    for (int side = 0; side < 2; ++side)  // the compiled tables must be the engine's derived ones
+      for (int p = 0; p < np; ++p)
+        for (int q = 0; q < 4; ++q)
+          if (xform2_table_coef(table, side, p, q) != (side == 0 ? co->a[p][q] : co->b[p][q]))
+            return fail(MK_ERR_ARG, "internal: compiled two-level transform table differs from the derived one");
+    const std::vector<BNode>& cur = lv[d];
+    for (const BNode& b : cur)
+      if (b.on && (b.x.sign < 0 || b.y.sign < 0)) return MK_OK;
+    auto in_grp = [&](int p) { return !grp || std::find(grp->begin(), grp->end(), p) != grp->end(); };
+    // grandchild extents (depth d + 2)
+    const int64_t gm = (M >> d) / 4, gn = (N >> d) / 4, gk = (K >> d) / 4;
+    std::vector<BNode> mid(cur.size() * np), next(cur.size() * np * np);
+    for (size_t i = 0; i < cur.size(); ++i)
+      for (int p = 0; p < np; ++p) {
+        const bool on = cur[i].on && (d > 0 || in_grp(p));
+        mid[i * np + p].on = on;
+        mid[i * np + p].x = mid[i * np + p].y = Blk{-1, 0, 0, 1.0};  // never materialised
+        for (int p2 = 0; p2 < np; ++p2) next[(i * np + p) * np + p2].on = on;
+      }
+    auto single = [&](const int* cf, int* q1) {
+      int terms = 0;
+      for (int q = 0; q < 4; ++q)
+        if (cf[q]) {
+          ++terms;
+          *q1 = q;
+        }
+      return terms == 1;
+    };
+    for (int side = 0; side < 2; ++side) {
+      const int64_t gr = side == 0 ? gm : gk, gc = side == 0 ? gk : gn;
+      auto cf_of = [&](int p) { return side == 0 ? co->a[p] : co->b[p]; };
+      int64_t count = 0;  // materialised grandchildren of this side
+      for (size_t i = 0; i < cur.size(); ++i)
+        for (int p = 0; p < np; ++p) {
+          if (!mid[i * np + p].on) continue;
+          int qa = -1, qb = -1;
+          const bool sp = single(cf_of(p), &qa);
+          for (int p2 = 0; p2 < np; ++p2)
+            if (!(sp && single(cf_of(p2), &qb))) ++count;
+        }
+      int arena = -1;
+      if (count) MK_TRY(alloc_slot(count * gr, gc, &arena));
+      int64_t arena_next = 0;
+      std::vector<MkXform2Job> jobs;
+      for (size_t i = 0; i < cur.size(); ++i) {
+        if (!cur[i].on) continue;
+        const Blk& src = side == 0 ? cur[i].x : cur[i].y;
+        MkXform2Job job{};
+        job.src = ptr_of(src);
+        job.lds = bases[src.base].ld;
+        job.ldd = arena >= 0 ? bases[arena].ld : 0;
+        bool any = false;
+        for (int p = 0; p < np; ++p) {
+          if (!mid[i * np + p].on) continue;
+          int q1 = -1;
+          const bool sp = single(cf_of(p), &q1);
+          for (int p2 = 0; p2 < np; ++p2) {
+            int q2 = -1;
+            Blk& tgt = side == 0 ? next[(i * np + p) * np + p2].x : next[(i * np + p) * np + p2].y;
+            if (sp && single(cf_of(p2), &q2)) {  // a view of the node's block
+              tgt = Blk{src.base, src.row + (q1 >> 1) * 2 * gr + (q2 >> 1) * gr, src.col + (q1 & 1) * 2 * gc + (q2 & 1) * gc,
+                        src.sign * cf_of(p)[q1] * cf_of(p2)[q2]};
+              continue;
+            }
+            tgt = Blk{arena, arena_next, 0, 1.0};
+            arena_next += gr;
+            job.dst[p * np + p2] = ptr_of(tgt);
+            any = true;
+          }
+        }
+        if (any) jobs.push_back(job);
+      }
+      if (!jobs.empty()) {
+        // widest access every source and destination row allows (W = 4 needs 178 registers: 2 at most)
+        int width = 2;
+        while (width > 1) {
+          bool ok = gc % width == 0;
+          const uintptr_t al = (uintptr_t)width * 8;
+          for (const MkXform2Job& j : jobs) {
+            ok = ok && j.lds % width == 0 && reinterpret_cast<uintptr_t>(j.src) % al == 0 && j.ldd % width == 0;
+            for (int t = 0; t < np * np; ++t) ok = ok && reinterpret_cast<uintptr_t>(j.dst[t]) % al == 0;
+          }
+          if (ok) break;
+          width /= 2;
+        }
+        void* dev = nullptr;
+        MK_TRY(upload(jobs.data(), jobs.size() * sizeof(MkXform2Job), &dev));
+        if (!dry && !no_launch) {
+          MK_CUDA_TRY(launch_xform2_batch(static_cast<const MkXform2Job*>(dev), (int)jobs.size(), table, side, gr, gc,
+                                          width, st));
+          ++g_launch_count;
+        }
+      }
+    }
+    lv.push_back(std::move(mid));
+    lv.push_back(std::move(next));
+    *done = true;
+    return MK_OK;
+  }
+
   // Breadth-first product of the root operands X (M x K), Y (K x N) into block D (store
   // semantics: D is fully overwritten) with `L` levels.
   //
@@ -1285,8 +1407,16 @@ struct Engine {
     auto in_grp = [&](int p) { return !grp || std::find(grp->begin(), grp->end(), p) != grp->end(); };
     std::vector<std::vector<BNode>> lv(1);
     lv[0].push_back(BNode{X, Y, Blk{-1, 0, 0, 1.0}});
-    // ---- operand sums, depth by depth ----
+    // ---- operand sums, depth by depth (two depths per pass where xform2 applies) ----
     for (int d = 0; d < L; ++d) {
+      if (xform2_pairs() && (L - d) % 2 == 0) {  // depths d and d + 1 in one pass (the deepest pairs)
+        bool done = false;
+        MK_TRY(bfs_xform2(d, M, N, K, grp, lv, &done));
+        if (done) {
+          ++d;
+          continue;
+        }
+      }
       const int64_t hm = (M >> d) / 2, hn = (N >> d) / 2, hk = (K >> d) / 2;
       const std::vector<BNode>& cur = lv[d];
       std::vector<BNode> next(cur.size() * np);

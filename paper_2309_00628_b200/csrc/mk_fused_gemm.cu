@@ -1140,7 +1140,10 @@ static cudaError_t launch_persistent_t(const CUtensorMap& tmA, const CUtensorMap
   auto dp = persistent_product_kernel<MT, BN, false>;
   err = cudaFuncSetAttribute(dp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
-  if (streamk_enabled() && total > G && rem != 0 && KT >= 8 && (int64_t)(rem + G) * KT * G < ((int64_t)1 << 31)) {
+  // only when the last wave is less than 3/4 full: a nearly full last wave loses less than the
+  // stream-K launch costs (measured on 1024-tile launches: 6.92 waves)
+  if (streamk_enabled() && total > G && rem != 0 && rem * 4 < G * 3 && KT >= 8 &&
+      (int64_t)(rem + G) * KT * G < ((int64_t)1 << 31)) {
     // Data-parallel waves, then stream-K over the partial last wave plus one full wave (every
     // CTA's share is one to two tiles of k-iterations), as two launches: the stream-K kernel's
     // extra state would cost the data-parallel main loop registers. Launches of less than one
