@@ -346,6 +346,166 @@ __global__ void __launch_bounds__(256) xform2_kernel(const MkXform2Job* __restri
   }
 }
 
+// ---- two-level post-addition (breadth-first plan) -------------------------------------------
+// One job = one recursion node at depth d - 2: its grandchildren's outputs G(p, p2) (depth d,
+// rows x cols each) -> the node's output block, 4 x 4 sub-blocks:
+//     out(q1, q2) = sum_p c[q1][p] * ( sum_p2 c[q2][p2] * G(p, p2) )
+// the children's outputs never touch memory. Sums run from zero in product order, exactly as
+// two one-level passes (bit-identical). C tables: reference kernels.py:66-160 post-additions.
+template <int TAB>
+struct XCTab;
+template <> struct XCTab<0> {  // Strassen
+  static constexpr int np = 7;
+  __host__ __device__ static constexpr int cf(int q, int p) {
+    constexpr int8_t c[4][8] = {{1, 0, 0, 1, -1, 0, 1, 0}, {0, 0, 1, 0, 1, 0, 0, 0},
+                                {0, 1, 0, 1, 0, 0, 0, 0}, {1, -1, 1, 0, 0, 1, 0, 0}};
+    return c[q][p];
+  }
+};
+template <> struct XCTab<1> {  // Winograd block
+  static constexpr int np = 7;
+  __host__ __device__ static constexpr int cf(int q, int p) {
+    constexpr int8_t c[4][8] = {{1, 1, 0, 0, 0, 0, 0, 0}, {1, 0, 1, 0, 1, 1, 0, 0},
+                                {1, 0, 0, -1, 0, 1, 1, 0}, {1, 0, 0, 0, 1, 1, 1, 0}};
+    return c[q][p];
+  }
+};
+template <> struct XCTab<2> {  // Winograd Knuth
+  static constexpr int np = 7;
+  __host__ __device__ static constexpr int cf(int q, int p) {
+    constexpr int8_t c[4][8] = {{1, 1, 0, 0, 0, 0, 0, 0}, {1, 0, 0, 1, 1, 1, 0, 0},
+                                {1, 0, 1, 0, 1, 0, 1, 0}, {1, 0, 1, 1, 1, 0, 0, 0}};
+    return c[q][p];
+  }
+};
+template <> struct XCTab<3> {  // Winograd Knuth, 8 calls
+  static constexpr int np = 8;
+  __host__ __device__ static constexpr int cf(int q, int p) {
+    constexpr int8_t c[4][8] = {{0, 1, 0, 0, 0, 0, 0, 1}, {1, 0, 0, 1, 1, 1, 0, 0},
+                                {1, 0, 1, 0, 1, 0, 1, 0}, {1, 0, 1, 1, 1, 0, 0, 0}};
+    return c[q][p];
+  }
+};
+
+int xpost2_table_coef(int tab, int q, int p) {
+  switch (tab) {
+    case 0: return XCTab<0>::cf(q, p);
+    case 1: return XCTab<1>::cf(q, p);
+    case 2: return XCTab<2>::cf(q, p);
+    default: return XCTab<3>::cf(q, p);
+  }
+}
+
+template <int TAB, int W>
+__global__ void __launch_bounds__(256) xpost2_kernel(const MkXpost2Job* __restrict__ jobs, int64_t rows,
+                                                     int64_t cols) {
+  using T = XCTab<TAB>;
+  constexpr int NP = T::np;
+  __shared__ const double* src_sh[MK_XFORM2_MAX];
+  const MkXpost2Job& jb = jobs[blockIdx.y];
+  if (threadIdx.x < NP * NP) src_sh[threadIdx.x] = jb.src[threadIdx.x];
+  __syncthreads();
+  const int64_t cv = cols / W;
+  const uint32_t total = (uint32_t)(rows * cv), ucv = (uint32_t)cv;
+  const int64_t lds = jb.lds, ldd = jb.ldd;
+  double* const dst = jb.dst;
+  for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    const uint32_t r = idx / ucv;
+    const int64_t c = (int64_t)(idx - r * ucv) * W;
+    const int64_t soff = (int64_t)r * lds + c;
+    Vec<W> out[16];
+#pragma unroll
+    for (int o = 0; o < 16; ++o)
+#pragma unroll
+      for (int u = 0; u < W; ++u) out[o].v[u] = 0.0;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      if (!src_sh[p * NP]) continue;  // job-uniform: product outside this pass
+      Vec<W> t[4];
+#pragma unroll
+      for (int q2 = 0; q2 < 4; ++q2)
+#pragma unroll
+        for (int u = 0; u < W; ++u) t[q2].v[u] = 0.0;
+#pragma unroll
+      for (int p2 = 0; p2 < NP; ++p2) {
+        const Vec<W> g = ld_vec<W>(src_sh[p * NP + p2] + soff);
+#pragma unroll
+        for (int q2 = 0; q2 < 4; ++q2) {
+          const int cf = T::cf(q2, p2);
+          if (cf > 0) {
+#pragma unroll
+            for (int u = 0; u < W; ++u) t[q2].v[u] += g.v[u];
+          } else if (cf < 0) {
+#pragma unroll
+            for (int u = 0; u < W; ++u) t[q2].v[u] -= g.v[u];
+          }
+        }
+      }
+#pragma unroll
+      for (int q1 = 0; q1 < 4; ++q1) {
+        const int cf = T::cf(q1, p);
+#pragma unroll
+        for (int q2 = 0; q2 < 4; ++q2) {
+          if (cf > 0) {
+#pragma unroll
+            for (int u = 0; u < W; ++u) out[q1 * 4 + q2].v[u] += t[q2].v[u];
+          } else if (cf < 0) {
+#pragma unroll
+            for (int u = 0; u < W; ++u) out[q1 * 4 + q2].v[u] -= t[q2].v[u];
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int q1 = 0; q1 < 4; ++q1)
+#pragma unroll
+      for (int q2 = 0; q2 < 4; ++q2) {
+        const int64_t rr = ((q1 >> 1) * 2 + (q2 >> 1)) * rows + r;
+        const int64_t cc = ((q1 & 1) * 2 + (q2 & 1)) * cols + c;
+        if (jb.acc_mask & (1u << (q1 * 4 + q2))) {
+          const Vec<W> old = ld_vec<W>(dst + rr * ldd + cc);
+#pragma unroll
+          for (int u = 0; u < W; ++u) out[q1 * 4 + q2].v[u] += old.v[u];
+        }
+        st_vec<W>(dst + rr * ldd + cc, out[q1 * 4 + q2]);
+      }
+  }
+}
+
+template <int TAB>
+static void launch_xpost2_t(dim3 grid, const MkXpost2Job* jobs, int64_t rows, int64_t cols, int width,
+                            cudaStream_t stream) {
+  if (width == 2)
+    xpost2_kernel<TAB, 2><<<grid, 256, 0, stream>>>(jobs, rows, cols);
+  else
+    xpost2_kernel<TAB, 1><<<grid, 256, 0, stream>>>(jobs, rows, cols);
+}
+
+cudaError_t launch_xpost2_batch(const MkXpost2Job* jobs_dev, int njobs, int table, int64_t rows, int64_t cols,
+                                int width, cudaStream_t stream) {
+  if (njobs <= 0 || rows <= 0 || cols <= 0) return cudaSuccess;
+  if (table < 0 || table > 3) return cudaErrorInvalidValue;
+  if (width != 2) width = 1;
+  const int64_t work = rows * (cols / width);
+  if (work >= (int64_t)1 << 32) return cudaErrorInvalidValue;
+  int64_t bx = (work + 255) / 256;
+  const int64_t cap = (148 * 16 + njobs - 1) / njobs;
+  if (bx > cap) bx = cap;
+  if (bx < 1) bx = 1;
+  for (int j0 = 0; j0 < njobs; j0 += 65535) {
+    const int nj = njobs - j0 < 65535 ? njobs - j0 : 65535;
+    dim3 grid((unsigned)bx, (unsigned)nj);
+    const MkXpost2Job* jb = jobs_dev + j0;
+    switch (table) {
+      case 0: launch_xpost2_t<0>(grid, jb, rows, cols, width, stream); break;
+      case 1: launch_xpost2_t<1>(grid, jb, rows, cols, width, stream); break;
+      case 2: launch_xpost2_t<2>(grid, jb, rows, cols, width, stream); break;
+      default: launch_xpost2_t<3>(grid, jb, rows, cols, width, stream); break;
+    }
+  }
+  return cudaGetLastError();
+}
+
 template <int TAB, int SIDE>
 static void launch_xform2_t(dim3 grid, const MkXform2Job* jobs, int64_t rows, int64_t cols, int width,
                             cudaStream_t stream) {

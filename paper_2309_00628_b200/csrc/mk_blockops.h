@@ -31,6 +31,21 @@ struct MkXform2Job {
   int64_t ldd;
 };
 
+// One job of the two-level post-addition: a node's grandchildren's outputs (src[p * np + p2],
+// common leading dimension lds, rows x cols each) -> the node's output block (dst, 4 x 4
+// sub-blocks of rows x cols, leading dimension ldd).
+// src entries may be nullptr (products outside a grouped pass: contribute nothing); bit
+// 4 * q1 + q2 of acc_mask adds the sub-block's previous contents after the sum (a grouped pass
+// accumulating onto the earlier passes' partial C).
+struct MkXpost2Job {
+  const double* src[MK_XFORM2_MAX];
+  int64_t lds;
+  double* dst;
+  int64_t ldd;
+  uint32_t acc_mask;
+  uint32_t pad_;
+};
+
 // One product of a batched leaf launch (device table, 64-byte aligned entries).
 struct alignas(64) MkBatchEntry {
   CUtensorMap tmA, tmB, tmC;
@@ -58,6 +73,9 @@ cudaError_t measure_dmma_peak(double* tflops_out, cudaStream_t st);
 cudaError_t launch_xform2_batch(const MkXform2Job* jobs_dev, int njobs, int table, int side, int64_t rows,
                                 int64_t cols, int width, cudaStream_t stream);
 int xform2_table_coef(int table, int side, int p, int q);
+cudaError_t launch_xpost2_batch(const MkXpost2Job* jobs_dev, int njobs, int table, int64_t rows, int64_t cols,
+                                int width, cudaStream_t stream);
+int xpost2_table_coef(int table, int q, int p);
 cudaError_t launch_fused_product(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
                                  const MkGemmArgs& args, const MkProduct& prod, cudaStream_t stream);
 int consumer_layout();

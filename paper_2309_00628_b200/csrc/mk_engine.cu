@@ -1279,6 +1279,76 @@ struct Engine {
     bool on = true;               // part of this pass (grouped plan: a subset of the top-level products)
   };
 
+  // Two depths of post-additions in one pass (xpost2_kernel): every active node of depth d - 2
+  // gets its output block straight from its grandchildren's outputs (depth d); the children's
+  // (depth d - 1) outputs are never materialised. The root (d - 2 == 0) writes D.
+  int bfs_xpost2(int d, int64_t M, int64_t N, const Blk& D, std::vector<std::vector<BNode>>& lv,
+                 const std::vector<int>* grp, bool* root_touched, bool* done) {
+    *done = false;
+    const int np = co->nprod;
+    const int table = algo == MK_ALGO_STRASSEN ? 0 : algo == MK_ALGO_WINOGRAD_BLOCK ? 1
+                    : algo == MK_ALGO_WINOGRAD_KNUTH ? 2 : algo == MK_ALGO_WINOGRAD_KNUTH_8CALL ? 3 : -1;
+    if (table < 0 || np * np > MK_XFORM2_MAX) return MK_OK;
+    for (int q = 0; q < 4; ++q)
+      for (int p = 0; p < np; ++p)
+        if (xpost2_table_coef(table, q, p) != co->c[q][p])
+          return fail(MK_ERR_ARG, "internal: compiled two-level post-addition table differs from the derived one");
+    std::vector<BNode>& gc = lv[d];
+    std::vector<BNode>& gp = lv[d - 2];
+    const int64_t cm = M >> d, cn = N >> d;  // grandchild output extents
+    std::vector<size_t> act;
+    for (size_t k = 0; k < gp.size(); ++k)
+      if (gp[k].on) act.push_back(k);
+    int64_t lds = -1;
+    for (size_t k : act)  // every grandchild output in one arena (one leading dimension), sign +1
+      for (int t = 0; t < np * np; ++t) {
+        const Blk& o = gc[k * np * np + t].o;
+        if (!gc[k * np * np + t].on) continue;
+        if (o.base < 0 || o.sign != 1.0 || (lds >= 0 && bases[o.base].ld != lds)) return MK_OK;
+        lds = bases[o.base].ld;
+      }
+    const bool root = d - 2 == 0;
+    int arena = -1;
+    if (!root) MK_TRY(alloc_slot((int64_t)act.size() * 4 * cm, 4 * cn, &arena, true));
+    std::vector<MkXpost2Job> jobs;
+    for (size_t kk = 0; kk < act.size(); ++kk) {
+      const size_t k = act[kk];
+      gp[k].o = root ? D : Blk{arena, (int64_t)kk * 4 * cm, 0, 1.0};
+      MkXpost2Job job{};
+      for (int p = 0; p < np; ++p) {
+        const bool on = gc[(k * np + p) * np].on;  // a grouped root pass runs only its products
+        for (int p2 = 0; p2 < np; ++p2) job.src[p * np + p2] = on ? ptr_of(gc[(k * np + p) * np + p2].o) : nullptr;
+      }
+      job.lds = lds;
+      job.dst = ptr_of(gp[k].o);
+      job.ldd = bases[gp[k].o.base].ld;
+      job.acc_mask = 0;
+      if (root && grp) {  // onto the earlier passes' partial sums
+        for (int q = 0; q < 4; ++q)
+          if (root_touched[q]) job.acc_mask |= 0xFu << (4 * q);
+      }
+      jobs.push_back(job);
+    }
+    if (root && grp)
+      for (int q = 0; q < 4; ++q) root_touched[q] = true;  // every quadrant is written (0 + ... when untouched)
+    if (!jobs.empty()) {
+      bool ok2 = cn % 2 == 0;
+      for (const MkXpost2Job& j : jobs) {
+        ok2 = ok2 && j.lds % 2 == 0 && j.ldd % 2 == 0 && reinterpret_cast<uintptr_t>(j.dst) % 16 == 0;
+        for (int t = 0; t < np * np; ++t) ok2 = ok2 && reinterpret_cast<uintptr_t>(j.src[t]) % 16 == 0;
+      }
+      void* dev = nullptr;
+      MK_TRY(upload(jobs.data(), jobs.size() * sizeof(MkXpost2Job), &dev));
+      if (!dry && !no_launch) {
+        MK_CUDA_TRY(launch_xpost2_batch(static_cast<const MkXpost2Job*>(dev), (int)jobs.size(), table, cm, cn,
+                                        ok2 ? 2 : 1, st));
+        ++g_launch_count;
+      }
+    }
+    *done = true;
+    return MK_OK;
+  }
+
   // Two depths of operand sums in one pass (xform2_kernel): every active node of depth d writes
   // its grandchildren's operands (depth d + 2) directly; the children's (depth d + 1) sums are
   // never materialised (their nodes get no operand blocks -- only leaves and the next pass read
@@ -1619,8 +1689,17 @@ struct Engine {
       }
     }
     if (!oz_items.empty()) MK_TRY(ozaki_batch(oz_items));
-    // ---- post-additions: child outputs -> parent quadrants, deepest first ----
+    // ---- post-additions: child outputs -> parent quadrants, deepest first (two depths per pass
+    // where xpost2 applies) ----
     for (int d = L - 1; d >= 1; --d) {
+      if (xform2_pairs() && d >= 2) {
+        bool done = false;
+        MK_TRY(bfs_xpost2(d, M, N, D, lv, grp, root_touched, &done));
+        if (done) {
+          --d;
+          continue;
+        }
+      }
       std::vector<BNode>& ch = lv[d];
       std::vector<BNode>& pa = lv[d - 1];
       const int64_t cm = M >> d, cn = N >> d;
