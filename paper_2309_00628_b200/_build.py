@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmk_strassen.so")
 SOURCES = ["mk_ozaki.cu", "mk_fused_gemm.cu", "mk_blockops.cu", "mk_peak.cu", "mk_hoststage.cu", "mk_engine.cu"]
-HEADERS = ["mk_ozaki.h", "mk_device.cuh", "mk_plan.h", "mk_blockops.h", "mk_hoststage.h"]
+HEADERS = ["mk_ozaki.h", "mk_device.cuh", "mk_plan.h", "mk_blockops.h", "mk_hoststage.h", "mk_xform.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

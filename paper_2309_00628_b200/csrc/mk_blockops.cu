@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include "mk_blockops.h"
+#include "mk_xform.cuh"
 
 namespace mk {
 
@@ -85,72 +86,14 @@ cudaError_t launch_combine(double* dst, int64_t ldd, const double* const* src, c
 // thread reads every source once (W consecutive doubles: 8, 16 or 32-byte accesses) and
 // writes every destination.
 template <int W>
-struct Vec {
-  double v[W];
-};
-template <int W>
-__device__ __forceinline__ Vec<W> ld_vec(const double* p) {
-  Vec<W> r;
-  if constexpr (W == 4) {
-    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
-                 : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3])
-                 : "l"(p));
-  } else if constexpr (W == 2) {
-    const double2 t = __ldg(reinterpret_cast<const double2*>(p));
-    r.v[0] = t.x;
-    r.v[1] = t.y;
-  } else {
-    r.v[0] = __ldg(p);
-  }
-  return r;
-}
-template <int W>
-__device__ __forceinline__ void st_vec(double* p, const Vec<W>& r) {
-  if constexpr (W == 4) {
-    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(r.v[0]), "d"(r.v[1]), "d"(r.v[2]),
-                 "d"(r.v[3])
-                 : "memory");
-  } else if constexpr (W == 2) {
-    *reinterpret_cast<double2*>(p) = make_double2(r.v[0], r.v[1]);
-  } else {
-    *p = r.v[0];
-  }
-}
-
-template <int W>
 __global__ void __launch_bounds__(256) xform_kernel(const MkXformJob* __restrict__ jobs, int64_t rows, int64_t cols) {
   const MkXformJob& jb = jobs[blockIdx.y];
-  const int ns = jb.nsrc, nd = jb.ndst;
   const int64_t cv = cols / W;
   // rows x cv < 2^32 for every block the planner forms (checked by the launcher)
   const uint32_t total = (uint32_t)(rows * cv), ucv = (uint32_t)cv;
   for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
     const uint32_t r = idx / ucv;
-    const int64_t c = (int64_t)(idx - r * ucv) * W;
-    Vec<W> v[MK_XFORM_MAX];
-#pragma unroll
-    for (int i = 0; i < MK_XFORM_MAX; ++i)
-      if (i < ns) v[i] = ld_vec<W>(jb.src[i] + r * jb.lds[i] + c);
-#pragma unroll
-    for (int j = 0; j < MK_XFORM_MAX; ++j) {
-      if (j < nd) {
-        Vec<W> acc;
-#pragma unroll
-        for (int u = 0; u < W; ++u) acc.v[u] = 0.0;
-#pragma unroll
-        for (int i = 0; i < MK_XFORM_MAX; ++i) {
-          const int cf = i < ns ? jb.coef[j][i] : 0;  // job-uniform: zero terms are skipped,
-          if (cf > 0) {                               // so an inf elsewhere cannot become NaN
-#pragma unroll
-            for (int u = 0; u < W; ++u) acc.v[u] += v[i].v[u];
-          } else if (cf < 0) {
-#pragma unroll
-            for (int u = 0; u < W; ++u) acc.v[u] -= v[i].v[u];
-          }
-        }
-        st_vec<W>(jb.dst[j] + r * jb.ldd[j] + c, acc);
-      }
-    }
+    xform_elem<W>(jb, r, (int64_t)(idx - r * ucv) * W);
   }
 }
 
@@ -190,74 +133,6 @@ cudaError_t launch_xform_batch(const MkXformJob* jobs_dev, int njobs, int64_t ro
 // compile time, so the kernel stays memory-bound; the round-1 runtime-table version was
 // instruction-bound); sums run in quadrant order from zero, exactly as two one-level passes
 // would compute them (bit-identical results). Tables: reference kernels.py:66-160.
-template <int TAB, int SIDE>
-struct X2Tab;
-// quadrant order 11, 12, 21, 22; [product][quadrant]
-template <> struct X2Tab<0, 0> {  // Strassen, A side
-  static constexpr int np = 7;
-  __host__ __device__ static constexpr int cf(int p, int q) {
-    constexpr int8_t c[8][4] = {{1, 0, 0, 1}, {0, 0, 1, 1}, {1, 0, 0, 0}, {0, 0, 0, 1},
-                                     {1, 1, 0, 0}, {-1, 0, 1, 0}, {0, 1, 0, -1}, {0, 0, 0, 0}};
-    return c[p][q];
-  }
-};
-template <> struct X2Tab<0, 1> {  // Strassen, B side
-  static constexpr int np = 7;
-  __host__ __device__ static constexpr int cf(int p, int q) {
-    constexpr int8_t c[8][4] = {{1, 0, 0, 1}, {1, 0, 0, 0}, {0, 1, 0, -1}, {-1, 0, 1, 0},
-                                     {0, 0, 0, 1}, {1, 1, 0, 0}, {0, 0, 1, 1}, {0, 0, 0, 0}};
-    return c[p][q];
-  }
-};
-template <> struct X2Tab<1, 0> {  // Winograd block, A side
-  static constexpr int np = 7;
-  __host__ __device__ static constexpr int cf(int p, int q) {
-    constexpr int8_t c[8][4] = {{1, 0, 0, 0}, {0, 1, 0, 0}, {1, 1, -1, -1}, {0, 0, 0, 1},
-                                     {0, 0, 1, 1}, {-1, 0, 1, 1}, {1, 0, -1, 0}, {0, 0, 0, 0}};
-    return c[p][q];
-  }
-};
-template <> struct X2Tab<1, 1> {  // Winograd block, B side
-  static constexpr int np = 7;
-  __host__ __device__ static constexpr int cf(int p, int q) {
-    constexpr int8_t c[8][4] = {{1, 0, 0, 0}, {0, 0, 1, 0}, {0, 0, 0, 1}, {1, -1, -1, 1},
-                                     {-1, 1, 0, 0}, {1, -1, 0, 1}, {0, -1, 0, 1}, {0, 0, 0, 0}};
-    return c[p][q];
-  }
-};
-template <> struct X2Tab<2, 0> {  // Winograd Knuth, A side
-  static constexpr int np = 7;
-  __host__ __device__ static constexpr int cf(int p, int q) {
-    constexpr int8_t c[8][4] = {{1, 0, 0, 0}, {0, 1, 0, 0}, {-1, 0, 1, 0}, {0, 0, 1, 1},
-                                     {-1, 0, 1, 1}, {1, 1, -1, -1}, {0, 0, 0, 1}, {0, 0, 0, 0}};
-    return c[p][q];
-  }
-};
-template <> struct X2Tab<2, 1> {  // Winograd Knuth, B side
-  static constexpr int np = 7;
-  __host__ __device__ static constexpr int cf(int p, int q) {
-    constexpr int8_t c[8][4] = {{1, 0, 0, 0}, {0, 0, 1, 0}, {0, 1, 0, -1}, {-1, 1, 0, 0},
-                                     {1, -1, 0, 1}, {0, 0, 0, 1}, {-1, 1, 1, -1}, {0, 0, 0, 0}};
-    return c[p][q];
-  }
-};
-template <> struct X2Tab<3, 0> {  // Winograd Knuth, 8 calls (first product recomputed), A side
-  static constexpr int np = 8;
-  __host__ __device__ static constexpr int cf(int p, int q) {
-    constexpr int8_t c[8][4] = {{1, 0, 0, 0}, {0, 1, 0, 0}, {-1, 0, 1, 0}, {0, 0, 1, 1},
-                                     {-1, 0, 1, 1}, {1, 1, -1, -1}, {0, 0, 0, 1}, {1, 0, 0, 0}};
-    return c[p][q];
-  }
-};
-template <> struct X2Tab<3, 1> {  // Winograd Knuth, 8 calls, B side
-  static constexpr int np = 8;
-  __host__ __device__ static constexpr int cf(int p, int q) {
-    constexpr int8_t c[8][4] = {{1, 0, 0, 0}, {0, 0, 1, 0}, {0, 1, 0, -1}, {-1, 1, 0, 0},
-                                     {1, -1, 0, 1}, {0, 0, 0, 1}, {-1, 1, 1, -1}, {1, 0, 0, 0}};
-    return c[p][q];
-  }
-};
-
 int xform2_table_coef(int tab, int side, int p, int q) {
   switch (tab * 2 + side) {
     case 0: return X2Tab<0, 0>::cf(p, q);
@@ -274,118 +149,19 @@ int xform2_table_coef(int tab, int side, int p, int q) {
 template <int TAB, int SIDE, int W>
 __global__ void __launch_bounds__(256) xform2_kernel(const MkXform2Job* __restrict__ jobs, int64_t rows,
                                                      int64_t cols) {
-  using T = X2Tab<TAB, SIDE>;
-  constexpr int NP = T::np;
+  constexpr int NP = X2Tab<TAB, SIDE>::np;
   __shared__ double* dst_sh[MK_XFORM2_MAX];
   const MkXform2Job& jb = jobs[blockIdx.y];
   if (threadIdx.x < NP * NP) dst_sh[threadIdx.x] = jb.dst[threadIdx.x];
   __syncthreads();
   const int64_t cv = cols / W;
   const uint32_t total = (uint32_t)(rows * cv), ucv = (uint32_t)cv;
-  const double* src = jb.src;
-  const int64_t lds = jb.lds, ldd = jb.ldd;
   for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
     const uint32_t r = idx / ucv;
-    const int64_t c = (int64_t)(idx - r * ucv) * W;
-    Vec<W> x[4][4];
-#pragma unroll
-    for (int q1 = 0; q1 < 4; ++q1)
-#pragma unroll
-      for (int q2 = 0; q2 < 4; ++q2) {
-        const int64_t rr = ((q1 >> 1) * 2 + (q2 >> 1)) * rows + r;
-        const int64_t cc = ((q1 & 1) * 2 + (q2 & 1)) * cols + c;
-        x[q1][q2] = ld_vec<W>(src + rr * lds + cc);
-      }
-    const int64_t off = (int64_t)r * ldd + c;
-#pragma unroll
-    for (int p = 0; p < NP; ++p) {
-      bool any = false;
-#pragma unroll
-      for (int p2 = 0; p2 < NP; ++p2) any = any || dst_sh[p * NP + p2] != nullptr;
-      if (!any) continue;  // job-uniform: this child is not in the pass, or all its grandchildren are views
-      Vec<W> t[4];
-#pragma unroll
-      for (int q2 = 0; q2 < 4; ++q2) {
-#pragma unroll
-        for (int u = 0; u < W; ++u) t[q2].v[u] = 0.0;
-#pragma unroll
-        for (int q1 = 0; q1 < 4; ++q1) {
-          if constexpr (true) {
-            const int cf = T::cf(p, q1);
-            if (cf > 0) {
-#pragma unroll
-              for (int u = 0; u < W; ++u) t[q2].v[u] += x[q1][q2].v[u];
-            } else if (cf < 0) {
-#pragma unroll
-              for (int u = 0; u < W; ++u) t[q2].v[u] -= x[q1][q2].v[u];
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int p2 = 0; p2 < NP; ++p2) {
-        double* d = dst_sh[p * NP + p2];
-        if (!d) continue;
-        Vec<W> o;
-#pragma unroll
-        for (int u = 0; u < W; ++u) o.v[u] = 0.0;
-#pragma unroll
-        for (int q2 = 0; q2 < 4; ++q2) {
-          const int cf = T::cf(p2, q2);
-          if (cf > 0) {
-#pragma unroll
-            for (int u = 0; u < W; ++u) o.v[u] += t[q2].v[u];
-          } else if (cf < 0) {
-#pragma unroll
-            for (int u = 0; u < W; ++u) o.v[u] -= t[q2].v[u];
-          }
-        }
-        st_vec<W>(d + off, o);
-      }
-    }
+    xform2_elem<TAB, SIDE, W>(jb.src, jb.lds, static_cast<double* const*>(dst_sh), jb.ldd, rows, cols, r,
+                              (int64_t)(idx - r * ucv) * W);
   }
 }
-
-// ---- two-level post-addition (breadth-first plan) -------------------------------------------
-// One job = one recursion node at depth d - 2: its grandchildren's outputs G(p, p2) (depth d,
-// rows x cols each) -> the node's output block, 4 x 4 sub-blocks:
-//     out(q1, q2) = sum_p c[q1][p] * ( sum_p2 c[q2][p2] * G(p, p2) )
-// the children's outputs never touch memory. Sums run from zero in product order, exactly as
-// two one-level passes (bit-identical). C tables: reference kernels.py:66-160 post-additions.
-template <int TAB>
-struct XCTab;
-template <> struct XCTab<0> {  // Strassen
-  static constexpr int np = 7;
-  __host__ __device__ static constexpr int cf(int q, int p) {
-    constexpr int8_t c[4][8] = {{1, 0, 0, 1, -1, 0, 1, 0}, {0, 0, 1, 0, 1, 0, 0, 0},
-                                {0, 1, 0, 1, 0, 0, 0, 0}, {1, -1, 1, 0, 0, 1, 0, 0}};
-    return c[q][p];
-  }
-};
-template <> struct XCTab<1> {  // Winograd block
-  static constexpr int np = 7;
-  __host__ __device__ static constexpr int cf(int q, int p) {
-    constexpr int8_t c[4][8] = {{1, 1, 0, 0, 0, 0, 0, 0}, {1, 0, 1, 0, 1, 1, 0, 0},
-                                {1, 0, 0, -1, 0, 1, 1, 0}, {1, 0, 0, 0, 1, 1, 1, 0}};
-    return c[q][p];
-  }
-};
-template <> struct XCTab<2> {  // Winograd Knuth
-  static constexpr int np = 7;
-  __host__ __device__ static constexpr int cf(int q, int p) {
-    constexpr int8_t c[4][8] = {{1, 1, 0, 0, 0, 0, 0, 0}, {1, 0, 0, 1, 1, 1, 0, 0},
-                                {1, 0, 1, 0, 1, 0, 1, 0}, {1, 0, 1, 1, 1, 0, 0, 0}};
-    return c[q][p];
-  }
-};
-template <> struct XCTab<3> {  // Winograd Knuth, 8 calls
-  static constexpr int np = 8;
-  __host__ __device__ static constexpr int cf(int q, int p) {
-    constexpr int8_t c[4][8] = {{0, 1, 0, 0, 0, 0, 0, 1}, {1, 0, 0, 1, 1, 1, 0, 0},
-                                {1, 0, 1, 0, 1, 0, 1, 0}, {1, 0, 1, 1, 1, 0, 0, 0}};
-    return c[q][p];
-  }
-};
 
 int xpost2_table_coef(int tab, int q, int p) {
   switch (tab) {
@@ -399,76 +175,17 @@ int xpost2_table_coef(int tab, int q, int p) {
 template <int TAB, int W>
 __global__ void __launch_bounds__(256) xpost2_kernel(const MkXpost2Job* __restrict__ jobs, int64_t rows,
                                                      int64_t cols) {
-  using T = XCTab<TAB>;
-  constexpr int NP = T::np;
+  constexpr int NP = XCTab<TAB>::np;
   __shared__ const double* src_sh[MK_XFORM2_MAX];
   const MkXpost2Job& jb = jobs[blockIdx.y];
   if (threadIdx.x < NP * NP) src_sh[threadIdx.x] = jb.src[threadIdx.x];
   __syncthreads();
   const int64_t cv = cols / W;
   const uint32_t total = (uint32_t)(rows * cv), ucv = (uint32_t)cv;
-  const int64_t lds = jb.lds, ldd = jb.ldd;
-  double* const dst = jb.dst;
   for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
     const uint32_t r = idx / ucv;
-    const int64_t c = (int64_t)(idx - r * ucv) * W;
-    const int64_t soff = (int64_t)r * lds + c;
-    Vec<W> out[16];
-#pragma unroll
-    for (int o = 0; o < 16; ++o)
-#pragma unroll
-      for (int u = 0; u < W; ++u) out[o].v[u] = 0.0;
-#pragma unroll
-    for (int p = 0; p < NP; ++p) {
-      if (!src_sh[p * NP]) continue;  // job-uniform: product outside this pass
-      Vec<W> t[4];
-#pragma unroll
-      for (int q2 = 0; q2 < 4; ++q2)
-#pragma unroll
-        for (int u = 0; u < W; ++u) t[q2].v[u] = 0.0;
-#pragma unroll
-      for (int p2 = 0; p2 < NP; ++p2) {
-        const Vec<W> g = ld_vec<W>(src_sh[p * NP + p2] + soff);
-#pragma unroll
-        for (int q2 = 0; q2 < 4; ++q2) {
-          const int cf = T::cf(q2, p2);
-          if (cf > 0) {
-#pragma unroll
-            for (int u = 0; u < W; ++u) t[q2].v[u] += g.v[u];
-          } else if (cf < 0) {
-#pragma unroll
-            for (int u = 0; u < W; ++u) t[q2].v[u] -= g.v[u];
-          }
-        }
-      }
-#pragma unroll
-      for (int q1 = 0; q1 < 4; ++q1) {
-        const int cf = T::cf(q1, p);
-#pragma unroll
-        for (int q2 = 0; q2 < 4; ++q2) {
-          if (cf > 0) {
-#pragma unroll
-            for (int u = 0; u < W; ++u) out[q1 * 4 + q2].v[u] += t[q2].v[u];
-          } else if (cf < 0) {
-#pragma unroll
-            for (int u = 0; u < W; ++u) out[q1 * 4 + q2].v[u] -= t[q2].v[u];
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int q1 = 0; q1 < 4; ++q1)
-#pragma unroll
-      for (int q2 = 0; q2 < 4; ++q2) {
-        const int64_t rr = ((q1 >> 1) * 2 + (q2 >> 1)) * rows + r;
-        const int64_t cc = ((q1 & 1) * 2 + (q2 & 1)) * cols + c;
-        if (jb.acc_mask & (1u << (q1 * 4 + q2))) {
-          const Vec<W> old = ld_vec<W>(dst + rr * ldd + cc);
-#pragma unroll
-          for (int u = 0; u < W; ++u) out[q1 * 4 + q2].v[u] += old.v[u];
-        }
-        st_vec<W>(dst + rr * ldd + cc, out[q1 * 4 + q2]);
-      }
+    xpost2_elem<TAB, W>(static_cast<const double* const*>(src_sh), jb.lds, jb.dst, jb.ldd, jb.acc_mask, rows, cols, r,
+                        (int64_t)(idx - r * ucv) * W);
   }
 }
 
@@ -544,6 +261,19 @@ cudaError_t launch_xform2_batch(const MkXform2Job* jobs_dev, int njobs, int tabl
     }
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_side_task(const MkSideTask& t, cudaStream_t stream) {
+  switch (t.kind) {
+    case 1: return launch_xform_batch(static_cast<const MkXformJob*>(t.jobs), t.njobs, t.rows, t.cols, t.width, stream);
+    case 2:
+      return launch_xform2_batch(static_cast<const MkXform2Job*>(t.jobs), t.njobs, t.table, t.side, t.rows, t.cols,
+                                 t.width, stream);
+    case 3:
+      return launch_xpost2_batch(static_cast<const MkXpost2Job*>(t.jobs), t.njobs, t.table, t.rows, t.cols, t.width,
+                                 stream);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 __global__ void i64_to_f64_kernel(const int64_t* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,

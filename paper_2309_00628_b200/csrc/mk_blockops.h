@@ -76,9 +76,12 @@ int xform2_table_coef(int table, int side, int p, int q);
 cudaError_t launch_xpost2_batch(const MkXpost2Job* jobs_dev, int njobs, int table, int64_t rows, int64_t cols,
                                 int width, cudaStream_t stream);
 int xpost2_table_coef(int table, int q, int p);
+// One side-work task (mk_plan.h) as a stand-alone launch (a leaf launch that cannot carry it).
+cudaError_t launch_side_task(const MkSideTask& task, cudaStream_t stream);
 cudaError_t launch_fused_product(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
                                  const MkGemmArgs& args, const MkProduct& prod, cudaStream_t stream);
 int consumer_layout();
+bool persistent_enabled();  // the persistent leaf kernel (env MK_PERSISTENT=0 disables it)
 // Tile width (64 or 128) the persistent kernel will use for a launch, and the row height of the
 // TMA epilogue's C boxes that launch needs (32 for narrow tiles and the 16-warp layout, else 64).
 int persistent_tile_n(int64_t tiles_m, int64_t N, int nprod);

@@ -72,6 +72,9 @@ __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* m, int c0, 
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 // wait until the smem sources of all committed bulk groups have been read
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+// wait until at most N of the most recently committed bulk groups still read their smem sources
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 
 // ---- Tensor memory as FP64 accumulator storage ---------------------------------------
 // (No tcgen05.mma is used: FP64 has no UMMA kind. TMEM only holds the second-level sums.)

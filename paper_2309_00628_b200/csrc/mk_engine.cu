@@ -1228,6 +1228,11 @@ struct Engine {
     void* dev = nullptr;
     MK_TRY(upload(jobs.data(), jobs.size() * sizeof(MkXformJob), &dev));
     if (dry || no_launch) return MK_OK;
+    if (defer) {
+      int64_t words = 0;
+      for (const MkXformJob& j : jobs) words += j.nsrc + j.ndst;
+      return side_task(dev, (int)jobs.size(), 1, 0, 0, rows, cols, width, words * rows * cols * 8);
+    }
     MK_CUDA_TRY(launch_xform_batch(static_cast<const MkXformJob*>(dev), (int)jobs.size(), rows, cols, width, st));
     ++g_launch_count;
     return MK_OK;
@@ -1278,6 +1283,36 @@ struct Engine {
     Blk o{-1, 0, 0, 1.0};         // output block (inner nodes; the root's is the caller's D)
     bool on = true;               // part of this pass (grouped plan: a subset of the top-level products)
   };
+  // State of one breadth-first pass across its three stages.
+  struct BfsPass {
+    int L = 0;
+    int64_t M = 0, N = 0, K = 0;
+    Blk X, Y, D;
+    bool grouped = false;
+    std::vector<int> grp;
+    std::vector<std::vector<BNode>> lv;
+    // Sub-ranges (pipelined driver): operand sums from depth d0 (lv prefilled to depth d0) up
+    // to depth d_end (-1: the leaves); post-additions down to depth post_stop, whose nodes write
+    // into preset output blocks (post_stop > 0).
+    int d0 = 0, d_end = -1, post_stop = 0;
+  };
+  // Deferral sink (pipelined driver): transform steps append side tasks to the last phase.
+  std::vector<std::vector<MkSideTask>>* defer = nullptr;
+  int side_task(const void* dev_jobs, int njobs, int kind, int table, int side, int64_t rows, int64_t cols, int width,
+                int64_t bytes) {
+    MkSideTask t{};
+    t.bytes = bytes;
+    t.jobs = dev_jobs;
+    t.njobs = njobs;
+    t.kind = (int8_t)kind;
+    t.table = (int8_t)table;
+    t.side = (int8_t)side;
+    t.width = (int8_t)width;
+    t.rows = rows;
+    t.cols = cols;
+    defer->back().push_back(t);
+    return MK_OK;
+  }
 
   // Two depths of post-additions in one pass (xpost2_kernel): every active node of depth d - 2
   // gets its output block straight from its grandchildren's outputs (depth d); the children's
@@ -1308,12 +1343,14 @@ struct Engine {
         lds = bases[o.base].ld;
       }
     const bool root = d - 2 == 0;
+    bool preset = !root;  // output blocks set by the caller (pipelined driver)
+    for (size_t k : act) preset = preset && gp[k].o.base >= 0;
     int arena = -1;
-    if (!root) MK_TRY(alloc_slot((int64_t)act.size() * 4 * cm, 4 * cn, &arena, true));
+    if (!root && !preset) MK_TRY(alloc_slot((int64_t)act.size() * 4 * cm, 4 * cn, &arena, true));
     std::vector<MkXpost2Job> jobs;
     for (size_t kk = 0; kk < act.size(); ++kk) {
       const size_t k = act[kk];
-      gp[k].o = root ? D : Blk{arena, (int64_t)kk * 4 * cm, 0, 1.0};
+      if (!preset) gp[k].o = root ? D : Blk{arena, (int64_t)kk * 4 * cm, 0, 1.0};
       MkXpost2Job job{};
       for (int p = 0; p < np; ++p) {
         const bool on = gc[(k * np + p) * np].on;  // a grouped root pass runs only its products
@@ -1339,7 +1376,14 @@ struct Engine {
       }
       void* dev = nullptr;
       MK_TRY(upload(jobs.data(), jobs.size() * sizeof(MkXpost2Job), &dev));
-      if (!dry && !no_launch) {
+      if (!dry && !no_launch && defer) {
+        int64_t words = 0;
+        for (const MkXpost2Job& j : jobs) {
+          words += 16 + __builtin_popcount(j.acc_mask);
+          for (int t = 0; t < np * np; ++t) words += j.src[t] ? 1 : 0;
+        }
+        MK_TRY(side_task(dev, (int)jobs.size(), 3, table, 0, cm, cn, ok2 ? 2 : 1, words * cm * cn * 8));
+      } else if (!dry && !no_launch) {
         MK_CUDA_TRY(launch_xpost2_batch(static_cast<const MkXpost2Job*>(dev), (int)jobs.size(), table, cm, cn,
                                         ok2 ? 2 : 1, st));
         ++g_launch_count;
@@ -1449,7 +1493,14 @@ struct Engine {
         }
         void* dev = nullptr;
         MK_TRY(upload(jobs.data(), jobs.size() * sizeof(MkXform2Job), &dev));
-        if (!dry && !no_launch) {
+        if (!dry && !no_launch && defer) {
+          int64_t words = 0;
+          for (const MkXform2Job& j : jobs) {
+            words += 16;
+            for (int t = 0; t < np * np; ++t) words += j.dst[t] ? 1 : 0;
+          }
+          MK_TRY(side_task(dev, (int)jobs.size(), 2, table, side, gr, gc, width, words * gr * gc * 8));
+        } else if (!dry && !no_launch) {
           MK_CUDA_TRY(launch_xform2_batch(static_cast<const MkXform2Job*>(dev), (int)jobs.size(), table, side, gr, gc,
                                           width, st));
           ++g_launch_count;
@@ -1470,16 +1521,45 @@ struct Engine {
   // whether quadrant q already holds an earlier pass's partial sum (accumulate) or not (store);
   // it is updated. The workspace of one pass is freed before the next, so the peak scales with
   // the largest group (run_square's grouped plan).
+  //
+  // The pass runs in three stages over one BfsPass state -- operand sums (bfs_operands), leaf
+  // launches (bfs_leaves), post-additions (bfs_post) -- so the pipelined driver
+  // (run_bfs_pipelined) can hand one pass's transforms to another pass's leaf launches as side
+  // work (defer != nullptr: every transform step becomes a phase of side tasks instead of a launch).
   int bfs(int L, int64_t M, int64_t N, int64_t K, Blk X, Blk Y, Blk D, const std::vector<int>* grp = nullptr,
           bool* root_touched = nullptr) {
-    const int np = co->nprod;
     if (grp && L < 2) return fail(MK_ERR_ARG, "internal: a grouped breadth-first pass needs >= 2 levels");
+    BfsPass ps;
+    ps.L = L;
+    ps.M = M;
+    ps.N = N;
+    ps.K = K;
+    ps.X = X;
+    ps.Y = Y;
+    ps.D = D;
+    ps.grouped = grp != nullptr;
+    if (grp) ps.grp = *grp;
+    MK_TRY(bfs_operands(ps));
+    MK_TRY(bfs_leaves(ps, nullptr));
+    return bfs_post(ps, root_touched);
+  }
+
+  int bfs_operands(BfsPass& ps) {
+    const int np = co->nprod;
+    const int L = ps.L;
+    const int64_t M = ps.M, N = ps.N, K = ps.K;
+    const std::vector<int>* grp = ps.grouped ? &ps.grp : nullptr;
     auto in_grp = [&](int p) { return !grp || std::find(grp->begin(), grp->end(), p) != grp->end(); };
-    std::vector<std::vector<BNode>> lv(1);
-    lv[0].push_back(BNode{X, Y, Blk{-1, 0, 0, 1.0}});
+    std::vector<std::vector<BNode>>& lv = ps.lv;
+    if (ps.d0 == 0) {
+      lv.assign(1, {});
+      lv[0].push_back(BNode{ps.X, ps.Y, Blk{-1, 0, 0, 1.0}});
+    }
+    const int d_end = ps.d_end < 0 ? L : ps.d_end;
     // ---- operand sums, depth by depth (two depths per pass where xform2 applies) ----
-    for (int d = 0; d < L; ++d) {
-      if (xform2_pairs() && (L - d) % 2 == 0) {  // depths d and d + 1 in one pass (the deepest pairs)
+    for (int d = ps.d0; d < d_end; ++d) {
+      if (defer) defer->emplace_back();  // one side-work phase per step
+      if (xform2_pairs() && (L - d) % 2 == 0 && d + 2 <= d_end) {  // depths d and d + 1 in one pass (the deepest pairs)
         bool done = false;
         MK_TRY(bfs_xform2(d, M, N, K, grp, lv, &done));
         if (done) {
@@ -1551,15 +1631,32 @@ struct Engine {
       MK_TRY(xform_batch(jb, hk, hn));
       lv.push_back(std::move(next));
     }
+    if (defer)  // steps with nothing to transform leave empty phases
+      defer->erase(std::remove_if(defer->begin(), defer->end(), [](const std::vector<MkSideTask>& ph) { return ph.empty(); }),
+                   defer->end());
+    return MK_OK;
+  }
+
+  // Leaf launches of a pass; side (optional): the side tasks each colour-group launch carries
+  // (index = launch order; tasks beyond the launches or MK_SIDE_MAX run as their own launches).
+  int bfs_leaves(BfsPass& ps, const std::vector<std::vector<MkSideTask>>* side) {
+    const int np = co->nprod;
+    const int L = ps.L;
+    const int64_t M = ps.M, N = ps.N, K = ps.K;
+    const Blk D = ps.D;
+    std::vector<std::vector<BNode>>& lv = ps.lv;
+    int launch_index = 0;
     // ---- leaves: one batched launch per sibling index ----
     std::vector<BNode>& par = lv[L - 1];
     const int64_t lm = M >> L, ln = N >> L, lk = K >> L;
     std::vector<size_t> act;  // the parents taking part in this pass
     for (size_t i = 0; i < par.size(); ++i)
       if (par[i].on) act.push_back(i);
+    bool preset = L > 1;  // parents' output blocks set by the caller (pipelined driver, L = 2)
+    for (size_t i : act) preset = preset && par[i].o.base >= 0;
     if (L == 1) {
       par[0].o = D;
-    } else {  // parents' outputs row-stacked in one arena
+    } else if (!preset) {  // parents' outputs row-stacked in one arena
       int ob;
       MK_TRY(alloc_slot((int64_t)act.size() * 2 * lm, 2 * ln, &ob, true));
       for (size_t j = 0; j < act.size(); ++j) par[act[j]].o = Blk{ob, (int64_t)j * 2 * lm, 0, 1.0};
@@ -1670,6 +1767,15 @@ struct Engine {
       g.group_m = 16;
       g.vec_ok = vec_ok ? 1 : 0;
       g.async_epi = async_ok ? 1 : 0;
+      if (side && launch_index < (int)side->size()) {
+        for (const MkSideTask& tk : (*side)[launch_index]) {
+          if (g.nside < MK_SIDE_MAX)
+            g.side[g.nside++] = tk;
+          else
+            MK_CUDA_TRY(launch_side_task(tk, st));
+        }
+      }
+      ++launch_index;
       cudaEvent_t t0 = nullptr, t1 = nullptr;
       if (g_timing.on) {
         MK_CUDA_TRY(cudaEventCreate(&t0));
@@ -1689,10 +1795,25 @@ struct Engine {
       }
     }
     if (!oz_items.empty()) MK_TRY(ozaki_batch(oz_items));
+    if (side)  // side work for launches that did not happen (fewer colour groups, INT8 leaves)
+      for (size_t k = (size_t)launch_index; k < side->size(); ++k)
+        for (const MkSideTask& tk : (*side)[k])
+          if (!dry && !no_launch) MK_CUDA_TRY(launch_side_task(tk, st));
+    return MK_OK;
+  }
+
+  int bfs_post(BfsPass& ps, bool* root_touched) {
+    const int np = co->nprod;
+    const int L = ps.L;
+    const int64_t M = ps.M, N = ps.N;
+    const Blk D = ps.D;
+    const std::vector<int>* grp = ps.grouped ? &ps.grp : nullptr;
+    std::vector<std::vector<BNode>>& lv = ps.lv;
     // ---- post-additions: child outputs -> parent quadrants, deepest first (two depths per pass
     // where xpost2 applies) ----
-    for (int d = L - 1; d >= 1; --d) {
-      if (xform2_pairs() && d >= 2) {
+    for (int d = L - 1; d >= ps.post_stop + 1; --d) {
+      if (defer) defer->emplace_back();  // one side-work phase per step
+      if (xform2_pairs() && d - 2 >= ps.post_stop) {
         bool done = false;
         MK_TRY(bfs_xpost2(d, M, N, D, lv, grp, root_touched, &done));
         if (done) {
@@ -1739,12 +1860,14 @@ struct Engine {
       for (size_t j = 0; j < pa.size(); ++j)
         if (pa[j].on) pact.push_back(j);
       int pb_arena = -1;
-      if (d - 1 != 0) MK_TRY(alloc_slot((int64_t)pact.size() * 2 * cm, 2 * cn, &pb_arena, true));
+      bool preset = d - 1 != 0;  // output blocks set by the caller (pipelined driver)
+      for (size_t j : pact) preset = preset && pa[j].o.base >= 0;
+      if (d - 1 != 0 && !preset) MK_TRY(alloc_slot((int64_t)pact.size() * 2 * cm, 2 * cn, &pb_arena, true));
       for (size_t jj = 0; jj < pact.size(); ++jj) {
         const size_t j = pact[jj];
         if (d - 1 == 0) {
           pa[j].o = D;
-        } else {
+        } else if (!preset) {
           pa[j].o = Blk{pb_arena, (int64_t)jj * 2 * cm, 0, 1.0};
         }
         MkXformJob job{};
@@ -1763,6 +1886,9 @@ struct Engine {
       }
       MK_TRY(xform_batch(jobs, cm, cn));
     }
+    if (defer)
+      defer->erase(std::remove_if(defer->begin(), defer->end(), [](const std::vector<MkSideTask>& ph) { return ph.empty(); }),
+                   defer->end());
     return MK_OK;
   }
 };
@@ -1842,6 +1968,271 @@ static int run_bfs_grouped(Engine& e, int64_t M, int64_t N, int64_t K) {
   return MK_OK;
 }
 
+// ---- pipelined breadth-first passes --------------------------------------------------------
+// Narrow-tile leaves (e.g. cfg5: 384 x 320 leaves) run in kernels whose producer warps carry side
+// work (mk_fused_gemm.cu, MkSideTask). Here pass i's leaf launches also stream pass i+1's operand
+// transforms and pass i-1's post-additions, so only the first pass's transforms and the last
+// pass's post-additions run as launches of their own; the rest hide under the FP64-tensor-bound
+// leaves (which leave ~80% of HBM bandwidth idle). Every transform and every leaf is the same
+// computation as in the sequential plan: results are bit-identical.
+// Workspace: three rotating pass regions (pass i's operands and outputs live from its transforms,
+// during pass i-1's leaves, to its post-additions, during pass i+1's leaves).
+static bool pipeline_enabled() {
+  static std::atomic<int> v{-1};
+  if (v < 0) {
+    const char* s = getenv("MK_PIPELINE");
+    v = (s && s[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+static bool use_pipeline(const Engine& e) {
+  // an explicit pass grouping (set_plan group=, MK_BFS_GROUP) asks for the grouped plan
+  if (!pipeline_enabled() || bfs_group_option() > 0 || e.L < 2 || e.tbl_mode != 0 || e.no_launch || e.leaf_count >= 0 || e.fuse_preadds) return false;
+  if (!persistent_enabled() || ozaki_leaf_for(e.leaf_m, e.leaf_n, e.leaf_k)) return false;
+  // the leaf launches must be narrow-tile ones (the layout that carries side work)
+  return persistent_tile_n((e.leaf_m + MK_BM - 1) / MK_BM, e.leaf_n, 1 << 12) == 64;
+}
+
+// Side work onto a pass's leaf launches, balanced by bytes: launch k takes cap[k] bytes (its leaf
+// time at MK_SIDE_GBPS, default 900 GB/s: the side warps stream ~2 TB/s alone, but they slow the
+// DMMA warps they share the SM with, so cfg5 is fastest when about half of that is hidden:
+// 600 / 900 / 1200 / 1500 / 1800 GB/s -> 70.6 / 69.5 / 70.2 / 71.6 / 74.2 ms, sequential 73.7). Each chain (the next pass's operand sums, the
+// previous pass's post-additions) is a sequence of phases that depend on each other: a phase may
+// start only in a launch after the one that finished its predecessor, so a launch carries at most
+// one phase per chain, possibly a slice of its jobs. Jobs of a phase are independent. Whatever
+// does not fit goes to `rest` (stand-alone launches after the leaves, each chain in order).
+using SidePhases = std::vector<std::vector<MkSideTask>>;
+static size_t side_job_bytes(int kind) {
+  return kind == 1 ? sizeof(MkXformJob) : kind == 2 ? sizeof(MkXform2Job) : sizeof(MkXpost2Job);
+}
+static void assign_side(const std::vector<const SidePhases*>& chains, const std::vector<double>& cap, SidePhases& per,
+                        SidePhases& rest) {
+  struct Cur {
+    const SidePhases* ph;
+    size_t phase = 0, task = 0;
+    int job = 0;
+    int done_at = -1;  // launch in which the previous phase finished
+  };
+  std::vector<Cur> cur;
+  for (const SidePhases* c : chains) cur.push_back(Cur{c});
+  auto phase_left = [](const Cur& c) { return c.phase < c.ph->size(); };
+  for (int k = 0; k < (int)per.size(); ++k) {
+    double budget = cap[k];
+    std::vector<std::vector<MkSideTask>> take(cur.size());
+    bool progress = true;
+    while (budget > 0 && progress) {  // round robin, one job at a time
+      progress = false;
+      for (size_t c = 0; c < cur.size() && budget > 0; ++c) {
+        Cur& u = cur[c];
+        if (!phase_left(u) || u.done_at >= k) continue;
+        const std::vector<MkSideTask>& tasks = (*u.ph)[u.phase];
+        const MkSideTask& tk = tasks[u.task];
+        // one-level transforms cannot ride on the leaf kernel (they run stand-alone before it)
+        const double jb = tk.kind == 1 ? 0.0 : (double)tk.bytes / std::max(tk.njobs, 1);
+        std::vector<MkSideTask>& tv = take[c];
+        const char* jp = static_cast<const char*>(tk.jobs) + (size_t)u.job * side_job_bytes(tk.kind);
+        if (!tv.empty() && static_cast<const char*>(tv.back().jobs) + (size_t)tv.back().njobs * side_job_bytes(tk.kind) == jp &&
+            tv.back().kind == tk.kind && tv.back().side == tk.side) {
+          tv.back().njobs += 1;
+          tv.back().bytes += (int64_t)jb;
+        } else {
+          MkSideTask part = tk;
+          part.jobs = jp;
+          part.njobs = 1;
+          part.bytes = (int64_t)jb;
+          tv.push_back(part);
+        }
+        budget -= jb;
+        progress = true;
+        if (++u.job == tk.njobs) {
+          u.job = 0;
+          if (++u.task == tasks.size()) {
+            u.task = 0;
+            ++u.phase;
+            u.done_at = k;
+          }
+        }
+      }
+    }
+    for (auto& tv : take) per[k].insert(per[k].end(), tv.begin(), tv.end());
+  }
+  for (Cur& u : cur) {  // leftovers, chain by chain in order
+    for (; phase_left(u); ++u.phase, u.task = 0, u.job = 0) {
+      std::vector<MkSideTask> ph;
+      const std::vector<MkSideTask>& tasks = (*u.ph)[u.phase];
+      for (size_t t = u.task; t < tasks.size(); ++t) {
+        MkSideTask part = tasks[t];
+        const int j0 = t == u.task ? u.job : 0;
+        part.jobs = static_cast<const char*>(part.jobs) + (size_t)j0 * side_job_bytes(part.kind);
+        part.njobs -= j0;
+        if (part.njobs > 0) ph.push_back(part);
+      }
+      if (!ph.empty()) rest.push_back(ph);
+    }
+  }
+}
+static double side_gbps() {
+  static std::atomic<int> v{-1};
+  if (v < 0) {
+    const char* s = getenv("MK_SIDE_GBPS");
+    v = s ? std::max(0, atoi(s)) : 900;
+  }
+  return (double)v;
+}
+
+// Pipelined plan: a prologue forms every top-level product's operand sums (one transform over
+// the quadrants, each read once); pass i then runs top-level product i's subtree (operand sums
+// from depth 1, leaves, post-additions up to its depth-1 output block) with its transforms
+// hidden under pass i-1's leaves and its post-additions under pass i+1's; an epilogue forms C's
+// quadrants from the seven depth-1 outputs. Workspace: the prologue's sums and the seven output
+// blocks, plus three rotating pass regions.
+static int run_bfs_pipelined(Engine& e, int64_t M, int64_t N, int64_t K) {
+  const Blk A{BASE_A, 0, 0, 1.0}, B{BASE_B, 0, 0, 1.0}, C{BASE_C, 0, 0, 1.0};
+  const int np = e.co->nprod;
+  const int64_t hm = M / 2, hn = N / 2;
+  Engine::BfsPass pro;
+  pro.L = e.L;
+  pro.M = M;
+  pro.N = N;
+  pro.K = K;
+  pro.X = A;
+  pro.Y = B;
+  pro.D = C;
+  pro.d_end = 1;
+  auto pass_of = [&](const Engine::BfsPass& pr, int p) {
+    Engine::BfsPass q = pr;
+    q.lv.resize(2);
+    for (int o = 0; o < np; ++o) q.lv[1][o].on = o == p;
+    q.d0 = 1;
+    q.d_end = -1;
+    q.post_stop = 1;
+    return q;
+  };
+  // sizing (host-only dry run): the persistent part, then the largest pass alone
+  size_t persist = 0, region = 0;
+  {
+    Engine probe = e;
+    probe.dry = true;
+    probe.ws_used = 0;
+    probe.ws_peak = 0;
+    Engine::BfsPass pr = pro;
+    MK_TRY(probe.bfs_operands(pr));
+    int slots = -1;
+    MK_TRY(probe.alloc_slot((int64_t)np * hm, hn, &slots, true));
+    for (int p = 0; p < np; ++p) pr.lv[1][p].o = Blk{slots, (int64_t)p * hm, 0, 1.0};
+    void* dummy = nullptr;
+    MK_TRY(probe.upload(nullptr, sizeof(MkXformJob), &dummy));  // the epilogue's job
+    persist = probe.ws_used;
+    for (int p = 0; p < np; ++p) {
+      Engine::BfsPass q = pass_of(pr, p);
+      probe.ws_used = 0;
+      probe.ws_peak = 0;
+      MK_TRY(probe.bfs_operands(q));
+      MK_TRY(probe.bfs_leaves(q, nullptr));
+      MK_TRY(probe.bfs_post(q, nullptr));
+      region = std::max(region, probe.ws_peak);
+    }
+  }
+  const int nregions = np < 3 ? np : 3;
+  const size_t base = e.ws_used;
+  const size_t need = base + persist + (size_t)nregions * region;
+  if (e.dry) {
+    e.ws_peak = std::max(e.ws_peak, need);
+    return MK_OK;
+  }
+  if (need > e.ws_bytes) return fail(MK_ERR_WORKSPACE, "workspace too small for the pipelined plan: need " + std::to_string(need));
+  const int nb_mark = e.nbases;
+  // ---- prologue: every top-level product's operand sums (launches of their own) ----
+  MK_TRY(e.bfs_operands(pro));
+  int slots = -1;
+  MK_TRY(e.alloc_slot((int64_t)np * hm, hn, &slots, true));
+  for (int p = 0; p < np; ++p) pro.lv[1][p].o = Blk{slots, (int64_t)p * hm, 0, 1.0};
+  MkXformJob ep{};  // the epilogue: C's quadrants from the depth-1 outputs (reference post-additions)
+  ep.nsrc = np;
+  for (int p = 0; p < np; ++p) {
+    ep.src[p] = e.ptr_of(pro.lv[1][p].o);
+    ep.lds[p] = e.bases[slots].ld;
+  }
+  ep.ndst = 4;
+  for (int q = 0; q < 4; ++q) {
+    ep.dst[q] = e.ptr_of(Blk{C.base, C.row + (q >> 1) * hm, C.col + (q & 1) * hn, 1.0});
+    ep.ldd[q] = e.bases[C.base].ld;
+    for (int p = 0; p < np; ++p) ep.coef[q][p] = (int8_t)e.co->c[q][p];
+  }
+  void* ep_dev = nullptr;
+  MK_TRY(e.upload(&ep, sizeof(MkXformJob), &ep_dev));
+  const size_t persist_end = base + persist;
+  if (e.ws_used != persist_end) return fail(MK_ERR_ARG, "internal: pipelined plan sizing differs from the run");
+  // ---- passes ----
+  size_t used[3];
+  auto enter = [&](int i, bool fresh) {
+    const int r = i % nregions;
+    if (fresh) used[r] = persist_end + (size_t)r * region;
+    e.ws_used = used[r];
+  };
+  auto leave = [&](int i) { used[i % nregions] = e.ws_used; };
+  std::vector<int> cap_products;
+  for (const auto& gr : e.colour_siblings()) cap_products.push_back((int)gr.size());
+  const int nl = (int)cap_products.size();
+  std::vector<Engine::BfsPass> ps;
+  for (int p = 0; p < np; ++p) ps.push_back(pass_of(pro, p));
+  // side bytes one launch can hide: its leaf time (FP64 tensor rate ~33 TF/s on these leaves)
+  // at the side warps' bandwidth
+  const int64_t lm = M >> e.L, ln = N >> e.L, lk = K >> e.L;
+  int64_t parents = 1;
+  for (int d = 1; d < e.L - 1; ++d) parents *= np;  // depth L-1 nodes under one top-level product
+  std::vector<double> cap;
+  for (int c : cap_products) cap.push_back((double)c * parents * 2.0 * lm * ln * lk / 33e12 * side_gbps() * 1e9);
+  enter(0, true);
+  MK_TRY(e.bfs_operands(ps[0]));  // the first pass's transforms: launches of their own
+  leave(0);
+  SidePhases post_prev;
+  for (int i = 0; i < np; ++i) {
+    SidePhases next_ops;
+    if (i + 1 < np) {
+      enter(i + 1, true);
+      e.defer = &next_ops;
+      const int rc = e.bfs_operands(ps[i + 1]);
+      e.defer = nullptr;
+      MK_TRY(rc);
+      leave(i + 1);
+    }
+    SidePhases per(nl), rest;
+    assign_side({&next_ops, &post_prev}, cap, per, rest);
+    enter(i, false);
+    MK_TRY(e.bfs_leaves(ps[i], &per));
+    for (const auto& ph : rest)
+      for (const MkSideTask& tk : ph) MK_CUDA_TRY(launch_side_task(tk, e.st));
+    post_prev.clear();
+    e.defer = &post_prev;
+    const int rc = e.bfs_post(ps[i], nullptr);
+    e.defer = nullptr;
+    MK_TRY(rc);
+    leave(i);
+  }
+  for (const auto& ph : post_prev)  // the last pass's post-additions: launches of their own
+    for (const MkSideTask& tk : ph) MK_CUDA_TRY(launch_side_task(tk, e.st));
+  // ---- epilogue ----
+  {
+    std::vector<MkXformJob> one{ep};
+    int width = 2;  // as xform_batch would choose
+    bool ok = hn % 2 == 0;
+    for (int p = 0; p < np; ++p) ok = ok && ep.lds[p] % 2 == 0 && reinterpret_cast<uintptr_t>(ep.src[p]) % 16 == 0;
+    for (int q = 0; q < 4; ++q) ok = ok && ep.ldd[q] % 2 == 0 && reinterpret_cast<uintptr_t>(ep.dst[q]) % 16 == 0;
+    if (!ok) width = 1;
+    MK_CUDA_TRY(launch_xform_batch(static_cast<const MkXformJob*>(ep_dev), 1, hm, hn, width, e.st));
+    ++g_launch_count;
+  }
+  e.ws_used = base;
+  while (e.nbases > nb_mark) {
+    --e.nbases;
+    e.written.pop_back();
+    e.cell_rows.pop_back();
+    e.cell_cols.pop_back();
+  }
+  return MK_OK;
+}
+
 static int run_square(Engine& e) {
   const int64_t n = e.n;
   if (plan_kind() == 2 && !e.fuse_preadds && e.leaf_count < 0 && e.L >= 2 && e.algo >= MK_ALGO_STRASSEN &&
@@ -1853,7 +2244,7 @@ static int run_square(Engine& e) {
     return MK_OK;
   }
   if (use_bfs(e, e.leaf_m, e.leaf_n))
-    return run_bfs_grouped(e, n, n, n);
+    return use_pipeline(e) ? run_bfs_pipelined(e, n, n, n) : run_bfs_grouped(e, n, n, n);
   if (e.algo == MK_ALGO_TWO_TEMP)
     return e.literal(kTwoTemp, true, e.L, Blk{BASE_A, 0, 0, 1.0}, Blk{BASE_B, 0, 0, 1.0}, Blk{BASE_C, 0, 0, 1.0}, n);
   if (e.algo == MK_ALGO_IN_PLACE)
@@ -2759,7 +3150,7 @@ static int run_rect(int algo, const double* A, int64_t lda, const double* B, int
     const Lin A0{Blk{BASE_A, 0, 0, 1.0}}, B0{Blk{BASE_B, 0, 0, 1.0}}, C0{Blk{BASE_C, 0, 0, 1.0}};
     for (int p = 0; p < e.co->nprod; ++p) MK_TRY(e.top_product_bfs(p, A0, B0, C0, mp / 2, np_ / 2, kp / 2));
   } else if (use_bfs(e, e.leaf_m, e.leaf_n))
-    MK_TRY(run_bfs_grouped(e, mp, np_, kp));
+    MK_TRY(use_pipeline(e) ? run_bfs_pipelined(e, mp, np_, kp) : run_bfs_grouped(e, mp, np_, kp));
   else
     MK_TRY(e.fused(levels, Lin{Blk{BASE_A, 0, 0, 1.0}}, Lin{Blk{BASE_B, 0, 0, 1.0}}, Lin{Blk{BASE_C, 0, 0, 1.0}},
                    mp, np_, kp, 0));

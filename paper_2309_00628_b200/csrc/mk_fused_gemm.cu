@@ -29,9 +29,11 @@
 #include <map>
 #include <mutex>
 #include <type_traits>
+#include <vector>
 #include "mk_device.cuh"
 #include "mk_plan.h"
 #include "mk_blockops.h"
+#include "mk_xform.cuh"
 
 namespace mk {
 
@@ -533,16 +535,139 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const __grid
 // 8*MT x 32 cover the 128 x BN tile. (8, 128): 8 warps of 64x32 (default); (4, 128): 16 warps of
 // 32x32 (MK_CONSUMER_WARPS=16); (4, 64): 8 warps of 32x32 for narrow leaves (BN = 64 halves the
 // column padding of leaves whose width is not a multiple of 128, e.g. cfg5's 316).
-template <int MT, int BN>
+#ifndef MK_EPI_BUFS_NARROW
+#define MK_EPI_BUFS_NARROW 1
+#endif
+#ifndef MK_TAIL_SKIP
+#define MK_TAIL_SKIP 1
+#endif
+template <int MT, int BN, bool SW = false>
 struct PLayout {
   static constexpr int kWarpsN = BN / 32;
   static constexpr int kConsumerWarps = (MK_BM / (8 * MT)) * kWarpsN;
-  static constexpr int kThreads = 128 + 32 * kConsumerWarps;
+  // SW (narrow tiles only): the launch carries side work (below); a second non-DMMA warpgroup
+  // joins the producer's, so 7 side warps stream the transforms (3 are latency-bound at ~1 TB/s).
+  // Launches without side work run the 384-thread layout (its consumers keep 224 registers).
+  static constexpr bool kSideWork = SW;
+  static constexpr int kLeadWarps = kSideWork ? 8 : 4;  // warps before the first DMMA consumer
+  static constexpr int kSideThreads = kSideWork ? 32 * (kLeadWarps - 1) : 0;
+  static constexpr int kThreads = 32 * kLeadWarps + 32 * kConsumerWarps;
   static constexpr int kStageBytes = MK_TILE_BYTES + BN * MK_BK * 8;
-  static constexpr int kBoxBytes = kConsumerWarps * 8 * MT * 128;  // one 16-column box per warp
-  static constexpr int kProducerRegs = kThreads == 384 ? 56 : 32;
-  static constexpr int kConsumerRegs = kThreads == 384 ? 224 : 112;
+  // epilogue boxes per warp (MK_EPI_BUFS_NARROW > 1 lets a narrow-tile warp fill its next box while
+  // the TMA unit still reads the last: measured no faster on cfg5, so one by default)
+  static constexpr int kEpiBufs = BN == 64 ? MK_EPI_BUFS_NARROW : 1;
+  static constexpr int kBoxBytes = kEpiBufs * kConsumerWarps * 8 * MT * 128;  // 16-column boxes
+  // Register split (setmaxnreg): the wide layout's 64 x 32 consumers take 224, its producer 56.
+  // The side-work layout (512 threads, 128 each at launch): the two lead warpgroups drop to 104
+  // (the two-level operand transform at 16-byte width needs 92; the post-addition runs at 8-byte
+  // width there, 64) and the 32 x 32 consumer warps rise to 152 (at 128 they reload loop state
+  // from local memory every k-stage: main loop -2.4%).
+  static constexpr int kProducerRegs = kSideWork ? 104 : (kThreads == 384 ? 56 : 32);
+  static constexpr int kConsumerRegs = kSideWork ? 152 : (kThreads == 384 ? 224 : 112);
 };
+
+// Side work: every task of the launch in order. A task's jobs are spread over groups of CTAs
+// (enough CTAs per job for >= 4 element groups per thread); within a group the NT side threads
+// of each CTA grid-stride over the job's element groups (row, W columns). The job's 49-64 block
+// pointers are staged in shared memory once per job (the stand-alone kernels do the same) --
+// read per element group from global memory, the pointer loads serialise every store behind an
+// L1 round trip. Kinds 2 and 3 only: the one-level transform's runtime source/destination loops
+// spill in the producer's register budget, so the launcher runs kind-1 tasks as their own launches.
+template <int NT>
+__device__ __forceinline__ void side_bar() { asm volatile("bar.sync 5, %0;" ::"n"(NT) : "memory"); }
+template <int NT, int W, typename Stage, typename F>
+__device__ __forceinline__ void side_loop(const MkSideTask& tk, uint32_t tid, uint32_t cta, uint32_t ncta, Stage&& stage,
+                                          F&& f) {
+  const uint32_t cv = (uint32_t)(tk.cols / W);
+  const uint32_t per = (uint32_t)tk.rows * cv;
+  uint32_t G = per / (NT * 4u);  // CTAs per job
+  G = G < 1 ? 1 : (G > ncta ? ncta : G);
+  const uint32_t ngroups = ncta / G;
+  const uint32_t grp = cta / G, sub = cta - grp * G;
+  if (grp >= ngroups) return;  // the CTAs past the last whole group sit this task out
+  for (uint32_t j = grp; j < (uint32_t)tk.njobs; j += ngroups) {
+    side_bar<NT>();  // the previous job's pointers are no longer read
+    stage(j);
+    side_bar<NT>();
+    for (uint32_t e = sub * NT + tid; e < per; e += G * NT) {
+      const uint32_t r = e / cv;
+      f(j, r, (int64_t)(e - r * cv) * W);
+    }
+  }
+}
+template <int NT, int TAB, int SIDE, int W>
+__device__ __forceinline__ void side_xform2(const MkSideTask& tk, uint32_t tid, uint32_t cta, uint32_t ncta,
+                                            double** ptr_sh) {
+  constexpr int NP = X2Tab<TAB, SIDE>::np;
+  const MkXform2Job* jobs = static_cast<const MkXform2Job*>(tk.jobs);
+  side_loop<NT, W>(
+      tk, tid, cta, ncta,
+      [&](uint32_t j) {
+        if (tid < NP * NP) ptr_sh[tid] = jobs[j].dst[tid];
+      },
+      [&](uint32_t j, uint32_t r, int64_t c) {
+        const MkXform2Job& jb = jobs[j];
+        xform2_elem<TAB, SIDE, W>(jb.src, jb.lds, static_cast<double* const*>(ptr_sh), jb.ldd, tk.rows, tk.cols, r, c);
+      });
+}
+template <int NT, int TAB, int W>
+__device__ __forceinline__ void side_xpost2(const MkSideTask& tk, uint32_t tid, uint32_t cta, uint32_t ncta,
+                                            double** ptr_sh) {
+  constexpr int NP = XCTab<TAB>::np;
+  const MkXpost2Job* jobs = static_cast<const MkXpost2Job*>(tk.jobs);
+  side_loop<NT, W>(
+      tk, tid, cta, ncta,
+      [&](uint32_t j) {
+        if (tid < NP * NP) ptr_sh[tid] = const_cast<double*>(jobs[j].src[tid]);
+      },
+      [&](uint32_t j, uint32_t r, int64_t c) {
+        const MkXpost2Job& jb = jobs[j];
+        xpost2_elem<TAB, W>(static_cast<const double* const*>(ptr_sh), jb.lds, jb.dst, jb.ldd, jb.acc_mask, tk.rows,
+                            tk.cols, r, c);
+      });
+}
+template <int NT>
+__device__ __forceinline__ void side_work(const MkGemmArgs& a, uint32_t tid, uint32_t cta, uint32_t ncta, double** ptr_sh) {
+  for (int t = 0; t < a.nside; ++t) {
+    const MkSideTask& tk = a.side[t];
+#ifdef MK_SIDE_W1
+    const bool w2 = false;
+#else
+    const bool w2 = tk.width == 2;
+#endif
+    if (tk.kind == 2) {
+      switch (tk.table * 4 + tk.side * 2 + (w2 ? 1 : 0)) {
+        case 0: side_xform2<NT, 0, 0, 1>(tk, tid, cta, ncta, ptr_sh); break;
+        case 1: side_xform2<NT, 0, 0, 2>(tk, tid, cta, ncta, ptr_sh); break;
+        case 2: side_xform2<NT, 0, 1, 1>(tk, tid, cta, ncta, ptr_sh); break;
+        case 3: side_xform2<NT, 0, 1, 2>(tk, tid, cta, ncta, ptr_sh); break;
+        case 4: side_xform2<NT, 1, 0, 1>(tk, tid, cta, ncta, ptr_sh); break;
+        case 5: side_xform2<NT, 1, 0, 2>(tk, tid, cta, ncta, ptr_sh); break;
+        case 6: side_xform2<NT, 1, 1, 1>(tk, tid, cta, ncta, ptr_sh); break;
+        case 7: side_xform2<NT, 1, 1, 2>(tk, tid, cta, ncta, ptr_sh); break;
+        case 8: side_xform2<NT, 2, 0, 1>(tk, tid, cta, ncta, ptr_sh); break;
+        case 9: side_xform2<NT, 2, 0, 2>(tk, tid, cta, ncta, ptr_sh); break;
+        case 10: side_xform2<NT, 2, 1, 1>(tk, tid, cta, ncta, ptr_sh); break;
+        case 11: side_xform2<NT, 2, 1, 2>(tk, tid, cta, ncta, ptr_sh); break;
+        case 12: side_xform2<NT, 3, 0, 1>(tk, tid, cta, ncta, ptr_sh); break;
+        case 13: side_xform2<NT, 3, 0, 2>(tk, tid, cta, ncta, ptr_sh); break;
+        case 14: side_xform2<NT, 3, 1, 1>(tk, tid, cta, ncta, ptr_sh); break;
+        default: side_xform2<NT, 3, 1, 2>(tk, tid, cta, ncta, ptr_sh); break;
+      }
+    } else if (tk.kind == 3) {
+      switch (tk.table * 2 + (w2 ? 1 : 0)) {
+        case 0: side_xpost2<NT, 0, 1>(tk, tid, cta, ncta, ptr_sh); break;
+        case 1: side_xpost2<NT, 0, 1>(tk, tid, cta, ncta, ptr_sh); break;
+        case 2: side_xpost2<NT, 1, 1>(tk, tid, cta, ncta, ptr_sh); break;
+        case 3: side_xpost2<NT, 1, 1>(tk, tid, cta, ncta, ptr_sh); break;
+        case 4: side_xpost2<NT, 2, 1>(tk, tid, cta, ncta, ptr_sh); break;
+        case 5: side_xpost2<NT, 2, 1>(tk, tid, cta, ncta, ptr_sh); break;
+        case 6: side_xpost2<NT, 3, 1>(tk, tid, cta, ncta, ptr_sh); break;
+        default: side_xpost2<NT, 3, 1>(tk, tid, cta, ncta, ptr_sh); break;
+      }
+    }
+  }
+}
 
 // Work units of one persistent CTA: its data-parallel tiles (t = b, b + G, ... < sk_tile0, whole
 // K), then its share [lo(b), lo(b + 1)) of the stream-K iterations (tile-major, k-minor) of the
@@ -564,22 +689,23 @@ __device__ __forceinline__ bool sk_unit(const MkGemmArgs& a, int it, int& t, int
   ke = min(KT, kb + (hi - it));
   return true;
 }
-template <int MT, int BN, bool SK>
-__global__ void __launch_bounds__(PLayout<MT, BN>::kThreads, 1)
+template <int MT, int BN, bool SK, bool SW = false>
+__global__ void __launch_bounds__(PLayout<MT, BN, SW>::kThreads, 1)
 persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const __grid_constant__ CUtensorMap tmB_param,
-                          const __grid_constant__ CUtensorMap tmC_param, const MkGemmArgs args,
+                          const __grid_constant__ CUtensorMap tmC_param, const __grid_constant__ MkGemmArgs args,
                           const __grid_constant__ MkProduct prod_param) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kMaxStages];
   __shared__ __align__(8) uint64_t empty_bar[kMaxStages];
   __shared__ uint32_t tmem_base_sh;
+  __shared__ double* side_ptr_sh[SW ? MK_XFORM2_MAX : 1];  // side work: a job's pointers
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int S = args.stages;
   const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* smem_gen = smem_raw + (smem_base - smem_u32(smem_raw));
-  using PL = PLayout<MT, BN>;
+  using PL = PLayout<MT, BN, SW>;
   uint8_t* box_area = smem_gen + (size_t)S * PL::kStageBytes;  // epilogue boxes, one per consumer warp
   const int tiles_per = args.tiles_m * args.tiles_n;
   const int total = tiles_per * (args.batch ? args.nprod : 1);
@@ -606,9 +732,15 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
   }
   __syncthreads();
 
-  if (warp < 4) {
+  if (warp < PL::kLeadWarps) {
     // ============================ TMA producer (one thread) ============================
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PL::kProducerRegs));
+    if constexpr (PL::kSideWork) {  // warps 1..7: the launch's side work
+      if (warp >= 1) {
+        if (!SK && args.nside > 0) side_work<PL::kSideThreads>(args, threadIdx.x - 32u, blockIdx.x, gridDim.x, side_ptr_sh);
+        return;
+      }
+    }
     if (threadIdx.x != 0) return;
     int s = 0;            // ring slot of the next stage (carried across tiles)
     uint32_t eph = 0;     // parity of the empty-barrier phase to wait for (first lap: no wait)
@@ -655,7 +787,7 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
 
   // ================================ DMMA consumers ================================
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(PL::kConsumerRegs));
-  const int cw = warp - 4;
+  const int cw = warp - PL::kLeadWarps;
   const int warp_m = cw / PL::kWarpsN;
   const int warp_n = cw % PL::kWarpsN;
   const int q = lane & 3, g = lane >> 2;
@@ -678,6 +810,9 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
     constexpr bool TAIL = decltype(tail_tag)::value;
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
+      // last k-stage: k-steps 8t.. past the end of K hold only zero padding; skip their DMMAs
+      // (they would add exact zeros: the accumulators are unchanged bit for bit)
+      if (TAIL && MK_TAIL_SKIP && 8 * t >= krem) break;
       const uint32_t a_chunk = t ? a_chunk1 : a_chunk0;
       double a0[MT], a1[MT];
 #pragma unroll
@@ -754,7 +889,8 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
   };
 
   constexpr int kBoxRows = 8 * MT;
-  uint8_t* box = box_area + (size_t)cw * (kBoxRows * 128);
+  uint8_t* const box0 = box_area + (size_t)cw * (kBoxRows * 128);
+  int ebuf = 0;  // next epilogue box of this warp (carried across tiles)
   const int c_first = (g & 1) ? 1 : 0;
   bool reads_pending = false;  // TMA reads of this warp's box still in flight
   const int krem_last = args.K - (KT - 1) * MK_BK;
@@ -872,13 +1008,13 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
     }
 
     // ---- epilogue: every destination of the product, signs grouped into two passes ----
-    const double out_sign = prod.a[0].sign * prod.b[0].sign;
-    const int nd = prod.nd;
     if (args.async_epi) {
       const CUtensorMap* tmC = ent ? &ent->tmC : &tmC_param;
       const int row0 = m0 + warp_m * kBoxRows;
       const int col0 = n0 + warp_n * 32;
       const bool slab_live = row0 < args.M && col0 < args.N;
+      const double out_sign = prod.a[0].sign * prod.b[0].sign;
+      const int nd = prod.nd;
       for (int pass = 0; pass < 2; ++pass) {
         const double want = pass == 0 ? 1.0 : -1.0;
         bool any = false;
@@ -886,8 +1022,10 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
         if (!any) continue;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
+          uint8_t* const box = box0 + (size_t)ebuf * (PL::kConsumerWarps * kBoxRows * 128);
           if (reads_pending) {  // the box's previous contents must have been read by the TMA unit
-            if (lane == 0) bulk_wait_read_all();
+            // one bulk group per box fill: the group that used this box is kEpiBufs fills old
+            if (lane == 0) bulk_wait_read<PL::kEpiBufs - 1>();
             __syncwarp();
           }
 #pragma unroll
@@ -905,22 +1043,27 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
           }
           fence_proxy_async();
           __syncwarp();
-          if (lane == 0 && slab_live && col0 + 16 * j < args.N) {
-            for (int d = 0; d < nd; ++d) {
-              const MkDest dst = prod.d[d];
-              if ((dst.sign * out_sign) != want) continue;
-              const int cc = (int)dst.col + col0 + 16 * j, rr = (int)dst.row + row0;
-              if (dst.accumulate)
-                tma_reduce_add_2d(tmC, cc, rr, box);
-              else
-                tma_store_2d(tmC, cc, rr, box);
+          if (lane == 0) {
+            if (slab_live && col0 + 16 * j < args.N) {
+              for (int d = 0; d < nd; ++d) {
+                const MkDest dst = prod.d[d];
+                if ((dst.sign * out_sign) != want) continue;
+                const int cc = (int)dst.col + col0 + 16 * j, rr = (int)dst.row + row0;
+                if (dst.accumulate)
+                  tma_reduce_add_2d(tmC, cc, rr, box);
+                else
+                  tma_store_2d(tmC, cc, rr, box);
+              }
             }
-            bulk_commit();
+            bulk_commit();  // (possibly empty) group per box fill, so wait_group counts box fills
           }
           reads_pending = true;
+          if (++ebuf == PL::kEpiBufs) ebuf = 0;
         }
       }
     } else {
+      const double out_sign = prod.a[0].sign * prod.b[0].sign;
+      const int nd = prod.nd;
       double* const Cbase = ent ? ent->C : args.C;
       const int64_t ldc = ent ? ent->ldc : args.ldc;
       for (int d = 0; d < nd; ++d) {
@@ -1119,7 +1262,34 @@ static cudaError_t launch_persistent_t(const CUtensorMap& tmA, const CUtensorMap
   using PL = PLayout<MT, BN>;
   args.tiles_n = (args.N + BN - 1) / BN;
   const int tiles = args.tiles_m * args.tiles_n;
-  if (tiles == 0) return cudaSuccess;
+  // side work rides on the data-parallel launch of a narrow-tile kernel; otherwise (or when
+  // this launch has no data-parallel part) it runs as stand-alone launches after the leaves
+  static const bool attach = [] {  // env MK_SIDE_ATTACH=0: side tasks always as their own launches
+    const char* e = getenv("MK_SIDE_ATTACH");
+    return !(e && e[0] == '0');
+  }();
+  MkSideTask carry[MK_SIDE_MAX];  // the tasks this kernel can carry (kinds 2, 3; see side_work)
+  int ncarry = 0;
+  std::vector<MkSideTask> own;   // the rest: stand-alone launches
+  for (int t = 0; t < args.nside; ++t) {
+    const MkSideTask& tk = args.side[t];
+    const int64_t groups = tk.rows * (tk.cols / (tk.width > 0 ? tk.width : 1)) * tk.njobs;
+    if (attach && BN == 64 && (tk.kind == 2 || tk.kind == 3) && (tk.width == 1 || tk.width == 2) && tk.cols % tk.width == 0 &&
+        groups < ((int64_t)1 << 32))
+      carry[ncarry++] = tk;
+    else
+      own.push_back(tk);
+  }
+  args.nside = 0;
+  for (const MkSideTask& tk : own) {  // independent of the leaves and of the other tasks: any order
+    const cudaError_t e = launch_side_task(tk, stream);
+    if (e != cudaSuccess) return e;
+  }
+  auto side_after = [&](cudaError_t e) {
+    for (int t = 0; e == cudaSuccess && t < ncarry; ++t) e = launch_side_task(carry[t], stream);
+    return e;
+  };
+  if (tiles == 0) return side_after(cudaSuccess);
   if ((int64_t)tiles * nprod > 0x7fffffff) return cudaErrorInvalidValue;
   args.tiles_per_prod = tiles;
   args.nprod = nprod;
@@ -1140,6 +1310,19 @@ static cudaError_t launch_persistent_t(const CUtensorMap& tmA, const CUtensorMap
   auto dp = persistent_product_kernel<MT, BN, false>;
   err = cudaFuncSetAttribute(dp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
+  // the data-parallel launch with the side work it carries (512-thread layout, same smem plan)
+  auto launch_dp_side = [&](int g) {
+    using PW = PLayout<MT, BN, BN == 64>;
+    static_assert(PW::kStageBytes == PL::kStageBytes && PW::kBoxBytes == PL::kBoxBytes, "side layout smem plan");
+    auto dw = persistent_product_kernel<MT, BN, false, BN == 64>;
+    cudaError_t e2 = cudaFuncSetAttribute(dw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e2 != cudaSuccess) return e2;
+    MkGemmArgs dargs = args;
+    dargs.nside = ncarry;
+    for (int t = 0; t < ncarry; ++t) dargs.side[t] = carry[t];
+    dw<<<g, PW::kThreads, smem, stream>>>(tmA, tmB, tmC, dargs, prod);
+    return cudaGetLastError();
+  };
   // only when the last wave is less than 3/4 full: a nearly full last wave loses less than the
   // stream-K launch costs (measured on 1024-tile launches: 6.92 waves)
   if (streamk_enabled() && total > G && rem != 0 && rem * 4 < G * 3 && KT >= 8 &&
@@ -1155,19 +1338,27 @@ static cudaError_t launch_persistent_t(const CUtensorMap& tmA, const CUtensorMap
     args.sk_tile0 = tile0;
     args.sk_partial = sc->partial;
     args.sk_flags = sc->flags;
+    bool side_done = false;
     if (tile0 > 0) {
-      dp<<<G, PL::kThreads, smem, stream>>>(tmA, tmB, tmC, args, prod);
-      err = cudaGetLastError();
+      if (ncarry > 0) {
+        err = launch_dp_side(G);
+        side_done = true;
+      } else {
+        dp<<<G, PL::kThreads, smem, stream>>>(tmA, tmB, tmC, args, prod);
+        err = cudaGetLastError();
+      }
       if (err != cudaSuccess) return err;
     }
     auto sk = persistent_product_kernel<MT, BN, true>;
     err = cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     sk<<<G, PL::kThreads, smem, stream>>>(tmA, tmB, tmC, args, prod);
-    return cudaGetLastError();
+    err = cudaGetLastError();
+    return side_done ? err : side_after(err);
   }
+  if (ncarry > 0) return launch_dp_side(grid);
   dp<<<grid, PL::kThreads, smem, stream>>>(tmA, tmB, tmC, args, prod);
-  return cudaGetLastError();
+  return side_after(cudaGetLastError());
 }
 
 static cudaError_t launch_persistent(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
@@ -1225,10 +1416,13 @@ cudaError_t launch_fused_product(const CUtensorMap& tmA, const CUtensorMap& tmB,
 
 cudaError_t launch_product_batch(const MkBatchEntry* entries_dev, int nprod, const MkGemmArgs& args_in,
                                  cudaStream_t stream) {
-  if (nprod <= 0) return cudaSuccess;
   MkGemmArgs args = args_in;
   const int tiles = args.tiles_m * args.tiles_n;
-  if (tiles == 0) return cudaSuccess;
+  if (nprod <= 0 || tiles == 0) {  // no leaves: only the side work
+    cudaError_t err = cudaSuccess;
+    for (int t = 0; err == cudaSuccess && t < args.nside; ++t) err = launch_side_task(args.side[t], stream);
+    return err;
+  }
   if ((int64_t)tiles * nprod > 0x7fffffff) return cudaErrorInvalidValue;
   args.stages = (int)(MK_SMEM_BUDGET / kOpStageBytes);
   if (args.stages > kMaxStages) args.stages = kMaxStages;
@@ -1254,8 +1448,12 @@ cudaError_t launch_product_batch(const MkBatchEntry* entries_dev, int nprod, con
   CUtensorMap z{};
   MkProduct zp{};
   zp.na = zp.nb = 1;
-  fn<<<(unsigned)(tiles * nprod), threads, smem, stream>>>(z, z, z, args, zp);
-  return cudaGetLastError();
+  MkGemmArgs largs = args;
+  largs.nside = 0;
+  fn<<<(unsigned)(tiles * nprod), threads, smem, stream>>>(z, z, z, largs, zp);
+  err = cudaGetLastError();
+  for (int t = 0; err == cudaSuccess && t < args.nside; ++t) err = launch_side_task(args.side[t], stream);
+  return err;
 }
 
 }  // namespace mk

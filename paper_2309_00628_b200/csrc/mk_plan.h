@@ -43,6 +43,23 @@ struct MkProduct {
 
 struct MkBatchEntry;
 
+// HBM-bound side work for the persistent leaf kernel: its producer warpgroup has one TMA thread,
+// so warps 1-3 (96 threads per CTA) stream block transforms that are independent of the launch's
+// leaves -- the next breadth-first pass's operand sums and the previous pass's post-additions --
+// while the DMMA warps run (the FP64 tensor pipe leaves HBM ~80% idle). Same element code as the
+// stand-alone kernels (mk_xform.cuh): results are bit-identical whichever kernel runs a task.
+#define MK_SIDE_MAX 8
+struct MkSideTask {
+  const void* jobs;  // device array of njobs jobs: MkXformJob / MkXform2Job / MkXpost2Job
+  int64_t rows, cols;
+  int32_t njobs;
+  int8_t kind;       // 1 one-level transform, 2 two-level operand transform, 3 two-level post-addition
+  int8_t table;      // kinds 2, 3: 0 Strassen, 1 Winograd block, 2 Winograd Knuth, 3 Knuth 8-call
+  int8_t side;       // kind 2: 0 A, 1 B
+  int8_t width;      // doubles per access: 1, 2 (or 4 for kind 1)
+  int64_t bytes;     // HBM bytes the task moves (host-side estimate for balancing; unused on the device)
+};
+
 struct MkGemmArgs {
   double* C;
   int64_t ldc;
@@ -71,4 +88,8 @@ struct MkGemmArgs {
   int32_t sk_tile0, pad_sk;
   double* sk_partial;
   int32_t* sk_flags;
+  // side work (persistent kernel, data-parallel launches): tasks run in order by every CTA's
+  // warps 1-3; the tasks of one launch must be independent of each other and of its leaves
+  int32_t nside, pad_side;
+  MkSideTask side[MK_SIDE_MAX];
 };

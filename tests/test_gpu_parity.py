@@ -551,11 +551,15 @@ def test_memory_lean_plans_exact(plan, tail, group):
     want = a @ b
     pol = pk.BasePolicy.naive_cutoff(32)  # 4 levels
     base = {}
-    for algo in ("strassen", "winograd-block", "two-temp"):
-        c = pk.Matrix.zeros(n, n)
-        ctr = CALL[algo](pk.Matrix(a), pk.Matrix(b), c, pol)
-        base[algo] = (ctr.snapshot(), pk.last_stats().workspace_bytes)
     try:
+        # the reference point: breadth-first in passes of 4 (the auto plan of wide-tile leaves; these
+        # 32-column leaves would otherwise take the pipelined plan, tests/test_gpu_pipeline.py)
+        pk.set_plan("breadth-first", group=4)
+        for algo in ("strassen", "winograd-block", "two-temp"):
+            c = pk.Matrix.zeros(n, n)
+            ctr = CALL[algo](pk.Matrix(a), pk.Matrix(b), c, pol)
+            base[algo] = (ctr.snapshot(), pk.last_stats().workspace_bytes)
+
         pk.set_plan(plan, two_temp_tail=tail, group=group)
         for algo in ("strassen", "winograd-block", "two-temp"):
             c = pk.Matrix.zeros(n, n)
