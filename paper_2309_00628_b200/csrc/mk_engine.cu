@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <atomic>
@@ -2685,6 +2686,8 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
   if (ldd < n || ldd % 2 || lda < n || ldb < n || ldc < n)
     return fail(MK_ERR_DIMENSION, "leading dimension smaller than the order (device ld must be even)");
   cudaStream_t st = static_cast<cudaStream_t>(stream), cp = static_cast<cudaStream_t>(copy_stream);
+  const auto h0 = std::chrono::steady_clock::now();
+  auto host_ms = [&]() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count(); };
   const std::vector<int> order0 = cached_order(algo, nullptr);
   const bool sub = levels == 2 && (n / 2) % 2 == 0;
   const std::vector<int> kids0 = sub ? cached_head_children(algo, order0[0]) : std::vector<int>();
@@ -2721,6 +2724,7 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
     if (!tbl_host.empty())
       MK_CUDA_TRY(cudaMemcpyAsync(tbl_dev, tbl_host.data(), tbl_host.size(), cudaMemcpyHostToDevice, st));
   }
+  const double h_tables = host_ms();
   Engine e;
   MK_TRY(setup_square(e, algo, dA, ldd, dB, ldd, dC, ldd, n, levels));
   e.st = st;
@@ -2818,11 +2822,15 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
     }
   }
   host_trace("downloads done", cp);
+  const double h_enqueued = host_ms();
   const cudaError_t fe = stg.finish();  // both staging streams (no-op when nothing was staged)
   cudaError_t se = cudaStreamSynchronize(cp);
   if (se == cudaSuccess) se = fe;
   if (rc == MK_OK && se == cudaSuccess) se = cudaStreamSynchronize(st);
   if (rc == MK_OK && se != cudaSuccess) rc = fail(MK_ERR_CUDA, std::string("sync: ") + cudaGetErrorString(se));
+  if (host_trace_on())
+    fprintf(stderr, "[host-time] plan tables %.2f ms, enqueue done %.2f ms, synchronised %.2f ms (host clock from entry)\n",
+            h_tables, h_enqueued, host_ms());
   if (host_trace_on() && !g_host_trace.empty()) {
     std::vector<unsigned long long> t(g_host_trace.size());
     cudaMemcpy(t.data(), g_trace_dev, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);

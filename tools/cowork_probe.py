@@ -4,7 +4,7 @@ producer warps, and the job alone through mk_block_combine -- DMMA slowdown vs s
 import ctypes, json, os, sys
 import torch
 HERE = os.path.dirname(os.path.abspath(__file__))
-lib = ctypes.CDLL(os.path.join(HERE, "..", "paper_2309_00628_b200", "libmk_strassen.so"))
+lib = ctypes.CDLL(os.environ.get("MK_LIB") or os.path.join(HERE, "..", "paper_2309_00628_b200", "libmk_strassen.so"))
 I64, VP = ctypes.c_int64, ctypes.c_void_p
 st = lambda: VP(torch.cuda.current_stream().cuda_stream)  # noqa: E731
 M, N, K = 148 * 128, 320, 14016
