@@ -16,6 +16,8 @@ ALGOS = {
     "strassen": pk.strassen_mul,
     "winograd-block": pk.winograd_block_mul,
     "winograd-knuth": pk.winograd_knuth_mul,
+    # eight top-level products (the first recomputed): eight passes, prologue and epilogue over 8
+    "winograd-knuth-8call": lambda a, b, c, pol: pk.winograd_knuth_mul(a, b, c, pol, recompute_first_product=True),
 }
 
 
@@ -24,7 +26,7 @@ def _grouped():
 
 
 @pytest.mark.parametrize("algo", sorted(ALGOS))
-@pytest.mark.parametrize("n,cut", [(512, 64), (1024, 64), (256, 32)])
+@pytest.mark.parametrize("n,cut", [(512, 64), (1024, 64), (256, 32), (128, 32)])
 def test_square_pipelined_matches_grouped_bitwise(algo, n, cut):
     """Square products with 64- and 32-column leaves (narrow tiles): integer data, pipelined
     (default) == grouped plan == exact product, bit for bit."""
@@ -77,3 +79,24 @@ def test_pipelined_workspace_below_grouped_at_cfg5_shape():
     finally:
         pk.set_plan()
     assert 0 < ws_pipe < ws_grp, (ws_pipe, ws_grp)
+
+
+@pytest.mark.parametrize("algo", sorted(ALGOS))
+def test_pipelined_real_data_agrees_with_grouped(algo):
+    """Real data: the pipelined plan (different pass structure, C formed by one epilogue) agrees
+    with the grouped plan within the stated tolerance."""
+    n, cut = 1024, 64
+    r = np.random.default_rng(5)
+    a = r.uniform(-1, 1, (n, n))
+    b = r.uniform(-1, 1, (n, n))
+    pol = pk.BasePolicy.naive_cutoff(cut)
+    c1 = pk.Matrix.zeros(n, n)
+    ALGOS[algo](pk.Matrix(a), pk.Matrix(b), c1, pol)
+    try:
+        _grouped()
+        c2 = pk.Matrix.zeros(n, n)
+        ALGOS[algo](pk.Matrix(a), pk.Matrix(b), c2, pol)
+    finally:
+        pk.set_plan()
+    assert float(np.abs(c1.arr - c2.arr).max()) <= o.tolerance(n, 1.0, 1.0)
+    assert float(np.abs(c1.arr - a @ b).max()) <= o.tolerance(n, 1.0, 1.0)
