@@ -263,6 +263,45 @@ cudaError_t launch_xform2_batch(const MkXform2Job* jobs_dev, int njobs, int tabl
   return cudaGetLastError();
 }
 
+// Padded copy: dst (rows_d x cols_d) = src (rows_s x cols_s) with zeros to the right and below
+// -- one pass over dst instead of a memset followed by a copy (rectangular driver, hybrid.py:130-146).
+template <bool VEC>
+__global__ void pad_copy_kernel(double* __restrict__ dst, int64_t ldd, int64_t rows_d, int64_t cols_d,
+                                const double* __restrict__ src, int64_t lds, int64_t rows_s, int64_t cols_s) {
+  const int64_t cv = VEC ? cols_d / 2 : cols_d;
+  const int64_t total = rows_d * cv;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / cv;
+    const int64_t c = (idx - r * cv) * (VEC ? 2 : 1);
+    if (VEC) {
+      double2 v = make_double2(0.0, 0.0);
+      if (r < rows_s) {
+        if (c + 1 < cols_s)
+          v = __ldg(reinterpret_cast<const double2*>(src + r * lds + c));
+        else if (c < cols_s)
+          v.x = __ldg(src + r * lds + c);
+      }
+      *reinterpret_cast<double2*>(dst + r * ldd + c) = v;
+    } else {
+      dst[r * ldd + c] = (r < rows_s && c < cols_s) ? __ldg(src + r * lds + c) : 0.0;
+    }
+  }
+}
+
+cudaError_t launch_pad_copy(double* dst, int64_t ldd, int64_t rows_d, int64_t cols_d, const double* src, int64_t lds,
+                            int64_t rows_s, int64_t cols_s, cudaStream_t stream) {
+  if (rows_d <= 0 || cols_d <= 0) return cudaSuccess;
+  const bool vec = cols_d % 2 == 0 && ldd % 2 == 0 && lds % 2 == 0 && (uintptr_t)dst % 16 == 0 &&
+                   (uintptr_t)src % 16 == 0;
+  if (vec)
+    pad_copy_kernel<true><<<grid_for(rows_d * (cols_d / 2), 256), 256, 0, stream>>>(dst, ldd, rows_d, cols_d, src, lds,
+                                                                                   rows_s, cols_s);
+  else
+    pad_copy_kernel<false><<<grid_for(rows_d * cols_d, 256), 256, 0, stream>>>(dst, ldd, rows_d, cols_d, src, lds,
+                                                                              rows_s, cols_s);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_side_task(const MkSideTask& t, cudaStream_t stream) {
   switch (t.kind) {
     case 1: return launch_xform_batch(static_cast<const MkXformJob*>(t.jobs), t.njobs, t.rows, t.cols, t.width, stream);

@@ -76,6 +76,9 @@ int xform2_table_coef(int table, int side, int p, int q);
 cudaError_t launch_xpost2_batch(const MkXpost2Job* jobs_dev, int njobs, int table, int64_t rows, int64_t cols,
                                 int width, cudaStream_t stream);
 int xpost2_table_coef(int table, int q, int p);
+// dst (rows_d x cols_d) = src (rows_s x cols_s) zero-padded to the right and below, one pass.
+cudaError_t launch_pad_copy(double* dst, int64_t ldd, int64_t rows_d, int64_t cols_d, const double* src, int64_t lds,
+                            int64_t rows_s, int64_t cols_s, cudaStream_t stream);
 // One side-work task (mk_plan.h) as a stand-alone launch (a leaf launch that cannot carry it).
 cudaError_t launch_side_task(const MkSideTask& task, cudaStream_t stream);
 cudaError_t launch_fused_product(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,

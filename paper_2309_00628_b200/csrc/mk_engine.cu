@@ -517,6 +517,9 @@ struct Engine {
   int64_t panels = 1;
   int launches = 0;
   bool fuse_preadds = false;  // K2 in-kernel combiner for the last level's operand sums
+  // rectangular driver, pipelined plan: BASE_C is the caller's unpadded C (only the epilogue writes
+  // it), clipped to clip_m x clip_n; 0 = BASE_C spans the padded extents
+  int64_t clip_m = 0, clip_n = 0;
   // fused multi-GPU reduce-scatter (mk_strassen_partial_slabs): C rows routed to owner slabs
   int nslab = 0;
   int64_t slab_rows = 0;
@@ -1986,12 +1989,18 @@ static bool pipeline_enabled() {
   }
   return v == 1;
 }
-static bool use_pipeline(const Engine& e) {
+// The pipelined plan for a breadth-first call with these leaves (before any engine exists: the
+// rectangular driver decides from it whether C needs a padded staging copy).
+static bool pipeline_for(int L, int64_t lm, int64_t ln, int64_t lk) {
   // an explicit pass grouping (set_plan group=, MK_BFS_GROUP) asks for the grouped plan
-  if (!pipeline_enabled() || bfs_group_option() > 0 || e.L < 2 || e.tbl_mode != 0 || e.no_launch || e.leaf_count >= 0 || e.fuse_preadds) return false;
-  if (!persistent_enabled() || ozaki_leaf_for(e.leaf_m, e.leaf_n, e.leaf_k)) return false;
+  if (!pipeline_enabled() || bfs_group_option() > 0 || L < 2) return false;
+  if (!persistent_enabled() || ozaki_leaf_for(lm, ln, lk)) return false;
   // the leaf launches must be narrow-tile ones (the layout that carries side work)
-  return persistent_tile_n((e.leaf_m + MK_BM - 1) / MK_BM, e.leaf_n, 1 << 12) == 64;
+  return persistent_tile_n((lm + MK_BM - 1) / MK_BM, ln, 1 << 12) == 64;
+}
+static bool use_pipeline(const Engine& e) {
+  if (e.tbl_mode != 0 || e.no_launch || e.leaf_count >= 0 || e.fuse_preadds) return false;
+  return pipeline_for(e.L, e.leaf_m, e.leaf_n, e.leaf_k);
 }
 
 // Side work onto a pass's leaf launches, balanced by bytes: launch k takes cap[k] bytes (its leaf
@@ -2122,7 +2131,7 @@ static int run_bfs_pipelined(Engine& e, int64_t M, int64_t N, int64_t K) {
     MK_TRY(probe.alloc_slot((int64_t)np * hm, hn, &slots, true));
     for (int p = 0; p < np; ++p) pr.lv[1][p].o = Blk{slots, (int64_t)p * hm, 0, 1.0};
     void* dummy = nullptr;
-    MK_TRY(probe.upload(nullptr, sizeof(MkXformJob), &dummy));  // the epilogue's job
+    for (int q = 0; q < 4; ++q) MK_TRY(probe.upload(nullptr, sizeof(MkXformJob), &dummy));  // the epilogue's jobs
     persist = probe.ws_used;
     for (int p = 0; p < np; ++p) {
       Engine::BfsPass q = pass_of(pr, p);
@@ -2148,20 +2157,31 @@ static int run_bfs_pipelined(Engine& e, int64_t M, int64_t N, int64_t K) {
   int slots = -1;
   MK_TRY(e.alloc_slot((int64_t)np * hm, hn, &slots, true));
   for (int p = 0; p < np; ++p) pro.lv[1][p].o = Blk{slots, (int64_t)p * hm, 0, 1.0};
-  MkXformJob ep{};  // the epilogue: C's quadrants from the depth-1 outputs (reference post-additions)
-  ep.nsrc = np;
-  for (int p = 0; p < np; ++p) {
-    ep.src[p] = e.ptr_of(pro.lv[1][p].o);
-    ep.lds[p] = e.bases[slots].ld;
-  }
-  ep.ndst = 4;
+  // the epilogue: C's quadrants from the depth-1 outputs (reference post-additions), one job per
+  // quadrant clipped to C's true extents when C is the caller's unpadded matrix (clip_m > 0)
+  struct EpJob {
+    void* dev = nullptr;
+    int64_t rows = 0, cols = 0;
+    int width = 1;
+  } epj[4];
   for (int q = 0; q < 4; ++q) {
-    ep.dst[q] = e.ptr_of(Blk{C.base, C.row + (q >> 1) * hm, C.col + (q & 1) * hn, 1.0});
-    ep.ldd[q] = e.bases[C.base].ld;
-    for (int p = 0; p < np; ++p) ep.coef[q][p] = (int8_t)e.co->c[q][p];
+    MkXformJob ep{};
+    ep.nsrc = np;
+    for (int p = 0; p < np; ++p) {
+      ep.src[p] = e.ptr_of(pro.lv[1][p].o);
+      ep.lds[p] = e.bases[slots].ld;
+    }
+    ep.ndst = 1;
+    ep.dst[0] = e.ptr_of(Blk{C.base, C.row + (q >> 1) * hm, C.col + (q & 1) * hn, 1.0});
+    ep.ldd[0] = e.bases[C.base].ld;
+    for (int p = 0; p < np; ++p) ep.coef[0][p] = (int8_t)e.co->c[q][p];
+    epj[q].rows = e.clip_m > 0 ? std::min(hm, e.clip_m - (q >> 1) * hm) : hm;
+    epj[q].cols = e.clip_n > 0 ? std::min(hn, e.clip_n - (q & 1) * hn) : hn;
+    bool w2 = epj[q].cols % 2 == 0 && ep.ldd[0] % 2 == 0 && reinterpret_cast<uintptr_t>(ep.dst[0]) % 16 == 0;
+    for (int p = 0; p < np; ++p) w2 = w2 && ep.lds[p] % 2 == 0 && reinterpret_cast<uintptr_t>(ep.src[p]) % 16 == 0;
+    epj[q].width = w2 ? 2 : 1;
+    MK_TRY(e.upload(&ep, sizeof(MkXformJob), &epj[q].dev));
   }
-  void* ep_dev = nullptr;
-  MK_TRY(e.upload(&ep, sizeof(MkXformJob), &ep_dev));
   const size_t persist_end = base + persist;
   if (e.ws_used != persist_end) return fail(MK_ERR_ARG, "internal: pipelined plan sizing differs from the run");
   // ---- passes ----
@@ -2214,14 +2234,10 @@ static int run_bfs_pipelined(Engine& e, int64_t M, int64_t N, int64_t K) {
   for (const auto& ph : post_prev)  // the last pass's post-additions: launches of their own
     for (const MkSideTask& tk : ph) MK_CUDA_TRY(launch_side_task(tk, e.st));
   // ---- epilogue ----
-  {
-    std::vector<MkXformJob> one{ep};
-    int width = 2;  // as xform_batch would choose
-    bool ok = hn % 2 == 0;
-    for (int p = 0; p < np; ++p) ok = ok && ep.lds[p] % 2 == 0 && reinterpret_cast<uintptr_t>(ep.src[p]) % 16 == 0;
-    for (int q = 0; q < 4; ++q) ok = ok && ep.ldd[q] % 2 == 0 && reinterpret_cast<uintptr_t>(ep.dst[q]) % 16 == 0;
-    if (!ok) width = 1;
-    MK_CUDA_TRY(launch_xform_batch(static_cast<const MkXformJob*>(ep_dev), 1, hm, hn, width, e.st));
+  for (int q = 0; q < 4; ++q) {
+    if (epj[q].rows <= 0 || epj[q].cols <= 0) continue;
+    MK_CUDA_TRY(launch_xform_batch(static_cast<const MkXformJob*>(epj[q].dev), 1, epj[q].rows, epj[q].cols, epj[q].width,
+                                   e.st));
     ++g_launch_count;
   }
   e.ws_used = base;
@@ -3115,21 +3131,18 @@ static int run_rect(int algo, const double* A, int64_t lda, const double* B, int
   const bool conform = mp == m && np_ == n && kp == k && !shard;  // shards always accumulate in a padded C
   const bool direct = conform && (dry || (tma_ok(A, lda) && tma_ok(B, ldb) && tma_ok(C, ldc)));
   if (conform && !direct) return fail(MK_ERR_ARG, "operands need 16-byte alignment and even leading dimensions");
+  // The pipelined plan writes C only in its epilogue, whose stores are clipped to C's extents: it
+  // takes the caller's C directly (no padded staging copy and no final copy-out).
+  const bool pipe_c = !direct && !shard && plan_kind() == 0 && !fuse_preadds_default() && levels >= 2 &&
+                      pipeline_for(levels, mp >> levels, np_ >> levels, kp >> levels);
   double* Ap = direct ? const_cast<double*>(A) : carve((size_t)mp * kp);
   double* Bp = direct ? const_cast<double*>(B) : carve((size_t)kp * np_);
-  double* Cp = direct ? C : carve((size_t)mp * np_);
-  const int64_t ldap = direct ? lda : kp, ldbp = direct ? ldb : np_, ldcp = direct ? ldc : np_;
+  double* Cp = (direct || pipe_c) ? C : carve((size_t)mp * np_);
+  const int64_t ldap = direct ? lda : kp, ldbp = direct ? ldb : np_, ldcp = (direct || pipe_c) ? ldc : np_;
   if (!dry && !direct) {
     if (off > ws_bytes) return fail(MK_ERR_WORKSPACE, "workspace too small for padded operands");
-    MK_CUDA_TRY(cudaMemsetAsync(Ap, 0, (size_t)mp * kp * 8, st));
-    MK_CUDA_TRY(cudaMemsetAsync(Bp, 0, (size_t)kp * np_ * 8, st));
-    const double* s[1] = {A};
-    int64_t l[1] = {lda};
-    double sg[1] = {1.0};
-    MK_CUDA_TRY(launch_combine(Ap, kp, s, l, sg, 1, m, k, st));
-    s[0] = B;
-    l[0] = ldb;
-    MK_CUDA_TRY(launch_combine(Bp, np_, s, l, sg, 1, k, n, st));
+    MK_CUDA_TRY(launch_pad_copy(Ap, kp, mp, kp, A, lda, m, k, st));  // zero margins in the same pass
+    MK_CUDA_TRY(launch_pad_copy(Bp, np_, kp, np_, B, ldb, k, n, st));
     if (shard) MK_CUDA_TRY(cudaMemsetAsync(Cp, 0, (size_t)mp * np_ * 8, st));
   }
   Engine e;
@@ -3153,6 +3166,10 @@ static int run_rect(int algo, const double* A, int64_t lda, const double* B, int
     e.panels = panels;
     e.set_state(BASE_C, 0, 0, mp, np_, 1);  // accumulate into the zeroed padded C
   }
+  if (pipe_c) {
+    e.clip_m = m;
+    e.clip_n = n;
+  }
   if (!shard && plan_kind() == 2 && levels >= 2 && !e.fuse_preadds && algo >= MK_ALGO_STRASSEN &&
       algo <= MK_ALGO_WINOGRAD_KNUTH_8CALL) {  // hybrid (see run_square)
     const Lin A0{Blk{BASE_A, 0, 0, 1.0}}, B0{Blk{BASE_B, 0, 0, 1.0}}, C0{Blk{BASE_C, 0, 0, 1.0}};
@@ -3162,8 +3179,10 @@ static int run_rect(int algo, const double* A, int64_t lda, const double* B, int
   else
     MK_TRY(e.fused(levels, Lin{Blk{BASE_A, 0, 0, 1.0}}, Lin{Blk{BASE_B, 0, 0, 1.0}}, Lin{Blk{BASE_C, 0, 0, 1.0}},
                    mp, np_, kp, 0));
+  if (pipe_c && !(use_bfs(e, e.leaf_m, e.leaf_n) && use_pipeline(e)))
+    return fail(MK_ERR_ARG, "internal: unpadded C handed to a plan other than the pipelined one");
   if (need_out) *need_out = off + e.ws_peak;
-  if (!dry && !direct) {
+  if (!dry && !direct && !pipe_c) {
     const double* s[1] = {Cp};
     int64_t l[1] = {np_};
     double sg[1] = {1.0};
