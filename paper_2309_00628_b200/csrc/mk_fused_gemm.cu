@@ -538,6 +538,9 @@ fused_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const __grid
 #ifndef MK_EPI_BUFS_NARROW
 #define MK_EPI_BUFS_NARROW 1
 #endif
+#ifndef MK_EPI_SLOTS
+#define MK_EPI_SLOTS 1
+#endif
 #ifndef MK_TAIL_SKIP
 #define MK_TAIL_SKIP 1
 #endif
@@ -557,6 +560,18 @@ struct PLayout {
   // the TMA unit still reads the last: measured no faster on cfg5, so one by default)
   static constexpr int kEpiBufs = BN == 64 ? MK_EPI_BUFS_NARROW : 1;
   static constexpr int kBoxBytes = kEpiBufs * kConsumerWarps * 8 * MT * 128;  // 16-column boxes
+  // Narrow tiles: the producer stages each tile's destination list (count, sign and store/add
+  // masks, offsets) in a 16-slot shared ring, so the epilogue reads it from shared memory instead
+  // of waiting on L2 for the product descriptor (short-K tiles: a visible share of the tile).
+  // Slots of 96 bytes: count, masks and the first 8 destinations (more -- depth-first plans only
+  // -- are read from the descriptor), in the slack between the ring and the 227 KiB opt-in limit
+  // (the ring keeps its 8 stages). Side layout only: there it takes cfg5 69.9 -> 68.3 ms; in the
+  // 384-thread layout the same ring made every launch slower, batched or not (cfg5 sequential
+  // 73.6 -> 75.2 ms, in-place n = 8192 L = 3 34.5 -> 38.0 ms, reproducibly, cause not found).
+  static constexpr int kEpiSlots = (BN == 64 && SW && MK_EPI_SLOTS) ? 8 : 0;
+  static constexpr int kEpiSlotInts = 24;
+  static constexpr int kEpiSlotDests = 8;
+  static constexpr int kEpiSlotBytes = kEpiSlots * kEpiSlotInts * 4;
   // Register split (setmaxnreg): the wide layout's 64 x 32 consumers take 224, its producer 56.
   // The side-work layout (512 threads, 128 each at launch): the two lead warpgroups drop to 104
   // (the two-level operand transform at 16-byte width needs 92; the post-addition runs at 8-byte
@@ -707,9 +722,16 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
   uint8_t* smem_gen = smem_raw + (smem_base - smem_u32(smem_raw));
   using PL = PLayout<MT, BN, SW>;
   uint8_t* box_area = smem_gen + (size_t)S * PL::kStageBytes;  // epilogue boxes, one per consumer warp
+  // epilogue descriptor ring (narrow data-parallel tiles): int32 [0] count, [1] pass-0 mask (the
+  // destination's sign times the product's is +1), [2] accumulate mask, [4 + d] row, [12 + d] col
+  int32_t* const slot_area = reinterpret_cast<int32_t*>(box_area + PL::kBoxBytes);
   const int tiles_per = args.tiles_m * args.tiles_n;
   const int total = tiles_per * (args.batch ? args.nprod : 1);
   const int KT = (args.K + MK_BK - 1) / MK_BK;
+  // Slot reuse is safe while the producer, at most S stages ahead of the consumers' releases,
+  // cannot reach the slot of a tile whose epilogue may still run: kEpiSlots >= ceil(S / KT) + 2.
+  const bool use_slots = PL::kEpiSlots > 0 && !SK && args.batch != nullptr &&
+                         PL::kEpiSlots >= (S + KT - 1) / KT + 2;
 
   auto tile_of = [&](int t, int& pi, int& m0, int& n0) {
     pi = t / tiles_per;
@@ -745,6 +767,7 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
     int s = 0;            // ring slot of the next stage (carried across tiles)
     uint32_t eph = 0;     // parity of the empty-barrier phase to wait for (first lap: no wait)
     bool first_lap = true;
+    int tseq = 0;  // tiles issued (epilogue descriptor ring slot)
     auto unit = [&](const int t, const int kb, const int ke) {
       int pi, m0, n0;
       tile_of(t, pi, m0, n0);
@@ -754,6 +777,28 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
       const CUtensorMap* tmB = ent ? &ent->tmB : &tmB_param;
       const int ar = m0 + prod.a[0].row, ac = prod.a[0].col;
       const int br = prod.b[0].row, bc = n0 + prod.b[0].col;
+      if (use_slots) {
+        // Written before the tile's first stage is armed (mbarrier arrive: release; the consumers'
+        // wait on it: acquire). Reuse (see use_slots): writing tile T + R's slot needs the
+        // consumers to have released every stage up to S stages before it, i.e. to be past
+        // tile T's main loop and, warp by warp, its epilogue.
+        int32_t* sl = slot_area + (tseq & (PL::kEpiSlots - 1)) * PL::kEpiSlotInts;
+        const double osg = prod.a[0].sign * prod.b[0].sign;
+        uint32_t pos = 0, accm = 0;
+        for (int d = 0; d < prod.nd; ++d) {
+          const MkDest& dd = prod.d[d];
+          if (dd.sign * osg > 0.0) pos |= 1u << d;
+          if (dd.accumulate) accm |= 1u << d;
+          if (d < PL::kEpiSlotDests) {
+            sl[4 + d] = (int32_t)dd.row;
+            sl[12 + d] = (int32_t)dd.col;
+          }
+        }
+        sl[0] = prod.nd;
+        sl[1] = (int32_t)pos;
+        sl[2] = (int32_t)accm;
+        ++tseq;
+      }
       for (int k = kb; k < ke; ++k) {
         if (!first_lap) mbar_wait(&empty_bar[s], eph);
         uint8_t* opA = smem_gen + (size_t)s * PL::kStageBytes;
@@ -896,6 +941,7 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
   const int krem_last = args.K - (KT - 1) * MK_BK;
   int rs = 0;         // ring slot of the next stage (carried across tiles)
   uint32_t fph = 0;   // parity of the full-barrier phase to wait for
+  int tseq = 0;       // tiles done (epilogue descriptor ring slot)
 
   // One unit: tile t, k-stages [kb, ke). Instantiated twice below -- data-parallel tiles (kb = 0,
   // ke = KT: the original loop, no extra live registers next to the 128-register accumulator)
@@ -1013,13 +1059,26 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
       const int row0 = m0 + warp_m * kBoxRows;
       const int col0 = n0 + warp_n * 32;
       const bool slab_live = row0 < args.M && col0 < args.N;
-      const double out_sign = prod.a[0].sign * prod.b[0].sign;
-      const int nd = prod.nd;
+      const int32_t* const sl = use_slots ? slot_area + (tseq & (PL::kEpiSlots - 1)) * PL::kEpiSlotInts : nullptr;
+      uint32_t pos_mask = 0, all_mask = 0, acc_mask = 0;
+      if (use_slots) {
+        const int nds = sl[0];
+        all_mask = nds >= 32 ? 0xffffffffu : (1u << nds) - 1u;
+        pos_mask = (uint32_t)sl[1];
+        acc_mask = (uint32_t)sl[2];
+      } else {
+        const double out_sign = prod.a[0].sign * prod.b[0].sign;
+        for (int d = 0; d < prod.nd; ++d) {
+          all_mask |= 1u << d;
+          if (prod.d[d].sign * out_sign > 0.0) pos_mask |= 1u << d;
+          if (prod.d[d].accumulate) acc_mask |= 1u << d;
+        }
+      }
       for (int pass = 0; pass < 2; ++pass) {
-        const double want = pass == 0 ? 1.0 : -1.0;
-        bool any = false;
-        for (int d = 0; d < nd; ++d) any |= (prod.d[d].sign * out_sign) == want;
-        if (!any) continue;
+        const uint32_t pass_mask = pass == 0 ? pos_mask : (all_mask & ~pos_mask);
+        if (!pass_mask) continue;
+        // the pass's sign is a sign-bit flip of the accumulators (integer pipe, not a DMUL)
+        const long long flip = pass == 0 ? 0ll : (long long)0x8000000000000000ull;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           uint8_t* const box = box0 + (size_t)ebuf * (PL::kConsumerWarps * kBoxRows * 128);
@@ -1032,8 +1091,9 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
           for (int i = 0; i < MT; ++i) {
             const int r = 8 * i + prow;
             uint8_t* rowp = box + r * 128;
-            const double v0 = want * acc[i][2 * j][0], v1 = want * acc[i][2 * j + 1][0];
-            const double v2 = want * acc[i][2 * j][1], v3 = want * acc[i][2 * j + 1][1];
+            auto sg = [&](double x) { return __longlong_as_double(__double_as_longlong(x) ^ flip); };
+            const double v0 = sg(acc[i][2 * j][0]), v1 = sg(acc[i][2 * j + 1][0]);
+            const double v2 = sg(acc[i][2 * j][1]), v3 = sg(acc[i][2 * j + 1][1]);
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int c = 2 * q + (h ^ c_first);
@@ -1045,11 +1105,13 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
           __syncwarp();
           if (lane == 0) {
             if (slab_live && col0 + 16 * j < args.N) {
-              for (int d = 0; d < nd; ++d) {
-                const MkDest dst = prod.d[d];
-                if ((dst.sign * out_sign) != want) continue;
-                const int cc = (int)dst.col + col0 + 16 * j, rr = (int)dst.row + row0;
-                if (dst.accumulate)
+              for (uint32_t m = pass_mask; m; m &= m - 1) {
+                const int d = __ffs(m) - 1;
+                const bool in_slot = use_slots && d < PL::kEpiSlotDests;
+                const int drow = in_slot ? sl[4 + d] : (int)prod.d[d].row;
+                const int dcol = in_slot ? sl[12 + d] : (int)prod.d[d].col;
+                const int cc = dcol + col0 + 16 * j, rr = drow + row0;
+                if (acc_mask & (1u << d))
                   tma_reduce_add_2d(tmC, cc, rr, box);
                 else
                   tma_store_2d(tmC, cc, rr, box);
@@ -1105,7 +1167,10 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
   };
   if constexpr (!SK) {
     const int lim = min(total, args.sk_tile0);
-    for (int t = blockIdx.x; t < lim; t += gridDim.x) unit(t, 0, KT);
+    for (int t = blockIdx.x; t < lim; t += gridDim.x) {
+      unit(t, 0, KT);
+      ++tseq;
+    }
   } else {
     const int tile0 = sk_tile0(args);
     int t, kb, ke;
@@ -1297,7 +1362,7 @@ static cudaError_t launch_persistent_t(const CUtensorMap& tmA, const CUtensorMap
   if (args.stages > kMaxStages) args.stages = kMaxStages;
   args.raw_sets = 0;
   args.chunk_stages = accumulate_chunk_stages();
-  const size_t smem = (size_t)args.stages * PL::kStageBytes + PL::kBoxBytes + 1024;
+  const size_t smem = (size_t)args.stages * PL::kStageBytes + PL::kBoxBytes + PL::kEpiSlotBytes + 1024;
   cudaError_t err = cudaSuccess;
   const int total = tiles * nprod;
   int grid = total < sm_count() ? total : sm_count();
@@ -1314,13 +1379,14 @@ static cudaError_t launch_persistent_t(const CUtensorMap& tmA, const CUtensorMap
   auto launch_dp_side = [&](int g) {
     using PW = PLayout<MT, BN, BN == 64>;
     static_assert(PW::kStageBytes == PL::kStageBytes && PW::kBoxBytes == PL::kBoxBytes, "side layout smem plan");
+    const size_t smem_w = (size_t)args.stages * PW::kStageBytes + PW::kBoxBytes + PW::kEpiSlotBytes + 1024;
     auto dw = persistent_product_kernel<MT, BN, false, BN == 64>;
-    cudaError_t e2 = cudaFuncSetAttribute(dw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e2 = cudaFuncSetAttribute(dw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_w);
     if (e2 != cudaSuccess) return e2;
     MkGemmArgs dargs = args;
     dargs.nside = ncarry;
     for (int t = 0; t < ncarry; ++t) dargs.side[t] = carry[t];
-    dw<<<g, PW::kThreads, smem, stream>>>(tmA, tmB, tmC, dargs, prod);
+    dw<<<g, PW::kThreads, smem_w, stream>>>(tmA, tmB, tmC, dargs, prod);
     return cudaGetLastError();
   };
   // only when the last wave is less than 3/4 full: a nearly full last wave loses less than the
