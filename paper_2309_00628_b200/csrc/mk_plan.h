@@ -16,7 +16,9 @@
 #define MK_BK 16
 // CTA = warpgroup 0 (TMA producer / pre-add combiner) + 2 or 4 DMMA consumer warpgroups
 #define MK_TILE_BYTES (MK_BM * MK_BK * 8)  // 16 KiB: one operand term tile per stage
+#ifndef MK_SMEM_BUDGET
 #define MK_SMEM_BUDGET (224 * 1024)
+#endif
 #define MK_MIN_LEAF 32    // smallest leaf order the level policy recurses to
 #define MK_MAX_LEVELS 5   // deepest recursion the level policy plans (7^5 leaves)
 #define MK_MAX_SLABS 8    // output row slabs (ranks) of the fused multi-GPU reduce-scatter
