@@ -17,6 +17,10 @@ struct MkXformJob {
   int64_t ldd[MK_XFORM_MAX];
   int32_t nsrc, ndst;
   int8_t coef[MK_XFORM_MAX][MK_XFORM_MAX];  // [dst][src] in {-1, 0, 1}
+  // destination j written only for rows < clip_rows[j] and columns < clip_cols[j] (0: whole
+  // block; a clipped column count is a multiple of the access width) -- the pipelined plan's
+  // epilogue writing the caller's unpadded C
+  int32_t clip_rows[MK_XFORM_MAX], clip_cols[MK_XFORM_MAX];
 };
 
 // One job of the two-level operand transform: a node's operand block (4 x 4 sub-blocks of

@@ -2131,7 +2131,7 @@ static int run_bfs_pipelined(Engine& e, int64_t M, int64_t N, int64_t K) {
     MK_TRY(probe.alloc_slot((int64_t)np * hm, hn, &slots, true));
     for (int p = 0; p < np; ++p) pr.lv[1][p].o = Blk{slots, (int64_t)p * hm, 0, 1.0};
     void* dummy = nullptr;
-    for (int q = 0; q < 4; ++q) MK_TRY(probe.upload(nullptr, sizeof(MkXformJob), &dummy));  // the epilogue's jobs
+    MK_TRY(probe.upload(nullptr, sizeof(MkXformJob), &dummy));  // the epilogue's job
     persist = probe.ws_used;
     for (int p = 0; p < np; ++p) {
       Engine::BfsPass q = pass_of(pr, p);
@@ -2157,31 +2157,36 @@ static int run_bfs_pipelined(Engine& e, int64_t M, int64_t N, int64_t K) {
   int slots = -1;
   MK_TRY(e.alloc_slot((int64_t)np * hm, hn, &slots, true));
   for (int p = 0; p < np; ++p) pro.lv[1][p].o = Blk{slots, (int64_t)p * hm, 0, 1.0};
-  // the epilogue: C's quadrants from the depth-1 outputs (reference post-additions), one job per
-  // quadrant clipped to C's true extents when C is the caller's unpadded matrix (clip_m > 0)
-  struct EpJob {
-    void* dev = nullptr;
-    int64_t rows = 0, cols = 0;
-    int width = 1;
-  } epj[4];
-  for (int q = 0; q < 4; ++q) {
-    MkXformJob ep{};
-    ep.nsrc = np;
-    for (int p = 0; p < np; ++p) {
-      ep.src[p] = e.ptr_of(pro.lv[1][p].o);
-      ep.lds[p] = e.bases[slots].ld;
-    }
-    ep.ndst = 1;
-    ep.dst[0] = e.ptr_of(Blk{C.base, C.row + (q >> 1) * hm, C.col + (q & 1) * hn, 1.0});
-    ep.ldd[0] = e.bases[C.base].ld;
-    for (int p = 0; p < np; ++p) ep.coef[0][p] = (int8_t)e.co->c[q][p];
-    epj[q].rows = e.clip_m > 0 ? std::min(hm, e.clip_m - (q >> 1) * hm) : hm;
-    epj[q].cols = e.clip_n > 0 ? std::min(hn, e.clip_n - (q & 1) * hn) : hn;
-    bool w2 = epj[q].cols % 2 == 0 && ep.ldd[0] % 2 == 0 && reinterpret_cast<uintptr_t>(ep.dst[0]) % 16 == 0;
-    for (int p = 0; p < np; ++p) w2 = w2 && ep.lds[p] % 2 == 0 && reinterpret_cast<uintptr_t>(ep.src[p]) % 16 == 0;
-    epj[q].width = w2 ? 2 : 1;
-    MK_TRY(e.upload(&ep, sizeof(MkXformJob), &epj[q].dev));
+  // the epilogue: C's quadrants from the depth-1 outputs (reference post-additions): one job, each
+  // output block read once, destinations clipped to C's true extents when C is the caller's
+  // unpadded matrix (clip_m > 0)
+  MkXformJob ep{};
+  ep.nsrc = np;
+  for (int p = 0; p < np; ++p) {
+    ep.src[p] = e.ptr_of(pro.lv[1][p].o);
+    ep.lds[p] = e.bases[slots].ld;
   }
+  int ep_width = 2;
+  bool ep_live = false;
+  for (int q = 0; q < 4; ++q) {
+    const int j = ep.ndst;
+    const int64_t rows = e.clip_m > 0 ? std::min(hm, e.clip_m - (q >> 1) * hm) : hm;
+    const int64_t cols = e.clip_n > 0 ? std::min(hn, e.clip_n - (q & 1) * hn) : hn;
+    if (rows <= 0 || cols <= 0) continue;  // a quadrant wholly in the padding
+    ep.dst[j] = e.ptr_of(Blk{C.base, C.row + (q >> 1) * hm, C.col + (q & 1) * hn, 1.0});
+    ep.ldd[j] = e.bases[C.base].ld;
+    for (int p = 0; p < np; ++p) ep.coef[j][p] = (int8_t)e.co->c[q][p];
+    ep.clip_rows[j] = rows < hm ? (int32_t)rows : 0;
+    ep.clip_cols[j] = cols < hn ? (int32_t)cols : 0;
+    if (cols % 2 || ep.ldd[j] % 2 || reinterpret_cast<uintptr_t>(ep.dst[j]) % 16) ep_width = 1;
+    ep.ndst = j + 1;
+    ep_live = true;
+  }
+  if (hn % 2) ep_width = 1;
+  for (int p = 0; p < np; ++p)
+    if (ep.lds[p] % 2 || reinterpret_cast<uintptr_t>(ep.src[p]) % 16) ep_width = 1;
+  void* ep_dev = nullptr;
+  MK_TRY(e.upload(&ep, sizeof(MkXformJob), &ep_dev));
   const size_t persist_end = base + persist;
   if (e.ws_used != persist_end) return fail(MK_ERR_ARG, "internal: pipelined plan sizing differs from the run");
   // ---- passes ----
@@ -2234,10 +2239,8 @@ static int run_bfs_pipelined(Engine& e, int64_t M, int64_t N, int64_t K) {
   for (const auto& ph : post_prev)  // the last pass's post-additions: launches of their own
     for (const MkSideTask& tk : ph) MK_CUDA_TRY(launch_side_task(tk, e.st));
   // ---- epilogue ----
-  for (int q = 0; q < 4; ++q) {
-    if (epj[q].rows <= 0 || epj[q].cols <= 0) continue;
-    MK_CUDA_TRY(launch_xform_batch(static_cast<const MkXformJob*>(epj[q].dev), 1, epj[q].rows, epj[q].cols, epj[q].width,
-                                   e.st));
+  if (ep_live) {
+    MK_CUDA_TRY(launch_xform_batch(static_cast<const MkXformJob*>(ep_dev), 1, hm, hn, ep_width, e.st));
     ++g_launch_count;
   }
   e.ws_used = base;

@@ -69,7 +69,8 @@ __device__ __forceinline__ void xform_elem(const MkXformJob& jb, uint32_t r, int
           for (int u = 0; u < W; ++u) acc.v[u] -= v[i].v[u];
         }
       }
-      st_vec<W>(jb.dst[j] + r * jb.ldd[j] + c, acc);
+      const int32_t cr = jb.clip_rows[j], cc = jb.clip_cols[j];
+      if ((cr == 0 || (int64_t)r < cr) && (cc == 0 || c < cc)) st_vec<W>(jb.dst[j] + r * jb.ldd[j] + c, acc);
     }
   }
 }
