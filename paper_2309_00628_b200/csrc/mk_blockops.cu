@@ -189,6 +189,54 @@ __global__ void __launch_bounds__(256) xpost2_kernel(const MkXpost2Job* __restri
   }
 }
 
+template <int TAB, int W>
+__global__ void __launch_bounds__(256) xpost1_kernel(const MkXpost2Job* __restrict__ jobs, int64_t rows,
+                                                     int64_t cols) {
+  constexpr int NP = XCTab<TAB>::np;
+  __shared__ const double* src_sh[MK_XFORM2_MAX];
+  const MkXpost2Job& jb = jobs[blockIdx.y];
+  if (threadIdx.x < NP) src_sh[threadIdx.x] = jb.src[threadIdx.x];
+  __syncthreads();
+  const int64_t cv = cols / W;
+  const uint32_t total = (uint32_t)(rows * cv), ucv = (uint32_t)cv;
+  for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    const uint32_t r = idx / ucv;
+    xpost1_elem<TAB, W>(static_cast<const double* const*>(src_sh), jb.lds, jb.dst, jb.ldd, jb.acc_mask, rows, cols, r,
+                        (int64_t)(idx - r * ucv) * W);
+  }
+}
+
+cudaError_t launch_xpost1_batch(const MkXpost2Job* jobs_dev, int njobs, int table, int64_t rows, int64_t cols,
+                                int width, cudaStream_t stream) {
+  if (njobs <= 0 || rows <= 0 || cols <= 0) return cudaSuccess;
+  if (table < 0 || table > 3) return cudaErrorInvalidValue;
+  if (width != 2) width = 1;
+  const int64_t work = rows * (cols / width);
+  if (work >= (int64_t)1 << 32) return cudaErrorInvalidValue;
+  int64_t bx = (work + 255) / 256;
+  const int64_t cap = (148 * 16 + njobs - 1) / njobs;
+  if (bx > cap) bx = cap;
+  if (bx < 1) bx = 1;
+  for (int j0 = 0; j0 < njobs; j0 += 65535) {
+    const int nj = njobs - j0 < 65535 ? njobs - j0 : 65535;
+    dim3 grid((unsigned)bx, (unsigned)nj);
+    const MkXpost2Job* jb = jobs_dev + j0;
+#define MK_XP1(T)                                                            \
+  if (width == 2)                                                            \
+    xpost1_kernel<T, 2><<<grid, 256, 0, stream>>>(jb, rows, cols);          \
+  else                                                                       \
+    xpost1_kernel<T, 1><<<grid, 256, 0, stream>>>(jb, rows, cols);
+    switch (table) {
+      case 0: MK_XP1(0) break;
+      case 1: MK_XP1(1) break;
+      case 2: MK_XP1(2) break;
+      default: MK_XP1(3) break;
+    }
+#undef MK_XP1
+  }
+  return cudaGetLastError();
+}
+
 template <int TAB>
 static void launch_xpost2_t(dim3 grid, const MkXpost2Job* jobs, int64_t rows, int64_t cols, int width,
                             cudaStream_t stream) {
@@ -310,6 +358,9 @@ cudaError_t launch_side_task(const MkSideTask& t, cudaStream_t stream) {
                                  t.width, stream);
     case 3:
       return launch_xpost2_batch(static_cast<const MkXpost2Job*>(t.jobs), t.njobs, t.table, t.rows, t.cols, t.width,
+                                 stream);
+    case 4:
+      return launch_xpost1_batch(static_cast<const MkXpost2Job*>(t.jobs), t.njobs, t.table, t.rows, t.cols, t.width,
                                  stream);
     default: return cudaErrorInvalidValue;
   }

@@ -80,6 +80,9 @@ int xform2_table_coef(int table, int side, int p, int q);
 cudaError_t launch_xpost2_batch(const MkXpost2Job* jobs_dev, int njobs, int table, int64_t rows, int64_t cols,
                                 int width, cudaStream_t stream);
 int xpost2_table_coef(int table, int q, int p);
+// One-level post-addition: a node's quadrants from its children's outputs (MkXpost2Job, src[0..np-1]).
+cudaError_t launch_xpost1_batch(const MkXpost2Job* jobs_dev, int njobs, int table, int64_t rows, int64_t cols,
+                                int width, cudaStream_t stream);
 // dst (rows_d x cols_d) = src (rows_s x cols_s) zero-padded to the right and below, one pass.
 cudaError_t launch_pad_copy(double* dst, int64_t ldd, int64_t rows_d, int64_t cols_d, const double* src, int64_t lds,
                             int64_t rows_s, int64_t cols_s, cudaStream_t stream);

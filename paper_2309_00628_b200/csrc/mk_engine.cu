@@ -1888,6 +1888,33 @@ struct Engine {
         }
         jobs.push_back(job);
       }
+      // side work (pipelined plan): the compiled-table form of the same sums (kind 4), when the
+      // children's outputs share one leading dimension
+      const int table = algo == MK_ALGO_STRASSEN ? 0 : algo == MK_ALGO_WINOGRAD_BLOCK ? 1
+                      : algo == MK_ALGO_WINOGRAD_KNUTH ? 2 : algo == MK_ALGO_WINOGRAD_KNUTH_8CALL ? 3 : -1;
+      bool compiled = defer && !dry && !no_launch && table >= 0 && !jobs.empty();
+      for (int q = 0; compiled && q < 4; ++q)
+        for (int p = 0; p < np; ++p) compiled = compiled && xpost2_table_coef(table, q, p) == co->c[q][p];
+      for (const MkXformJob& jb : jobs)
+        for (int p = 0; compiled && p < np; ++p) compiled = jb.lds[p] == jobs[0].lds[0] && jb.src[p] != nullptr;
+      if (compiled) {
+        std::vector<MkXpost2Job> pj(jobs.size());
+        bool w2 = cn % 2 == 0 && jobs[0].lds[0] % 2 == 0;
+        for (size_t t = 0; t < jobs.size(); ++t) {
+          MkXpost2Job x{};
+          for (int p = 0; p < np; ++p) x.src[p] = jobs[t].src[p];
+          x.lds = jobs[t].lds[0];
+          x.dst = jobs[t].dst[0];
+          x.ldd = jobs[t].ldd[0];
+          w2 = w2 && x.ldd % 2 == 0 && reinterpret_cast<uintptr_t>(x.dst) % 16 == 0;
+          for (int p = 0; p < np; ++p) w2 = w2 && reinterpret_cast<uintptr_t>(x.src[p]) % 16 == 0;
+          pj[t] = x;
+        }
+        void* dev = nullptr;
+        MK_TRY(upload(pj.data(), pj.size() * sizeof(MkXpost2Job), &dev));
+        MK_TRY(side_task(dev, (int)pj.size(), 4, table, 0, cm, cn, w2 ? 2 : 1, (int64_t)pj.size() * (np + 4) * cm * cn * 8));
+        continue;
+      }
       MK_TRY(xform_batch(jobs, cm, cn));
     }
     if (defer)

@@ -321,4 +321,45 @@ __device__ __forceinline__ void xpost2_elem(SrcPtrs src, int64_t lds, double* ds
     }
 }
 
+// ---- one-level post-addition (side work of the pipelined plan) -------------------------------
+// One job = one node: its children's outputs (src[p], common leading dimension lds, rows x cols)
+// -> the node's four quadrants (dst, 2 x 2 blocks of rows x cols, leading dimension ldd):
+//     out(q) = sum_p c[q][p] * G(p)   (+ the quadrant's previous contents when bit q of acc_mask)
+// summed from zero in product order, as the generic transform job does (bit-identical). Reuses
+// MkXpost2Job (src[0 .. np-1]).
+template <int TAB, int W, typename SrcPtrs>
+__device__ __forceinline__ void xpost1_elem(SrcPtrs src, int64_t lds, double* dst, int64_t ldd, uint32_t acc_mask,
+                                            int64_t rows, int64_t cols, uint32_t r, int64_t c) {
+  using T = XCTab<TAB>;
+  constexpr int NP = T::np;
+  const int64_t soff = (int64_t)r * lds + c;
+  Vec<W> g[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) g[p] = ld_vec<W>(src[p] + soff);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    Vec<W> o;
+#pragma unroll
+    for (int u = 0; u < W; ++u) o.v[u] = 0.0;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const int cf = T::cf(q, p);
+      if (cf > 0) {
+#pragma unroll
+        for (int u = 0; u < W; ++u) o.v[u] += g[p].v[u];
+      } else if (cf < 0) {
+#pragma unroll
+        for (int u = 0; u < W; ++u) o.v[u] -= g[p].v[u];
+      }
+    }
+    double* d = dst + ((q >> 1) * rows + r) * ldd + (q & 1) * cols + c;
+    if (acc_mask & (1u << q)) {
+      const Vec<W> old = ld_vec<W>(d);
+#pragma unroll
+      for (int u = 0; u < W; ++u) o.v[u] += old.v[u];
+    }
+    st_vec<W>(d, o);
+  }
+}
+
 }  // namespace mk
