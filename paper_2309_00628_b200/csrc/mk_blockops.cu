@@ -189,6 +189,58 @@ __global__ void __launch_bounds__(256) xpost2_kernel(const MkXpost2Job* __restri
   }
 }
 
+template <int TAB, int SIDE, int W>
+__global__ void __launch_bounds__(256) xform1_kernel(const MkXform2Job* __restrict__ jobs, int64_t rows,
+                                                     int64_t cols) {
+  constexpr int NP = X2Tab<TAB, SIDE>::np;
+  __shared__ double* dst_sh[MK_XFORM2_MAX];
+  const MkXform2Job& jb = jobs[blockIdx.y];
+  if (threadIdx.x < NP) dst_sh[threadIdx.x] = jb.dst[threadIdx.x];
+  __syncthreads();
+  const int64_t cv = cols / W;
+  const uint32_t total = (uint32_t)(rows * cv), ucv = (uint32_t)cv;
+  for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    const uint32_t r = idx / ucv;
+    xform1_elem<TAB, SIDE, W>(jb.src, jb.lds, static_cast<double* const*>(dst_sh), jb.ldd, rows, cols, r,
+                              (int64_t)(idx - r * ucv) * W);
+  }
+}
+
+cudaError_t launch_xform1_batch(const MkXform2Job* jobs_dev, int njobs, int table, int side, int64_t rows,
+                                int64_t cols, int width, cudaStream_t stream) {
+  if (njobs <= 0 || rows <= 0 || cols <= 0) return cudaSuccess;
+  if (table < 0 || table > 3 || side < 0 || side > 1) return cudaErrorInvalidValue;
+  if (width != 2) width = 1;
+  const int64_t work = rows * (cols / width);
+  if (work >= (int64_t)1 << 32) return cudaErrorInvalidValue;
+  int64_t bx = (work + 255) / 256;
+  const int64_t cap = (148 * 16 + njobs - 1) / njobs;
+  if (bx > cap) bx = cap;
+  if (bx < 1) bx = 1;
+  for (int j0 = 0; j0 < njobs; j0 += 65535) {
+    const int nj = njobs - j0 < 65535 ? njobs - j0 : 65535;
+    dim3 grid((unsigned)bx, (unsigned)nj);
+    const MkXform2Job* jb = jobs_dev + j0;
+#define MK_XF1(T, S)                                                         \
+  if (width == 2)                                                            \
+    xform1_kernel<T, S, 2><<<grid, 256, 0, stream>>>(jb, rows, cols);       \
+  else                                                                       \
+    xform1_kernel<T, S, 1><<<grid, 256, 0, stream>>>(jb, rows, cols);
+    switch (table * 2 + side) {
+      case 0: MK_XF1(0, 0) break;
+      case 1: MK_XF1(0, 1) break;
+      case 2: MK_XF1(1, 0) break;
+      case 3: MK_XF1(1, 1) break;
+      case 4: MK_XF1(2, 0) break;
+      case 5: MK_XF1(2, 1) break;
+      case 6: MK_XF1(3, 0) break;
+      default: MK_XF1(3, 1) break;
+    }
+#undef MK_XF1
+  }
+  return cudaGetLastError();
+}
+
 template <int TAB, int W>
 __global__ void __launch_bounds__(256) xpost1_kernel(const MkXpost2Job* __restrict__ jobs, int64_t rows,
                                                      int64_t cols) {
@@ -359,6 +411,9 @@ cudaError_t launch_side_task(const MkSideTask& t, cudaStream_t stream) {
     case 3:
       return launch_xpost2_batch(static_cast<const MkXpost2Job*>(t.jobs), t.njobs, t.table, t.rows, t.cols, t.width,
                                  stream);
+    case 5:
+      return launch_xform1_batch(static_cast<const MkXform2Job*>(t.jobs), t.njobs, t.table, t.side, t.rows, t.cols,
+                                 t.width, stream);
     case 4:
       return launch_xpost1_batch(static_cast<const MkXpost2Job*>(t.jobs), t.njobs, t.table, t.rows, t.cols, t.width,
                                  stream);

@@ -80,6 +80,9 @@ int xform2_table_coef(int table, int side, int p, int q);
 cudaError_t launch_xpost2_batch(const MkXpost2Job* jobs_dev, int njobs, int table, int64_t rows, int64_t cols,
                                 int width, cudaStream_t stream);
 int xpost2_table_coef(int table, int q, int p);
+// One-level operand transform: a node's quadrants -> its children's operands (MkXform2Job, dst[0..np-1]).
+cudaError_t launch_xform1_batch(const MkXform2Job* jobs_dev, int njobs, int table, int side, int64_t rows,
+                                int64_t cols, int width, cudaStream_t stream);
 // One-level post-addition: a node's quadrants from its children's outputs (MkXpost2Job, src[0..np-1]).
 cudaError_t launch_xpost1_batch(const MkXpost2Job* jobs_dev, int njobs, int table, int64_t rows, int64_t cols,
                                 int width, cudaStream_t stream);

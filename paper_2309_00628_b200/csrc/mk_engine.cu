@@ -1548,6 +1548,72 @@ struct Engine {
     return bfs_post(ps, root_touched);
   }
 
+  // The one-level operand transform of a depth as compiled-table side tasks (kind 5: one job per
+  // node, dst[p] = child p's operand or nullptr for a view / a child outside the pass). *done =
+  // false (the caller launches the generic jobs) when a source carries a negative sign, the table
+  // has no compiled form or the destinations do not share one leading dimension.
+  int defer_xform1(const std::vector<MkXformJob>& ja, const std::vector<MkXformJob>& jb, const std::vector<BNode>& cur,
+                   const std::vector<BNode>& next, int64_t hm, int64_t hn, int64_t hk, bool* done) {
+    *done = false;
+    const int np = co->nprod;
+    const int table = algo == MK_ALGO_STRASSEN ? 0 : algo == MK_ALGO_WINOGRAD_BLOCK ? 1
+                    : algo == MK_ALGO_WINOGRAD_KNUTH ? 2 : algo == MK_ALGO_WINOGRAD_KNUTH_8CALL ? 3 : -1;
+    if (table < 0 || np * np > MK_XFORM2_MAX) return MK_OK;
+    for (int side = 0; side < 2; ++side)
+      for (int p = 0; p < np; ++p)
+        for (int q = 0; q < 4; ++q)
+          if (xform2_table_coef(table, side, p, q) != (side == 0 ? co->a[p][q] : co->b[p][q])) return MK_OK;
+    std::vector<MkXform2Job> out[2];
+    for (int side = 0; side < 2; ++side) {
+      const int64_t hr = side == 0 ? hm : hk, hc = side == 0 ? hk : hn;
+      int64_t ldd = -1;
+      for (size_t i = 0; i < cur.size(); ++i) {
+        if (!cur[i].on) continue;
+        const Blk& src = side == 0 ? cur[i].x : cur[i].y;
+        if (src.sign < 0) return MK_OK;
+        MkXform2Job x{};
+        x.src = ptr_of(src);
+        x.lds = bases[src.base].ld;
+        bool any = false;
+        for (int p = 0; p < np; ++p) {
+          const BNode& ch = next[i * np + p];
+          const Blk& t = side == 0 ? ch.x : ch.y;
+          if (!ch.on || t.base == src.base) continue;  // not in the pass, or a view of the node's block
+          if (ldd >= 0 && bases[t.base].ld != ldd) return MK_OK;
+          ldd = bases[t.base].ld;
+          x.dst[p] = ptr_of(t);
+          any = true;
+        }
+        x.ldd = ldd < 0 ? 0 : ldd;
+        if (any) out[side].push_back(x);
+      }
+      (void)hr;
+      (void)hc;
+    }
+    const size_t n_generic = ja.size() + jb.size(), n_comp = out[0].size() + out[1].size();
+    if (n_generic != n_comp) return MK_OK;  // every generic job must have its compiled twin
+    for (int side = 0; side < 2; ++side) {
+      if (out[side].empty()) continue;
+      const int64_t hr = side == 0 ? hm : hk, hc = side == 0 ? hk : hn;
+      bool w2 = hc % 2 == 0;
+      int64_t words = 0;
+      for (const MkXform2Job& x : out[side]) {
+        w2 = w2 && x.lds % 2 == 0 && x.ldd % 2 == 0 && reinterpret_cast<uintptr_t>(x.src) % 16 == 0;
+        words += 4;
+        for (int p = 0; p < np; ++p)
+          if (x.dst[p]) {
+            w2 = w2 && reinterpret_cast<uintptr_t>(x.dst[p]) % 16 == 0;
+            ++words;
+          }
+      }
+      void* dev = nullptr;
+      MK_TRY(upload(out[side].data(), out[side].size() * sizeof(MkXform2Job), &dev));
+      MK_TRY(side_task(dev, (int)out[side].size(), 5, table, side, hr, hc, w2 ? 2 : 1, words * hr * hc * 8));
+    }
+    *done = true;
+    return MK_OK;
+  }
+
   int bfs_operands(BfsPass& ps) {
     const int np = co->nprod;
     const int L = ps.L;
@@ -1629,6 +1695,14 @@ struct Engine {
             for (int q = 0; q < 4; ++q) job.coef[j][q] = (int8_t)(cf[q] * (src.sign < 0 ? -1 : 1));
           }
           if (job.ndst) (side == 0 ? ja : jb).push_back(job);
+        }
+      }
+      if (defer && !dry && !no_launch) {  // side work: the compiled-table form (kind 5) when it applies
+        bool done = false;
+        MK_TRY(defer_xform1(ja, jb, cur, next, hm, hn, hk, &done));
+        if (done) {
+          lv.push_back(std::move(next));
+          continue;
         }
       }
       MK_TRY(xform_batch(ja, hm, hk));
@@ -2179,8 +2253,27 @@ static int run_bfs_pipelined(Engine& e, int64_t M, int64_t N, int64_t K) {
   }
   if (need > e.ws_bytes) return fail(MK_ERR_WORKSPACE, "workspace too small for the pipelined plan: need " + std::to_string(need));
   const int nb_mark = e.nbases;
-  // ---- prologue: every top-level product's operand sums (launches of their own) ----
-  MK_TRY(e.bfs_operands(pro));
+  // ---- prologue: every top-level product's operand sums. They ride on the first pass's leaf
+  // launches (ahead of the second pass's transforms) unless the first pass's own product needs
+  // them, in which case they run as launches of their own first.
+  SidePhases pro_phases;
+  e.defer = &pro_phases;
+  {
+    const int rc = e.bfs_operands(pro);
+    e.defer = nullptr;
+    MK_TRY(rc);
+  }
+  int ta = 0, tb = 0;
+  for (int q = 0; q < 4; ++q) {
+    ta += e.co->a[0][q] != 0;
+    tb += e.co->b[0][q] != 0;
+  }
+  const bool first_needs = ta > 1 || tb > 1;  // the first pass's product has an operand sum
+  if (first_needs) {
+    for (const auto& ph : pro_phases)
+      for (const MkSideTask& tk : ph) MK_CUDA_TRY(launch_side_task(tk, e.st));
+    pro_phases.clear();
+  }
   int slots = -1;
   MK_TRY(e.alloc_slot((int64_t)np * hm, hn, &slots, true));
   for (int p = 0; p < np; ++p) pro.lv[1][p].o = Blk{slots, (int64_t)p * hm, 0, 1.0};
@@ -2250,6 +2343,7 @@ static int run_bfs_pipelined(Engine& e, int64_t M, int64_t N, int64_t K) {
       MK_TRY(rc);
       leave(i + 1);
     }
+    if (i == 0 && !pro_phases.empty()) next_ops.insert(next_ops.begin(), pro_phases.begin(), pro_phases.end());
     SidePhases per(nl), rest;
     assign_side({&next_ops, &post_prev}, cap, per, rest);
     enter(i, false);

@@ -625,6 +625,21 @@ __device__ __forceinline__ void side_xform2(const MkSideTask& tk, uint32_t tid, 
         xform2_elem<TAB, SIDE, W>(jb.src, jb.lds, static_cast<double* const*>(ptr_sh), jb.ldd, tk.rows, tk.cols, r, c);
       });
 }
+template <int NT, int TAB, int SIDE, int W>
+__device__ __forceinline__ void side_xform1(const MkSideTask& tk, uint32_t tid, uint32_t cta, uint32_t ncta,
+                                            double** ptr_sh) {
+  constexpr int NP = X2Tab<TAB, SIDE>::np;
+  const MkXform2Job* jobs = static_cast<const MkXform2Job*>(tk.jobs);
+  side_loop<NT, W>(
+      tk, tid, cta, ncta,
+      [&](uint32_t j) {
+        if (tid < NP) ptr_sh[tid] = jobs[j].dst[tid];
+      },
+      [&](uint32_t j, uint32_t r, int64_t c) {
+        const MkXform2Job& jb = jobs[j];
+        xform1_elem<TAB, SIDE, W>(jb.src, jb.lds, static_cast<double* const*>(ptr_sh), jb.ldd, tk.rows, tk.cols, r, c);
+      });
+}
 template <int NT, int TAB, int W>
 __device__ __forceinline__ void side_xpost1(const MkSideTask& tk, uint32_t tid, uint32_t cta, uint32_t ncta,
                                             double** ptr_sh) {
@@ -695,6 +710,25 @@ __device__ __forceinline__ void side_work(const MkGemmArgs& a, uint32_t tid, uin
         case 5: side_xpost2<NT, 2, 1>(tk, tid, cta, ncta, ptr_sh); break;
         case 6: side_xpost2<NT, 3, 1>(tk, tid, cta, ncta, ptr_sh); break;
         default: side_xpost2<NT, 3, 1>(tk, tid, cta, ncta, ptr_sh); break;
+      }
+    } else if (tk.kind == 5) {
+      switch (tk.table * 4 + tk.side * 2 + (w2 ? 1 : 0)) {
+        case 0: side_xform1<NT, 0, 0, 1>(tk, tid, cta, ncta, ptr_sh); break;
+        case 1: side_xform1<NT, 0, 0, 2>(tk, tid, cta, ncta, ptr_sh); break;
+        case 2: side_xform1<NT, 0, 1, 1>(tk, tid, cta, ncta, ptr_sh); break;
+        case 3: side_xform1<NT, 0, 1, 2>(tk, tid, cta, ncta, ptr_sh); break;
+        case 4: side_xform1<NT, 1, 0, 1>(tk, tid, cta, ncta, ptr_sh); break;
+        case 5: side_xform1<NT, 1, 0, 2>(tk, tid, cta, ncta, ptr_sh); break;
+        case 6: side_xform1<NT, 1, 1, 1>(tk, tid, cta, ncta, ptr_sh); break;
+        case 7: side_xform1<NT, 1, 1, 2>(tk, tid, cta, ncta, ptr_sh); break;
+        case 8: side_xform1<NT, 2, 0, 1>(tk, tid, cta, ncta, ptr_sh); break;
+        case 9: side_xform1<NT, 2, 0, 2>(tk, tid, cta, ncta, ptr_sh); break;
+        case 10: side_xform1<NT, 2, 1, 1>(tk, tid, cta, ncta, ptr_sh); break;
+        case 11: side_xform1<NT, 2, 1, 2>(tk, tid, cta, ncta, ptr_sh); break;
+        case 12: side_xform1<NT, 3, 0, 1>(tk, tid, cta, ncta, ptr_sh); break;
+        case 13: side_xform1<NT, 3, 0, 2>(tk, tid, cta, ncta, ptr_sh); break;
+        case 14: side_xform1<NT, 3, 1, 1>(tk, tid, cta, ncta, ptr_sh); break;
+        default: side_xform1<NT, 3, 1, 2>(tk, tid, cta, ncta, ptr_sh); break;
       }
     } else if (tk.kind == 4) {
       switch (tk.table * 2 + (w2 ? 1 : 0)) {
@@ -1366,7 +1400,7 @@ static cudaError_t launch_persistent_t(const CUtensorMap& tmA, const CUtensorMap
   for (int t = 0; t < args.nside; ++t) {
     const MkSideTask& tk = args.side[t];
     const int64_t groups = tk.rows * (tk.cols / (tk.width > 0 ? tk.width : 1)) * tk.njobs;
-    if (attach && BN == 64 && (tk.kind == 2 || tk.kind == 3 || tk.kind == 4) && (tk.width == 1 || tk.width == 2) && tk.cols % tk.width == 0 &&
+    if (attach && BN == 64 && (tk.kind >= 2 && tk.kind <= 5) && (tk.width == 1 || tk.width == 2) && tk.cols % tk.width == 0 &&
         groups < ((int64_t)1 << 32))
       carry[ncarry++] = tk;
     else

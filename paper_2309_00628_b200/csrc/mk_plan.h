@@ -56,7 +56,7 @@ struct MkSideTask {
   int64_t rows, cols;
   int32_t njobs;
   int8_t kind;       // 1 one-level transform, 2 two-level operand transform, 3 two-level post-addition,
-                     // 4 one-level post-addition (compiled table)
+                     // 4 one-level post-addition, 5 one-level operand transform (compiled tables)
   int8_t table;      // kinds 2, 3: 0 Strassen, 1 Winograd block, 2 Winograd Knuth, 3 Knuth 8-call
   int8_t side;       // kind 2: 0 A, 1 B
   int8_t width;      // doubles per access: 1, 2 (or 4 for kind 1)

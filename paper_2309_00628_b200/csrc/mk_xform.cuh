@@ -321,6 +321,42 @@ __device__ __forceinline__ void xpost2_elem(SrcPtrs src, int64_t lds, double* ds
     }
 }
 
+// ---- one-level operand transform (side work of the pipelined plan) -----------------------------
+// One job = one node: its operand block (2 x 2 quadrants of rows x cols at src, leading dimension
+// lds) -> the children's operands G(p) = sum_q c[p][q] X(q) for every p with dst[p] set (others:
+// views or not in the pass), summed from zero in quadrant order as the generic transform job does
+// (bit-identical). Reuses MkXform2Job (dst[0 .. np-1]).
+template <int TAB, int SIDE, int W, typename DstPtrs>
+__device__ __forceinline__ void xform1_elem(const double* src, int64_t lds, DstPtrs dst, int64_t ldd, int64_t rows,
+                                            int64_t cols, uint32_t r, int64_t c) {
+  using T = X2Tab<TAB, SIDE>;
+  constexpr int NP = T::np;
+  Vec<W> x[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) x[q] = ld_vec<W>(src + ((q >> 1) * rows + r) * lds + (q & 1) * cols + c);
+  const int64_t off = (int64_t)r * ldd + c;
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    double* d = dst[p];
+    if (!d) continue;
+    Vec<W> o;
+#pragma unroll
+    for (int u = 0; u < W; ++u) o.v[u] = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int cf = T::cf(p, q);
+      if (cf > 0) {
+#pragma unroll
+        for (int u = 0; u < W; ++u) o.v[u] += x[q].v[u];
+      } else if (cf < 0) {
+#pragma unroll
+        for (int u = 0; u < W; ++u) o.v[u] -= x[q].v[u];
+      }
+    }
+    st_vec<W>(d + off, o);
+  }
+}
+
 // ---- one-level post-addition (side work of the pipelined plan) -------------------------------
 // One job = one node: its children's outputs (src[p], common leading dimension lds, rows x cols)
 // -> the node's four quadrants (dst, 2 x 2 blocks of rows x cols, leading dimension ldd):
