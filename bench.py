@@ -219,10 +219,11 @@ def blas_threads():
 
 
 def cpu_operands(n):
-    """The workload's operands (cfg4 generator at order n) for the CPU legs."""
-    from oracle import strassen_oracle as o
+    """The workload's operands (cfg4 generator at order n): standard normal, A then B from one
+    seeded generator -- shared by the GPU arm and the CPU legs."""
+    from paper_2309_00628_b200.metrics import BASELINE_SEED
 
-    rng = np.random.default_rng(o.SEED)
+    rng = np.random.default_rng(BASELINE_SEED)
     return rng.standard_normal((n, n)), rng.standard_normal((n, n))
 
 
@@ -389,12 +390,12 @@ def ozaki_leg(args, pk, lib, _lib, torch, A, B, C, dc, host_a, host_b, policy, s
 def baseline_legs(args, pk, lib, _lib, torch, stream, peak_tflops, legs):
     """BASELINE cfg3 and cfg5 on their seeded inputs, and cuBLAS DGEMM as a comparison point
     (torch.matmul on FP64 CUDA tensors; never on the product path)."""
-    from oracle import strassen_oracle as o
+    from paper_2309_00628_b200.metrics import baseline_operands
 
     timed = event_timer(torch, stream)
     out = {}
     if "cfg3" in legs:
-        a, b = o.operands(3)
+        a, b = baseline_operands(3)
         da, db = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
         c = torch.empty_like(da)
         pol = pk.BasePolicy.naive_cutoff(1024)
@@ -416,7 +417,7 @@ def baseline_legs(args, pk, lib, _lib, torch, stream, peak_tflops, legs):
         del da, db, c, a2, b2
         torch.cuda.empty_cache()
     if "cfg5" in legs:
-        a, b = o.operands(5)
+        a, b = baseline_operands(5)
         da, db = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
         m, k = a.shape
         n = b.shape[1]

@@ -73,9 +73,14 @@ int mk_version(void);
  * MK_OPT_BFS_GROUP (breadth-first plan, L >= 2): top-level products per pass. 0 = auto (4: two
  *   passes over the 7 products, each keeping only its own operand sums and outputs -- about half
  *   the single-pass workspace); 7 or 8 = one pass (largest workspace); 1 = one top-level subtree
- *   at a time (smallest). Results differ only in the order C's partial sums are added. */
+ *   at a time (smallest). Results differ only in the order C's partial sums are added.
+ * MK_OPT_LITERAL_STREAMS (two-temp / in-place): 1 = block additions the next product does not
+ *   depend on are issued on internal side streams, ordered by block-level hazard tracking, and
+ *   run beside the leaf products (default); 0 = every step on the caller's stream. Same steps,
+ *   same operands, bit-identical results either way; the side streams are joined into `stream`
+ *   before the call returns. */
 enum mk_option { MK_OPT_FUSE_PREADDS = 1, MK_OPT_PLAN = 2, MK_OPT_LITERAL_TAIL = 3, MK_OPT_LEAF_SLICES = 4,
-                 MK_OPT_LEAF_MIN_LOG2 = 5, MK_OPT_BFS_GROUP = 6 };
+                 MK_OPT_LEAF_MIN_LOG2 = 5, MK_OPT_BFS_GROUP = 6, MK_OPT_LITERAL_STREAMS = 7 };
 int mk_set_option(int key, int value);
 int mk_get_option(int key, int* value);
 /* Calling-thread override of MK_OPT_PLAN / MK_OPT_LITERAL_TAIL (value -1 removes it). Applies to

@@ -49,6 +49,44 @@ __global__ void combine_kernel(const __grid_constant__ CombineArgs a) {
   }
 }
 
+// Two-source sums (every step of the literal schedules is X = Y +- Z, schedules.py:62-112). The
+// generic kernel keeps two 16-byte loads per thread in flight, which holds a lone SM to ~57 GB/s
+// -- and a handful of SMs is what an addition gets when it runs beside a one-at-a-time leaf launch
+// (128 tiles on 148 SMs). Here a thread issues 2 x U loads before its first use. Same arithmetic
+// as combine_kernel (fma from zero in source order): bit-identical. dst may alias a source
+// exactly: a thread reads its elements before it writes them.
+template <int U>
+__global__ void __launch_bounds__(256) combine2_kernel(const __grid_constant__ CombineArgs a) {
+  const uint32_t cv = (uint32_t)(a.cols >> 1);
+  const uint32_t total = (uint32_t)a.rows * cv;  // < 2^31 (checked by the launcher)
+  const double s0 = a.sign[0], s1 = a.sign[1];
+  for (uint32_t base = blockIdx.x * (256u * U) + threadIdx.x; base < total; base += gridDim.x * (256u * U)) {
+    double2 x[U], y[U];
+    int64_t off[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const uint32_t idx = base + (uint32_t)k * 256u;
+      if (idx < total) {
+        const uint32_t r = idx / cv;
+        const int64_t c = (int64_t)(idx - r * cv) * 2;
+        x[k] = __ldg(reinterpret_cast<const double2*>(a.src[0] + (int64_t)r * a.lds[0] + c));
+        y[k] = __ldg(reinterpret_cast<const double2*>(a.src[1] + (int64_t)r * a.lds[1] + c));
+        off[k] = (int64_t)r * a.ldd + c;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const uint32_t idx = base + (uint32_t)k * 256u;
+      if (idx < total) {
+        double2 acc;
+        acc.x = fma(s1, y[k].x, fma(s0, x[k].x, 0.0));
+        acc.y = fma(s1, y[k].y, fma(s0, x[k].y, 0.0));
+        *reinterpret_cast<double2*>(a.dst + off[k]) = acc;
+      }
+    }
+  }
+}
+
 static int grid_for(int64_t work, int threads) {
   int64_t blocks = (work + threads - 1) / threads;
   const int64_t cap = 148 * 16;  // 16 resident 256-thread CTAs per SM
@@ -75,7 +113,13 @@ cudaError_t launch_combine(double* dst, int64_t ldd, const double* const* src, c
     vec = vec && (lds[t] % 2 == 0) && ((uintptr_t)src[t] % 16 == 0);
   }
   const int threads = 256;
-  if (vec)
+  if (vec && nsrc == 2 && rows * (cols / 2) < ((int64_t)1 << 31)) {
+    constexpr int U = 4;
+    const int64_t work = rows * (cols / 2);
+    int64_t blocks = (work + threads * U - 1) / (threads * U);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    combine2_kernel<U><<<(unsigned)blocks, threads, 0, stream>>>(a);
+  } else if (vec)
     combine_kernel<true><<<grid_for(rows * (cols / 2), threads), threads, 0, stream>>>(a);
   else
     combine_kernel<false><<<grid_for(rows * cols, threads), threads, 0, stream>>>(a);

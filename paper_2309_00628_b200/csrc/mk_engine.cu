@@ -31,6 +31,8 @@
 #include <vector>
 #include <cmath>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/mk_strassen.h"
 #include "mk_blockops.h"
 #include "mk_hoststage.h"
@@ -43,6 +45,21 @@ namespace mk {
 // Error reporting
 // ----------------------------------------------------------------------------------
 static thread_local std::string g_last_error;
+
+// NVTX ranges (tracing): one per C-ABI call (with its shape) and one per plan
+// phase -- operand transforms, leaf launches, post-additions -- so a timeline viewer shows the
+// passes of a product. Header-only NVTX v3: the calls are no-ops unless a tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  explicit NvtxRange(const std::string& name) { nvtxRangePushA(name.c_str()); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+static std::string nvtx_label(const char* fn, int algo, int64_t m, int64_t n, int64_t k, int levels) {
+  return std::string(fn) + " algo=" + std::to_string(algo) + " " + std::to_string(m) + "x" + std::to_string(k) + "." +
+         std::to_string(k) + "x" + std::to_string(n) + " L=" + std::to_string(levels);
+}
 
 static int fail(int code, const std::string& msg) {
   g_last_error = msg;
@@ -480,6 +497,115 @@ static bool table_ring_copy(void* dev_dst, const void* host, size_t bytes, cudaS
   return true;
 }
 
+// ---- side streams of the literal schedules ------------------------------------------------
+// The Table-2 / Table-3 schedules are a fixed sequence of block additions and products over a
+// handful of blocks; executed on one stream every addition sits on the critical path between two
+// leaf products (n = 8192, 3 levels: 855 additions, ~7 ms of 35). Most of them do not feed the
+// next product (Table 3: S2 can run under P7, T2 under P5, S4 under P6, U2 under P2, U1..U7 under
+// P3), and a one-at-a-time leaf launch of a literal schedule leaves SMs idle (128 narrow tiles on
+// 148 SMs). So additions that the next product does not read are issued on side streams (one per
+// recursion depth), ordered against the other streams by block-level hazard tracking: every
+// issued operation records its read and write rectangles and an event; an operation first waits
+// for the latest conflicting (RAW / WAR / WAW) operation of every other stream. Same program,
+// same operands, same results (each block still sees the same sequence of writers and readers).
+struct LitRegion {
+  const double* p = nullptr;
+  int64_t ld = 0, rows = 0, cols = 0;
+};
+static bool lit_conflict(const LitRegion& a, const LitRegion& b) {
+  if (!a.p || !b.p) return false;
+  if (a.ld == b.ld && a.cols <= a.ld && b.cols <= b.ld) {
+    // exact: both are rectangles of one virtual row-major matrix of pitch ld
+    const int64_t delta = b.p - a.p;
+    int64_t dr = delta / a.ld, dc = delta % a.ld;
+    if (dc < 0) {
+      dc += a.ld;
+      --dr;
+    }
+    auto hit = [&](int64_t r, int64_t c) { return r < a.rows && r + b.rows > 0 && c < a.cols && c + b.cols > 0; };
+    return hit(dr, dc) || hit(dr + 1, dc - a.ld);
+  }
+  const double* a1 = a.p + (a.rows - 1) * a.ld + a.cols;  // conservative address-range test
+  const double* b1 = b.p + (b.rows - 1) * b.ld + b.cols;
+  return a.p < b1 && b.p < a1;
+}
+constexpr int kLitStreams = 4;    // the caller's stream + one side stream per depth (deeper ones share the last)
+constexpr int kLitEvents = 1024;  // event ring per stream (a stale slot waits for a later operation: still correct)
+struct LitStreams {               // per host thread and device, created once
+  cudaStream_t side[kLitStreams - 1] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev[kLitStreams][kLitEvents] = {};
+  cudaEvent_t fork = nullptr;
+  bool ok = false;
+};
+static LitStreams* lit_streams() {
+  static thread_local std::map<int, LitStreams> per_dev;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  LitStreams& ls = per_dev[dev];
+  if (!ls.ok) {
+    for (auto& sd : ls.side)
+      if (cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    for (auto& ring : ls.ev)
+      for (auto& e : ring)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    if (cudaEventCreateWithFlags(&ls.fork, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    ls.ok = true;
+  }
+  return &ls;
+}
+// Which additions of a 22-step table stay on the caller's stream: those on a dependency chain
+// (RAW / WAR / WAW over storage locations) to the next product, and the ones after the last
+// product. Every other addition can run beside the next product. Table 3: S3, T1, T3, T4, U5 stay;
+// S1, S2, T2, S4, U2, U1, U4, U3, U6, U7 go to a side stream.
+struct LitCritical {
+  bool main[22];
+};
+static const LitCritical& lit_critical(const SchedStep* steps) {
+  static std::mutex mu;
+  static std::map<const SchedStep*, LitCritical> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(steps);
+  if (it != cache.end()) return it->second;
+  // storage locations of every step (the symbol -> location bindings of schedules.py:149-179)
+  std::map<std::string, std::string> where;
+  for (const char* nm : {"A11", "A12", "A21", "A22", "B11", "B12", "B21", "B22"}) where[nm] = nm;
+  std::string rd0[22], rd1[22], wr[22];
+  for (int i = 0; i < 22; ++i) {
+    rd0[i] = where.at(steps[i].lhs);
+    rd1[i] = where.at(steps[i].rhs);
+    wr[i] = steps[i].store;
+    where[steps[i].symbol] = steps[i].store;
+  }
+  auto conflict = [&](int a, int b) {
+    return wr[a] == wr[b] || wr[a] == rd0[b] || wr[a] == rd1[b] || wr[b] == rd0[a] || wr[b] == rd1[a];
+  };
+  LitCritical c{};
+  int end = 22;  // the next product of the segment being swept (22: none follows)
+  std::vector<int> chain;
+  for (int i = 21; i >= 0; --i) {
+    if (steps[i].op == '*') {
+      end = i;
+      chain.assign(1, i);
+      c.main[i] = true;
+      continue;
+    }
+    bool m = end == 22;
+    for (int j : chain) m = m || conflict(i, j);
+    c.main[i] = m;
+    if (m && end != 22) chain.push_back(i);
+  }
+  return cache.emplace(steps, c).first->second;
+}
+
+static std::atomic<int> g_literal_streams{-1};  // -1: unset (env MK_LITERAL_STREAMS), 0/1 explicit
+static bool literal_streams_enabled() {
+  if (g_literal_streams < 0) {
+    const char* s = getenv("MK_LITERAL_STREAMS");
+    g_literal_streams = (s && s[0] == '0') ? 0 : 1;
+  }
+  return g_literal_streams == 1;
+}
+
 struct Engine {
   int algo = 0;
   const Coeffs* co = nullptr;
@@ -602,8 +728,77 @@ struct Engine {
     return MK_OK;
   }
 
+  // ---- side streams of the literal schedules (see LitStreams) ----
+  struct LitOp {
+    LitRegion rd[2], wr;
+  };
+  LitStreams* lit = nullptr;  // non-null while a literal schedule issues on several streams
+  std::vector<LitOp> lit_ops[kLitStreams];
+  size_t lit_seen[kLitStreams][kLitStreams] = {};  // [s][t]: operations of stream t that stream s has waited for
+  cudaStream_t lit_stream(int s) const { return s == 0 ? st : lit->side[s - 1]; }
+  LitRegion region(const Blk& b, int64_t rows, int64_t cols) const {
+    return LitRegion{bases[b.base].ptr + b.row * bases[b.base].ld + b.col, bases[b.base].ld, rows, cols};
+  }
+  int lit_begin() {
+    if (dry || no_launch || tbl_mode != 0 || !literal_streams_enabled()) return MK_OK;
+    lit = lit_streams();
+    if (!lit) {
+      (void)cudaGetLastError();
+      return MK_OK;  // no side streams: everything stays on the caller's stream
+    }
+    for (int s = 0; s < kLitStreams; ++s) {
+      lit_ops[s].clear();
+      for (int t = 0; t < kLitStreams; ++t) lit_seen[s][t] = 0;
+    }
+    // side streams start after prior work on the caller's stream
+    MK_CUDA_TRY(cudaEventRecord(lit->fork, st));
+    for (int s = 1; s < kLitStreams; ++s) MK_CUDA_TRY(cudaStreamWaitEvent(lit_stream(s), lit->fork, 0));
+    return MK_OK;
+  }
+  // before launching an operation on stream s: wait for the latest conflicting operation of
+  // every other stream that s has not yet waited for
+  int lit_wait(int s, const LitOp& op) {
+    for (int t = 0; t < kLitStreams; ++t) {
+      if (t == s) continue;
+      const std::vector<LitOp>& ops = lit_ops[t];
+      for (size_t j = ops.size(); j > lit_seen[s][t]; --j) {
+        const LitOp& o = ops[j - 1];
+        const bool hit = lit_conflict(op.wr, o.wr) || lit_conflict(op.wr, o.rd[0]) || lit_conflict(op.wr, o.rd[1]) ||
+                         lit_conflict(op.rd[0], o.wr) || lit_conflict(op.rd[1], o.wr);
+        if (!hit) continue;
+        MK_CUDA_TRY(cudaStreamWaitEvent(lit_stream(s), lit->ev[t][(j - 1) % kLitEvents], 0));
+        lit_seen[s][t] = j;
+        // what stream t had waited for when it issued that operation is complete as well
+        break;
+      }
+    }
+    return MK_OK;
+  }
+  int lit_done(int s, const LitOp& op) {  // after the launch
+    MK_CUDA_TRY(cudaEventRecord(lit->ev[s][lit_ops[s].size() % kLitEvents], lit_stream(s)));
+    lit_ops[s].push_back(op);
+    return MK_OK;
+  }
+  int lit_end() {  // the caller's stream waits for the side streams
+    if (!lit) return MK_OK;
+    for (int s = 1; s < kLitStreams; ++s) {
+      if (lit_ops[s].empty()) continue;
+      MK_CUDA_TRY(cudaStreamWaitEvent(st, lit->ev[s][(lit_ops[s].size() - 1) % kLitEvents], 0));
+    }
+    lit = nullptr;
+    if (host_trace_on() && !g_host_trace.empty()) {  // dev aid: per-operation timeline of the schedule
+      cudaStreamSynchronize(st);
+      std::vector<unsigned long long> t(g_host_trace.size());
+      cudaMemcpy(t.data(), g_trace_dev, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+      for (size_t i = 0; i < t.size(); ++i)
+        fprintf(stderr, "[lit-trace] %9.1f us  %s\n", (double)(t[i] - t[0]) * 1e-3, g_host_trace[i].c_str());
+      g_host_trace.clear();
+    }
+    return MK_OK;
+  }
+
   // ---- block combine: dst := dst.sign * sum_i src_i.sign * src_i (chained past 8 sources) ----
-  int combine(const Blk& dst, const Lin& src, int64_t rows, int64_t cols) {
+  int combine(const Blk& dst, const Lin& src, int64_t rows, int64_t cols, cudaStream_t on = nullptr) {
     if (dry || no_launch) return MK_OK;
     double* dp = bases[dst.base].ptr + dst.row * bases[dst.base].ld + dst.col;
     const int64_t ldd = bases[dst.base].ld;
@@ -626,7 +821,7 @@ struct Engine {
         lds[ns] = bases[b.base].ld;
         sg[ns] = b.sign * dst.sign;
       }
-      MK_CUDA_TRY(launch_combine(dp, ldd, sp, lds, sg, ns, rows, cols, st));
+      MK_CUDA_TRY(launch_combine(dp, ldd, sp, lds, sg, ns, rows, cols, on ? on : st));
       ++g_launch_count;
       first = false;
     } while (i < src.size());
@@ -1110,15 +1305,29 @@ struct Engine {
   int literal(const SchedStep* steps, bool use_xy, int remaining, Blk X, Blk Y, Blk D, int64_t s) {
     // product of single blocks X*Y -> D (store semantics: D's old contents are replaced)
     set_state(D.base, D.row, D.col, s, s, 0);
-    if (remaining == 0 || (remaining == 1 && fuse_preadds))
-      return fused(remaining, Lin{X}, Lin{Y}, Lin{D}, s, s, s, L - remaining);
+    LitOp prod;  // a product launched from here: reads X and Y, writes D (the caller's stream)
+    if (lit) {
+      prod.rd[0] = region(X, s, s);
+      prod.rd[1] = region(Y, s, s);
+      prod.wr = region(D, s, s);
+    }
+    if (remaining == 0 || (remaining == 1 && fuse_preadds)) {
+      if (lit) MK_TRY(lit_wait(0, prod));
+      if (lit) host_trace("s0 leaf B", st);
+      MK_TRY(fused(remaining, Lin{X}, Lin{Y}, Lin{D}, s, s, s, L - remaining));
+      if (lit) host_trace("s0 leaf E", st);
+      if (lit) MK_TRY(lit_done(0, prod));
+      return MK_OK;
+    }
     // Two-temp may use scratch: its last two levels run breadth-first (leaf products of the
     // 7 sub-parents batched per launch) under the literal Table-2 levels above. In-place keeps
     // the literal schedule to the leaves (zero workspace). MK_LITERAL_TAIL=0 disables this.
     if (use_xy && remaining == 2 && !fuse_preadds && literal_bfs_tail()) {
       const size_t mark = ws_used;
       const int nb_mark = nbases;
+      if (lit) MK_TRY(lit_wait(0, prod));  // its scratch lies above every slot a side stream touches
       MK_TRY(bfs(2, s, s, s, X, Y, D));
+      if (lit) MK_TRY(lit_done(0, prod));
       ws_used = mark;
       while (nbases > nb_mark) {
         --nbases;
@@ -1159,7 +1368,24 @@ struct Engine {
         MK_TRY(literal(steps, use_xy, remaining - 1, l, r, d, h));
       } else {
         const double sg = st_.op == '+' ? 1.0 : -1.0;
-        MK_TRY(combine(d, Lin{l, Blk{r.base, r.row, r.col, sg}}, h, h));
+        const Lin terms{l, Blk{r.base, r.row, r.col, sg}};
+        if (!lit) {
+          MK_TRY(combine(d, terms, h, h));
+        } else {
+          // an addition the next product depends on (or one after the node's last product) stays
+          // on the caller's stream; every other one goes to this depth's side stream
+          const int sid = lit_critical(steps).main[i] ? 0 : 1 + std::min(L - remaining, kLitStreams - 2);
+          LitOp op;
+          op.rd[0] = region(l, h, h);
+          op.rd[1] = region(r, h, h);
+          op.wr = region(d, h, h);
+          MK_TRY(lit_wait(sid, op));
+          const std::string tag = "s" + std::to_string(sid) + " " + st_.symbol + " d" + std::to_string(L - remaining);
+          host_trace(tag + " B", lit_stream(sid));
+          MK_TRY(combine(d, terms, h, h, lit_stream(sid)));
+          host_trace(tag + " E", lit_stream(sid));
+          MK_TRY(lit_done(sid, op));
+        }
         set_state(d.base, d.row, d.col, h, h, 1);
       }
       where[st_.symbol] = st_.store;
@@ -1615,6 +1841,7 @@ struct Engine {
   }
 
   int bfs_operands(BfsPass& ps) {
+    NvtxRange nvtx_("mk: operand transforms");
     const int np = co->nprod;
     const int L = ps.L;
     const int64_t M = ps.M, N = ps.N, K = ps.K;
@@ -1718,6 +1945,7 @@ struct Engine {
   // Leaf launches of a pass; side (optional): the side tasks each colour-group launch carries
   // (index = launch order; tasks beyond the launches or MK_SIDE_MAX run as their own launches).
   int bfs_leaves(BfsPass& ps, const std::vector<std::vector<MkSideTask>>* side) {
+    NvtxRange nvtx_("mk: leaf products");
     const int np = co->nprod;
     const int L = ps.L;
     const int64_t M = ps.M, N = ps.N, K = ps.K;
@@ -1881,6 +2109,7 @@ struct Engine {
   }
 
   int bfs_post(BfsPass& ps, bool* root_touched) {
+    NvtxRange nvtx_("mk: post-additions");
     const int np = co->nprod;
     const int L = ps.L;
     const int64_t M = ps.M, N = ps.N;
@@ -2386,10 +2615,14 @@ static int run_square(Engine& e) {
   }
   if (use_bfs(e, e.leaf_m, e.leaf_n))
     return use_pipeline(e) ? run_bfs_pipelined(e, n, n, n) : run_bfs_grouped(e, n, n, n);
-  if (e.algo == MK_ALGO_TWO_TEMP)
-    return e.literal(kTwoTemp, true, e.L, Blk{BASE_A, 0, 0, 1.0}, Blk{BASE_B, 0, 0, 1.0}, Blk{BASE_C, 0, 0, 1.0}, n);
-  if (e.algo == MK_ALGO_IN_PLACE)
-    return e.literal(kInPlace, false, e.L, Blk{BASE_A, 0, 0, 1.0}, Blk{BASE_B, 0, 0, 1.0}, Blk{BASE_C, 0, 0, 1.0}, n);
+  if (e.algo == MK_ALGO_TWO_TEMP || e.algo == MK_ALGO_IN_PLACE) {
+    const bool tt = e.algo == MK_ALGO_TWO_TEMP;
+    MK_TRY(e.lit_begin());
+    const int rc = e.literal(tt ? kTwoTemp : kInPlace, tt, e.L, Blk{BASE_A, 0, 0, 1.0}, Blk{BASE_B, 0, 0, 1.0},
+                             Blk{BASE_C, 0, 0, 1.0}, n);
+    const int rj = e.lit_end();  // join even after a failure: nothing may outlive the call on a side stream
+    return rc != MK_OK ? rc : rj;
+  }
   return e.fused(e.L, Lin{Blk{BASE_A, 0, 0, 1.0}}, Lin{Blk{BASE_B, 0, 0, 1.0}}, Lin{Blk{BASE_C, 0, 0, 1.0}}, n, n, n, 0);
 }
 
@@ -2480,6 +2713,10 @@ int mk_set_option(int key, int value) {
     g_bfs_group = value;
     return MK_OK;
   }
+  if (key == MK_OPT_LITERAL_STREAMS) {
+    g_literal_streams = value ? 1 : 0;
+    return MK_OK;
+  }
   return fail(MK_ERR_ARG, "unknown option key");
 }
 
@@ -2513,6 +2750,8 @@ int mk_get_option(int key, int* value) {
     *value = leaf_min_log2();
   } else if (key == MK_OPT_BFS_GROUP) {
     *value = bfs_group_option();
+  } else if (key == MK_OPT_LITERAL_STREAMS) {
+    *value = literal_streams_enabled() ? 1 : 0;
   } else {
     return fail(MK_ERR_ARG, "unknown option key");
   }
@@ -2524,6 +2763,7 @@ const char* mk_last_error(void) { return g_last_error.c_str(); }
 int mk_dgemm(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int64_t m,
              int64_t n, int64_t k, void* stream) {
   g_last_error.clear();
+  NvtxRange nvtx_(nvtx_label("mk_dgemm", 0, m, n, k, 0));
   if (m < 1 || n < 1 || k < 1) return fail(MK_ERR_DIMENSION, "extents must be positive");
   if (lda < k || ldb < n || ldc < n) return fail(MK_ERR_DIMENSION, "leading dimension smaller than the extent");
   if (overlaps(C, ldc, m, n, A, lda, m, k) || overlaps(C, ldc, m, n, B, ldb, k, n))
@@ -2548,6 +2788,7 @@ size_t mk_ozaki_workspace_bytes(int64_t m, int64_t n, int64_t k, int slices) {
 int mk_ozaki_dgemm(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int64_t m,
                    int64_t n, int64_t k, int slices, void* ws, size_t ws_bytes, void* stream) {
   g_last_error.clear();
+  NvtxRange nvtx_(nvtx_label("mk_ozaki_dgemm", 0, m, n, k, 0));
   if (m < 1 || n < 1 || k < 1) return fail(MK_ERR_DIMENSION, "extents must be positive");
   if (lda < k || ldb < n || ldc < n) return fail(MK_ERR_DIMENSION, "leading dimension smaller than the extent");
   if (overlaps(C, ldc, m, n, A, lda, m, k) || overlaps(C, ldc, m, n, B, ldb, k, n))
@@ -2607,6 +2848,7 @@ size_t mk_workspace_bytes(int algo, int64_t n, int levels) {
 int mk_strassen(int algo, double* A, int64_t lda, double* B, int64_t ldb, double* C, int64_t ldc, int64_t n,
                 int levels, void* ws, size_t ws_bytes, void* stream) {
   g_last_error.clear();
+  NvtxRange nvtx_(nvtx_label("mk_strassen", algo, n, n, n, levels));
   Engine e;
   MK_TRY(setup_square(e, algo, A, lda, B, ldb, C, ldc, n, levels));
   if (overlaps(C, ldc, n, n, A, lda, n, n) || overlaps(C, ldc, n, n, B, ldb, n, n))
@@ -2820,6 +3062,7 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
                      int64_t n, int levels, double* dA, double* dB, double* dC, int64_t ldd, void* ws,
                      size_t ws_bytes, void* stream, void* copy_stream) {
   g_last_error.clear();
+  NvtxRange nvtx_(nvtx_label("mk_strassen_host", algo, n, n, n, levels));
   if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_WINOGRAD_KNUTH_8CALL)
     return fail(MK_ERR_ARG, "the overlapped host path supports the fused algorithms");
   if (levels < 1) return fail(MK_ERR_ARG, "the overlapped host path needs at least one level");
@@ -3009,6 +3252,7 @@ int mk_strassen_partial(int algo, const double* A, int64_t lda, const double* B,
                         int64_t ldc, int64_t n, int levels, int first, int count, int panels, void* ws,
                         size_t ws_bytes, void* stream) {
   g_last_error.clear();
+  NvtxRange nvtx_(nvtx_label("mk_strassen_partial", algo, n, n, n, levels));
   if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_WINOGRAD_KNUTH_8CALL)
     return fail(MK_ERR_ARG, "partial products support the fused algorithms only");
   if (panels < 1 || ((n >> levels) % panels) != 0 || (((n >> levels) / panels) % 2) != 0)
@@ -3071,6 +3315,7 @@ int mk_multi_gpu_winograd(int algo, int ngpu, const int* devices, const double* 
                           int64_t ldb, double* C, int64_t ldc, int64_t n, int levels, void* const* ws,
                           const size_t* ws_bytes, void* const* streams) {
   g_last_error.clear();
+  NvtxRange nvtx_(nvtx_label("mk_multi_gpu_winograd", algo, n, n, n, levels));
   if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_WINOGRAD_KNUTH_8CALL)
     return fail(MK_ERR_ARG, "multi-GPU products support the fused algorithms only");
   if (ngpu < 1 || ngpu > 64 || !devices || !ws || !ws_bytes || !streams) return fail(MK_ERR_ARG, "bad device list");
@@ -3195,6 +3440,7 @@ int mk_strassen_partial_slabs(int algo, const double* A, int64_t lda, const doub
                               double* const* slabs, int nslabs, int64_t slab_rows, int64_t ldc, int64_t n, int levels,
                               int first, int count, int panels, void* ws, size_t ws_bytes, void* stream) {
   g_last_error.clear();
+  NvtxRange nvtx_(nvtx_label("mk_strassen_partial_slabs", algo, n, n, n, levels));
   if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_WINOGRAD_KNUTH_8CALL)
     return fail(MK_ERR_ARG, "partial products support the fused algorithms only");
   if (!slabs || nslabs < 1 || nslabs > MK_MAX_SLABS) return fail(MK_ERR_ARG, "1..8 output slabs");
@@ -3327,6 +3573,7 @@ size_t mk_rect_workspace_bytes(int algo, int64_t m, int64_t n, int64_t k, int le
 int mk_multiply_rect(int algo, const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                      int64_t m, int64_t n, int64_t k, int levels, void* ws, size_t ws_bytes, void* stream) {
   g_last_error.clear();
+  NvtxRange nvtx_(nvtx_label("mk_multiply_rect", algo, m, n, k, levels));
   if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_WINOGRAD_KNUTH_8CALL)
     return fail(MK_ERR_ARG, "rectangular driver supports the fused algorithms");
   if (m < 1 || n < 1 || k < 1) return fail(MK_ERR_DIMENSION, "extents must be positive");
@@ -3355,6 +3602,7 @@ int mk_multiply_rect_partial(int algo, const double* A, int64_t lda, const doubl
                              int64_t ldc, int64_t m, int64_t n, int64_t k, int levels, int first, int count,
                              int panels, void* ws, size_t ws_bytes, void* stream) {
   g_last_error.clear();
+  NvtxRange nvtx_(nvtx_label("mk_multiply_rect_partial", algo, m, n, k, levels));
   if (algo < MK_ALGO_STRASSEN || algo > MK_ALGO_WINOGRAD_KNUTH_8CALL)
     return fail(MK_ERR_ARG, "rectangular driver supports the fused algorithms");
   if (m < 1 || n < 1 || k < 1) return fail(MK_ERR_DIMENSION, "extents must be positive");

@@ -256,3 +256,18 @@ def test_ozaki_workspace_and_chunking_bounds():
     assert lib.mk_ozaki_workspace_bytes(4096, 4096, 4096, 4) < w8
     # K = 4096 fits one chunk at 8 slices; 3 x 4096 runs as three chunks of 4096 (same workspace)
     assert lib.mk_ozaki_workspace_bytes(4096, 4096, 3 * 4096, 8) == w8
+
+
+def test_baseline_operands_match_the_oracle_generators():
+    """bench.py's GPU legs draw their inputs from the package (metrics.baseline_operands); the
+    parity tests draw theirs from the oracle. Same seed, same draws, same bytes."""
+    from oracle import strassen_oracle as o
+    from paper_2309_00628_b200.metrics import BASELINE_SEED, ParameterError, baseline_operands
+
+    assert BASELINE_SEED == o.SEED
+    for cfg, scale in ((1, 1), (2, 4), (3, 32), (4, 64), (5, 20)):
+        a, b = baseline_operands(cfg, scale=scale)
+        ra, rb = o.operands(cfg, scale=scale)
+        assert a.dtype == np.float64 and np.array_equal(a, ra) and np.array_equal(b, rb)
+    with pytest.raises(ParameterError):
+        baseline_operands(6)

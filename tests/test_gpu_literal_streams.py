@@ -1,0 +1,87 @@
+"""Side streams of the literal schedules (mk_engine.cu LitStreams / lit_wait): block additions of
+Table 2 / Table 3 (reference schedules.py:62-112) that the next product does not depend on are
+issued on side streams, ordered against the products by block-level hazard tracking. The steps,
+their operands and their order per block are unchanged, so results -- and, for the in-place
+schedule, the clobbered operands -- must be bit-identical to the one-stream execution, on real
+data, at every depth, call after call (a missed hazard shows up as a differing or varying bit)."""
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2309_00628_b200 as pk
+from paper_2309_00628_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+
+def _set_streams(on: bool):
+    lib = _lib.load(required=True)
+    _lib.check(lib.mk_set_option(_lib.MK_OPT_LITERAL_STREAMS, 1 if on else 0), "mk_set_option")
+
+
+def _run(fn, a, b, pol):
+    """One call on device copies; returns (C, A after, B after)."""
+    da, db = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    dc = torch.full_like(da, float("nan"))
+    fn(pk.Matrix(da), pk.Matrix(db), pk.Matrix(dc), pol)
+    torch.cuda.synchronize()
+    return dc.cpu().numpy(), da.cpu().numpy(), db.cpu().numpy()
+
+
+def test_option_round_trip():
+    lib = _lib.load(required=True)
+    v = ctypes.c_int(-1)
+    assert lib.mk_get_option(_lib.MK_OPT_LITERAL_STREAMS, ctypes.byref(v)) == 0 and v.value == 1
+    try:
+        _set_streams(False)
+        assert lib.mk_get_option(_lib.MK_OPT_LITERAL_STREAMS, ctypes.byref(v)) == 0 and v.value == 0
+    finally:
+        _set_streams(True)
+    assert lib.mk_get_option(_lib.MK_OPT_LITERAL_STREAMS, ctypes.byref(v)) == 0 and v.value == 1
+
+
+@pytest.mark.parametrize("name", ["in-place", "two-temp"])
+@pytest.mark.parametrize("n,cut", [(256, 128), (512, 128), (512, 64), (1024, 128), (2048, 256), (2048, 1024), (256, 32)])
+def test_side_streams_bit_identical_to_one_stream(name, n, cut):
+    fn = pk.in_place_winograd if name == "in-place" else pk.two_temp_winograd
+    r = np.random.default_rng(n * 7 + cut)
+    a, b = r.standard_normal((n, n)), r.standard_normal((n, n))
+    pol = pk.BasePolicy.naive_cutoff(cut)
+    try:
+        _set_streams(False)
+        ref = _run(fn, a, b, pol)
+    finally:
+        _set_streams(True)
+    for rep in range(3):
+        got = _run(fn, a, b, pol)
+        for x, y, what in zip(got, ref, ("C", "A after the call", "B after the call")):
+            assert np.array_equal(x, y, equal_nan=True), (name, n, cut, rep, what)
+    if name == "two-temp":  # operands untouched (schedules.py:332-341)
+        assert np.array_equal(ref[1], a) and np.array_equal(ref[2], b)
+    assert np.max(np.abs(ref[0] - a @ b)) < 1e-9 * n
+
+
+@pytest.mark.parametrize("name", ["in-place", "two-temp"])
+def test_side_streams_exact_on_integers_and_on_a_user_stream(name):
+    """Integer data, 4 levels, issued on a non-default torch stream with work queued before and
+    after on that stream: the fork / join around the side streams orders both."""
+    fn = pk.in_place_winograd if name == "in-place" else pk.two_temp_winograd
+    n = 1024
+    r = np.random.default_rng(11)
+    a = r.integers(-8, 9, (n, n)).astype(np.float64)
+    b = r.integers(-8, 9, (n, n)).astype(np.float64)
+    want = a @ b
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        da = torch.from_numpy(a).cuda(non_blocking=True) * 1.0  # produced on the same stream
+        db = torch.from_numpy(b).cuda(non_blocking=True) * 1.0
+        dc = torch.zeros_like(da)
+        for _ in range(4):
+            xa, xb = da.clone(), db.clone()
+            fn(pk.Matrix(xa), pk.Matrix(xb), pk.Matrix(dc), pk.BasePolicy.naive_cutoff(64))
+            out = dc * 1.0  # consumed on the same stream, no synchronisation in between
+            dc.zero_()
+    s.synchronize()
+    assert np.array_equal(out.cpu().numpy(), want)

@@ -7,9 +7,9 @@ import torch
 
 sys.path.insert(0, ".")
 import paper_2309_00628_b200 as pk  # noqa: E402
-from oracle import strassen_oracle as o  # noqa: E402
+from paper_2309_00628_b200.metrics import baseline_operands  # noqa: E402
 
-a, b = o.operands(4)
+a, b = baseline_operands(4)
 da, db = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
 del a, b
 A, B = pk.Matrix(da), pk.Matrix(db)
