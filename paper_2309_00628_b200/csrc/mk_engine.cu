@@ -750,14 +750,15 @@ struct Engine {
       lit_ops[s].clear();
       for (int t = 0; t < kLitStreams; ++t) lit_seen[s][t] = 0;
     }
-    // side streams start after prior work on the caller's stream
+    // a side stream starts after the work queued on the caller's stream before this call (it
+    // waits for this event the first time it is used; unused side streams are never touched)
     MK_CUDA_TRY(cudaEventRecord(lit->fork, st));
-    for (int s = 1; s < kLitStreams; ++s) MK_CUDA_TRY(cudaStreamWaitEvent(lit_stream(s), lit->fork, 0));
     return MK_OK;
   }
   // before launching an operation on stream s: wait for the latest conflicting operation of
   // every other stream that s has not yet waited for
   int lit_wait(int s, const LitOp& op) {
+    if (s != 0 && lit_ops[s].empty()) MK_CUDA_TRY(cudaStreamWaitEvent(lit_stream(s), lit->fork, 0));
     for (int t = 0; t < kLitStreams; ++t) {
       if (t == s) continue;
       const std::vector<LitOp>& ops = lit_ops[t];
