@@ -77,7 +77,8 @@ def config(args, levels, world=1):
         "workload": f"BASELINE cfg4: n={args.n} standard-normal FP64, {args.algo}, naive_cutoff({args.cutoff}) "
                     f"-> {levels} levels ({7 ** levels} DMMA leaf GEMMs)",
         "n": args.n, "cutoff": args.cutoff, "levels": levels, "algo": args.algo,
-        "l2": "inputs 2 GiB each > 126 MB L2 (no flush needed)",
+        "l2": (f"inputs {args.n * args.n * 8 / 2 ** 30:g} GiB each > 126 MB L2 (no flush needed)"
+               if args.n * args.n * 8 > 126e6 else "inputs fit in L2 (non-default order: no flush between steps)"),
     }
     if world > 1:
         c["parallelism"] = (f"leaf row panels over {world} ranks; " +
