@@ -530,13 +530,14 @@ static bool lit_conflict(const LitRegion& a, const LitRegion& b) {
   return a.p < b1 && b.p < a1;
 }
 constexpr int kLitStreams = 4;    // the caller's stream + one side stream per depth (deeper ones share the last)
-constexpr int kLitEvents = 1024;  // event ring per stream (a stale slot waits for a later operation: still correct)
+constexpr int kLitEvents = 256;   // event ring per stream (a stale slot waits for a later operation: still correct)
 struct LitStreams {               // per host thread and device, created once
   cudaStream_t side[kLitStreams - 1] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev[kLitStreams][kLitEvents] = {};
   cudaEvent_t fork = nullptr;
   bool ok = false;
-};
+};  // never destroyed: a thread's streams and events live until the process exits (no CUDA calls from
+    // thread-exit or static destructors, which may run after the runtime has shut down)
 static LitStreams* lit_streams() {
   static thread_local std::map<int, LitStreams> per_dev;
   int dev = 0;
