@@ -78,9 +78,14 @@ int mk_version(void);
  *   depend on are issued on internal side streams, ordered by block-level hazard tracking, and
  *   run beside the leaf products (default); 0 = every step on the caller's stream. Same steps,
  *   same operands, bit-identical results either way; the side streams are joined into `stream`
- *   before the call returns. */
+ *   before the call returns.
+ * MK_OPT_HOST_GROUP (mk_strassen_host, 2 levels, DMMA leaves): the top-level products between the
+ *   first few and the last run as one grouped breadth-first pass once every upload has landed
+ *   (instead of child by child behind the sub-block uploads). -1 = auto (the pass starts after as
+ *   many products as outlast the uploads: 3 at n = 16384, none at n <= 8192), 0 = off, k in 1..6 =
+ *   start after k products. Results differ only in the order C's partial sums are added. */
 enum mk_option { MK_OPT_FUSE_PREADDS = 1, MK_OPT_PLAN = 2, MK_OPT_LITERAL_TAIL = 3, MK_OPT_LEAF_SLICES = 4,
-                 MK_OPT_LEAF_MIN_LOG2 = 5, MK_OPT_BFS_GROUP = 6, MK_OPT_LITERAL_STREAMS = 7 };
+                 MK_OPT_LEAF_MIN_LOG2 = 5, MK_OPT_BFS_GROUP = 6, MK_OPT_LITERAL_STREAMS = 7, MK_OPT_HOST_GROUP = 8 };
 int mk_set_option(int key, int value);
 int mk_get_option(int key, int* value);
 /* Calling-thread override of MK_OPT_PLAN / MK_OPT_LITERAL_TAIL (value -1 removes it). Applies to

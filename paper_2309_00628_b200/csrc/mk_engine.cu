@@ -598,6 +598,14 @@ static const LitCritical& lit_critical(const SchedStep* steps) {
   return cache.emplace(steps, c).first->second;
 }
 
+static std::atomic<int> g_host_group{-2};  // -2: unset (env MK_HOST_GROUP), -1 auto, 0 off, k > 0 forced
+static int host_group_option() {
+  if (g_host_group == -2) {
+    const char* s = getenv("MK_HOST_GROUP");
+    g_host_group = s ? std::max(-1, atoi(s)) : -1;
+  }
+  return g_host_group;
+}
 static std::atomic<int> g_literal_streams{-1};  // -1: unset (env MK_LITERAL_STREAMS), 0/1 explicit
 static bool literal_streams_enabled() {
   if (g_literal_streams < 0) {
@@ -1150,15 +1158,56 @@ struct Engine {
       if (!dry && !no_launch && ev) MK_CUDA_TRY(cudaEventRecord(ev, st));
       return MK_OK;
     };
+    // a whole operand quadrant (0..3: A11..A22, 4..7: B11..B22) has landed. In sub-block mode the
+    // per-sub-block events are the authoritative ones (staged pageable uploads alternate between
+    // two copy streams, so an event recorded on one of them does not cover a whole quadrant)
+    auto wait_quadrant = [&](int qq) -> int {
+      if (sub_in == nullptr) return wait_ev(in_ev[qq]);
+      for (int sb = 0; sb < 4; ++sb) MK_TRY(wait_ev(sub_in[4 * qq + sb]));
+      return MK_OK;
+    };
     const bool inner_bfs = L >= 3 && !fuse_preadds && !plan_dfs();  // depth-first on request
+    int glo = 0, ghi = 0;
+    host_group_range(np, sub_in != nullptr, &glo, &ghi);
     for (int i = 0; i < np; ++i) {
+      if (i == glo && ghi > glo) {  // the middle products as one grouped breadth-first pass
+        const std::vector<int> grp(order.begin() + glo, order.begin() + ghi);
+        for (int p : grp)
+          for (int q = 0; q < 4; ++q) {
+            if (co->a[p][q]) MK_TRY(wait_quadrant(q));
+            if (co->b[p][q]) MK_TRY(wait_quadrant(4 + q));
+          }
+        bool touched[4];
+        for (int q = 0; q < 4; ++q) {
+          const int s = state(BASE_C, (q >> 1) * h, (q & 1) * h, h, h);
+          if (s == 2) return fail(MK_ERR_ARG, "internal: partially written C quadrant before a grouped pass");
+          touched[q] = s == 1;
+        }
+        const size_t mark = ws_used;
+        const int nb_mark = nbases;
+        MK_TRY(bfs(L, n, n, n, A0[0], B0[0], C0[0], &grp, touched));
+        ws_used = mark;
+        while (nbases > nb_mark) {
+          --nbases;
+          written.pop_back();
+          cell_rows.pop_back();
+          cell_cols.pop_back();
+        }
+        for (int q = 0; q < 4; ++q)
+          if (touched[q]) set_state(BASE_C, (q >> 1) * h, (q & 1) * h, h, h, 1);
+        if (!dry && !no_launch) host_trace("grouped pass (" + std::to_string(ghi - glo) + " products) done", st);
+        for (int q = 0; q < 4; ++q)
+          if (last[q] >= glo && last[q] < ghi) MK_TRY(record_ev(out_ev[q]));
+        i = ghi - 1;
+        continue;
+      }
       const int p = order[i];
       const bool split = !inner_bfs && sub_in != nullptr && L >= 2 && split_fits(p);
       const bool tail = split && i == np - 1 && i != 0 && sub_out != nullptr;
       if (!split) {
         for (int q = 0; q < 4; ++q) {
-          if (co->a[p][q]) MK_TRY(wait_ev(in_ev[q]));
-          if (co->b[p][q]) MK_TRY(wait_ev(in_ev[4 + q]));
+          if (co->a[p][q]) MK_TRY(wait_quadrant(q));
+          if (co->b[p][q]) MK_TRY(wait_quadrant(4 + q));
         }
         if (inner_bfs)
           MK_TRY(top_product_bfs(p, A0, B0, C0, h));
@@ -1265,6 +1314,34 @@ struct Engine {
     }
     return MK_OK;
   }
+  // Sub-block mode (L = 2, FP64 tensor-core leaves): the top-level products between the first few and
+  // the last run as ONE grouped breadth-first pass (the device-resident plan's pass: two-level
+  // operand transforms from A and B, batched leaf launches, one post-addition into C) instead of
+  // child by child -- by then every upload has landed (three products of compute outlast the
+  // 4 GiB of uploads), so the sub-block pipeline has nothing left to hide, while its operand sums
+  // between the leaves cost ~1.9 ms per product against ~0.6 ms in a pass. The last product stays
+  // child by child so that C's last quadrant goes home sub-block by sub-block. Positions
+  // [lo, hi) of `order`; lo == hi: none. MK_OPT_HOST_GROUP / env MK_HOST_GROUP: -1 auto, 0 off,
+  // k > 0 forces the pass to start after k products (tests).
+  void host_group_range(int np, bool sub_mode, int* lo, int* hi) const {
+    const int opt = host_group_option();  // -1 auto, 0 off, k > 0: the pass starts after k products
+    *lo = *hi = 0;
+    if (opt == 0 || !sub_mode || L != 2 || fuse_preadds || plan_dfs() || np < 6) return;
+    if (ozaki_leaf_for(leaf_m, leaf_n, leaf_k)) return;  // INT8 leaves: products finish before their uploads
+    // The pass waits for whole quadrants, so it must not start before the uploads end: the
+    // child-by-child products ahead of it have to outlast the 8 quadrant uploads. One product is
+    // 14 (n/4)^3 flops at ~34 TF/s, one quadrant 2 n^2 bytes at ~55 GB/s (this pool's PCIe rate):
+    // 1.77e-4 n quadrant-times per product -- 2.9 at n = 16384 (3 products ahead), 1.45 at
+    // n = 8192 (6: no pass; measured 38.7 ms with a pass after 3 against 38.0 without).
+    const double kprod = 1.7694e-4 * (double)n;
+    int ahead = opt > 0 ? opt : std::max(2, (int)std::ceil(8.0 / kprod));
+    // at most 4 products per pass: its root post-addition reads the pass's products plus C's four
+    // quadrants (MK_XFORM_MAX sources)
+    ahead = std::max(ahead, np - 1 - 4);
+    if (np - 1 - ahead < 2) return;
+    *lo = ahead;
+    *hi = np - 1;
+  }
   // A top-level product can run child by child when its destination fan-out fits the epilogue
   // without a materialised product (fused_child's own test).
   bool split_fits(int p) const {
@@ -1284,8 +1361,12 @@ struct Engine {
         ups.emplace_back(q, sb);
       }
     };
-    for (int p : order) {
-      const bool split = split_fits(p) && L < 3;  // fused_overlapped splits at L = 2 only
+    int glo = 0, ghi = 0;
+    host_group_range((int)order.size(), true, &glo, &ghi);
+    for (size_t pi = 0; pi < order.size(); ++pi) {
+      const int p = order[pi];
+      // fused_overlapped splits at L = 2 only; the grouped middle pass reads whole quadrants
+      const bool split = split_fits(p) && L < 3 && !((int)pi >= glo && (int)pi < ghi);
       const std::vector<int>& kids = (p == order[0] && !head_children.empty()) ? head_children : order;
       for (int pc : kids) {
         for (int side = 0; side < 2; ++side) {
@@ -2719,6 +2800,11 @@ int mk_set_option(int key, int value) {
     g_literal_streams = value ? 1 : 0;
     return MK_OK;
   }
+  if (key == MK_OPT_HOST_GROUP) {
+    if (value < -1 || value > 6) return fail(MK_ERR_ARG, "MK_OPT_HOST_GROUP takes -1 (auto), 0 (off) or 1..6");
+    g_host_group = value;
+    return MK_OK;
+  }
   return fail(MK_ERR_ARG, "unknown option key");
 }
 
@@ -2754,6 +2840,8 @@ int mk_get_option(int key, int* value) {
     *value = bfs_group_option();
   } else if (key == MK_OPT_LITERAL_STREAMS) {
     *value = literal_streams_enabled() ? 1 : 0;
+  } else if (key == MK_OPT_HOST_GROUP) {
+    *value = host_group_option();
   } else {
     return fail(MK_ERR_ARG, "unknown option key");
   }
