@@ -36,7 +36,7 @@ __global__ void combine_kernel(const __grid_constant__ CombineArgs a) {
     if (VEC) {
       double2 acc = make_double2(0.0, 0.0);
       for (int t = 0; t < a.nsrc; ++t) {
-        const double2 v = __ldg(reinterpret_cast<const double2*>(a.src[t] + r * a.lds[t] + c));
+        const double2 v = *reinterpret_cast<const double2*>(a.src[t] + r * a.lds[t] + c);  // dst may be a source
         acc.x = fma(a.sign[t], v.x, acc.x);
         acc.y = fma(a.sign[t], v.y, acc.y);
       }
@@ -69,8 +69,9 @@ __global__ void __launch_bounds__(256) combine2_kernel(const __grid_constant__ C
       if (idx < total) {
         const uint32_t r = idx / cv;
         const int64_t c = (int64_t)(idx - r * cv) * 2;
-        x[k] = __ldg(reinterpret_cast<const double2*>(a.src[0] + (int64_t)r * a.lds[0] + c));
-        y[k] = __ldg(reinterpret_cast<const double2*>(a.src[1] + (int64_t)r * a.lds[1] + c));
+        // plain loads, not ld.global.nc: dst may be one of the sources (Table 3 stores S1 over A21)
+        x[k] = *reinterpret_cast<const double2*>(a.src[0] + (int64_t)r * a.lds[0] + c);
+        y[k] = *reinterpret_cast<const double2*>(a.src[1] + (int64_t)r * a.lds[1] + c);
         off[k] = (int64_t)r * a.ldd + c;
       }
     }
