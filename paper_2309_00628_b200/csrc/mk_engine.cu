@@ -606,6 +606,15 @@ static int host_group_option() {
   }
   return g_host_group;
 }
+constexpr int kTailPartsMax = 4;
+static int tail_row_parts() {  // env MK_HOST_TAIL_ROWS: row ranges of the host path's last leaf (1 = one launch)
+  static const int parts = [] {
+    const char* s = getenv("MK_HOST_TAIL_ROWS");
+    const int v = s ? atoi(s) : 2;
+    return v < 1 ? 1 : (v > kTailPartsMax ? kTailPartsMax : v);
+  }();
+  return parts;
+}
 static std::atomic<int> g_literal_streams{-1};  // -1: unset (env MK_LITERAL_STREAMS), 0/1 explicit
 static bool literal_streams_enabled() {
   if (g_literal_streams < 0) {
@@ -655,6 +664,13 @@ struct Engine {
   // rectangular driver, pipelined plan: BASE_C is the caller's unpadded C (only the epilogue writes
   // it), clipped to clip_m x clip_n; 0 = BASE_C spans the padded extents
   int64_t clip_m = 0, clip_n = 0;
+  // Overlapped host path, last child of the last top-level product: the leaf runs as row_parts
+  // launches over contiguous row ranges, row_part_done(part) after each, so that the last C
+  // sub-block goes home in halves while the second half still computes (tail_halved: it did)
+  int row_parts = 1;
+  std::function<int(int)> row_part_done;
+  bool tail_halved = false;
+  cudaEvent_t* tail_half_ev = nullptr;  // row_parts events of the real run (null in sizing / recording passes)
   // fused multi-GPU reduce-scatter (mk_strassen_partial_slabs): C rows routed to owner slabs
   int nslab = 0;
   int64_t slab_rows = 0;
@@ -1012,6 +1028,26 @@ struct Engine {
     return MK_OK;
   }
 
+  // One leaf as row_parts launches over contiguous row ranges (same tiles, same k order: the
+  // same bits). Only when every destination block already holds a partial sum (each part then
+  // accumulates; the first-writer state is tracked per leaf cell, not per row range) and the
+  // ranges are whole tile rows; otherwise the leaf runs as one launch.
+  int product_in_row_parts(const Lin& X, const Lin& Y, const Lin& D, int64_t M, int64_t N, int64_t K) {
+    bool ok = M % ((int64_t)row_parts * MK_BM) == 0;
+    for (const Blk& d : D) ok = ok && state(d.base, d.row, d.col, M, N) == 1;
+    if (!ok) return product(X, Y, D, M, N, K);
+    const int64_t rows = M / row_parts;
+    for (int part = 0; part < row_parts; ++part) {
+      Lin Xs = X, Ds = D;
+      for (Blk& t : Xs) t.row += part * rows;
+      for (Blk& t : Ds) t.row += part * rows;
+      MK_TRY(product(Xs, Y, Ds, rows, N, K));
+      if (row_part_done) MK_TRY(row_part_done(part));
+    }
+    tail_halved = true;
+    return MK_OK;
+  }
+
   static Lin kron(const Lin& X, const int* coef, int64_t hr, int64_t hc) {
     Lin out;
     for (const Blk& b : X)
@@ -1045,6 +1081,7 @@ struct Engine {
     if (remaining == 0) {
       const int64_t u0 = leaf_counter;
       leaf_counter += panels;
+      if (leaf_count < 0 && row_parts > 1) return product_in_row_parts(X, Y, D, M, N, K);
       if (leaf_count < 0 || panels == 1) return product(X, Y, D, M, N, K);
       // only this rank's contiguous row panels of the leaf: shift operand and destination rows
       const int64_t lo = std::max(u0, leaf_first) - u0, hi = std::min(u0 + panels, leaf_first + leaf_count) - u0;
@@ -1244,7 +1281,14 @@ struct Engine {
               formed[side][sb] = true;
             }
           }
-          MK_TRY(fused_child(L - 1, pc, Op[0], Op[1], Dp, h, h, h, 1));
+          if (tail && j == np - 1 && tail_row_parts() > 1) {  // the very last leaf: in row ranges
+            row_parts = tail_row_parts();
+            row_part_done = [&](int part) { return record_ev(tail_half_ev ? tail_half_ev[part] : nullptr); };
+          }
+          const int rc_child = fused_child(L - 1, pc, Op[0], Op[1], Dp, h, h, h, 1);
+          row_parts = 1;
+          row_part_done = nullptr;
+          MK_TRY(rc_child);
           if (!dry && !no_launch) host_trace("P" + std::to_string(p + 1) + "." + std::to_string(pc + 1) + " done", st);
           if (tail)
             for (int q = 0; q < 4; ++q)
@@ -3212,10 +3256,11 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
   const std::vector<int> order = cached_order(algo, &up);
   const int64_t h = n / 2, hh = h / 2;
   // events: 8 quadrant uploads, 4 quadrant completions, start, 32 sub-block uploads, 16 sub-block completions
-  constexpr int kEv = 61;
+  constexpr int kEv = 61 + kTailPartsMax;  // ... and the row ranges of the last leaf
   cudaEvent_t ev[kEv];
   for (int i = 0; i < kEv; ++i) MK_CUDA_TRY(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
   cudaEvent_t *in_ev = ev, *out_ev = ev + 8, start = ev[12], *sub_in = ev + 13, *sub_out = ev + 45;
+  e.tail_half_ev = ev + 61;
   int rc = MK_OK;
   auto quad_ptr = [&](double* base, int64_t ld, int q) { return base + ((q >> 1) * h) * ld + (q & 1) * h; };
   auto sub_ptr = [&](double* base, int64_t ld, int q, int s) {
@@ -3230,18 +3275,19 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
   const bool staged = rc == MK_OK && (page_a || page_b || page_c) && stg.prepare(cp);
   // H2D of an r x r block (ready -> event `done`), or D2H once `ready` has completed
   auto copy = [&](double* dst, int64_t dld, const double* src, int64_t sld, int64_t r, cudaMemcpyKind kind,
-                  cudaEvent_t done, const char* what, cudaEvent_t ready = nullptr) {
+                  cudaEvent_t done, const char* what, cudaEvent_t ready = nullptr, int64_t nrows = -1) {
     if (rc != MK_OK) return;
+    const int64_t rows_ = nrows < 0 ? r : nrows;  // r columns by rows_ rows (square by default)
     const bool up = kind == cudaMemcpyHostToDevice;
     const bool via = staged && (up ? ((src >= hA && page_a && (src < hA + (size_t)lda * n)) ||
                                       (src >= hB && page_b && (src < hB + (size_t)ldb * n)))
                                    : page_c);
     cudaError_t ce = cudaSuccess;
     if (via) {
-      ce = up ? stg.upload(dst, dld, src, sld, r, r, done) : stg.download(dst, dld, src, sld, r, r, ready);
+      ce = up ? stg.upload(dst, dld, src, sld, rows_, r, done) : stg.download(dst, dld, src, sld, rows_, r, ready);
     } else {
       if (ready) ce = cudaStreamWaitEvent(cp, ready, 0);
-      if (ce == cudaSuccess) ce = cudaMemcpy2DAsync(dst, dld * 8, src, sld * 8, r * 8, r, kind, cp);
+      if (ce == cudaSuccess) ce = cudaMemcpy2DAsync(dst, dld * 8, src, sld * 8, r * 8, rows_, kind, cp);
       if (ce == cudaSuccess && done) ce = cudaEventRecord(done, cp);
     }
     if (ce != cudaSuccess) rc = fail(MK_ERR_CUDA, std::string(what) + cudaGetErrorString(ce));
@@ -3289,9 +3335,18 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
              out_ev[q]);
         continue;
       }
-      for (int s : ss)
+      for (int s : ss) {
+        if (e.tail_halved && child_last[s] == (int)order.size() - 1) {  // finished by the last leaf: row range by row range
+          const int parts = tail_row_parts();
+          const int64_t pr = hh / parts;
+          for (int part = 0; part < parts; ++part)
+            copy(sub_ptr(hC, ldc, q, s) + part * pr * ldc, ldc, sub_ptr(dC, ldd, q, s) + part * pr * ldd, ldd, hh,
+                 cudaMemcpyDeviceToHost, nullptr, "download: ", e.tail_half_ev[part], pr);
+          continue;
+        }
         copy(sub_ptr(hC, ldc, q, s), ldc, sub_ptr(dC, ldd, q, s), ldd, hh, cudaMemcpyDeviceToHost, nullptr,
              "download: ", sub_out[4 * q + s]);
+      }
     }
   }
   host_trace("downloads done", cp);
