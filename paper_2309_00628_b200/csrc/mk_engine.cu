@@ -1440,9 +1440,9 @@ struct Engine {
     }
     if (remaining == 0 || (remaining == 1 && fuse_preadds)) {
       if (lit) MK_TRY(lit_wait(0, prod));
-      if (lit) host_trace("s0 leaf B", st);
+      if (lit && host_trace_on()) host_trace("s0 leaf B", st);
       MK_TRY(fused(remaining, Lin{X}, Lin{Y}, Lin{D}, s, s, s, L - remaining));
-      if (lit) host_trace("s0 leaf E", st);
+      if (lit && host_trace_on()) host_trace("s0 leaf E", st);
       if (lit) MK_TRY(lit_done(0, prod));
       return MK_OK;
     }
@@ -1507,10 +1507,11 @@ struct Engine {
           op.rd[1] = region(r, h, h);
           op.wr = region(d, h, h);
           MK_TRY(lit_wait(sid, op));
-          const std::string tag = "s" + std::to_string(sid) + " " + st_.symbol + " d" + std::to_string(L - remaining);
-          host_trace(tag + " B", lit_stream(sid));
+          const bool tr = host_trace_on();
+          const std::string tag = tr ? "s" + std::to_string(sid) + " " + st_.symbol + " d" + std::to_string(L - remaining) : "";
+          if (tr) host_trace(tag + " B", lit_stream(sid));
           MK_TRY(combine(d, terms, h, h, lit_stream(sid)));
-          host_trace(tag + " E", lit_stream(sid));
+          if (tr) host_trace(tag + " E", lit_stream(sid));
           MK_TRY(lit_done(sid, op));
         }
         set_state(d.base, d.row, d.col, h, h, 1);
