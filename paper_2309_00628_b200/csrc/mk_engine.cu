@@ -556,8 +556,10 @@ static LitStreams* lit_streams() {
 }
 // Which additions of a 22-step table stay on the caller's stream: those on a dependency chain
 // (RAW / WAR / WAW over storage locations) to the next product, and the ones after the last
-// product. Every other addition can run beside the next product. Table 3: S3, T1, T3, T4, U5 stay;
-// S1, S2, T2, S4, U2, U1, U4, U3, U6, U7 go to a side stream.
+// product. Every other addition can run beside the next
+// product; so can the smaller of two independent chains to the same product. Table 3: T1, T3, T4,
+// U5 stay; S3, S1, S2, T2, S4, U2, U1, U4, U3, U6, U7 go to a side stream. Table 2: the T sums and
+// the U chain stay; S3, S1, S2, U7 and T4 go.
 struct LitCritical {
   bool main[22];
 };
@@ -583,8 +585,39 @@ static const LitCritical& lit_critical(const SchedStep* steps) {
   LitCritical c{};
   int end = 22;  // the next product of the segment being swept (22: none follows)
   std::vector<int> chain;
+  // Additions on the way to one product that do not depend on each other (S3 and T1 -> T3 before
+  // P7; Table 2's S_i and T_i) need not queue behind one another either: of the connected
+  // components of the conflict graph among a segment's critical additions, the largest (ties: the
+  // one ending last) stays on the caller's stream and the others go to the side stream; the
+  // product then waits for their events.
+  auto split_components = [&](const std::vector<int>& seg) {
+    std::vector<int> adds;
+    for (int j : seg)
+      if (steps[j].op != '*') adds.push_back(j);
+    if (adds.size() < 2) return;
+    std::sort(adds.begin(), adds.end());
+    std::map<int, int> comp;
+    for (int a : adds) comp[a] = a;
+    auto find = [&](int x) {
+      while (comp[x] != x) x = comp[x];
+      return x;
+    };
+    for (int a : adds)
+      for (int b : adds)
+        if (a < b && conflict(a, b)) comp[find(a)] = find(b);
+    std::map<int, std::vector<int>> groups;
+    for (int a : adds) groups[find(a)].push_back(a);
+    const std::vector<int>* keep = nullptr;
+    for (const auto& g : groups)
+      if (!keep || g.second.size() > keep->size() || (g.second.size() == keep->size() && g.second.back() > keep->back()))
+        keep = &g.second;
+    for (const auto& g : groups)
+      if (&g.second != keep)
+        for (int a : g.second) c.main[a] = false;
+  };
   for (int i = 21; i >= 0; --i) {
     if (steps[i].op == '*') {
+      if (end != 22) split_components(chain);
       end = i;
       chain.assign(1, i);
       c.main[i] = true;
@@ -595,6 +628,7 @@ static const LitCritical& lit_critical(const SchedStep* steps) {
     c.main[i] = m;
     if (m && end != 22) chain.push_back(i);
   }
+  if (end != 22) split_components(chain);
   return cache.emplace(steps, c).first->second;
 }
 
