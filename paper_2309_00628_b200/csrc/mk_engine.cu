@@ -503,7 +503,7 @@ static bool table_ring_copy(void* dev_dst, const void* host, size_t bytes, cudaS
 // leaf products (n = 8192, 3 levels: 855 additions, ~7 ms of 35). Most of them do not feed the
 // next product (Table 3: S2 can run under P7, T2 under P5, S4 under P6, U2 under P2, U1..U7 under
 // P3), and a one-at-a-time leaf launch of a literal schedule leaves SMs idle (128 narrow tiles on
-// 148 SMs). So additions that the next product does not read are issued on side streams (one per
+// 148 SMs). So additions that the next product does not read are issued on side streams (two per
 // recursion depth), ordered against the other streams by block-level hazard tracking: every
 // issued operation records its read and write rectangles and an event; an operation first waits
 // for the latest conflicting (RAW / WAR / WAW) operation of every other stream. Same program,
@@ -529,10 +529,10 @@ static bool lit_conflict(const LitRegion& a, const LitRegion& b) {
   const double* b1 = b.p + (b.rows - 1) * b.ld + b.cols;
   return a.p < b1 && b.p < a1;
 }
-constexpr int kLitStreams = 4;    // the caller's stream + one side stream per depth (deeper ones share the last)
+constexpr int kLitStreams = 7;    // the caller's stream + two side streams per depth (deeper ones share the last pair)
 constexpr int kLitEvents = 256;   // event ring per stream (a stale slot waits for a later operation: still correct)
 struct LitStreams {               // per host thread and device, created once
-  cudaStream_t side[kLitStreams - 1] = {nullptr, nullptr, nullptr};
+  cudaStream_t side[kLitStreams - 1] = {};
   cudaEvent_t ev[kLitStreams][kLitEvents] = {};
   cudaEvent_t fork = nullptr;
   bool ok = false;
@@ -794,6 +794,30 @@ struct Engine {
   LitStreams* lit = nullptr;  // non-null while a literal schedule issues on several streams
   std::vector<LitOp> lit_ops[kLitStreams];
   size_t lit_seen[kLitStreams][kLitStreams] = {};  // [s][t]: operations of stream t that stream s has waited for
+  uint64_t lit_seq = 0, lit_last_seq[kLitStreams] = {};  // issue order (which side stream has been idle longer)
+  static bool lit_dual() {  // MK_LIT_DUAL=0: one side stream per depth
+    static const bool on = [] {
+      const char* e = getenv("MK_LIT_DUAL");
+      return !(e && e[0] == '0');
+    }();
+    return on;
+  }
+  // The side stream for an addition at `depth`: of the depth's two, the one whose latest operation
+  // this one depends on (it would have to wait for it anyway), else the one idle for longer -- so
+  // independent additions (U1 beside U4 -> U3 -> U6 -> U7) do not queue behind each other.
+  int lit_side_for(int depth, const LitOp& op) const {
+    const int a = 1 + 2 * std::min(depth, (kLitStreams - 1) / 2 - 1), b = a + 1;
+    if (!lit_dual()) return a;
+    auto dep = [&](int t) {
+      if (lit_ops[t].empty()) return false;
+      const LitOp& o = lit_ops[t].back();
+      return lit_conflict(op.wr, o.wr) || lit_conflict(op.wr, o.rd[0]) || lit_conflict(op.wr, o.rd[1]) ||
+             lit_conflict(op.rd[0], o.wr) || lit_conflict(op.rd[1], o.wr);
+    };
+    if (dep(a)) return a;
+    if (dep(b)) return b;
+    return lit_last_seq[a] <= lit_last_seq[b] ? a : b;
+  }
   cudaStream_t lit_stream(int s) const { return s == 0 ? st : lit->side[s - 1]; }
   LitRegion region(const Blk& b, int64_t rows, int64_t cols) const {
     return LitRegion{bases[b.base].ptr + b.row * bases[b.base].ld + b.col, bases[b.base].ld, rows, cols};
@@ -837,6 +861,7 @@ struct Engine {
   int lit_done(int s, const LitOp& op) {  // after the launch
     MK_CUDA_TRY(cudaEventRecord(lit->ev[s][lit_ops[s].size() % kLitEvents], lit_stream(s)));
     lit_ops[s].push_back(op);
+    lit_last_seq[s] = ++lit_seq;
     return MK_OK;
   }
   int lit_end() {  // the caller's stream waits for the side streams
@@ -1535,11 +1560,11 @@ struct Engine {
         } else {
           // an addition the next product depends on (or one after the node's last product) stays
           // on the caller's stream; every other one goes to this depth's side stream
-          const int sid = lit_critical(steps).main[i] ? 0 : 1 + std::min(L - remaining, kLitStreams - 2);
           LitOp op;
           op.rd[0] = region(l, h, h);
           op.rd[1] = region(r, h, h);
           op.wr = region(d, h, h);
+          const int sid = lit_critical(steps).main[i] ? 0 : lit_side_for(L - remaining, op);
           MK_TRY(lit_wait(sid, op));
           const bool tr = host_trace_on();
           const std::string tag = tr ? "s" + std::to_string(sid) + " " + st_.symbol + " d" + std::to_string(L - remaining) : "";
