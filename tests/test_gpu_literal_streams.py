@@ -85,3 +85,38 @@ def test_side_streams_exact_on_integers_and_on_a_user_stream(name):
             dc.zero_()
     s.synchronize()
     assert np.array_equal(out.cpu().numpy(), want)
+
+
+def test_side_streams_from_two_host_threads():
+    """Each host thread owns its side streams and event rings (thread-local LitStreams): two
+    threads running the schedules at once, each on its own torch stream, both stay exact."""
+    import threading
+
+    n = 512
+    r = np.random.default_rng(3)
+    a = r.integers(-8, 9, (n, n)).astype(np.float64)
+    b = r.integers(-8, 9, (n, n)).astype(np.float64)
+    want = a @ b
+    errors = []
+
+    def work(fn, reps):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(reps):
+                    da, db = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+                    dc = torch.zeros_like(da)
+                    fn(pk.Matrix(da), pk.Matrix(db), pk.Matrix(dc), pk.BasePolicy.naive_cutoff(64))
+                    s.synchronize()
+                    if not np.array_equal(dc.cpu().numpy(), want):
+                        errors.append(fn.__name__)
+        except Exception as e:  # pragma: no cover
+            errors.append(repr(e))
+
+    ts = [threading.Thread(target=work, args=(pk.in_place_winograd, 6)),
+          threading.Thread(target=work, args=(pk.two_temp_winograd, 6))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
