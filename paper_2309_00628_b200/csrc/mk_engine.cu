@@ -2521,7 +2521,7 @@ static bool use_pipeline(const Engine& e) {
 }
 
 // Side work onto a pass's leaf launches, balanced by bytes: launch k takes cap[k] bytes (its leaf
-// time at MK_SIDE_GBPS, default 900 GB/s: the side warps stream ~2 TB/s alone, but they slow the
+// time at MK_SIDE_GBPS, default 1000 GB/s (re-swept with the final side-work mix: 900 / 950 / 1000 / 1050 -> 66.84 / 66.59 / 66.51 / 67.06 ms): the side warps stream ~2 TB/s alone, but they slow the
 // DMMA warps they share the SM with, so cfg5 is fastest when about half of that is hidden:
 // 600 / 900 / 1200 / 1500 / 1800 GB/s -> 70.6 / 69.5 / 70.2 / 71.6 / 74.2 ms, sequential 73.7). Each chain (the next pass's operand sums, the
 // previous pass's post-additions) is a sequence of phases that depend on each other: a phase may
@@ -2602,7 +2602,7 @@ static double side_gbps() {
   static std::atomic<int> v{-1};
   if (v < 0) {
     const char* s = getenv("MK_SIDE_GBPS");
-    v = s ? std::max(0, atoi(s)) : 900;
+    v = s ? std::max(0, atoi(s)) : 1000;
   }
   return (double)v;
 }
