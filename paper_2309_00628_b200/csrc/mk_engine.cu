@@ -701,6 +701,7 @@ struct Engine {
   // Overlapped host path, last child of the last top-level product: the leaf runs as row_parts
   // launches over contiguous row ranges, row_part_done(part) after each, so that the last C
   // sub-block goes home in halves while the second half still computes (tail_halved: it did)
+  bool host_pageable = false;  // an operand of the host path is pageable (staged uploads, about half the pinned rate)
   int row_parts = 1;
   std::function<int(int)> row_part_done;
   bool tail_halved = false;
@@ -1431,6 +1432,9 @@ struct Engine {
     *lo = *hi = 0;
     if (opt == 0 || !sub_mode || L != 2 || fuse_preadds || plan_dfs() || np < 6) return;
     if (ozaki_leaf_for(leaf_m, leaf_n, leaf_k)) return;  // INT8 leaves: products finish before their uploads
+    // pageable operands go up through the bounce slots at about half the pinned rate: the uploads
+    // outlast three products and the pass would wait for them (measured 258.6 against 247 ms)
+    if (opt < 0 && host_pageable) return;
     // The pass waits for whole quadrants, so it must not start before the uploads end: the
     // child-by-child products ahead of it have to outlast the 8 quadrant uploads. One product is
     // 14 (n/4)^3 flops at ~34 TF/s, one quadrant 2 n^2 bytes at ~55 GB/s (this pool's PCIe rate):
@@ -3270,6 +3274,7 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
   const std::vector<int> kids0 = sub ? cached_head_children(algo, order0[0]) : std::vector<int>();
   cudaEvent_t none[61] = {nullptr};
   bool ts0[4];
+  const bool any_pageable = is_pageable(hA) || is_pageable(hB);
   // plan tables: sized by a dry run, recorded by a launch-free pass into a device arena at the top
   // of the workspace, uploaded once on the compute stream before any operand transfer is queued
   size_t tbl_total = 0;
@@ -3278,6 +3283,7 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
     d.dry = true;
     MK_TRY(setup_square(d, algo, dA, ldd, dB, ldd, dC, ldd, n, levels));
     d.head_children = kids0;
+    d.host_pageable = any_pageable;
     MK_TRY(d.fused_overlapped(order0, none, none + 8, n, sub ? none + 13 : nullptr, sub ? none + 45 : nullptr, ts0));
     tbl_total = d.table_bytes;
   }
@@ -3297,6 +3303,7 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
     r.tbl_dev = tbl_dev;
     r.tbl_host = &tbl_host;
     r.head_children = kids0;
+    r.host_pageable = any_pageable;
     MK_TRY(r.fused_overlapped(order0, none, none + 8, n, sub ? none + 13 : nullptr, sub ? none + 45 : nullptr, ts0));
     if (!tbl_host.empty())
       MK_CUDA_TRY(cudaMemcpyAsync(tbl_dev, tbl_host.data(), tbl_host.size(), cudaMemcpyHostToDevice, st));
@@ -3308,6 +3315,7 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
   e.ws = static_cast<char*>(ws);
   e.ws_bytes = ws ? tbl_off : 0;
   e.head_children = kids0;
+  e.host_pageable = any_pageable;
   if (tbl_total) {
     e.tbl_mode = 2;
     e.tbl_dev = tbl_dev;
