@@ -701,7 +701,7 @@ struct Engine {
   // Overlapped host path, last child of the last top-level product: the leaf runs as row_parts
   // launches over contiguous row ranges, row_part_done(part) after each, so that the last C
   // sub-block goes home in halves while the second half still computes (tail_halved: it did)
-  bool host_pageable = false;  // an operand of the host path is pageable (staged uploads, about half the pinned rate)
+  bool host_pageable = false;  // an operand or the result of the host path is pageable (staged transfers)
   int row_parts = 1;
   std::function<int(int)> row_part_done;
   bool tail_halved = false;
@@ -1432,8 +1432,10 @@ struct Engine {
     *lo = *hi = 0;
     if (opt == 0 || !sub_mode || L != 2 || fuse_preadds || plan_dfs() || np < 6) return;
     if (ozaki_leaf_for(leaf_m, leaf_n, leaf_k)) return;  // INT8 leaves: products finish before their uploads
-    // pageable operands go up through the bounce slots at about half the pinned rate: the uploads
-    // outlast three products and the pass would wait for them (measured 258.6 against 247 ms)
+    // pageable operands or results move through the bounce slots (uploads at ~43 GB/s, downloads at
+    // ~22 GB/s): C12 and C22, which the pass finishes together, would then still be on their way
+    // home long after the last product (timeline: compute done at 210 ms, downloads at 230;
+    // 258.6 against 247 ms per call)
     if (opt < 0 && host_pageable) return;
     // The pass waits for whole quadrants, so it must not start before the uploads end: the
     // child-by-child products ahead of it have to outlast the 8 quadrant uploads. One product is
@@ -3274,7 +3276,7 @@ int mk_strassen_host(int algo, const double* hA, int64_t lda, const double* hB, 
   const std::vector<int> kids0 = sub ? cached_head_children(algo, order0[0]) : std::vector<int>();
   cudaEvent_t none[61] = {nullptr};
   bool ts0[4];
-  const bool any_pageable = is_pageable(hA) || is_pageable(hB);
+  const bool any_pageable = is_pageable(hA) || is_pageable(hB) || is_pageable(hC);
   // plan tables: sized by a dry run, recorded by a launch-free pass into a device arena at the top
   // of the workspace, uploaded once on the compute stream before any operand transfer is queued
   size_t tbl_total = 0;
