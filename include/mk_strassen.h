@@ -83,9 +83,16 @@ int mk_version(void);
  *   first few and the last run as one grouped breadth-first pass once every upload has landed
  *   (instead of child by child behind the sub-block uploads). -1 = auto (the pass starts after as
  *   many products as outlast the uploads: 3 at n = 16384, none at n <= 8192), 0 = off, k in 1..6 =
- *   start after k products. Results differ only in the order C's partial sums are added. */
+ *   start after k products. Results differ only in the order C's partial sums are added.
+ * MK_OPT_PDL: 1 = sub-wave leaf launches and small block additions (the one-at-a-time launch
+ *   chains of the two-temp / in-place schedules) are launched as programmatic dependents
+ *   (cudaLaunchAttributeProgrammaticStreamSerialization): the next kernel of a stream is resident
+ *   and past its shared-memory prologue when the previous one ends, and touches global memory only
+ *   after griddepcontrol.wait (default); 0 = plain stream-ordered launches. Same kernels, same
+ *   order, bit-identical results. */
 enum mk_option { MK_OPT_FUSE_PREADDS = 1, MK_OPT_PLAN = 2, MK_OPT_LITERAL_TAIL = 3, MK_OPT_LEAF_SLICES = 4,
-                 MK_OPT_LEAF_MIN_LOG2 = 5, MK_OPT_BFS_GROUP = 6, MK_OPT_LITERAL_STREAMS = 7, MK_OPT_HOST_GROUP = 8 };
+                 MK_OPT_LEAF_MIN_LOG2 = 5, MK_OPT_BFS_GROUP = 6, MK_OPT_LITERAL_STREAMS = 7, MK_OPT_HOST_GROUP = 8,
+                 MK_OPT_PDL = 9 };
 int mk_set_option(int key, int value);
 int mk_get_option(int key, int* value);
 /* Calling-thread override of MK_OPT_PLAN / MK_OPT_LITERAL_TAIL (value -1 removes it). Applies to

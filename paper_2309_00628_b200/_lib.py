@@ -35,6 +35,7 @@ MK_OPT_LITERAL_TAIL = 3  # two-temp: 0 literal to the leaves (default), 1 breadt
 MK_OPT_LEAF_SLICES = 4  # 0 DMMA leaves (default), 4..8 INT8 tensor-core (Ozaki) leaves with that many slices
 MK_OPT_LEAF_MIN_LOG2 = 5  # INT8 leaves only for products with m*n*k >= 2^v (default 29)
 MK_OPT_BFS_GROUP = 6  # top-level products per breadth-first pass (0 = auto)
+MK_OPT_PDL = 9  # sub-wave leaf launches / small additions as programmatic dependent launches: 1 (default), 0 plain
 MK_OPT_HOST_GROUP = 8  # host path, 2 levels: middle products as one grouped pass (-1 auto, 0 off, k: after k products)
 MK_OPT_LITERAL_STREAMS = 7  # two-temp / in-place: 1 additions off the critical path on side streams (default), 0 one stream
 

@@ -8,11 +8,31 @@
 //             conftest.py:29-30), and an |x|max reduction for the exactness guard.
 // Roofline: every kernel here is bandwidth-bound (FP64: 8 B per element per stream).
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include "mk_blockops.h"
+#include "mk_device.cuh"
 #include "mk_xform.cuh"
 
 namespace mk {
+
+static std::atomic<int> g_pdl{-1};
+bool pdl_enabled() {
+  if (g_pdl < 0) {
+    const char* e = getenv("MK_PDL");
+    g_pdl = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_pdl == 1;
+}
+void set_pdl(bool on) { g_pdl = on ? 1 : 0; }
+
+static int64_t pdl_max_elems() {
+  const char* e = getenv("MK_PDL_MAX_LOG2");  // study knob: largest addition launched as a dependent
+  const int v = e ? atoi(e) : 22;
+  return (int64_t)1 << (v < 0 ? 0 : v > 40 ? 40 : v);
+}
+static const int64_t kPdlMaxElems = pdl_max_elems();
 
 struct CombineArgs {
   double* dst;
@@ -27,6 +47,8 @@ struct CombineArgs {
 // Each thread handles 2 consecutive columns (16 B) when vectorisable.
 template <bool VEC>
 __global__ void combine_kernel(const __grid_constant__ CombineArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t cols_v = VEC ? (a.cols >> 1) : a.cols;
   const int64_t total = a.rows * cols_v;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -57,6 +79,8 @@ __global__ void combine_kernel(const __grid_constant__ CombineArgs a) {
 // exactly: a thread reads its elements before it writes them.
 template <int U>
 __global__ void __launch_bounds__(256) combine2_kernel(const __grid_constant__ CombineArgs a) {
+  pdl_trigger();  // short kernel: the next launch's CTAs may queue up behind this one's at once
+  pdl_wait();
   const uint32_t cv = (uint32_t)(a.cols >> 1);
   const uint32_t total = (uint32_t)a.rows * cv;  // < 2^31 (checked by the launcher)
   const double s0 = a.sign[0], s1 = a.sign[1];
@@ -114,17 +138,16 @@ cudaError_t launch_combine(double* dst, int64_t ldd, const double* const* src, c
     vec = vec && (lds[t] % 2 == 0) && ((uintptr_t)src[t] % 16 == 0);
   }
   const int threads = 256;
+  const bool dep = rows * cols <= kPdlMaxElems;  // see launch_dep
   if (vec && nsrc == 2 && rows * (cols / 2) < ((int64_t)1 << 31)) {
     constexpr int U = 4;
     const int64_t work = rows * (cols / 2);
     int64_t blocks = (work + threads * U - 1) / (threads * U);
     if (blocks > 148 * 8) blocks = 148 * 8;
-    combine2_kernel<U><<<(unsigned)blocks, threads, 0, stream>>>(a);
+    return launch_dep(dep, combine2_kernel<U>, dim3((unsigned)blocks), dim3(threads), 0, stream, a);
   } else if (vec)
-    combine_kernel<true><<<grid_for(rows * (cols / 2), threads), threads, 0, stream>>>(a);
-  else
-    combine_kernel<false><<<grid_for(rows * cols, threads), threads, 0, stream>>>(a);
-  return cudaGetLastError();
+    return launch_dep(dep, combine_kernel<true>, dim3(grid_for(rows * (cols / 2), threads)), dim3(threads), 0, stream, a);
+  return launch_dep(dep, combine_kernel<false>, dim3(grid_for(rows * cols, threads)), dim3(threads), 0, stream, a);
 }
 
 // Batched quadrant transform: blockIdx.y = job, grid-stride over the job's elements. Each

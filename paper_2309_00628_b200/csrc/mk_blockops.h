@@ -59,6 +59,32 @@ struct alignas(64) MkBatchEntry {
 };
 
 namespace mk {
+
+// Programmatic dependent launch for the one-at-a-time launch chains of the literal schedules
+// (MK_OPT_PDL; env MK_PDL=0 disables): sub-wave leaf launches and small two-source additions carry
+// cudaLaunchAttributeProgrammaticStreamSerialization (`dep`), so the next kernel of the stream
+// is resident, past its shared-memory prologue and parked in pdl_wait() when the previous one
+// ends. Larger launches stay plain: a parked grid would hold the SMs that fall idle in a big
+// launch's tail, which the side streams' additions use (measured +0.2-0.4 ms on the n = 16384
+// literal plans with every launch dependent). Only kernels that call pdl_wait() before their
+// first global access may be launched through launch_dep.
+bool pdl_enabled();
+void set_pdl(bool on);  // mk_set_option(MK_OPT_PDL, ...)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_dep(bool dep, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = (dep && pdl_enabled()) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 cudaError_t launch_combine(double* dst, int64_t ldd, const double* const* src, const int64_t* lds,
                            const double* sign, int nsrc, int64_t rows, int64_t cols, cudaStream_t stream);
 cudaError_t launch_i64_to_f64(const int64_t* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,

@@ -10,6 +10,15 @@
 
 namespace mk {
 
+// Programmatic dependent launch (sm_90+): a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may become resident before the previous
+// kernel of its stream has finished; pdl_wait() blocks until every prerequisite grid has
+// completed and its memory operations are visible (a no-op for plain launches), so everything a
+// kernel does before it must not touch global memory a predecessor writes. pdl_trigger() lets the
+// runtime schedule the dependent grid once every CTA of this grid has issued it or exited.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

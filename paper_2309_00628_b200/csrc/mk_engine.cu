@@ -2915,6 +2915,10 @@ int mk_set_option(int key, int value) {
     g_host_group = value;
     return MK_OK;
   }
+  if (key == MK_OPT_PDL) {
+    set_pdl(value != 0);
+    return MK_OK;
+  }
   return fail(MK_ERR_ARG, "unknown option key");
 }
 
@@ -2952,6 +2956,8 @@ int mk_get_option(int key, int* value) {
     *value = literal_streams_enabled() ? 1 : 0;
   } else if (key == MK_OPT_HOST_GROUP) {
     *value = host_group_option();
+  } else if (key == MK_OPT_PDL) {
+    *value = pdl_enabled() ? 1 : 0;
   } else {
     return fail(MK_ERR_ARG, "unknown option key");
   }

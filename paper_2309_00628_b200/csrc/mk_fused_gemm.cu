@@ -814,6 +814,9 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
     fence_barrier_init();
   }
   __syncthreads();
+  // launched as a programmatic dependent (MK_PDL), the CTA may be resident before the previous
+  // kernel of the stream has finished: everything above touches only shared memory
+  pdl_wait();
 
   if (warp < PL::kLeadWarps) {
     // ============================ TMA producer (one thread) ============================
@@ -888,6 +891,9 @@ persistent_product_kernel(const __grid_constant__ CUtensorMap tmA_param, const _
            live = sk_unit(args, (t - tile0) * KT + ke, t, kb, ke))
         unit(t, kb, ke);
     }
+    // every load of this CTA is issued: its consumers are at most S stages and one epilogue from
+    // the end, so the stream's next kernel may start taking the SMs that fall idle
+    pdl_trigger();
     return;
   }
 
@@ -1472,21 +1478,18 @@ static cudaError_t launch_persistent_t(const CUtensorMap& tmA, const CUtensorMap
         err = launch_dp_side(G);
         side_done = true;
       } else {
-        dp<<<G, PL::kThreads, smem, stream>>>(tmA, tmB, tmC, args, prod);
-        err = cudaGetLastError();
+        err = launch_dep(false, dp, dim3(G), dim3(PL::kThreads), smem, stream, tmA, tmB, tmC, args, prod);
       }
       if (err != cudaSuccess) return err;
     }
     auto sk = persistent_product_kernel<MT, BN, true>;
     err = cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
-    sk<<<G, PL::kThreads, smem, stream>>>(tmA, tmB, tmC, args, prod);
-    err = cudaGetLastError();
+    err = launch_dep(false, sk, dim3(G), dim3(PL::kThreads), smem, stream, tmA, tmB, tmC, args, prod);
     return side_done ? err : side_after(err);
   }
   if (ncarry > 0) return launch_dp_side(grid);
-  dp<<<grid, PL::kThreads, smem, stream>>>(tmA, tmB, tmC, args, prod);
-  return side_after(cudaGetLastError());
+  return side_after(launch_dep(total <= G, dp, dim3(grid), dim3(PL::kThreads), smem, stream, tmA, tmB, tmC, args, prod));
 }
 
 static cudaError_t launch_persistent(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,

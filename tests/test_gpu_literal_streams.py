@@ -120,3 +120,37 @@ def test_side_streams_from_two_host_threads():
     for t in ts:
         t.join()
     assert not errors, errors
+
+
+def _set_pdl(on: bool):
+    lib = _lib.load(required=True)
+    _lib.check(lib.mk_set_option(_lib.MK_OPT_PDL, 1 if on else 0), "mk_set_option")
+
+
+@pytest.mark.parametrize("name", ["in-place", "two-temp", "winograd-block"])
+@pytest.mark.parametrize("n,cut", [(256, 32), (1024, 128), (2048, 256), (2048, 1024)])
+def test_programmatic_dependent_launches_bit_identical(name, n, cut):
+    """MK_OPT_PDL (default on): sub-wave leaf launches and small additions become resident before
+    their predecessor in the stream has finished and wait in griddepcontrol.wait. Same kernels in
+    the same order: C -- and the in-place schedule's clobbered A and B -- must equal the plain
+    stream-ordered run bit for bit on real data, call after call (a kernel touching global memory
+    ahead of its wait would show up as a differing or varying bit)."""
+    fn = {"in-place": pk.in_place_winograd, "two-temp": pk.two_temp_winograd,
+          "winograd-block": pk.winograd_block_mul}[name]
+    lib = _lib.load(required=True)
+    v = ctypes.c_int(-1)
+    assert lib.mk_get_option(_lib.MK_OPT_PDL, ctypes.byref(v)) == 0 and v.value == 1
+    r = np.random.default_rng(n * 13 + cut)
+    a, b = r.standard_normal((n, n)), r.standard_normal((n, n))
+    pol = pk.BasePolicy.naive_cutoff(cut)
+    try:
+        _set_pdl(False)
+        assert lib.mk_get_option(_lib.MK_OPT_PDL, ctypes.byref(v)) == 0 and v.value == 0
+        ref = _run(fn, a, b, pol)
+    finally:
+        _set_pdl(True)
+    for rep in range(3):
+        got = _run(fn, a, b, pol)
+        for x, y, what in zip(got, ref, ("C", "A after the call", "B after the call")):
+            assert np.array_equal(x, y, equal_nan=True), (name, n, cut, rep, what)
+    assert np.max(np.abs(ref[0] - a @ b)) < 1e-9 * n
