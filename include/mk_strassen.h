@@ -89,10 +89,16 @@ int mk_version(void);
  *   (cudaLaunchAttributeProgrammaticStreamSerialization): the next kernel of a stream is resident
  *   and past its shared-memory prologue when the previous one ends, and touches global memory only
  *   after griddepcontrol.wait (default); 0 = plain stream-ordered launches. Same kernels, same
- *   order, bit-identical results. */
+ *   order, bit-identical results.
+ * MK_OPT_PIPELINE (breadth-first plan, L >= 2, narrow-tile leaves): the pipelined plan -- one pass
+ *   per top-level product, each pass's transforms carried as side work by its neighbours' leaf
+ *   launches. 1 = when the leaves are long enough to hide transforms under (leaf volume >= 2^24
+ *   and 7^L leaves >= 2^36; default: smaller calls are launch-bound and take the grouped plan),
+ *   0 = never, 2 = for every call with narrow-tile leaves. Integer results are identical; real
+ *   results differ only in the order C's partial sums are added. */
 enum mk_option { MK_OPT_FUSE_PREADDS = 1, MK_OPT_PLAN = 2, MK_OPT_LITERAL_TAIL = 3, MK_OPT_LEAF_SLICES = 4,
                  MK_OPT_LEAF_MIN_LOG2 = 5, MK_OPT_BFS_GROUP = 6, MK_OPT_LITERAL_STREAMS = 7, MK_OPT_HOST_GROUP = 8,
-                 MK_OPT_PDL = 9 };
+                 MK_OPT_PDL = 9, MK_OPT_PIPELINE = 10 };
 int mk_set_option(int key, int value);
 int mk_get_option(int key, int* value);
 /* Calling-thread override of MK_OPT_PLAN / MK_OPT_LITERAL_TAIL (value -1 removes it). Applies to

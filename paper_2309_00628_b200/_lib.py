@@ -36,6 +36,7 @@ MK_OPT_LEAF_SLICES = 4  # 0 DMMA leaves (default), 4..8 INT8 tensor-core (Ozaki)
 MK_OPT_LEAF_MIN_LOG2 = 5  # INT8 leaves only for products with m*n*k >= 2^v (default 29)
 MK_OPT_BFS_GROUP = 6  # top-level products per breadth-first pass (0 = auto)
 MK_OPT_PDL = 9  # sub-wave leaf launches / small additions as programmatic dependent launches: 1 (default), 0 plain
+MK_OPT_PIPELINE = 10  # pipelined breadth-first plan: 0 never, 1 auto (default: leaves long enough to hide transforms), 2 every narrow-leaf call
 MK_OPT_HOST_GROUP = 8  # host path, 2 levels: middle products as one grouped pass (-1 auto, 0 off, k: after k products)
 MK_OPT_LITERAL_STREAMS = 7  # two-temp / in-place: 1 additions off the critical path on side streams (default), 0 one stream
 

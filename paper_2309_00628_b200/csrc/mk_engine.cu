@@ -2504,13 +2504,21 @@ static int run_bfs_grouped(Engine& e, int64_t M, int64_t N, int64_t K) {
 // computation as in the sequential plan: results are bit-identical.
 // Workspace: three rotating pass regions (pass i's operands and outputs live from its transforms,
 // during pass i-1's leaves, to its post-additions, during pass i+1's leaves).
-static bool pipeline_enabled() {
-  static std::atomic<int> v{-1};
-  if (v < 0) {
+// MK_OPT_PIPELINE / env MK_PIPELINE: 0 = never, 1 = when the leaves are narrow-tile ones and long
+// enough to hide transforms under (default), 2 = for every call with narrow-tile leaves.
+static std::atomic<int> g_pipeline{-1};
+static int pipeline_mode() {
+  if (g_pipeline < 0) {
     const char* s = getenv("MK_PIPELINE");
-    v = (s && s[0] == '0') ? 0 : 1;
+    g_pipeline = (s && s[0] == '0') ? 0 : (s && s[0] == '2') ? 2 : 1;
   }
-  return v == 1;
+  return g_pipeline;
+}
+static bool pipeline_enabled() { return pipeline_mode() != 0; }
+static int pipe_min_log2(const char* name, int dflt) {
+  const char* s = getenv(name);
+  const int v = s ? atoi(s) : dflt;
+  return v < 0 ? 0 : v > 62 ? 62 : v;
 }
 // The pipelined plan for a breadth-first call with these leaves (before any engine exists: the
 // rectangular driver decides from it whether C needs a padded staging copy).
@@ -2519,7 +2527,19 @@ static bool pipeline_for(int L, int64_t lm, int64_t ln, int64_t lk) {
   if (!pipeline_enabled() || bfs_group_option() > 0 || L < 2) return false;
   if (!persistent_enabled() || ozaki_leaf_for(lm, ln, lk)) return false;
   // the leaf launches must be narrow-tile ones (the layout that carries side work)
-  return persistent_tile_n((lm + MK_BM - 1) / MK_BM, ln, 1 << 12) == 64;
+  if (persistent_tile_n((lm + MK_BM - 1) / MK_BM, ln, 1 << 12) != 64) return false;
+  if (pipeline_mode() == 2) return true;
+  // ... and long enough to hide transforms under: with small leaves or little work in total the
+  // seven passes are launch-bound and the grouped plan's few launches win (BASELINE cfg1, n = 256
+  // cutoff 32: 0.68 ms pipelined against 0.33 ms grouped; cfg2, n = 1024 cutoff 64: 2.03 against
+  // 0.78 ms; 6000 x 7000 . 7000 x 5000 at cutoff 256, 188 x 219 x 157 leaves: 23 against 19 ms;
+  // 3000 x 3500 . 3500 x 2500 at cutoff 512, 343 leaves: 2.37 against 1.92 ms), while cfg5 gains
+  // 8% and the 6000-row product at cutoff 512 2% (profiles/r02_pipeline_thresholds.txt). Leaf
+  // volume >= 2^24 (256^3) and 7^L leaves of it >= 2^36 (about 2 ms of DMMA).
+  static const int min_leaf = pipe_min_log2("MK_PIPE_MIN_LEAF_LOG2", 24);
+  static const int min_total = pipe_min_log2("MK_PIPE_MIN_TOTAL_LOG2", 36);
+  const double leaf = (double)lm * (double)ln * (double)lk;
+  return leaf >= std::ldexp(1.0, min_leaf) && leaf * std::pow(7.0, L) >= std::ldexp(1.0, min_total);
 }
 static bool use_pipeline(const Engine& e) {
   if (e.tbl_mode != 0 || e.no_launch || e.leaf_count >= 0 || e.fuse_preadds) return false;
@@ -2919,6 +2939,11 @@ int mk_set_option(int key, int value) {
     set_pdl(value != 0);
     return MK_OK;
   }
+  if (key == MK_OPT_PIPELINE) {
+    if (value < 0 || value > 2) return fail(MK_ERR_ARG, "MK_OPT_PIPELINE takes 0 (off), 1 (auto) or 2 (every narrow-leaf call)");
+    g_pipeline = value;
+    return MK_OK;
+  }
   return fail(MK_ERR_ARG, "unknown option key");
 }
 
@@ -2958,6 +2983,8 @@ int mk_get_option(int key, int* value) {
     *value = host_group_option();
   } else if (key == MK_OPT_PDL) {
     *value = pdl_enabled() ? 1 : 0;
+  } else if (key == MK_OPT_PIPELINE) {
+    *value = pipeline_mode();
   } else {
     return fail(MK_ERR_ARG, "unknown option key");
   }

@@ -25,6 +25,38 @@ def _grouped():
     pk.set_plan("breadth-first", group=4)
 
 
+@pytest.fixture(autouse=True)
+def _pipelined_for_every_narrow_leaf_call():
+    """By default the pipelined plan is taken only when the leaves are long enough to hide
+    transforms under (MK_OPT_PIPELINE = 1); these cases are small, so ask for it explicitly."""
+    from paper_2309_00628_b200 import _lib
+
+    lib = _lib.load(required=True)
+    _lib.check(lib.mk_set_option(_lib.MK_OPT_PIPELINE, 2), "mk_set_option")
+    yield
+    _lib.check(lib.mk_set_option(_lib.MK_OPT_PIPELINE, 1), "mk_set_option")
+
+
+def test_small_calls_take_the_grouped_plan_by_default():
+    """MK_OPT_PIPELINE = 1 (default): BASELINE cfg1 / cfg2 sized calls are launch-bound and run
+    the grouped plan (same workspace as an explicit grouping of 4); cfg5 runs the pipelined one."""
+    import ctypes
+
+    from paper_2309_00628_b200 import _lib
+
+    lib = _lib.load(required=True)
+    v = ctypes.c_int(-1)
+    assert lib.mk_get_option(_lib.MK_OPT_PIPELINE, ctypes.byref(v)) == 0 and v.value == 2
+    assert lib.mk_set_option(_lib.MK_OPT_PIPELINE, 3) == _lib.MK_ERR_ARG
+    forced = lib.mk_workspace_bytes(2, 1024, 4), lib.mk_rect_workspace_bytes(2, 12000, 10000, 14000, 5)
+    _lib.check(lib.mk_set_option(_lib.MK_OPT_PIPELINE, 1), "mk_set_option")
+    auto = lib.mk_workspace_bytes(2, 1024, 4), lib.mk_rect_workspace_bytes(2, 12000, 10000, 14000, 5)
+    _lib.check(lib.mk_set_option(_lib.MK_OPT_PIPELINE, 0), "mk_set_option")
+    off = lib.mk_workspace_bytes(2, 1024, 4), lib.mk_rect_workspace_bytes(2, 12000, 10000, 14000, 5)
+    assert auto[0] == off[0] != forced[0]  # n = 1024, 64^3 leaves: grouped
+    assert auto[1] == forced[1] != off[1]  # cfg5: pipelined
+
+
 @pytest.mark.parametrize("algo", sorted(ALGOS))
 @pytest.mark.parametrize("n,cut", [(512, 64), (1024, 64), (256, 32), (128, 32)])
 def test_square_pipelined_matches_grouped_bitwise(algo, n, cut):
