@@ -1,6 +1,7 @@
 """Per-kernel SASS instruction counts of the built engine (cuobjdump -sass): the mnemonics that
 prove the FP64 tensor path (DMMA), TMA (UTMALDG / UTMASTG / UTMAREDG / UBLKCP), tensor memory
-(LDTM / STTM) and the INT8 tcgen05 path (UTCIMMA).
+(LDTM / STTM), the INT8 tcgen05 path (UTCIMMA) and programmatic dependent launch
+(ACQBULK = griddepcontrol.wait, PREEXIT = griddepcontrol.launch_dependents).
 
   python tools/sass_summary.py [path/to/libmk_strassen.so] > profiles/r02_sass_summary.txt
 """
@@ -13,7 +14,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "paper_2309_00628_b200", "libmk_strassen.so")
 OPS = ["DMMA", "DFMA", "DADD", "UTMALDG", "UTMASTG", "UTMAREDG", "UBLKCP", "LDTM", "STTM", "UTCIMMA", "UTCBAR",
-       "REDG", "LDS", "LDG", "STG", "SYNCS"]
+       "REDG", "LDS", "LDG", "STG", "SYNCS", "ACQBULK", "PREEXIT"]  # the last two: griddepcontrol.wait / .launch_dependents
 
 out = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True, check=True).stdout
 arch = sorted(set(re.findall(r"arch = (sm_\w+)", out)))
@@ -52,7 +53,7 @@ print(f"# SASS summary of {os.path.relpath(LIB, ROOT)} ({', '.join(arch)}), cuob
 for raw, nice in zip(names, pretty):
     c = counts[raw]
     keys = [k for k in OPS if c.get(k)] + sorted(k for k in c if k.startswith("DMMA shape"))
-    if not any(c.get(k) for k in ("DMMA", "UTMALDG", "UTCIMMA", "LDTM", "UBLKCP", "UTMAREDG")):
+    if not any(c.get(k) for k in ("DMMA", "UTMALDG", "UTCIMMA", "LDTM", "UBLKCP", "UTMAREDG", "ACQBULK")):
         continue
     print(f"\n{nice[:160]}")
     print("  " + ", ".join(f"{k} {c[k]}" for k in keys))
