@@ -164,3 +164,28 @@ def test_thread_plan_override_is_per_thread(lib):
         lib.mk_set_thread_option(_lib.MK_OPT_PLAN, -1)
         lib.mk_set_thread_option(_lib.MK_OPT_LITERAL_TAIL, -1)
         lib.mk_set_option(_lib.MK_OPT_PLAN, 0)
+
+
+def test_option_enum_matches_the_binding_and_round_trips_without_a_gpu():
+    """include/mk_strassen.h's `enum mk_option` and _lib.py's MK_OPT_* constants name the same keys
+    with the same values; the launch-shape options (MK_OPT_PDL, MK_OPT_PIPELINE) are plain process
+    settings, so they round-trip through mk_set_option / mk_get_option with no device present."""
+    import re
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    text = open(os.path.join(root, "include", "mk_strassen.h")).read()
+    body = re.search(r"enum mk_option \{(.*?)\};", text, re.S).group(1)
+    header = {k: int(v) for k, v in re.findall(r"(MK_OPT_\w+)\s*=\s*(\d+)", body)}
+    binding = {k: v for k, v in vars(_lib).items() if k.startswith("MK_OPT_")}
+    assert header == binding and len(set(header.values())) == len(header)
+    lib = _lib.load(required=True)
+    v = ctypes.c_int(-1)
+    for key, default, other in ((_lib.MK_OPT_PDL, 1, 0), (_lib.MK_OPT_PIPELINE, 1, 2), (_lib.MK_OPT_PIPELINE, 1, 0)):
+        assert lib.mk_get_option(key, ctypes.byref(v)) == 0 and v.value == default
+        try:
+            assert lib.mk_set_option(key, other) == 0
+            assert lib.mk_get_option(key, ctypes.byref(v)) == 0 and v.value == other
+        finally:
+            assert lib.mk_set_option(key, default) == 0
+    assert lib.mk_set_option(_lib.MK_OPT_PIPELINE, 3) == _lib.MK_ERR_ARG
+    assert lib.mk_set_option(_lib.MK_OPT_PIPELINE, -1) == _lib.MK_ERR_ARG
