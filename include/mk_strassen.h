@@ -72,7 +72,7 @@ int mk_version(void);
  *   smaller leaves stay on DMMA (the per-leaf INT8 kernels are launch- and wave-bound there).
  * MK_OPT_BFS_GROUP (breadth-first plan, L >= 2): top-level products per pass. 0 = auto (4: two
  *   passes over the 7 products, each keeping only its own operand sums and outputs -- about half
- *   the single-pass workspace); 7 or 8 = one pass (largest workspace); 1 = one top-level subtree
+ *   the single-pass workspace; one pass for products of at most 4096 in every extent); 7 or 8 = one pass (largest workspace); 1 = one top-level subtree
  *   at a time (smallest). Results differ only in the order C's partial sums are added.
  * MK_OPT_LITERAL_STREAMS (two-temp / in-place): 1 = block additions the next product does not
  *   depend on are issued on internal side streams, ordered by block-level hazard tracking, and

@@ -2466,16 +2466,21 @@ static bool use_bfs(const Engine& e, int64_t lm, int64_t ln) {
 // 7-product tables: each pass keeps only its own products' operand sums and outputs, so the peak
 // workspace is about half of a single pass -- n = 16384, L = 2: 7.5 GiB instead of 14.5 -- while
 // every leaf launch still spans several thousand tiles); the passes add into C.
-static int bfs_group_for(const Engine& e) {
+// Products of at most 4096 in every extent run as one pass: their whole single-pass workspace is
+// about 1 GiB or less, and the second pass's extra launches and re-read of C cost more than at
+// large orders (n = 4096, cutoff 512: 3.69 -> 3.39 ms; n = 2048, cutoff 128: 1.13 -> 0.91 ms;
+// n = 1024, cutoff 64: 0.76 -> 0.65 ms; profiles/r02_pipeline_thresholds.txt).
+static int bfs_group_for(const Engine& e, int64_t M, int64_t N, int64_t K) {
   const int opt = bfs_group_option();
   if (opt > 0) return opt;
+  if (std::max(M, std::max(N, K)) <= 4096) return e.co->nprod;
   return e.L >= 2 ? 4 : e.co->nprod;
 }
 
 static int run_bfs_grouped(Engine& e, int64_t M, int64_t N, int64_t K) {
   const Blk A{BASE_A, 0, 0, 1.0}, B{BASE_B, 0, 0, 1.0}, C{BASE_C, 0, 0, 1.0};
   const int np = e.co->nprod;
-  const int g = bfs_group_for(e);
+  const int g = bfs_group_for(e, M, N, K);
   if (g >= np || e.L < 2) return e.bfs(e.L, M, N, K, A, B, C);
   bool touched[4] = {false, false, false, false};
   for (int p0 = 0; p0 < np; p0 += g) {
